@@ -1,0 +1,438 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// C-ABI shim over the *unmodified* reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/).  It lets the
+// pytest suite, the golden-vector generator (tests/golden/make_golden.py) and
+// bench.py's reference arm drive the reference's own public API through
+// ctypes.  Every entry point forwards to the reference symbol named in its
+// comment; nothing here re-implements reference arithmetic.
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "opencap/cfcomplete.hpp"
+#include "opencap/core.hpp"
+#include "opencap/kernels.hpp"
+#include "opencap/policy.hpp"
+#include "opencap/predictor.hpp"
+#include "opencap/rng.hpp"
+#include "opencap/simnode.hpp"
+
+using namespace opencap;
+
+namespace {
+
+thread_local std::string g_err;
+
+// error codes follow include/ocg.h (OCG_E_*) so tests can compare them
+int map_exception() {
+    try {
+        throw;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const missing_artifact_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const config_error& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        std::string w = e.what();
+        if (w.find("cold") != std::string::npos) return 5;
+        if (w.find("divergence") != std::string::npos) return 6;
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+PowerGrid make_grid(const int* cpu, size_t ncpu, const int* gpu, size_t ngpu) {
+    return PowerGrid(std::vector<int>(cpu, cpu + ncpu), std::vector<int>(gpu, gpu + ngpu));
+}
+
+std::vector<std::string> app_ids(size_t m) {
+    std::vector<std::string> ids;
+    ids.reserve(m);
+    for (size_t i = 0; i < m; ++i) ids.push_back("a" + std::to_string(i));
+    return ids;
+}
+
+PerformanceMatrix make_matrix(size_t m, const PowerGrid& grid, const double* values,
+                              const uint8_t* mask) {
+    PerformanceMatrix pm(app_ids(m), grid);
+    const size_t n = pm.cols();
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j)
+            if (mask[i * n + j]) pm.set(i, j, values[i * n + j]);
+    return pm;
+}
+
+int copy_text(const std::string& s, char* out, size_t cap, size_t* len) {
+    if (len) *len = s.size();
+    if (out == nullptr || cap <= s.size()) {
+        g_err = "buffer too small";
+        return 7;
+    }
+    std::memcpy(out, s.data(), s.size());
+    out[s.size()] = 0;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+struct ref_ncf_hyper {
+    uint64_t app_dim, setting_dim;
+    uint64_t hidden[8];
+    uint64_t n_hidden;
+    double lr;
+    int32_t max_epochs, patience;
+    double val_fraction;
+    int32_t batch_size;
+};
+
+struct ref_ncf_meta {
+    uint64_t seed;
+    int32_t epochs_run;
+    double initial_train_mse, final_train_mse, best_val_mse;
+};
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// kern::force_lane (kernels.hpp:38) — 0 scalar, 1 avx2
+int ref_force_lane(int lane) {
+    return kern::force_lane(lane == 0 ? kern::Lane::scalar : kern::Lane::avx2) ? 0 : 1;
+}
+int ref_active_lane() { return kern::active_lane() == kern::Lane::scalar ? 0 : 1; }
+
+// derive_seed (rng.hpp:53)
+uint64_t ref_derive_seed(uint64_t root, const char* tag, uint64_t n) { return derive_seed(root, tag, n); }
+
+// Rng::next_u64 / uniform / uniform_int / normal (rng.hpp:19-38)
+void ref_rng_u64(uint64_t seed, uint64_t* out, size_t n) {
+    Rng r(seed);
+    for (size_t i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+void ref_rng_uniform(uint64_t seed, double lo, double hi, double* out, size_t n) {
+    Rng r(seed);
+    for (size_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+}
+void ref_rng_normal(uint64_t seed, double* out, size_t n) {
+    Rng r(seed);
+    for (size_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+// policy::select_caps (policy.cpp:17-64) applied to `rows` rows of length n
+int ref_select_caps(const double* rowsv, size_t rows, const int* cpu, size_t ncpu, const int* gpu,
+                    size_t ngpu, double gamma, int32_t* idx, double* saving, double* loss,
+                    int32_t* ncand) {
+    try {
+        policy::SelectionConfig cfg{make_grid(cpu, ncpu, gpu, ngpu), gamma};
+        const auto settings = cfg.grid.settings();
+        const size_t n = settings.size();
+        for (size_t r = 0; r < rows; ++r) {
+            const auto d = policy::select_caps(std::span<const double>(rowsv + r * n, n), cfg);
+            idx[r] = static_cast<int32_t>(std::find(settings.begin(), settings.end(), d.setting) -
+                                          settings.begin());
+            saving[r] = d.pred_saving;
+            loss[r] = d.pred_loss;
+            ncand[r] = static_cast<int32_t>(d.candidates_considered);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ProbePlan::default_plan (policy.cpp:66-82) -> setting column indices, in plan order
+int ref_default_plan(const int* cpu, size_t ncpu, const int* gpu, size_t ngpu, int32_t* out,
+                     size_t* count) {
+    try {
+        const auto grid = make_grid(cpu, ncpu, gpu, ngpu);
+        const auto plan = policy::ProbePlan::default_plan(grid);
+        const auto settings = grid.settings();
+        *count = plan.settings.size();
+        for (size_t k = 0; k < plan.settings.size(); ++k)
+            out[k] = static_cast<int32_t>(
+                std::find(settings.begin(), settings.end(), plan.settings[k]) - settings.begin());
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+static cf::NcfHyper to_hyper(const ref_ncf_hyper* h) {
+    cf::NcfHyper hy;
+    if (h == nullptr) return hy;
+    hy.app_dim = h->app_dim;
+    hy.setting_dim = h->setting_dim;
+    hy.hidden.assign(h->hidden, h->hidden + h->n_hidden);
+    hy.lr = h->lr;
+    hy.max_epochs = h->max_epochs;
+    hy.patience = h->patience;
+    hy.val_fraction = h->val_fraction;
+    hy.batch_size = h->batch_size;
+    return hy;
+}
+
+// cf::fit (cfcomplete.cpp:63-196) + NcfModel::to_json (:215-236)
+int ref_ncf_fit(size_t m, const int* cpu, size_t ncpu, const int* gpu, size_t ngpu,
+                const double* values, const uint8_t* mask, const ref_ncf_hyper* h, uint64_t seed,
+                char* json_out, size_t cap, size_t* len, ref_ncf_meta* meta) {
+    try {
+        const auto pm = make_matrix(m, make_grid(cpu, ncpu, gpu, ngpu), values, mask);
+        const auto model = cf::fit(pm, to_hyper(h), seed);
+        if (meta) {
+            meta->seed = model.meta().seed;
+            meta->epochs_run = model.meta().epochs_run;
+            meta->initial_train_mse = model.meta().initial_train_mse;
+            meta->final_train_mse = model.meta().final_train_mse;
+            meta->best_val_mse = model.meta().best_val_mse;
+        }
+        return copy_text(model.to_json(), json_out, cap, len);
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// cf::complete (cfcomplete.cpp:198-213): completed values, row-major m x n
+int ref_ncf_complete(size_t m, const int* cpu, size_t ncpu, const int* gpu, size_t ngpu,
+                     const double* values, const uint8_t* mask, const ref_ncf_hyper* h,
+                     uint64_t seed, double* out) {
+    try {
+        const auto pm = make_matrix(m, make_grid(cpu, ncpu, gpu, ngpu), values, mask);
+        const auto done = cf::complete(pm, to_hyper(h), seed);
+        for (size_t i = 0; i < done.rows(); ++i)
+            for (size_t j = 0; j < done.cols(); ++j) out[i * done.cols() + j] = done.value(i, j);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// NcfModel::from_json (:238-265) + NcfModel::predict (:47-58)
+int ref_ncf_predict(const char* json, const int64_t* rows, const int64_t* cols, size_t count,
+                    double* out) {
+    try {
+        const auto model = cf::NcfModel::from_json(json);
+        for (size_t k = 0; k < count; ++k)
+            out[k] = model.predict(static_cast<size_t>(rows[k]), static_cast<size_t>(cols[k]));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// pred::predictor_from_json (predictor.cpp:302) + pred::predict_perf (:151-157)
+int ref_predict_perf(const char* json, const double* counters, size_t count, double* out) {
+    try {
+        const auto model = pred::predictor_from_json(json);
+        for (size_t k = 0; k < count; ++k) {
+            const double* c = counters + 7 * k;
+            CounterSample s{c[0], c[1], c[2], c[3], c[4], c[5], c[6]};
+            out[k] = pred::predict_perf(model, s);
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ---- reference pipeline pieces used as input generators for goldens ------
+
+struct ref_spec {
+    int32_t archetype;
+    double kappa_c, alpha_c, kappa_g, alpha_g, base_runtime_s, cpu_phase_s, noise_sigma;
+    double ips_max, mem_tput_max, sm_clock_max;
+};
+
+static ref_spec to_c(const sim::WorkloadSpec& w) {
+    return {static_cast<int32_t>(w.archetype), w.kappa_c, w.alpha_c, w.kappa_g, w.alpha_g,
+            w.base_runtime_s, w.cpu_phase_s, w.noise_sigma, w.counter_scales.ips_max,
+            w.counter_scales.mem_tput_max, w.counter_scales.sm_clock_max};
+}
+
+// sim::make_suite (simnode.cpp:192-244); role 0 training, 1 evaluation
+int ref_make_suite(int32_t g, int32_t c, int32_t b, int32_t ins, uint64_t seed, double noise,
+                   int32_t role, double cpu_phase_fraction, const int* cpu, size_t ncpu,
+                   const int* gpu, size_t ngpu, ref_spec* out) {
+    try {
+        sim::SuiteParams p;
+        p.counts = {g, c, b, ins};
+        p.seed = seed;
+        p.noise_sigma = noise;
+        p.role = role == 0 ? sim::SuiteRole::training : sim::SuiteRole::evaluation;
+        p.cpu_phase_fraction = cpu_phase_fraction;
+        const auto suite = sim::make_suite(p, make_grid(cpu, ncpu, gpu, ngpu));
+        for (size_t k = 0; k < suite.size(); ++k) out[k] = to_c(suite[k]);
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+static sim::WorkloadSpec from_c(const ref_spec& s) {
+    sim::WorkloadSpec w;
+    w.app_id = "x";
+    w.archetype = static_cast<sim::Archetype>(s.archetype);
+    w.kappa_c = s.kappa_c;
+    w.alpha_c = s.alpha_c;
+    w.kappa_g = s.kappa_g;
+    w.alpha_g = s.alpha_g;
+    w.base_runtime_s = s.base_runtime_s;
+    w.cpu_phase_s = s.cpu_phase_s;
+    w.noise_sigma = s.noise_sigma;
+    w.counter_scales.ips_max = s.ips_max;
+    w.counter_scales.mem_tput_max = s.mem_tput_max;
+    w.counter_scales.sm_clock_max = s.sm_clock_max;
+    return w;
+}
+
+// sim::true_perf (simnode.cpp:43-45)
+double ref_true_perf(const ref_spec* s, int cpu_cap, int gpu_cap) {
+    return sim::true_perf(from_c(*s), PowerSetting{cpu_cap, gpu_cap});
+}
+
+// sim::sample_counters (simnode.cpp:98-110) -> 7 doubles
+void ref_sample_counters(const ref_spec* s, int cpu_cap, int gpu_cap, double* out7) {
+    const auto c = sim::sample_counters(from_c(*s), PowerSetting{cpu_cap, gpu_cap});
+    const double v[7] = {c.cpu_cap_w, c.gpu_cap_w, c.ips, c.mem_tput, c.sm_clock, c.fp_active, c.dram_active};
+    std::memcpy(out7, v, sizeof v);
+}
+
+// The reference CLI's offline phase (opencap_main.cpp:44-64) with RunConfig
+// defaults and the given root seed: dense profile matrix + predictor JSON.
+int ref_offline_default(uint64_t seed, double* dense_out, size_t* rows, char* pred_json, size_t cap,
+                        size_t* len) {
+    try {
+        const auto grid = PowerGrid::default_grid();
+        const auto suite = sim::make_suite(sim::default_training_params(seed), grid);
+        const auto profiled = pred::profile_suite(suite, grid, derive_seed(seed, "offline.profile"));
+        pred::PredictorHyper hyper;
+        hyper.seed = derive_seed(seed, "offline.predictor");
+        const auto model = pred::train_predictor(profiled.dataset, hyper);
+        const auto& mtx = profiled.matrix;
+        *rows = mtx.rows();
+        if (dense_out)
+            for (size_t i = 0; i < mtx.rows(); ++i)
+                for (size_t j = 0; j < mtx.cols(); ++j) dense_out[i * mtx.cols() + j] = mtx.value(i, j);
+        return copy_text(pred::predictor_to_json(model), pred_json, cap, len);
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+struct ref_online_out {
+    int32_t setting_idx;
+    double pred_saving, pred_loss;
+    int32_t candidates;
+    int32_t transition;
+    int32_t n_probes;
+    int32_t probe_idx[64];
+    double probe_val[64];
+    double completed_row[4096];
+};
+
+// policy::run_open_online (policy.cpp:114-191) for eval-suite app `eval_index`
+// with the CLI's seeds (opencap_main.cpp:79-87) against the offline block.
+int ref_online_default(uint64_t seed, int eval_index, const double* dense, size_t dense_rows,
+                       const char* pred_json, ref_online_out* out) {
+    try {
+        const auto grid = PowerGrid::default_grid();
+        const auto train = sim::make_suite(sim::default_training_params(seed), grid);
+        std::vector<std::string> ids;
+        for (const auto& s : train) ids.push_back(s.app_id);
+        if (ids.size() != dense_rows) throw std::invalid_argument("dense rows mismatch");
+        PerformanceMatrix dm(ids, grid);
+        for (size_t i = 0; i < dm.rows(); ++i)
+            for (size_t j = 0; j < dm.cols(); ++j) dm.set(i, j, dense[i * dm.cols() + j]);
+        const auto predictor = pred::predictor_from_json(pred_json);
+        const auto eval = sim::make_suite(sim::default_evaluation_params(seed), grid);
+        const auto& spec = eval.at(static_cast<size_t>(eval_index));
+        const auto cfg = policy::OnlineConfig::defaults(grid);
+        const auto oc = policy::run_open_online(spec, dm, predictor, cfg, derive_seed(seed, "open." + spec.app_id));
+        const auto settings = grid.settings();
+        out->setting_idx = static_cast<int32_t>(
+            std::find(settings.begin(), settings.end(), oc.decision.setting) - settings.begin());
+        out->pred_saving = oc.decision.pred_saving;
+        out->pred_loss = oc.decision.pred_loss;
+        out->candidates = static_cast<int32_t>(oc.decision.candidates_considered);
+        out->transition = oc.transition_detected ? 1 : 0;
+        out->n_probes = static_cast<int32_t>(oc.probes.size());
+        for (size_t k = 0; k < oc.probes.size(); ++k) {
+            out->probe_idx[k] = static_cast<int32_t>(
+                std::find(settings.begin(), settings.end(), oc.probes[k].first) - settings.begin());
+            out->probe_val[k] = oc.probes[k].second;
+        }
+        for (size_t j = 0; j < oc.completed_row.size(); ++j) out->completed_row[j] = oc.completed_row[j];
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// ---- reference arm of bench.py ------------------------------------------
+//
+// Per-app online completion (cf::complete on dense block + one probed row,
+// then policy::select_caps on the completed row) exactly as run_open_online
+// steps 3-4 (policy.cpp:178-189), for `napps` apps given as rows of
+// `probe_vals`/`probe_mask` (napps x n).  Apps are split over `threads`
+// std::threads (independent apps, evaluate_suite policy.cpp:360).  Returns the
+// wall seconds spent.
+double ref_online_batch(size_t d_rows, const int* cpu, size_t ncpu, const int* gpu, size_t ngpu,
+                        const double* dense, const double* probe_vals, const uint8_t* probe_mask,
+                        const uint64_t* seeds, size_t napps, double gamma, const ref_ncf_hyper* h,
+                        int threads, int32_t* sel_idx, double* sel_saving) {
+    const auto grid = make_grid(cpu, ncpu, gpu, ngpu);
+    const size_t n = grid.settings().size();
+    const auto hy = to_hyper(h);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    int nt = std::max(1, threads);
+    for (int t = 0; t < nt; ++t) {
+        pool.emplace_back([&, t] {
+            for (size_t a = static_cast<size_t>(t); a < napps; a += static_cast<size_t>(nt)) {
+                try {
+                    auto ids = app_ids(d_rows);
+                    ids.push_back("new");
+                    PerformanceMatrix pm(ids, grid);
+                    for (size_t i = 0; i < d_rows; ++i)
+                        for (size_t j = 0; j < n; ++j) pm.set(i, j, dense[i * n + j]);
+                    for (size_t j = 0; j < n; ++j)
+                        if (probe_mask[a * n + j]) pm.set(d_rows, j, probe_vals[a * n + j]);
+                    const auto done = cf::complete(pm, hy, seeds[a]);
+                    std::vector<double> row(n);
+                    for (size_t j = 0; j < n; ++j) row[j] = done.value(d_rows, j);
+                    const auto d = policy::select_caps(row, policy::SelectionConfig{grid, gamma});
+                    const auto settings = grid.settings();
+                    sel_idx[a] = static_cast<int32_t>(
+                        std::find(settings.begin(), settings.end(), d.setting) - settings.begin());
+                    sel_saving[a] = d.pred_saving;
+                } catch (...) {
+                    sel_idx[a] = -1;
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"
