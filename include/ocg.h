@@ -1,0 +1,144 @@
+/* ocg.h — C-ABI of the B200-native online CF completion + selection path
+ * (OPEN, arXiv 2508.07605, online phase).  Plain pointers and sizes only.
+ *
+ * Every entry point replaces a reference interface; the citation after each
+ * declaration names it (paths under the reference's proj/).  Semantics and
+ * error behaviour follow the reference; return codes map its exception types:
+ *
+ *   OCG_OK           0
+ *   OCG_E_INVALID    1  std::invalid_argument / config_error
+ *   OCG_E_MISSING    2  missing_artifact_error
+ *   OCG_E_LOGIC      3  std::logic_error / other runtime errors
+ *   OCG_E_RANGE      4  std::out_of_range
+ *   OCG_E_COLD       5  std::runtime_error "cold app row / setting column"
+ *   OCG_E_DIVERGE    6  std::runtime_error "ncf: divergence"
+ *   OCG_E_CUDA       7  CUDA / NCCL / allocation failure (no reference analogue)
+ *   OCG_E_UNSUPPORTED 8 shape outside what the compiled kernels handle
+ *
+ * All calls are synchronous on the context's stream.  A context is owned by
+ * one thread at a time (as cf::fit is single-owner, SPEC.md "Concurrency
+ * Model"); models are immutable after fit and may be shared for predict.
+ * "host" pointers are ordinary CPU memory; "_dev" entry points take device
+ * pointers already resident in HBM (used by bench.py's kernel-only timing).
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point returns OCG_E_CUDA. */
+#ifndef OCG_H
+#define OCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    OCG_OK = 0,
+    OCG_E_INVALID = 1,
+    OCG_E_MISSING = 2,
+    OCG_E_LOGIC = 3,
+    OCG_E_RANGE = 4,
+    OCG_E_COLD = 5,
+    OCG_E_DIVERGE = 6,
+    OCG_E_CUDA = 7,
+    OCG_E_UNSUPPORTED = 8
+};
+
+/* FP-order lane to reproduce: the reference's kern::Lane (kernels.hpp:28). */
+enum { OCG_LANE_SCALAR = 0, OCG_LANE_AVX2 = 1 };
+
+typedef struct ocg_ctx ocg_ctx;
+
+/* cf::NcfHyper (cfcomplete.hpp:11-20) */
+typedef struct {
+    int64_t app_dim, setting_dim;
+    int64_t hidden[8];
+    int64_t n_hidden;
+    double lr;
+    int32_t max_epochs, patience;
+    double val_fraction;
+    int32_t batch_size;
+} ocg_ncf_hyper;
+
+/* cf::NcfModel::Meta (cfcomplete.hpp:34-40) */
+typedef struct {
+    uint64_t seed;
+    int32_t epochs_run;
+    double initial_train_mse, final_train_mse, best_val_mse;
+} ocg_ncf_meta;
+
+const char* ocg_last_error(void);   /* thread-local message of the last failure */
+int ocg_version(void);
+void ocg_ncf_hyper_default(ocg_ncf_hyper* h);            /* NcfHyper{} defaults */
+uint64_t ocg_derive_seed(uint64_t root, const char* tag, uint64_t n); /* rng.hpp:53-60 */
+
+int ocg_ctx_create(int device, ocg_ctx** out);
+void ocg_ctx_destroy(ocg_ctx* ctx);
+int ocg_ctx_device_info(ocg_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- K1: Algorithm 2 selection ---------------------------------------
+ * policy::select_caps (policy.cpp:17-64; policy.hpp:34) batched over `nrows`
+ * completed rows, row-major nrows x (ncpu*ngpu) FP64, columns in
+ * PowerGrid::settings() order (core.cpp:59-65).  Outputs per row: column
+ * index of the chosen setting, pred_saving, pred_loss, candidates_considered.
+ * Bit-exact with the reference (FP64, same operation order). */
+int ocg_select_caps(ocg_ctx* ctx, const double* rows, int64_t nrows, const int32_t* cpu_caps,
+                    int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu, double gamma,
+                    int32_t* idx, double* saving, double* loss, int32_t* ncand);
+/* same, device pointers; rows FP64 (dtype 0) or FP32 (dtype 1, widened to
+ * double exactly before the FP64 arithmetic) */
+int ocg_select_caps_dev(ocg_ctx* ctx, const void* d_rows, int dtype, int64_t nrows,
+                        const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
+                        int32_t ngpu, double gamma, int32_t* d_idx, double* d_saving,
+                        double* d_loss, int32_t* d_ncand);
+
+/* ProbePlan::default_plan (policy.cpp:66-82): the sampled-setting set as
+ * column indices in plan order; returns the count through *count (<= 6). */
+int ocg_default_plan(const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                     int32_t* cols, int32_t* count);
+
+/* ---- per-app online completion (reference orchestration semantics) -----
+ * run_open_online steps 3-4 (policy.cpp:178-189) for `napps` independent
+ * unseen apps: for app a, sparse = dense block (d_rows x n, values + mask)
+ * with the app's probe row appended (probe_vals/probe_mask row a), then
+ * cf::complete(sparse, hyper, seeds[a]) (cfcomplete.cpp:198-213, i.e. a full
+ * cf::fit :63-196 + NcfModel::predict :47-58 of every missing cell), then
+ * policy::select_caps on the app's completed row.  One CTA owns one app's
+ * whole fit on the device; FP64, operation order of `lane`.
+ * Outputs (host, each may be NULL except status): completed row (napps x n),
+ * decision (idx/saving/loss/ncand), meta, per-app status (OCG_* code of the
+ * exception the reference would have thrown for that app). */
+int ocg_online_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_vals,
+                              const uint8_t* block_mask, int64_t napps, const double* probe_vals,
+                              const uint8_t* probe_mask, const uint64_t* seeds,
+                              const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
+                              int32_t ngpu, const ocg_ncf_hyper* hyper, double gamma, int lane,
+                              double* completed, int32_t* idx, double* saving, double* loss,
+                              int32_t* ncand, ocg_ncf_meta* meta, int32_t* status);
+
+/* Fit-only variant returning every app's parameters in the flat layout
+ * [app table | setting table | W0 b0 W1 b1 ... ] (the reference's Adam block
+ * order, cfcomplete.cpp:107-110) for parameter-level parity tests. */
+int ocg_online_fit_batch_params(ocg_ctx* ctx, int64_t d_rows, const double* block_vals,
+                                const uint8_t* block_mask, int64_t napps,
+                                const double* probe_vals, const uint8_t* probe_mask,
+                                const uint64_t* seeds, int32_t n, const ocg_ncf_hyper* hyper,
+                                int lane, double* params, int64_t params_stride,
+                                ocg_ncf_meta* meta, int32_t* status);
+
+/* NCF inference on given parameters (NcfModel::predict, cfcomplete.cpp:47-58):
+ * FP64 lane-exact forward + clamp for (rows[k], cols[k]) pairs. */
+int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* hyper,
+                    const double* params, const uint8_t* app_seen, const uint8_t* setting_seen,
+                    const int64_t* rows, const int64_t* cols, int64_t count, int lane,
+                    double* out);
+
+/* debug / parity probes of device building blocks */
+int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */
+double ocg_debug_exp_host(double x);                                       /* same code, host build */
+int ocg_debug_rng(ocg_ctx* ctx, uint64_t seed, int64_t n, uint64_t* out);  /* device mt19937_64 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCG_H */

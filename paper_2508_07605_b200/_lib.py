@@ -1,0 +1,129 @@
+"""ctypes binding of the in-tree C-ABI library ``libocg.so`` (include/ocg.h).
+
+The library is the only compute path: importing this module fails loudly if it
+is missing, and every compute entry point returns ``OCG_E_CUDA`` when no sm_100
+device is usable — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("OCG_LIB", _HERE / "libocg.so"))
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C paper_2508_07605_b200/csrc` "
+        "or `python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)"
+    )
+
+lib = ctypes.CDLL(str(LIB_PATH))
+
+OCG_OK, OCG_E_INVALID, OCG_E_MISSING, OCG_E_LOGIC = 0, 1, 2, 3
+OCG_E_RANGE, OCG_E_COLD, OCG_E_DIVERGE, OCG_E_CUDA, OCG_E_UNSUPPORTED = 4, 5, 6, 7, 8
+LANE_SCALAR, LANE_AVX2 = 0, 1
+
+c_i32, c_i64, c_u64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+
+
+class NcfHyperC(ctypes.Structure):
+    """ocg_ncf_hyper == cf::NcfHyper (cfcomplete.hpp:11-20)."""
+
+    _fields_ = [
+        ("app_dim", c_i64),
+        ("setting_dim", c_i64),
+        ("hidden", c_i64 * 8),
+        ("n_hidden", c_i64),
+        ("lr", c_dbl),
+        ("max_epochs", c_i32),
+        ("patience", c_i32),
+        ("val_fraction", c_dbl),
+        ("batch_size", c_i32),
+    ]
+
+
+class NcfMetaC(ctypes.Structure):
+    """ocg_ncf_meta == NcfModel::Meta (cfcomplete.hpp:34-40)."""
+
+    _fields_ = [
+        ("seed", c_u64),
+        ("epochs_run", c_i32),
+        ("initial_train_mse", c_dbl),
+        ("final_train_mse", c_dbl),
+        ("best_val_mse", c_dbl),
+    ]
+
+
+def _sig(name, restype, *argtypes):
+    fn = getattr(lib, name)
+    fn.restype = restype
+    fn.argtypes = list(argtypes)
+    return fn
+
+
+_sig("ocg_last_error", ctypes.c_char_p)
+_sig("ocg_version", ctypes.c_int)
+_sig("ocg_ncf_hyper_default", None, c_vp)
+_sig("ocg_derive_seed", c_u64, c_u64, ctypes.c_char_p, c_u64)
+_sig("ocg_ctx_create", ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_vp))
+_sig("ocg_ctx_destroy", None, c_vp)
+_sig("ocg_ctx_device_info", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_select_caps", ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_select_caps_dev", ctypes.c_int, c_vp, c_vp, ctypes.c_int, c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl,
+     c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_default_plan", ctypes.c_int, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp)
+_sig("ocg_online_complete_batch", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32,
+     c_vp, c_i32, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_online_fit_batch_params", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp,
+     ctypes.c_int, c_vp, c_i64, c_vp, c_vp)
+_sig("ocg_ncf_predict", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+     ctypes.c_int, c_vp)
+_sig("ocg_debug_exp", ctypes.c_int, c_vp, c_vp, c_i64, c_vp)
+_sig("ocg_debug_exp_host", c_dbl, c_dbl)
+_sig("ocg_debug_rng", ctypes.c_int, c_vp, c_u64, c_i64, c_vp)
+
+
+class OcgError(RuntimeError):
+    """Raised for a non-zero ocg return code; ``code`` is the OCG_E_* value."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[ocg code {code}] {msg}")
+        self.code = code
+
+
+# reference exception types each return code stands for (ocg.h)
+class InvalidArgument(OcgError, ValueError):
+    pass
+
+
+class OutOfRange(OcgError, IndexError):
+    pass
+
+
+class ColdError(OcgError):
+    pass
+
+
+class DivergenceError(OcgError):
+    pass
+
+
+class CudaError(OcgError):
+    pass
+
+
+_EXC = {OCG_E_INVALID: InvalidArgument, OCG_E_RANGE: OutOfRange, OCG_E_COLD: ColdError,
+        OCG_E_DIVERGE: DivergenceError, OCG_E_CUDA: CudaError}
+
+
+def check(rc: int) -> None:
+    if rc != OCG_OK:
+        msg = (lib.ocg_last_error() or b"").decode(errors="replace")
+        raise _EXC.get(rc, OcgError)(rc, msg)
+
+
+def ptr(a):
+    """Data pointer of a numpy array (or None)."""
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)

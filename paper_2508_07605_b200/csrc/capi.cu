@@ -1,0 +1,543 @@
+// C-ABI (include/ocg.h): host-side orchestration in C++ around the sm_100a
+// kernels.  Validation and error behaviour mirror the reference call sites
+// named in ocg.h; compute always runs on the GPU (no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ocg.h"
+#include "ncf_batch.h"
+#include "ncf_infer.h"
+#include "ocg_common.cuh"
+#include "select.h"
+
+struct ocg_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int cc_major = 0, cc_minor = 0;
+    cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define OCG_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return fail(OCG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// owning device buffer
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t count) {
+        n = count;
+        if (count == 0) return cudaSuccess;
+        return cudaMalloc(&p, sizeof(T) * count);
+    }
+    cudaError_t upload(const T* h, size_t count, cudaStream_t s) {
+        cudaError_t e = alloc(count);
+        if (e != cudaSuccess || count == 0) return e;
+        return cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s);
+    }
+    cudaError_t download(T* h, size_t count, cudaStream_t s) const {
+        if (h == nullptr || count == 0) return cudaSuccess;
+        return cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s);
+    }
+};
+
+// PowerGrid ctor checks (core.cpp:38-45): non-empty, positive, strictly increasing
+int check_caps(const int32_t* caps, int32_t k, const char* which) {
+    if (caps == nullptr || k <= 0) return fail(OCG_E_INVALID, std::string(which) + " cap list is empty");
+    for (int32_t i = 0; i < k; ++i) {
+        if (caps[i] <= 0) return fail(OCG_E_INVALID, std::string(which) + " caps must be positive watts");
+        if (i > 0 && caps[i] <= caps[i - 1])
+            return fail(OCG_E_INVALID, std::string(which) + " caps must be strictly increasing");
+    }
+    return OCG_OK;
+}
+
+int check_grid(const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu) {
+    int rc = check_caps(cpu, ncpu, "cpu");
+    if (rc) return rc;
+    return check_caps(gpu, ngpu, "gpu");
+}
+
+// cf::fit hyper checks (cfcomplete.cpp:64-66) + MlpModel widths (nnkit.cpp:51-53)
+int check_hyper(const ocg_ncf_hyper* h) {
+    if (h == nullptr) return fail(OCG_E_INVALID, "ncf: null hyperparameters");
+    if (h->app_dim == 0 || h->setting_dim == 0 || h->lr <= 0 || h->max_epochs <= 0 || h->batch_size <= 0 ||
+        h->val_fraction < 0 || h->val_fraction >= 1)
+        return fail(OCG_E_INVALID, "ncf: bad hyperparameters");
+    if (h->app_dim < 0 || h->setting_dim < 0 || h->n_hidden < 0 || h->n_hidden > 7)
+        return fail(OCG_E_INVALID, "ncf: bad hyperparameters");
+    for (int64_t l = 0; l < h->n_hidden; ++l)
+        if (h->hidden[l] <= 0) return fail(OCG_E_INVALID, "zero layer width");
+    return OCG_OK;
+}
+
+// MLP layer table shared by the geometry builders
+struct MlpShape {
+    int L = 0;
+    int dims[ocg::kMaxLayers + 1] = {};
+};
+
+int mlp_shape(const ocg_ncf_hyper* h, MlpShape& s) {
+    if (h->n_hidden + 1 > ocg::kMaxLayers)
+        return fail(OCG_E_UNSUPPORTED, "ncf: more than " + std::to_string(ocg::kMaxLayers - 1) + " hidden layers");
+    s.L = static_cast<int>(h->n_hidden) + 1;
+    s.dims[0] = static_cast<int>(h->app_dim + h->setting_dim);
+    for (int l = 0; l < h->n_hidden; ++l) s.dims[l + 1] = static_cast<int>(h->hidden[l]);
+    s.dims[s.L] = 1;
+    for (int l = 0; l <= s.L; ++l)
+        if (s.dims[l] > ocg::kMaxWidth)
+            return fail(OCG_E_UNSUPPORTED, "ncf: layer wider than " + std::to_string(ocg::kMaxWidth));
+    return OCG_OK;
+}
+
+const uint64_t kFitTagMix = ocg::splitmix64(ocg::fnv1a("ncf.fit"));
+
+struct BatchInputs {
+    int64_t d_rows;
+    const double* block_vals;
+    const uint8_t* block_mask;
+    int64_t napps;
+    const double* probe_vals;
+    const uint8_t* probe_mask;
+    const uint64_t* seeds;
+    int32_t n;
+};
+
+// Builds geometry + uploads the shared block; per-app rows validated on host.
+int prepare_batch(ocg_ctx* ctx, const BatchInputs& in, const ocg_ncf_hyper* h, ocg::BatchGeom& g,
+                  std::vector<double>& bval, std::vector<uint32_t>& brc, std::vector<uint8_t>& bseen,
+                  std::vector<int32_t>& status) {
+    (void)ctx;
+    int rc = check_hyper(h);
+    if (rc) return rc;
+    MlpShape ms;
+    if ((rc = mlp_shape(h, ms))) return rc;
+    if (in.napps < 0 || in.d_rows < 0 || in.n <= 0) return fail(OCG_E_INVALID, "bad batch shape");
+    if (h->batch_size > ocg::kMaxBatch)
+        return fail(OCG_E_UNSUPPORTED, "per-app kernel supports batch_size <= 32");
+    const int64_t m = in.d_rows + 1, n = in.n;
+    if (m > 4095 || n > 4095) return fail(OCG_E_UNSUPPORTED, "per-app kernel supports <= 4095 rows/cols");
+    std::memset(&g, 0, sizeof g);
+    g.m = static_cast<int>(m);
+    g.n = static_cast<int>(n);
+    g.ka = static_cast<int>(h->app_dim);
+    g.ks = static_cast<int>(h->setting_dim);
+    g.L = ms.L;
+    for (int l = 0; l <= ms.L; ++l) g.dims[l] = ms.dims[l];
+    int64_t off = m * g.ka;
+    g.set_off = static_cast<int>(off);
+    off += n * g.ks;
+    for (int l = 0; l < g.L; ++l) {
+        g.off_w[l] = static_cast<int>(off);
+        off += static_cast<int64_t>(g.dims[l]) * g.dims[l + 1];
+        g.off_b[l] = static_cast<int>(off);
+        off += g.dims[l + 1];
+    }
+    if (off > ocg::kMaxParams)
+        return fail(OCG_E_UNSUPPORTED, "per-app model has " + std::to_string(off) + " parameters (> " +
+                                           std::to_string(ocg::kMaxParams) + ")");
+    g.T = static_cast<int>(off);
+    for (int l = 0; l <= g.L; ++l) g.stride[l] = g.dims[l] | 1;  // odd stride: no bank conflicts
+    // shared block cells, row-major (cfcomplete.cpp:68-71)
+    bval.clear();
+    brc.clear();
+    bseen.assign(static_cast<size_t>(n), 0);
+    for (int64_t i = 0; i < in.d_rows; ++i) {
+        bool any = false;
+        for (int64_t j = 0; j < n; ++j) {
+            if (!in.block_mask[i * n + j]) continue;
+            const double v = in.block_vals[i * n + j];
+            if (!std::isfinite(v) || v <= 0.0 || v > 1.25)  // PerformanceMatrix::set (core.cpp:142-148)
+                return fail(OCG_E_INVALID, "normalized performance outside (0, 1.25]");
+            bval.push_back(v);
+            brc.push_back((static_cast<uint32_t>(i) << 16) | static_cast<uint32_t>(j));
+            bseen[j] = 1;
+            any = true;
+        }
+        if (!any) return fail(OCG_E_INVALID, "complete: app row has no observed entries (probe it first)");
+    }
+    g.block_nnz = static_cast<int>(bval.size());
+    g.block_full = g.block_nnz == in.d_rows * n ? 1 : 0;
+    g.max_cells = static_cast<int>(g.block_nnz + n);
+    if (g.max_cells > ocg::kMaxCells) return fail(OCG_E_UNSUPPORTED, "per-app matrix has too many cells");
+    g.batch = h->batch_size;
+    g.max_epochs = h->max_epochs;
+    g.patience = h->patience;
+    g.lr = h->lr;
+    g.val_fraction = h->val_fraction;
+    g.fit_tag_mix = kFitTagMix;
+    status.assign(static_cast<size_t>(in.napps), OCG_OK);
+    for (int64_t a = 0; a < in.napps; ++a)
+        for (int64_t j = 0; j < n; ++j)
+            if (in.probe_mask[a * n + j]) {
+                const double v = in.probe_vals[a * n + j];
+                if (!std::isfinite(v) || v <= 0.0 || v > 1.25) {
+                    status[a] = OCG_E_INVALID;
+                    break;
+                }
+            }
+    return OCG_OK;
+}
+
+int run_batch(ocg_ctx* ctx, const BatchInputs& in, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
+              int32_t ngpu, const ocg_ncf_hyper* h, double gamma, int lane, double* completed, int32_t* idx,
+              double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta, int32_t* status_out,
+              double* params, int64_t params_stride) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (lane != OCG_LANE_SCALAR && lane != OCG_LANE_AVX2) return fail(OCG_E_INVALID, "unknown lane");
+    if (!status_out) return fail(OCG_E_INVALID, "status output is required");
+    ocg::BatchGeom g;
+    std::vector<double> bval;
+    std::vector<uint32_t> brc;
+    std::vector<uint8_t> bseen;
+    std::vector<int32_t> hstatus;
+    int rc = prepare_batch(ctx, in, h, g, bval, brc, bseen, hstatus);
+    if (rc) return rc;
+    g.ngpu = ngpu;
+    g.e_base = cpu ? static_cast<double>(cpu[ncpu - 1] + gpu[ngpu - 1]) : 0.0;
+    g.gamma = gamma;
+    const int64_t n = in.n, napps = in.napps;
+    if (napps == 0) return OCG_OK;
+    cudaStream_t s = ctx->stream;
+    DBuf<double> d_bval, d_pv, d_comp, d_sav, d_loss, d_params;
+    DBuf<uint32_t> d_brc;
+    DBuf<uint8_t> d_bseen, d_pm;
+    DBuf<uint64_t> d_seeds;
+    DBuf<int32_t> d_cpu, d_gpu, d_idx, d_ncand, d_status;
+    DBuf<ocg::OcgMetaDev> d_meta;
+    OCG_CUDA(d_bval.upload(bval.data(), bval.size(), s));
+    OCG_CUDA(d_brc.upload(brc.data(), brc.size(), s));
+    OCG_CUDA(d_bseen.upload(bseen.data(), bseen.size(), s));
+    OCG_CUDA(d_pv.upload(in.probe_vals, static_cast<size_t>(napps * n), s));
+    OCG_CUDA(d_pm.upload(in.probe_mask, static_cast<size_t>(napps * n), s));
+    OCG_CUDA(d_seeds.upload(in.seeds, static_cast<size_t>(napps), s));
+    if (cpu) {
+        OCG_CUDA(d_cpu.upload(cpu, static_cast<size_t>(ncpu), s));
+        OCG_CUDA(d_gpu.upload(gpu, static_cast<size_t>(ngpu), s));
+    }
+    OCG_CUDA(d_status.upload(hstatus.data(), hstatus.size(), s));
+    ocg::BatchIO io{};
+    io.napps = napps;
+    io.block_val = d_bval.p;
+    io.block_rc = d_brc.p;
+    io.block_col_seen = d_bseen.p;
+    io.probe_vals = d_pv.p;
+    io.probe_mask = d_pm.p;
+    io.seeds = d_seeds.p;
+    io.cpu_caps = d_cpu.p;
+    io.gpu_caps = d_gpu.p;
+    io.status = d_status.p;
+    if (completed) {
+        OCG_CUDA(d_comp.alloc(static_cast<size_t>(napps * n)));
+        io.completed = d_comp.p;
+    }
+    if (cpu) {
+        OCG_CUDA(d_idx.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(d_sav.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(d_loss.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(d_ncand.alloc(static_cast<size_t>(napps)));
+        io.sel_idx = d_idx.p;
+        io.sel_saving = d_sav.p;
+        io.sel_loss = d_loss.p;
+        io.sel_ncand = d_ncand.p;
+    }
+    if (meta) {
+        OCG_CUDA(d_meta.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(cudaMemsetAsync(d_meta.p, 0, sizeof(ocg::OcgMetaDev) * static_cast<size_t>(napps), s));
+        io.meta = d_meta.p;
+    }
+    if (params) {
+        OCG_CUDA(d_params.alloc(static_cast<size_t>(napps * params_stride)));
+        io.params = d_params.p;
+        io.params_stride = params_stride;
+    }
+    const size_t smem = ocg::batch_smem_bytes(g);
+    if (smem > 227 * 1024) return fail(OCG_E_UNSUPPORTED, "per-app working set exceeds shared memory");
+    int per_sm = ocg::batch_max_active_per_sm(g, lane);
+    if (per_sm < 1) return fail(OCG_E_CUDA, "per-app kernel cannot be resident (smem " + std::to_string(smem) + ")");
+    const int64_t grid = std::min<int64_t>(napps, static_cast<int64_t>(per_sm) * ctx->sm_count);
+    OCG_CUDA(ocg::launch_app_batch(g, io, lane, static_cast<int>(grid), s));
+    std::vector<int32_t> dev_status(static_cast<size_t>(napps));
+    OCG_CUDA(d_status.download(dev_status.data(), dev_status.size(), s));
+    if (completed) OCG_CUDA(d_comp.download(completed, static_cast<size_t>(napps * n), s));
+    if (cpu) {
+        OCG_CUDA(d_idx.download(idx, static_cast<size_t>(napps), s));
+        OCG_CUDA(d_sav.download(saving, static_cast<size_t>(napps), s));
+        OCG_CUDA(d_loss.download(loss, static_cast<size_t>(napps), s));
+        OCG_CUDA(d_ncand.download(ncand, static_cast<size_t>(napps), s));
+    }
+    if (meta)
+        OCG_CUDA(d_meta.download(reinterpret_cast<ocg::OcgMetaDev*>(meta), static_cast<size_t>(napps), s));
+    if (params) OCG_CUDA(d_params.download(params, static_cast<size_t>(napps * params_stride), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    for (int64_t a = 0; a < napps; ++a)
+        status_out[a] = hstatus[a] != OCG_OK ? hstatus[a] : dev_status[a];
+    return OCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ocg_last_error(void) { return g_err.c_str(); }
+int ocg_version(void) { return 1; }
+
+void ocg_ncf_hyper_default(ocg_ncf_hyper* h) {
+    std::memset(h, 0, sizeof *h);
+    h->app_dim = 8;
+    h->setting_dim = 8;
+    h->hidden[0] = 32;
+    h->hidden[1] = 16;
+    h->n_hidden = 2;
+    h->lr = 1e-3;
+    h->max_epochs = 2000;
+    h->patience = 100;
+    h->val_fraction = 0.1;
+    h->batch_size = 32;
+}
+
+uint64_t ocg_derive_seed(uint64_t root, const char* tag, uint64_t n) {
+    return ocg::derive_seed_h(root, ocg::splitmix64(ocg::fnv1a(tag)), n);
+}
+
+int ocg_ctx_create(int device, ocg_ctx** out) {
+    if (!out) return fail(OCG_E_INVALID, "null output");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(OCG_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(OCG_E_INVALID, "device index out of range");
+    OCG_CUDA(cudaSetDevice(device));
+    auto* c = new ocg_ctx;
+    c->device = device;
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, device);
+    c->sm_count = prop.multiProcessorCount;
+    c->cc_major = prop.major;
+    c->cc_minor = prop.minor;
+    if (prop.major != 10) {
+        delete c;
+        return fail(OCG_E_CUDA, "kernels are built for sm_100a only (found sm_" + std::to_string(prop.major) +
+                                    std::to_string(prop.minor) + ")");
+    }
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(OCG_E_CUDA, cudaGetErrorString(e));
+    }
+    *out = c;
+    return OCG_OK;
+}
+
+void ocg_ctx_destroy(ocg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int ocg_ctx_device_info(ocg_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (cc_major) *cc_major = ctx->cc_major;
+    if (cc_minor) *cc_minor = ctx->cc_minor;
+    return OCG_OK;
+}
+
+int ocg_default_plan(const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu, int32_t* cols,
+                     int32_t* count) {
+    int rc = check_grid(cpu, ncpu, gpu, ngpu);
+    if (rc) return rc;
+    const int32_t wc[6] = {ncpu - 1, 0, 0, ncpu - 1, ncpu / 2, ncpu / 4};
+    const int32_t wg[6] = {ngpu - 1, 0, ngpu - 1, 0, ngpu / 2, ngpu / 4};
+    int32_t k = 0;
+    for (int w = 0; w < 6; ++w) {
+        const int32_t col = wc[w] * ngpu + wg[w];
+        if (std::find(cols, cols + k, col) == cols + k) cols[k++] = col;
+    }
+    *count = k;
+    return OCG_OK;
+}
+
+int ocg_select_caps_dev(ocg_ctx* ctx, const void* d_rows, int dtype, int64_t nrows, const int32_t* cpu,
+                        int32_t ncpu, const int32_t* gpu, int32_t ngpu, double gamma, int32_t* d_idx,
+                        double* d_saving, double* d_loss, int32_t* d_ncand) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    int rc = check_grid(cpu, ncpu, gpu, ngpu);
+    if (rc) return rc;
+    if (gamma <= 0.0 || gamma >= 1.0) return fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
+    if (dtype != 0 && dtype != 1) return fail(OCG_E_INVALID, "dtype must be 0 (f64) or 1 (f32)");
+    if (nrows == 0) return OCG_OK;
+    cudaStream_t s = ctx->stream;
+    DBuf<int32_t> dc, dg;
+    DBuf<int> dbad;
+    OCG_CUDA(dc.upload(cpu, static_cast<size_t>(ncpu), s));
+    OCG_CUDA(dg.upload(gpu, static_cast<size_t>(ngpu), s));
+    OCG_CUDA(dbad.alloc(1));
+    OCG_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), s));
+    const double e_base = static_cast<double>(cpu[ncpu - 1] + gpu[ngpu - 1]);
+    OCG_CUDA(ocg::launch_select_rows(d_rows, dtype, nrows, ncpu * ngpu, dc.p, dg.p, ngpu, e_base, gamma, d_idx,
+                                     d_saving, d_loss, d_ncand, dbad.p, ctx->sm_count, s));
+    int bad = 0;
+    OCG_CUDA(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    if (bad) return fail(OCG_E_INVALID, "select_caps: performance entries must be positive");
+    return OCG_OK;
+}
+
+int ocg_select_caps(ocg_ctx* ctx, const double* rows, int64_t nrows, const int32_t* cpu, int32_t ncpu,
+                    const int32_t* gpu, int32_t ngpu, double gamma, int32_t* idx, double* saving, double* loss,
+                    int32_t* ncand) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    int rc = check_grid(cpu, ncpu, gpu, ngpu);
+    if (rc) return rc;
+    if (gamma <= 0.0 || gamma >= 1.0) return fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
+    if (nrows == 0) return OCG_OK;
+    const size_t n = static_cast<size_t>(ncpu) * ngpu, R = static_cast<size_t>(nrows);
+    cudaStream_t s = ctx->stream;
+    DBuf<double> dr, ds, dl;
+    DBuf<int32_t> di, dn;
+    OCG_CUDA(dr.upload(rows, R * n, s));
+    OCG_CUDA(ds.alloc(R));
+    OCG_CUDA(dl.alloc(R));
+    OCG_CUDA(di.alloc(R));
+    OCG_CUDA(dn.alloc(R));
+    rc = ocg_select_caps_dev(ctx, dr.p, 0, nrows, cpu, ncpu, gpu, ngpu, gamma, di.p, ds.p, dl.p, dn.p);
+    if (rc) return rc;
+    OCG_CUDA(di.download(idx, R, s));
+    OCG_CUDA(ds.download(saving, R, s));
+    OCG_CUDA(dl.download(loss, R, s));
+    OCG_CUDA(dn.download(ncand, R, s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+int ocg_online_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_vals, const uint8_t* block_mask,
+                              int64_t napps, const double* probe_vals, const uint8_t* probe_mask,
+                              const uint64_t* seeds, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
+                              int32_t ngpu, const ocg_ncf_hyper* hyper, double gamma, int lane, double* completed,
+                              int32_t* idx, double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta,
+                              int32_t* status) {
+    int rc = check_grid(cpu, ncpu, gpu, ngpu);
+    if (rc) return rc;
+    if (gamma <= 0.0 || gamma >= 1.0) return fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
+    std::vector<int32_t> tmp_i;
+    std::vector<double> tmp_s, tmp_l;
+    std::vector<int32_t> tmp_n;
+    if (!idx) { tmp_i.resize(static_cast<size_t>(napps)); idx = tmp_i.data(); }
+    if (!saving) { tmp_s.resize(static_cast<size_t>(napps)); saving = tmp_s.data(); }
+    if (!loss) { tmp_l.resize(static_cast<size_t>(napps)); loss = tmp_l.data(); }
+    if (!ncand) { tmp_n.resize(static_cast<size_t>(napps)); ncand = tmp_n.data(); }
+    BatchInputs in{d_rows, block_vals, block_mask, napps, probe_vals, probe_mask, seeds, ncpu * ngpu};
+    return run_batch(ctx, in, cpu, ncpu, gpu, ngpu, hyper, gamma, lane, completed, idx, saving, loss, ncand, meta,
+                     status, nullptr, 0);
+}
+
+int ocg_online_fit_batch_params(ocg_ctx* ctx, int64_t d_rows, const double* block_vals, const uint8_t* block_mask,
+                                int64_t napps, const double* probe_vals, const uint8_t* probe_mask,
+                                const uint64_t* seeds, int32_t n, const ocg_ncf_hyper* hyper, int lane,
+                                double* params, int64_t params_stride, ocg_ncf_meta* meta, int32_t* status) {
+    BatchInputs in{d_rows, block_vals, block_mask, napps, probe_vals, probe_mask, seeds, n};
+    return run_batch(ctx, in, nullptr, 0, nullptr, 1, hyper, 0.05, lane, nullptr, nullptr, nullptr, nullptr,
+                     nullptr, meta, status, params, params_stride);
+}
+
+int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* h, const double* params,
+                    const uint8_t* app_seen, const uint8_t* setting_seen, const int64_t* rows, const int64_t* cols,
+                    int64_t count, int lane, double* out) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (!h) return fail(OCG_E_INVALID, "null hyper");
+    MlpShape ms;
+    int rc = mlp_shape(h, ms);
+    if (rc) return rc;
+    // NcfModel::predict checks, first offending query wins (cfcomplete.cpp:48-55)
+    for (int64_t k = 0; k < count; ++k) {
+        if (rows[k] < 0 || rows[k] >= m) return fail(OCG_E_RANGE, "ncf: app index out of range");
+        if (cols[k] < 0 || cols[k] >= n) return fail(OCG_E_RANGE, "ncf: setting index out of range");
+        if (!app_seen[rows[k]])
+            return fail(OCG_E_COLD, "ncf: cold app row " + std::to_string(rows[k]) + " (no observed entries at fit time)");
+        if (!setting_seen[cols[k]])
+            return fail(OCG_E_COLD,
+                        "ncf: cold setting column " + std::to_string(cols[k]) + " (no observed entries at fit time)");
+    }
+    if (count == 0) return OCG_OK;
+    ocg::InferGeom g{};
+    g.m = m;
+    g.n = n;
+    g.ka = static_cast<int>(h->app_dim);
+    g.ks = static_cast<int>(h->setting_dim);
+    g.L = ms.L;
+    for (int l = 0; l <= ms.L; ++l) g.dims[l] = ms.dims[l];
+    int64_t off = m * g.ka;
+    g.set_off = off;
+    off += n * g.ks;
+    for (int l = 0; l < g.L; ++l) {
+        g.off_w[l] = off;
+        off += static_cast<int64_t>(g.dims[l]) * g.dims[l + 1];
+        g.off_b[l] = off;
+        off += g.dims[l + 1];
+    }
+    cudaStream_t s = ctx->stream;
+    DBuf<double> dp, dout;
+    DBuf<int64_t> dr, dc;
+    OCG_CUDA(dp.upload(params, static_cast<size_t>(off), s));
+    OCG_CUDA(dr.upload(rows, static_cast<size_t>(count), s));
+    OCG_CUDA(dc.upload(cols, static_cast<size_t>(count), s));
+    OCG_CUDA(dout.alloc(static_cast<size_t>(count)));
+    OCG_CUDA(ocg::launch_ncf_predict(g, dp.p, dr.p, dc.p, count, dout.p, lane, s));
+    OCG_CUDA(dout.download(out, static_cast<size_t>(count), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    cudaStream_t s = ctx->stream;
+    DBuf<double> dx, dy;
+    OCG_CUDA(dx.upload(x, static_cast<size_t>(n), s));
+    OCG_CUDA(dy.alloc(static_cast<size_t>(n)));
+    OCG_CUDA(ocg::launch_exp_probe(dx.p, n, dy.p, s));
+    OCG_CUDA(dy.download(out, static_cast<size_t>(n), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+double ocg_debug_exp_host(double x) { return ocg::glibc_exp(x); }
+
+int ocg_debug_rng(ocg_ctx* ctx, uint64_t seed, int64_t n, uint64_t* out) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    cudaStream_t s = ctx->stream;
+    DBuf<uint64_t> d;
+    OCG_CUDA(d.alloc(static_cast<size_t>(n)));
+    OCG_CUDA(ocg::launch_rng_probe(seed, n, d.p, s));
+    OCG_CUDA(d.download(out, static_cast<size_t>(n), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,621 @@
+// Per-app batched NCF completion + selection — the reference's online phase
+// (run_open_online steps 3-4, policy.cpp:178-189) for many independent apps.
+//
+// One CTA owns one app's entire cf::complete (cfcomplete.cpp:198-213):
+//   init (cfcomplete.cpp:74-86) -> validation split (:92-103) -> epochs of
+//   shuffled minibatches with dense Adam (:150-178) -> validation MSE + early
+//   stop + best snapshot (:179-190) -> impute the app's missing cells with
+//   NcfModel::predict (:47-58) -> policy::select_caps (policy.cpp:17-64).
+// Everything runs in FP64 with the operation order of the chosen reference
+// kernel lane (scalar: kernels_scalar.cpp, AVX2: kernels_avx2.cpp), so the
+// result is bit-identical to the reference on the same inputs.
+//
+// CTA layout: 8 compute warps + 1 RNG warp.  The RNG warp owns the app's
+// mt19937_64 stream (rng.hpp) in shared memory: it draws the parameter init,
+// the validation split and, one epoch ahead, the next epoch's Fisher-Yates
+// permutation while the compute warps train on the current one (the shuffle
+// of epoch e+1 depends only on epoch e's permutation, never on parameters).
+//
+// Within a minibatch step lanes map to samples (<=32) and warps to neurons,
+// so every weight read is a shared-memory broadcast and every activation read
+// hits a padded (odd-stride) per-sample row.  Parameters live in shared
+// memory; Adam moments and the best snapshot live in the registers of the
+// thread that owns each parameter (owner-computes: the owner reduces its
+// gradient over the batch in sample order — the reference's accumulation
+// order — then applies Adam immediately).
+#include <cuda_runtime.h>
+
+#include "ncf_batch.h"
+#include "ocg_common.cuh"
+#include "select_dev.cuh"
+#include "lane_ops.cuh"
+
+namespace ocg {
+
+namespace {
+
+constexpr int kCW = 8;              // compute warps
+constexpr int kCT = kCW * 32;       // compute threads
+constexpr int kThreads = kCT + 32;  // + RNG warp
+constexpr int kEPT = kMaxParams / kCT;
+
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory"); }
+
+// ---- shared-memory carve-up ---------------------------------------------
+struct Smem {
+    double* P;                   // [T] parameters
+    double* act[kMaxLayers + 1]; // act[0] = gathered inputs X; act[l+1] = layer l output
+    double* del[kMaxLayers];     // del[l]: act-grad factors, then deltas, of layer l output
+    double* ig;                  // input grads [B x stride0]
+    double* cval;                // cell values [nc]
+    uint32_t* crc;               // cell (row<<16 | col) [nc]
+    uint16_t* tset;              // train cell ids
+    uint16_t* vset;              // validation cell ids
+    uint16_t* perm[2];           // epoch permutations of train positions
+    uint32_t* draw;              // per-epoch swap targets from the RNG warp
+    uint64_t* mt;                // [312]
+    double* row;                 // [n] completed app row
+    int* s_app;                  // [32]
+    int* s_set;                  // [32]
+    double* s_y;                 // [32]
+    int* ctrl;                   // scalars
+};
+
+__device__ inline char* carve(char*& p, size_t bytes) {
+    char* r = p;
+    p += (bytes + 15) & ~size_t(15);
+    return r;
+}
+
+__device__ inline void setup_smem(Smem& S, const BatchGeom& g, char* base) {
+    char* p = base;
+    S.P = reinterpret_cast<double*>(carve(p, sizeof(double) * g.T));
+    for (int l = 0; l <= g.L; ++l)
+        S.act[l] = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[l]));
+    for (int l = 0; l < g.L; ++l)
+        S.del[l] = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[l + 1]));
+    S.ig = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[0]));
+    S.cval = reinterpret_cast<double*>(carve(p, sizeof(double) * g.max_cells));
+    S.crc = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * g.max_cells));
+    S.tset = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
+    S.vset = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
+    S.perm[0] = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
+    S.perm[1] = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
+    S.draw = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * g.max_cells));
+    S.mt = reinterpret_cast<uint64_t*>(carve(p, sizeof(uint64_t) * 313));
+    S.row = reinterpret_cast<double*>(carve(p, sizeof(double) * g.n));
+    S.s_app = reinterpret_cast<int*>(carve(p, sizeof(int) * 32));
+    S.s_set = reinterpret_cast<int*>(carve(p, sizeof(int) * 32));
+    S.s_y = reinterpret_cast<double*>(carve(p, sizeof(double) * 32));
+    S.ctrl = reinterpret_cast<int*>(carve(p, sizeof(int) * 16));
+}
+
+enum Ctrl { kMtIdx = 0, kStop = 1, kImproved = 2, kNt = 3, kNv = 4, kNc = 5, kDiverged = 6 };
+
+// ---- RNG warp helpers ---------------------------------------------------
+// Fisher-Yates over a[0..len): for i = len..2: swap(a[i-1], a[uniform_int(0, i-1)])
+// (cfcomplete.cpp:98-99, :153-154).  Draws in parallel, swaps on lane 0.
+__device__ void shuffle_warp(uint16_t* a, int len, uint32_t* draw, MtWarp& mt, int lane) {
+    const int nd = len > 1 ? len - 1 : 0;
+    for (int base = 0; base < nd; base += 32) {
+        const int cnt = min(32, nd - base);
+        const uint64_t r = mt.take(cnt, lane);
+        if (lane < cnt) {
+            const uint64_t span = static_cast<uint64_t>(len - (base + lane));  // i for this draw
+            draw[base + lane] = static_cast<uint32_t>(r % span);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        for (int k = 0; k < nd; ++k) {
+            const int i = len - k;
+            const uint32_t j = draw[k];
+            const uint16_t t = a[i - 1];
+            a[i - 1] = a[j];
+            a[j] = t;
+        }
+    }
+    __syncwarp();
+}
+
+// uniform(lo, hi) draws into dst[0..cnt) (rng.hpp:22-24)
+__device__ void uniform_fill(double* dst, int cnt, double lo, double hi, MtWarp& mt, int lane) {
+    const double span = dsub(hi, lo);
+    for (int base = 0; base < cnt; base += 32) {
+        const int c = min(32, cnt - base);
+        const uint64_t r = mt.take(c, lane);
+        if (lane < c) {
+            const double u = static_cast<double>(r >> 11) * 0x1.0p-53;
+            dst[base + lane] = dadd(lo, dmul(span, u));
+        }
+    }
+}
+
+// ---- compute-warp helpers -----------------------------------------------
+// forward() / forward_tape() (nnkit.cpp:74-89, :124-138) for cnt <= 32 cells
+// whose (app, setting) ids are in s_app/s_set.  Leaves layer outputs in act[],
+// and (tape) SELU derivative factors in del[].
+template <int LANE>
+__device__ void forward_chunk(const Smem& S, const BatchGeom& g, int cnt, bool tape, int warp,
+                              int lane, int ctid) {
+    const int in0 = g.dims[0];
+    for (int w = ctid; w < cnt * in0; w += kCT) {
+        const int s = w / in0, i = w - s * in0;
+        const double v = i < g.ka ? S.P[S.s_app[s] * g.ka + i]
+                                  : S.P[g.set_off + S.s_set[s] * g.ks + (i - g.ka)];
+        S.act[0][s * g.stride[0] + i] = v;
+    }
+    bar_compute();
+    for (int l = 0; l < g.L; ++l) {
+        const int in = g.dims[l], out = g.dims[l + 1];
+        const double* W = S.P + g.off_w[l];
+        const double* b = S.P + g.off_b[l];
+        const double* ain = S.act[l] + lane * g.stride[l];
+        const bool hidden = l + 1 < g.L;
+        if (lane < cnt) {
+            for (int o = warp; o < out; o += kCW) {
+                const double z = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
+                double a = z, gf = 1.0;
+                if (hidden) selu_fwd(z, a, gf);
+                S.act[l + 1][lane * g.stride[l + 1] + o] = a;
+                if (tape) S.del[l][lane * g.stride[l + 1] + o] = gf;
+            }
+        }
+        bar_compute();
+    }
+}
+
+// backprop_sample (nnkit.cpp:184-212) deltas for a minibatch already
+// forwarded with tape; writes del[l] = deltas and ig = input gradients.
+template <int LANE>
+__device__ void backward_chunk(const Smem& S, const BatchGeom& g, int cnt, double scale, int warp,
+                               int lane) {
+    const int L = g.L;
+    if (warp == 0 && lane < cnt) {
+        const double err = dsub(S.act[L][lane * g.stride[L]], S.s_y[lane]);
+        // delta = 2*err*scale, then *= identity grad 1.0
+        S.del[L - 1][lane * g.stride[L]] = dmul(dmul(dmul(2.0, err), scale), 1.0);
+    }
+    bar_compute();
+    for (int l = L - 1; l >= 0; --l) {
+        const int in = g.dims[l], out = g.dims[l + 1];
+        const double* W = S.P + g.off_w[l];
+        const double* d = S.del[l] + lane * g.stride[l + 1];
+        if (lane < cnt) {
+            for (int c = warp; c < in; c += kCW) {
+                double nd = 0.0;  // matvec_t: out[c] = 0; out[c] += d[r]*w[r][c]
+                for (int r = 0; r < out; ++r) nd = LaneOps<LANE>::axpy(nd, d[r], W[r * in + c]);
+                if (l > 0) {
+                    double* gf = S.del[l - 1] + lane * g.stride[l] + c;
+                    *gf = dmul(nd, *gf);  // delta[o] *= activate_grad
+                } else {
+                    S.ig[lane * g.stride[0] + c] = nd;
+                }
+            }
+        }
+        bar_compute();
+    }
+}
+
+// sequential MSE over a list of cells (cells_mse, cfcomplete.cpp:34-43)
+template <int LANE>
+__device__ double cells_mse(const Smem& S, const BatchGeom& g, const uint16_t* ids, int count,
+                            int warp, int lane, int ctid) {
+    double acc = 0.0;  // meaningful on ctid 0 only
+    for (int base = 0; base < count; base += 32) {
+        const int cnt = min(32, count - base);
+        if (ctid < cnt) {
+            const int c = ids[base + ctid];
+            const uint32_t rc = S.crc[c];
+            S.s_app[ctid] = static_cast<int>(rc >> 16);
+            S.s_set[ctid] = static_cast<int>(rc & 0xffff);
+            S.s_y[ctid] = S.cval[c];
+        }
+        bar_compute();
+        forward_chunk<LANE>(S, g, cnt, false, warp, lane, ctid);
+        if (ctid == 0)
+            for (int s = 0; s < cnt; ++s) {
+                const double err = dsub(S.act[g.L][s * g.stride[g.L]], S.s_y[s]);
+                acc = dadd(acc, dmul(err, err));
+            }
+        bar_compute();
+    }
+    return count == 0 ? 0.0 : ddiv(acc, static_cast<double>(count));
+}
+
+// An owned parameter, packed: c[0,12) r[12,24) kind[24,26) layer[26,29) vec[29] valid[31]
+// kind: 0 app emb, 1 setting emb, 2 weight, 3 bias
+__device__ __forceinline__ int own_c(uint32_t d) { return d & 0xfff; }
+__device__ __forceinline__ int own_r(uint32_t d) { return (d >> 12) & 0xfff; }
+__device__ __forceinline__ int own_kind(uint32_t d) { return (d >> 24) & 3; }
+__device__ __forceinline__ int own_layer(uint32_t d) { return (d >> 26) & 7; }
+__device__ __forceinline__ bool own_vec(uint32_t d) { return (d >> 29) & 1; }
+__device__ __forceinline__ bool own_valid(uint32_t d) { return (d >> 31) & 1; }
+
+__device__ inline uint32_t describe(const BatchGeom& g, int e) {
+    if (e >= g.T) return 0u;
+    int kind, layer = 0, r, c = 0, start, size;
+    if (e < g.set_off) {
+        kind = 0;
+        r = e / g.ka;
+        c = e - r * g.ka;
+        start = 0;
+        size = g.set_off;
+    } else if (e < g.off_w[0]) {
+        kind = 1;
+        const int q = e - g.set_off;
+        r = q / g.ks;
+        c = q - r * g.ks;
+        start = g.set_off;
+        size = g.off_w[0] - g.set_off;
+    } else {
+        while (layer + 1 < g.L && e >= g.off_w[layer + 1]) ++layer;
+        if (e < g.off_b[layer]) {
+            kind = 2;
+            const int q = e - g.off_w[layer];
+            r = q / g.dims[layer];
+            c = q - r * g.dims[layer];
+            start = g.off_w[layer];
+            size = g.off_b[layer] - g.off_w[layer];
+        } else {
+            kind = 3;
+            r = e - g.off_b[layer];
+            start = g.off_b[layer];
+            size = g.dims[layer + 1];
+        }
+    }
+    const uint32_t vec = (e - start) < (size & ~3) ? 1u : 0u;
+    return 0x80000000u | (vec << 29) | (static_cast<uint32_t>(layer) << 26) |
+           (static_cast<uint32_t>(kind) << 24) | (static_cast<uint32_t>(r) << 12) | static_cast<uint32_t>(c);
+}
+
+}  // namespace
+
+template <int LANE>
+__global__ void __launch_bounds__(kThreads, 2)
+ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
+    extern __shared__ __align__(16) char smem_raw[];
+    Smem S;
+    setup_smem(S, g, smem_raw);
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool is_rng = warp == kCW;
+    const int ctid = tid;  // valid for compute threads
+    MtWarp mt{S.mt, S.ctrl + kMtIdx};
+
+    // owned parameters (compile-time indexed so moments stay in registers)
+    uint32_t own[kEPT];
+    double M1[kEPT], V1[kEPT], BEST[kEPT];
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) {
+        own[k] = is_rng ? 0u : describe(g, ctid + k * kCT);
+        M1[k] = V1[k] = BEST[k] = 0.0;
+    }
+
+    const double lr = g.lr, b1 = 0.9, b2 = 0.999, eps = 1e-8;  // nnkit.hpp:95
+    const double omb1 = dsub(1.0, b1), omb2 = dsub(1.0, b2);
+
+    for (int64_t app = blockIdx.x; app < io.napps; app += gridDim.x) {
+        // ---------------- load cells: block rows, then the app row ---------
+        const double* prow = io.probe_vals + app * g.n;
+        const uint8_t* pmask = io.probe_mask + app * g.n;
+        const int D = g.m - 1;
+        if (tid < 16) S.ctrl[tid] = 0;
+        __syncthreads();
+        if (tid == 0) {
+            S.ctrl[kMtIdx] = 312;
+            int napp = 0;
+            for (int j = 0; j < g.n; ++j) napp += pmask[j] != 0;
+            S.ctrl[kNc] = g.block_nnz + napp;
+        }
+        for (int q = tid; q < g.block_nnz; q += kThreads) {
+            S.cval[q] = io.block_val[q];
+            S.crc[q] = io.block_rc[q];
+        }
+        if (tid < 32) {  // app row cells in column order (ballot compaction)
+            int base = g.block_nnz;
+            for (int j0 = 0; j0 < g.n; j0 += 32) {
+                const int j = j0 + lane;
+                const bool obs = j < g.n && pmask[j] != 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, obs);
+                if (obs) {
+                    const int pos = base + __popc(bal & ((1u << lane) - 1));
+                    S.cval[pos] = prow[j];
+                    S.crc[pos] = (static_cast<uint32_t>(D) << 16) | static_cast<uint32_t>(j);
+                }
+                base += __popc(bal);
+            }
+        }
+        for (int j = tid; j < g.n; j += kThreads) S.row[j] = prow[j];
+        __syncthreads();
+        const int nc = S.ctrl[kNc];
+        const int napp_obs = nc - g.block_nnz;
+
+        int status = OCG_OK;
+        if (napp_obs == 0) status = OCG_E_INVALID;  // complete(): row without probes (:199-205)
+        bool cold = false;
+        if (status == OCG_OK && napp_obs < g.n) {
+            for (int j = 0; j < g.n; ++j)
+                if (!io.block_col_seen[j] && pmask[j] == 0) cold = true;
+        }
+        const bool full = status == OCG_OK && napp_obs == g.n && g.block_full;
+        if (status == OCG_OK && full) {
+            // fully observed -> returned unchanged, no fit (:206)
+        } else if (status == OCG_OK) {
+            const uint64_t seed = io.seeds[app];
+            // ------------- init + split (RNG warp) -----------------------
+            if (is_rng) {
+                mt.seed(derive_seed_h(seed, g.fit_tag_mix, 0), lane);
+                const double ba = dsqrt(ddiv(6.0, static_cast<double>(g.m + g.ka)));
+                uniform_fill(S.P, g.m * g.ka, -ba, ba, mt, lane);
+                const double bs = dsqrt(ddiv(6.0, static_cast<double>(g.n + g.ks)));
+                uniform_fill(S.P + g.set_off, g.n * g.ks, -bs, bs, mt, lane);
+                for (int l = 0; l < g.L; ++l) {
+                    const double bw = dsqrt(ddiv(6.0, static_cast<double>(g.dims[l] + g.dims[l + 1])));
+                    uniform_fill(S.P + g.off_w[l], g.dims[l] * g.dims[l + 1], -bw, bw, mt, lane);
+                    for (int q = lane; q < g.dims[l + 1]; q += 32) S.P[g.off_b[l] + q] = 0.0;
+                }
+                // validation split: order = shuffled iota(nc)
+                uint16_t* order = S.perm[1];
+                for (int q = lane; q < nc; q += 32) order[q] = static_cast<uint16_t>(q);
+                __syncwarp();
+                shuffle_warp(order, nc, S.draw, mt, lane);
+                const int val_count = static_cast<int>(g.val_fraction * static_cast<double>(nc));
+                int nv = 0, nt = 0;
+                for (int q = lane; q < nc; q += 32) {
+                    if (q < val_count) S.vset[q] = order[q];
+                    else S.tset[q - val_count] = order[q];
+                }
+                nv = val_count;
+                nt = nc - val_count;
+                __syncwarp();
+                if (nt == 0) {  // std::swap(train, val)
+                    for (int q = lane; q < nv; q += 32) S.tset[q] = S.vset[q];
+                    nt = nv;
+                    nv = 0;
+                }
+                if (lane == 0) {
+                    S.ctrl[kNt] = nt;
+                    S.ctrl[kNv] = nv;
+                }
+                __syncwarp();
+            }
+            __syncthreads();
+            const int nt = S.ctrl[kNt], nv = S.ctrl[kNv];
+            const uint16_t* mon = nv == 0 ? S.tset : S.vset;
+            const int nmon = nv == 0 ? nt : nv;
+
+            double init_train = 0.0, best_val = 0.0;
+            if (!is_rng) {
+#pragma unroll
+                for (int k = 0; k < kEPT; ++k) {
+                    M1[k] = V1[k] = 0.0;
+                    if (own_valid(own[k])) BEST[k] = S.P[ctid + k * kCT];
+                }
+                init_train = cells_mse<LANE>(S, g, S.tset, nt, warp, lane, ctid);
+                best_val = cells_mse<LANE>(S, g, mon, nmon, warp, lane, ctid);
+            } else {
+                // epoch-0 permutation of train positions
+                for (int q = lane; q < nt; q += 32) S.perm[0][q] = static_cast<uint16_t>(q);
+                __syncwarp();
+                shuffle_warp(S.perm[0], nt, S.draw, mt, lane);
+            }
+            __syncthreads();
+
+            int stale = 0, epoch = 0;
+            double b1p = 1.0, b2p = 1.0;
+            bool diverged = false;
+            for (; epoch < g.max_epochs; ++epoch) {
+                const uint16_t* perm = S.perm[epoch & 1];
+                if (is_rng) {
+                    uint16_t* nxt = S.perm[(epoch + 1) & 1];
+                    for (int q = lane; q < nt; q += 32) nxt[q] = perm[q];
+                    __syncwarp();
+                    shuffle_warp(nxt, nt, S.draw, mt, lane);
+                } else {
+                    for (int start = 0; start < nt; start += g.batch) {
+                        const int cnt = min(g.batch, nt - start);
+                        const double scale = ddiv(1.0, static_cast<double>(cnt));
+                        if (ctid < cnt) {
+                            const int c = S.tset[perm[start + ctid]];
+                            const uint32_t rc = S.crc[c];
+                            S.s_app[ctid] = static_cast<int>(rc >> 16);
+                            S.s_set[ctid] = static_cast<int>(rc & 0xffff);
+                            S.s_y[ctid] = S.cval[c];
+                        }
+                        bar_compute();
+                        forward_chunk<LANE>(S, g, cnt, true, warp, lane, ctid);
+                        backward_chunk<LANE>(S, g, cnt, scale, warp, lane);
+                        // AdamState::step (nnkit.cpp:239-251): dense over every block
+                        b1p = dmul(b1p, b1);
+                        b2p = dmul(b2p, b2);
+                        const double mc = ddiv(1.0, dsub(1.0, b1p)), vc = ddiv(1.0, dsub(1.0, b2p));
+#pragma unroll
+                        for (int k = 0; k < kEPT; ++k) {
+                            const uint32_t o = own[k];
+                            if (!own_valid(o)) continue;
+                            const int e = ctid + k * kCT, kind = own_kind(o), lay = own_layer(o);
+                            const int orow = own_r(o), ocol = own_c(o);
+                            double gsum = 0.0;
+                            if (kind == 2) {  // outer_acc: G[r][c] += d[r] * x[c]
+                                const double* dl = S.del[lay] + orow;
+                                const double* al = S.act[lay] + ocol;
+                                const int sd = g.stride[lay + 1], sa = g.stride[lay];
+                                for (int s = 0; s < cnt; ++s) gsum = LaneOps<LANE>::axpy(gsum, dl[s * sd], al[s * sa]);
+                            } else if (kind == 3) {  // bias: G[o] += delta[o]
+                                const double* dl = S.del[lay] + orow;
+                                const int sd = g.stride[lay + 1];
+                                for (int s = 0; s < cnt; ++s) gsum = dadd(gsum, dl[s * sd]);
+                            } else if (kind == 0) {  // app-embedding scatter (:171-172)
+                                for (int s = 0; s < cnt; ++s)
+                                    if (S.s_app[s] == orow) gsum = dadd(gsum, S.ig[s * g.stride[0] + ocol]);
+                            } else {  // setting-embedding scatter (:173-174)
+                                for (int s = 0; s < cnt; ++s)
+                                    if (S.s_set[s] == orow) gsum = dadd(gsum, S.ig[s * g.stride[0] + g.ka + ocol]);
+                            }
+                            double p = S.P[e];
+                            LaneOps<LANE>::adam(p, M1[k], V1[k], gsum, lr, b1, omb1, b2, omb2, eps, mc, vc, own_vec(o));
+                            S.P[e] = p;
+                        }
+                        bar_compute();
+                    }
+                    const double vl = cells_mse<LANE>(S, g, mon, nmon, warp, lane, ctid);
+                    if (ctid == 0) {
+                        int improved = 0, stop = 0, div = 0;
+                        if (!isfinite(vl)) {
+                            div = 1;
+                            stop = 1;
+                        } else if (vl < best_val) {
+                            best_val = vl;
+                            improved = 1;
+                            stale = 0;
+                        } else if (++stale > g.patience) {
+                            stop = 1;
+                        }
+                        S.ctrl[kImproved] = improved;
+                        S.ctrl[kStop] = stop;
+                        S.ctrl[kDiverged] = div;
+                    }
+                }
+                __syncthreads();
+                const bool stop = S.ctrl[kStop] != 0;
+                if (S.ctrl[kDiverged]) {
+                    diverged = true;
+                    break;
+                }
+                if (!is_rng && S.ctrl[kImproved]) {
+#pragma unroll
+                    for (int k = 0; k < kEPT; ++k)
+                        if (own_valid(own[k])) BEST[k] = S.P[ctid + k * kCT];
+                }
+                if (stop) {
+                    ++epoch;
+                    break;
+                }
+            }
+            if (diverged) {
+                status = OCG_E_DIVERGE;
+            } else {
+                // restore(best) (:190)
+                if (!is_rng) {
+#pragma unroll
+                    for (int k = 0; k < kEPT; ++k)
+                        if (own_valid(own[k])) S.P[ctid + k * kCT] = BEST[k];
+                }
+                __syncthreads();
+                double final_train = 0.0;
+                if (!is_rng) final_train = cells_mse<LANE>(S, g, S.tset, nt, warp, lane, ctid);
+                if (tid == 0) {
+                    for (int q = g.off_w[0]; q < g.T; ++q)  // check_finite (nnkit.cpp:106-113)
+                        if (!isfinite(S.P[q])) {
+                            S.ctrl[kDiverged] = 2;
+                            break;
+                        }
+                    if (io.meta) {
+                        OcgMetaDev m;
+                        m.seed = seed;
+                        m.epochs_run = epoch;
+                        m.initial_train_mse = init_train;
+                        m.final_train_mse = final_train;
+                        m.best_val_mse = best_val;
+                        io.meta[app] = m;
+                    }
+                }
+                if (io.params) {
+                    __syncthreads();
+                    for (int q = tid; q < g.T; q += kThreads) io.params[app * io.params_stride + q] = S.P[q];
+                }
+                __syncthreads();
+                if (S.ctrl[kDiverged] == 2) status = OCG_E_LOGIC;
+                else if (cold) status = OCG_E_COLD;
+                // ------------ impute the app's missing cells ---------------
+                if (status == OCG_OK && !is_rng) {
+                    for (int j0 = 0; j0 < g.n; j0 += 32) {
+                        if (ctid < 32) {
+                            const int j = j0 + ctid;
+                            S.s_app[ctid] = D;
+                            S.s_set[ctid] = j < g.n ? j : 0;
+                        }
+                        bar_compute();
+                        const int cnt = min(32, g.n - j0);
+                        forward_chunk<LANE>(S, g, cnt, false, warp, lane, ctid);
+                        if (ctid < cnt && pmask[j0 + ctid] == 0) {
+                            const double v = S.act[g.L][ctid * g.stride[g.L]];
+                            S.row[j0 + ctid] = v < 0.01 ? 0.01 : (1.25 < v ? 1.25 : v);  // std::clamp
+                        }
+                        bar_compute();
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---------------- select_caps on the completed row -----------------
+        if (warp == 0) {
+            SelResult r{};
+            if (status == OCG_OK) {
+                r = select_row_warp(S.row, g.n, io.cpu_caps, io.gpu_caps, g.ngpu, g.e_base, g.gamma, lane);
+                if (r.idx < 0) status = OCG_E_LOGIC;
+            }
+            if (lane == 0) {
+                io.status[app] = status;
+                if (io.sel_idx) io.sel_idx[app] = status == OCG_OK ? r.idx : -1;
+                if (io.sel_saving) io.sel_saving[app] = r.saving;
+                if (io.sel_loss) io.sel_loss[app] = r.loss;
+                if (io.sel_ncand) io.sel_ncand[app] = r.ncand;
+            }
+        }
+        if (io.completed)
+            for (int j = tid; j < g.n; j += kThreads) io.completed[app * g.n + j] = S.row[j];
+        __syncthreads();
+    }
+}
+
+size_t batch_smem_bytes(const BatchGeom& g) {
+    size_t b = 0;
+    auto add = [&](size_t x) { b += (x + 15) & ~size_t(15); };
+    add(sizeof(double) * g.T);
+    for (int l = 0; l <= g.L; ++l) add(sizeof(double) * 32 * g.stride[l]);
+    for (int l = 0; l < g.L; ++l) add(sizeof(double) * 32 * g.stride[l + 1]);
+    add(sizeof(double) * 32 * g.stride[0]);
+    add(sizeof(double) * g.max_cells);
+    add(sizeof(uint32_t) * g.max_cells);
+    for (int k = 0; k < 4; ++k) add(sizeof(uint16_t) * g.max_cells);
+    add(sizeof(uint32_t) * g.max_cells);
+    add(sizeof(uint64_t) * 313);
+    add(sizeof(double) * g.n);
+    add(sizeof(int) * 32);
+    add(sizeof(int) * 32);
+    add(sizeof(double) * 32);
+    add(sizeof(int) * 16);
+    return b;
+}
+
+int batch_threads() { return kThreads; }
+
+cudaError_t launch_app_batch(const BatchGeom& g, const BatchIO& io, int lane, int grid,
+                             cudaStream_t stream) {
+    const size_t smem = batch_smem_bytes(g);
+    if (lane == 0) {
+        cudaFuncSetAttribute(ncf_app_batch_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        ncf_app_batch_kernel<0><<<grid, kThreads, smem, stream>>>(g, io);
+    } else {
+        cudaFuncSetAttribute(ncf_app_batch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        ncf_app_batch_kernel<1><<<grid, kThreads, smem, stream>>>(g, io);
+    }
+    return cudaGetLastError();
+}
+
+int batch_max_active_per_sm(const BatchGeom& g, int lane) {
+    int n = 0;
+    const size_t smem = batch_smem_bytes(g);
+    if (lane == 0) {
+        cudaFuncSetAttribute(ncf_app_batch_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ncf_app_batch_kernel<0>, kThreads, smem);
+    } else {
+        cudaFuncSetAttribute(ncf_app_batch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ncf_app_batch_kernel<1>, kThreads, smem);
+    }
+    return n;
+}
+
+}  // namespace ocg
