@@ -101,6 +101,11 @@ class Port:
         L.ocgo_ncf_param_count.argtypes = [c_i64, c_i64, c_vp]
         L.ocgo_ncf_fit.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]
         L.ocgo_ncf_predict.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]
+        L.ocgo_set_lane.argtypes = [ctypes.c_int]
+
+    def set_lane(self, lane):
+        """0: reference scalar lane FP order, 1: AVX2/FMA lane."""
+        self.L.ocgo_set_lane(lane)
 
     def err(self):
         return self.L.ocgo_last_error().decode()

@@ -2,9 +2,10 @@
  * completion + selection path, used as the CPU oracle by tests/ and as the
  * "port" CPU baseline.  Never linked into the product.
  *
- * Arithmetic follows the reference's SCALAR kernel lane op for op
- * (kernels_scalar.cpp, compiled for baseline x86-64, i.e. no FMA); this file
- * is compiled with -ffp-contract=off for the same reason.  exp() is the host
+ * Arithmetic follows either reference kernel lane op for op (ocgo_set_lane):
+ * the scalar lane (kernels_scalar.cpp, baseline x86-64, no FMA) or the AVX2
+ * lane as g++ compiles kernels_avx2.cpp; this file is compiled with
+ * -ffp-contract=off so only the explicit fma() calls fuse.  exp() is the host
  * libm exp, exactly what the reference calls (nnkit.cpp:30, :41).
  *
  * Parity: pinned against oracle/_ref (the reference library itself) and the
@@ -220,7 +221,60 @@ static double act_grad(int hidden, double z) {
     return z > 0 ? kLambda : kLambda * kAlpha * exp(z);
 }
 
-/* forward with tape (nnkit.cpp:124-138); kernels_scalar.cpp:9-21 dot/matvec */
+/* The reference's two kernel lanes (kern::Ops, kernels.hpp:12-26).
+ * lane 0: kernels_scalar.cpp (baseline x86-64, no FMA).
+ * lane 1: kernels_avx2.cpp as g++ -O3 -mavx2 -mfma compiles it: dot = four
+ *   FMA partial sums over full 4-chunks, hsum (a0+a2)+(a1+a3), plus a tail
+ *   that g++ vectorises as unfused products for the first two leftover
+ *   elements and an FMA for a third/lone one; axpy = FMA everywhere;
+ *   adam = FMA moment updates and p = fnma(lr, num/den, p) (g++ contracts the
+ *   intrinsics' sub(p, mul(lr, q))) on full 4-chunks of each block, scalar
+ *   formula on the block tail. */
+static int g_lane = 0;
+static double lane_dot(const double* w, const double* x, int64_t n) {
+    if (g_lane == 0) {
+        double acc = 0.0;
+        for (int64_t i = 0; i < n; ++i) acc += w[i] * x[i];
+        return acc;
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t i = 0;
+    for (; i + 4 <= n; i += 4) {
+        a0 = fma(w[i], x[i], a0);
+        a1 = fma(w[i + 1], x[i + 1], a1);
+        a2 = fma(w[i + 2], x[i + 2], a2);
+        a3 = fma(w[i + 3], x[i + 3], a3);
+    }
+    double tail = 0.0;
+    const int64_t r = n - i;
+    if (r >= 2) {
+        tail = tail + w[i] * x[i];
+        tail = tail + w[i + 1] * x[i + 1];
+        if (r == 3) tail = fma(w[i + 2], x[i + 2], tail);
+    } else if (r == 1) {
+        tail = fma(w[i], x[i], tail);
+    }
+    return ((a0 + a2) + (a1 + a3)) + tail;
+}
+static double lane_axpy(double y, double a, double x) { return g_lane == 0 ? y + a * x : fma(a, x, y); }
+static void lane_adam(double* p, const double* g, double* m, double* v, int64_t n, double lr, double b1, double b2,
+                      double eps, double b1p, double b2p) {
+    const double mc = 1.0 / (1.0 - b1p), vc = 1.0 / (1.0 - b2p);
+    const int64_t nvec = g_lane == 0 ? 0 : (n & ~(int64_t)3);
+    for (int64_t i = 0; i < nvec; ++i) {
+        m[i] = fma(b1, m[i], (1.0 - b1) * g[i]);
+        v[i] = fma(b2, v[i], (1.0 - b2) * (g[i] * g[i]));
+        const double num = m[i] * mc, den = sqrt(v[i] * vc) + eps;
+        p[i] = fma(-lr, num / den, p[i]); /* g++ fuses sub(p, mul(lr, q)) into vfnmadd */
+    }
+    for (int64_t i = nvec; i < n; ++i) {
+        m[i] = b1 * m[i] + (1.0 - b1) * g[i];
+        v[i] = b2 * v[i] + (1.0 - b2) * g[i] * g[i];
+        p[i] -= lr * (m[i] * mc) / (sqrt(v[i] * vc) + eps);
+    }
+}
+
+/* forward with tape (nnkit.cpp:124-138); matvec = dot per row */
 static double forward(const layout* L, const double* P, const double* x, double acts[][MAXW],
                       double pre[][MAXW]) {
     double a[MAXW], z[MAXW];
@@ -231,9 +285,7 @@ static double forward(const layout* L, const double* P, const double* x, double 
         const double* b = P + L->off_b[l];
         if (acts) memcpy(acts[l], a, sizeof(double) * (size_t)in);
         for (int64_t o = 0; o < out; ++o) {
-            double acc = 0.0;
-            for (int64_t i = 0; i < in; ++i) acc += W[o * in + i] * a[i];
-            z[o] = acc + b[o];
+            z[o] = lane_dot(W + o * in, a, in) + b[o];
         }
         if (pre) memcpy(pre[l], z, sizeof(double) * (size_t)out);
         const int hidden = l + 1 < L->nl;
@@ -280,16 +332,18 @@ static void backprop(const layout* L, const double* P, const cell* c, double sca
         double* Gb = G + L->off_b[l];
         for (int64_t o = 0; o < outd; ++o) delta[o] *= act_grad(hidden, pre[l][o]);
         for (int64_t r = 0; r < outd; ++r) /* outer_acc kernels_scalar.cpp:28-30 */
-            for (int64_t q = 0; q < in; ++q) GW[r * in + q] += delta[r] * acts[l][q];
+            for (int64_t q = 0; q < in; ++q) GW[r * in + q] = lane_axpy(GW[r * in + q], delta[r], acts[l][q]);
         for (int64_t o = 0; o < outd; ++o) Gb[o] += delta[o];
         for (int64_t q = 0; q < in; ++q) nd[q] = 0.0; /* matvec_t kernels_scalar.cpp:23-26 */
         for (int64_t r = 0; r < outd; ++r)
-            for (int64_t q = 0; q < in; ++q) nd[q] += delta[r] * W[r * in + q];
+            for (int64_t q = 0; q < in; ++q) nd[q] = lane_axpy(nd[q], delta[r], W[r * in + q]);
         memcpy(delta, nd, sizeof(double) * (size_t)in);
     }
     for (int64_t k = 0; k < L->ka; ++k) G[c->app * L->ka + k] += delta[k];
     for (int64_t k = 0; k < L->ks; ++k) G[L->m * L->ka + c->setting * L->ks + k] += delta[L->ka + k];
 }
+
+void ocgo_set_lane(int lane) { g_lane = lane; }
 
 int ocgo_ncf_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col,
                  const double* val, const ocgo_hyper* h, uint64_t seed, double* P, ocgo_meta* meta,
@@ -387,15 +441,15 @@ int ocgo_ncf_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* co
             const double scale = 1.0 / (double)(end - start);
             memset(G, 0, sizeof(double) * (size_t)T);
             for (int64_t i = start; i < end; ++i) backprop(&L, P, &tset[idx[i]], scale, G);
-            /* AdamState::step (nnkit.cpp:239-251) -> adam_update_scalar
-             * (kernels_scalar.cpp:32-41) over every block, dense */
+            /* AdamState::step (nnkit.cpp:239-251): adam_update over every block, dense */
             b1p *= b1;
             b2p *= b2;
-            const double mc = 1.0 / (1.0 - b1p), vc = 1.0 / (1.0 - b2p);
-            for (int64_t q = 0; q < T; ++q) {
-                M1[q] = b1 * M1[q] + (1.0 - b1) * G[q];
-                V1[q] = b2 * V1[q] + (1.0 - b2) * G[q] * G[q];
-                P[q] -= lr * (M1[q] * mc) / (sqrt(V1[q] * vc) + eps);
+            lane_adam(P, G, M1, V1, m * L.ka, lr, b1, b2, eps, b1p, b2p);
+            lane_adam(P + m * L.ka, G + m * L.ka, M1 + m * L.ka, V1 + m * L.ka, n * L.ks, lr, b1, b2, eps, b1p, b2p);
+            for (int64_t l = 0; l < L.nl; ++l) {
+                const int64_t ow = L.off_w[l], ob = L.off_b[l];
+                lane_adam(P + ow, G + ow, M1 + ow, V1 + ow, ob - ow, lr, b1, b2, eps, b1p, b2p);
+                lane_adam(P + ob, G + ob, M1 + ob, V1 + ob, L.dims[l + 1], lr, b1, b2, eps, b1p, b2p);
             }
         }
         const double vl = cells_mse(&L, P, mon, nmon); /* cfcomplete.cpp:179-188 */

@@ -47,6 +47,8 @@ int ocgo_select_caps(const double* rows, int64_t nrows, const int32_t* cpu, int3
 int ocgo_default_plan(const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
                       int32_t* out_cols, int32_t* count);
 
+/* reference kernel lane to follow: 0 scalar (default), 1 AVX2/FMA */
+void ocgo_set_lane(int lane);
 int64_t ocgo_ncf_param_count(int64_t m, int64_t n, const ocgo_hyper* h);
 int ocgo_ncf_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col,
                  const double* val, const ocgo_hyper* h, uint64_t seed, double* params,

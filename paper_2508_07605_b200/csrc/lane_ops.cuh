@@ -2,8 +2,9 @@
 // device code with explicit rounding, so a kernel templated on LANE repeats
 // the reference's floating-point operation order exactly:
 //   LANE 0 = scalar lane (kernels_scalar.cpp, baseline x86-64: no FMA)
-//   LANE 1 = AVX2/FMA lane (kernels_avx2.cpp, -mavx2 -mfma; scalar tails are
-//            FMA-contracted by g++'s default -ffp-contract=fast)
+//   LANE 1 = AVX2/FMA lane (kernels_avx2.cpp as g++ 13 -O3 -mavx2 -mfma emits it,
+//            incl. the contractions -ffp-contract=fast adds; see the
+//            disassembly notes in DESIGN.md)
 #pragma once
 
 #include "ocg_common.cuh"
@@ -48,8 +49,17 @@ struct LaneOps<1> {
             a2 = dfma(w[i + 2], x[i + 2], a2);
             a3 = dfma(w[i + 3], x[i + 3], a3);
         }
+        // scalar tail as g++ vectorises it: the first two leftovers as unfused
+        // products added in order, a third (or lone) leftover fused
         double tail = 0.0;
-        for (; i < n; ++i) tail = dfma(w[i], x[i], tail);
+        const int r = n - i;
+        if (r >= 2) {
+            tail = dadd(tail, dmul(w[i], x[i]));
+            tail = dadd(tail, dmul(w[i + 1], x[i + 1]));
+            if (r == 3) tail = dfma(w[i + 2], x[i + 2], tail);
+        } else if (r == 1) {
+            tail = dfma(w[i], x[i], tail);
+        }
         return dadd(dadd(dadd(a0, a2), dadd(a1, a3)), tail);
     }
     __device__ static double axpy(double y, double a, double x) { return dfma(a, x, y); }
@@ -64,7 +74,7 @@ struct LaneOps<1> {
         v = dfma(b2, v, dmul(omb2, dmul(g, g)));
         const double num = dmul(m, mc);
         const double den = dadd(dsqrt(dmul(v, vc)), eps);
-        p = dsub(p, dmul(lr, ddiv(num, den)));
+        p = dfma(-lr, ddiv(num, den), p);  // g++ fuses _mm256_sub_pd(p, _mm256_mul_pd(lr, q)) -> vfnmadd
     }
 };
 

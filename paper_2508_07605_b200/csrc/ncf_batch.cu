@@ -552,7 +552,7 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
         // ---------------- select_caps on the completed row -----------------
         if (warp == 0) {
             SelResult r{};
-            if (status == OCG_OK) {
+            if (status == OCG_OK && io.cpu_caps != nullptr) {
                 r = select_row_warp(S.row, g.n, io.cpu_caps, io.gpu_caps, g.ngpu, g.e_base, g.gamma, lane);
                 if (r.idx < 0) status = OCG_E_LOGIC;
             }

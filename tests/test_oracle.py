@@ -60,30 +60,36 @@ def test_default_plan(port, golden):
         assert port.default_plan(cpu, gpu) == plan
 
 
+@pytest.mark.parametrize("lane", [0, 1])
 @pytest.mark.parametrize("k", range(5))
-def test_ncf_fit_bit_exact_scalar_lane(port, golden, gold_npz, k):
+def test_ncf_fit_bit_exact(port, golden, gold_npz, k, lane):
     name, values, mask, seed, hyper = fit_case(golden, gold_npz, k)
-    rc, params, meta, aseen, sseen = port.ncf_fit(values, mask, seed, **hyper)
-    assert rc == 0, port.err()
-    np.testing.assert_array_equal(params, gold_npz["fit"][f"f{k}_lane0_params"])
-    g = golden["fit_cases"][k]["lane0"]
+    port.set_lane(lane)
+    try:
+        rc, params, meta, aseen, sseen = port.ncf_fit(values, mask, seed, **hyper)
+        m, n = mask.shape
+        ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+        rc2, pred = port.ncf_predict(m, n, params, aseen, sseen, ii.ravel(), jj.ravel(), **hyper)
+    finally:
+        port.set_lane(0)
+    assert rc == 0 and rc2 == 0, port.err()
+    np.testing.assert_array_equal(params, gold_npz["fit"][f"f{k}_lane{lane}_params"])
+    np.testing.assert_array_equal(pred.reshape(m, n), gold_npz["fit"][f"f{k}_lane{lane}_pred"])
+    g = golden["fit_cases"][k][f"lane{lane}"]
     assert meta.epochs_run == g["epochs_run"]
     assert meta.initial_train_mse == g["initial_train_mse"]
     assert meta.final_train_mse == g["final_train_mse"]
     assert meta.best_val_mse == g["best_val_mse"]
-    m, n = mask.shape
-    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
-    rc, pred = port.ncf_predict(m, n, params, aseen, sseen, ii.ravel(), jj.ravel(), **hyper)
-    assert rc == 0
-    np.testing.assert_array_equal(pred.reshape(m, n), gold_npz["fit"][f"f{k}_lane0_pred"])
 
 
-def test_oracle_vs_reference_random_fits(port, ref):
-    """Fresh random matrices: port == reference (scalar lane), params and meta."""
-    rng = np.random.default_rng(4242)
-    ref.force_lane(0)
+@pytest.mark.parametrize("lane", [0, 1])
+def test_oracle_vs_reference_random_fits(port, ref, lane):
+    """Fresh random matrices: port == reference in either lane, params and meta."""
+    rng = np.random.default_rng(4242 + lane)
+    ref.force_lane(lane)
+    port.set_lane(lane)
     try:
-        for trial in range(3):
+        for trial in range(4):
             m, n = rng.integers(4, 14), rng.integers(3, 9)
             v = rng.uniform(0.05, 1.25, (m, n))
             mk = (rng.random((m, n)) < 0.5).astype(np.uint8)
@@ -101,3 +107,4 @@ def test_oracle_vs_reference_random_fits(port, ref):
             assert meta_p.epochs_run == meta_r.epochs_run and meta_p.best_val_mse == meta_r.best_val_mse
     finally:
         ref.force_lane(1)
+        port.set_lane(0)
