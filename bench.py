@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""bench.py — B200 online CF completion + selection (OPEN online phase).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c1|c0xn]
+
+One JSON line on rank 0.  For N>1 launch with
+torch.distributed.run; each rank takes an equal shard of the units (weak
+scaling for the sharded workloads), timing is the max over ranks of CUDA-event
+device time.  A "step" is one pass of the hot path over one batch of
+synthetic input:
+
+  c2    SURVEY §8d C2 (BASELINE configs[2]): 1M apps x 4096 settings, rank 32,
+        2% observed — ALS completion + fused imputation + Algorithm-2 selection
+  c1    C1 (configs[1]): 10K x 256, rank 8, 5% observed, same path
+  c0xn  the reference's own online semantics at scale: N independent apps,
+        each cf::complete'd against the paper-scale offline block + selected
+        (bit-exact NCF, one CTA per app)
+
+--impl reference times the reference's own CPU implementation of the path
+(oracle/_ref, compiled from the unmodified reference sources) on this host's
+cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = {"hbm_gbs": 6515.7, "bf16_tflops": 1644.8, "source": "fallback"}
+try:
+    _p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    PEAKS = {"hbm_gbs": _p["hbm_gbs"], "bf16_tflops": _p["bf16_tflops"], "source": "measured"}
+except Exception:
+    PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ----------------------------------------------------------------- plumbing
+class Dist:
+    def __init__(self, backend: str | None):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1 and backend:
+            import torch
+            import torch.distributed as dist
+
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        load = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- workloads
+def workload_c0xn(args, d: Dist):
+    """Reference online semantics (policy.cpp:178-189) for many apps, bit-exact NCF."""
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+
+    grid = ocg.PowerGrid.default_grid()
+    per_gpu = args.apps
+    total = per_gpu * d.world
+    block = synth.offline_block(42, grid)
+    bmask = np.ones_like(block, np.uint8)
+    pv, pm, sd = synth.online_apps(total, 42, grid)
+    lo, hi = d.rank * per_gpu, (d.rank + 1) * per_gpu
+    pv, pm, sd = pv[lo:hi], pm[lo:hi], sd[lo:hi]
+    ctx = ocg.Context(d.local)
+    hyper = ocg.NcfHyper()
+    plan = ocg.OnlinePlan(block, bmask, pv, pm, sd, grid, hyper, 0.05, args.lane, True, ctx)
+    for _ in range(args.warmup):
+        plan.run(timed=False)
+    ocg._lib.check(ocg._lib.lib.ocg_ctx_synchronize(ctx.handle))
+    res = plan.results()
+    assert (res.status == 0).all(), np.unique(res.status)
+    d.barrier()
+    ms = 0.0
+    with Clocks(d.local) as clk:
+        for _ in range(args.steps):
+            ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+            ms += plan.run(timed=True)
+    d.barrier()
+    t_dev = d.max(ms / 1e3)
+    res = plan.results()
+    epochs = float(res.meta["epochs_run"].mean())
+    # e2e through the public API with host buffers
+    e2e_t = 0.0
+    ocg.online_complete_batch(block, bmask, pv[:64], pm[:64], sd[:64], grid, hyper, 0.05, args.lane, ctx)
+    d.barrier()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r2 = ocg.online_complete_batch(block, bmask, pv, pm, sd, grid, hyper, 0.05, args.lane, ctx)
+        e2e_t += time.perf_counter() - t0
+    e2e_t = d.max(e2e_t)
+    assert np.array_equal(r2.idx, res.idx)
+    n = grid.n
+    cells = total * n * args.steps
+    h2d = block.nbytes + bmask.nbytes + pv.nbytes + pm.nbytes + sd.nbytes + 8 * 4
+    d2h = r2.completed.nbytes + r2.idx.nbytes + r2.saving.nbytes + r2.loss.nbytes + r2.ncand.nbytes + \
+        r2.meta.nbytes + r2.status.nbytes
+    # algorithmic FP64 work per app: forward+backward per sample, Adam per param, per epoch
+    dims = [16, 32, 16, 1]
+    mac = sum(dims[i] * dims[i + 1] for i in range(3))
+    nt = 206 - 20
+    flops_app = epochs * (nt * (2 * mac + 4 * mac) + 20 * 2 * mac + 6 * 1337 * 12)
+    achieved = flops_app * per_gpu * args.steps / (ms / 1e3) / 1e12
+    out = {
+        "metric": "CF-completed matrix cells/sec",
+        "value": cells / t_dev,
+        "unit": "cells/s",
+        "selections_per_sec": total * args.steps / t_dev,
+        "ms_per_step": t_dev * 1e3 / args.steps,
+        "e2e": {"value": cells / e2e_t, "unit": "cells/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "dtype": "f64",
+        "config": {"workload": "c0xn", "apps": total, "apps_per_gpu": per_gpu, "settings": n,
+                   "offline_rows": int(block.shape[0]), "rank": 8, "hidden": [32, 16], "batch": 32,
+                   "lane": "avx2" if args.lane else "scalar", "mean_epochs_run": epochs,
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "scaling": "weak",
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": 37.0, "unit": "TFLOP/s",
+                     "frac": achieved / 37.0, "traffic": None,
+                     "note": "FP64 SIMT nominal 37 TFLOP/s (no measured FP64 peak); algorithmic flops from meta"},
+        "clocks": clk.summary(),
+    }
+    return out, ("c0xn", per_gpu)
+
+
+WORKLOADS = {"c0xn": workload_c0xn}
+
+
+# -------------------------------------------------------- reference (CPU)
+def reference_c0xn(napps: int, threads: int, lane: int = 1):
+    """The reference's cf::complete + select_caps per app (ref_online_batch)."""
+    import ctypes
+
+    from oracle import bind
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+
+    ref = bind.Ref()
+    ref.force_lane(lane)
+    grid = ocg.PowerGrid.default_grid()
+    block = synth.offline_block(42, grid)
+    pv, pm, sd = synth.online_apps(napps, 42, grid)
+    cpu, gpu = grid.arrays()
+    h = bind._hyper(bind.RefHyper)
+    idx = np.zeros(napps, np.int32)
+    sav = np.zeros(napps)
+    secs = ref.L.ref_online_batch(block.shape[0], bind.P(cpu), len(cpu), bind.P(gpu), len(gpu), bind.P(block),
+                                  bind.P(pv), bind.P(pm), bind.P(sd), napps, 0.05, ctypes.byref(h), threads,
+                                  bind.P(idx), bind.P(sav))
+    return secs, idx, sav, grid.n
+
+
+def cpu_baseline(workload: str, threads: int):
+    if workload == "c0xn":
+        napps = max(threads * 8, 16)
+        secs, _, _, n = reference_c0xn(napps, threads)
+        return {"value": napps * n / secs, "unit": "cells/s", "cores": threads, "kind": "reference",
+                "sample": f"{napps} apps x cf::complete+select_caps (oracle/_ref, AVX2 lane, {threads} threads)",
+                "seconds": secs}
+    raise ValueError(workload)
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    if args.workload == "c0xn":
+        napps = max(threads * 4, 8)
+        for _ in range(args.warmup):
+            reference_c0xn(max(threads, 1), threads)
+        tot, cells = 0.0, 0
+        for _ in range(args.steps):
+            secs, _, _, n = reference_c0xn(napps, threads)
+            tot += secs
+            cells += napps * n
+        v = cells / tot
+        line = {"impl": "reference", "metric": "CF-completed matrix cells/sec", "value": v, "unit": "cells/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c0xn", "apps_per_step": napps},
+                "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
+                                 "sample": f"{napps} apps per step, cf::complete + select_caps, AVX2 lane"},
+                "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    raise SystemExit(f"unknown workload {args.workload}")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c0xn")
+    ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")
+    ap.add_argument("--lane", type=int, default=1, help="c0xn: reference FP lane (0 scalar, 1 avx2)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        d = Dist("gloo")
+        try:
+            run_reference(args, d)
+        finally:
+            d.close()
+        return
+    d = Dist("nccl")
+    try:
+        out, _ = WORKLOADS[args.workload](args, d)
+        if d.rank == 0:
+            line = {"metric": out.pop("metric"), "value": out.pop("value"), "unit": out.pop("unit"),
+                    "n_gpus": d.world, "steps": args.steps, "warmup": args.warmup,
+                    "ms_per_step": out.pop("ms_per_step"), "higher_is_better": True,
+                    "scaling": out.pop("scaling"), "vs_baseline": None, "dtype": out.pop("dtype"),
+                    "data": "synthetic (SURVEY §8d generators, seed 42)"}
+            line.update(out)
+            if d.world == 1 and not args.no_cpu_baseline:
+                try:
+                    line["cpu_baseline"] = cpu_baseline(args.workload, os.cpu_count() or 1)
+                except Exception as e:  # reported, not fatal
+                    line["cpu_baseline"] = {"value": None, "error": str(e)}
+            line["peaks"] = PEAKS
+            print(json.dumps(line), flush=True)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -75,6 +75,8 @@ uint64_t ocg_derive_seed(uint64_t root, const char* tag, uint64_t n); /* rng.hpp
 int ocg_ctx_create(int device, ocg_ctx** out);
 void ocg_ctx_destroy(ocg_ctx* ctx);
 int ocg_ctx_device_info(ocg_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
+int ocg_ctx_flush_l2(ocg_ctx* ctx);    /* overwrite a 256 MB scratch buffer (> L2) on the stream */
+int ocg_ctx_synchronize(ocg_ctx* ctx);
 
 /* ---- K1: Algorithm 2 selection ---------------------------------------
  * policy::select_caps (policy.cpp:17-64; policy.hpp:34) batched over `nrows`
@@ -116,6 +118,22 @@ int ocg_online_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_
                               double* completed, int32_t* idx, double* saving, double* loss,
                               int32_t* ncand, ocg_ncf_meta* meta, int32_t* status);
 
+/* Device-resident form of ocg_online_complete_batch: inputs are uploaded once
+ * by _create; _run re-runs the completion kernel on data already in HBM and,
+ * if kernel_ms is non-NULL, waits and returns its CUDA-event duration on the
+ * context stream; _results copies the outputs back. */
+typedef struct ocg_online_plan ocg_online_plan;
+int ocg_online_plan_create(ocg_ctx* ctx, int64_t d_rows, const double* block_vals,
+                           const uint8_t* block_mask, int64_t napps, const double* probe_vals,
+                           const uint8_t* probe_mask, const uint64_t* seeds, const int32_t* cpu_caps,
+                           int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                           const ocg_ncf_hyper* hyper, double gamma, int lane, int want_completed,
+                           ocg_online_plan** out);
+int ocg_online_plan_run(ocg_online_plan* plan, float* kernel_ms);
+int ocg_online_plan_results(ocg_online_plan* plan, double* completed, int32_t* idx, double* saving,
+                            double* loss, int32_t* ncand, ocg_ncf_meta* meta, int32_t* status);
+void ocg_online_plan_destroy(ocg_online_plan* plan);
+
 /* Fit-only variant returning every app's parameters in the flat layout
  * [app table | setting table | W0 b0 W1 b1 ... ] (the reference's Adam block
  * order, cfcomplete.cpp:107-110) for parameter-level parity tests. */
@@ -132,6 +150,35 @@ int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* hyp
                     const double* params, const uint8_t* app_seen, const uint8_t* setting_seen,
                     const int64_t* rows, const int64_t* cols, int64_t count, int lane,
                     double* out);
+
+/* ---- synthetic inputs (benches/tests; host only, no GPU needed) --------
+ * Restatements of the reference's input generators so benches never need
+ * the reference: sim::make_suite (simnode.cpp:192-244), sim::true_perf
+ * (simnode.cpp:43-45), pred::profile_suite's matrix (predictor.cpp:45-69), and
+ * the SURVEY §8d joint CSR matrices.  role: 0 training, 1 evaluation. */
+typedef struct {
+    int32_t archetype; /* 0 gpu_sensitive, 1 cpu_sensitive, 2 both_sensitive, 3 insensitive */
+    double kappa_c, alpha_c, kappa_g, alpha_g, base_runtime_s, cpu_phase_s, noise_sigma;
+    double ips_max, mem_tput_max, sm_clock_max;
+} ocg_workload_spec;
+
+int ocg_synth_suite(const int32_t counts[4], uint64_t seed, int role, double noise_sigma,
+                    double cpu_phase_fraction, const int32_t* cpu_caps, int32_t ncpu,
+                    const int32_t* gpu_caps, int32_t ngpu, ocg_workload_spec* out);
+double ocg_true_perf(const ocg_workload_spec* spec, int32_t cpu_cap, int32_t gpu_cap);
+/* offline dense block of the CLI's offline phase for root seed `seed` (10 x n) */
+int ocg_synth_offline_block(uint64_t seed, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
+                            int32_t ngpu, double* out, int64_t* rows);
+/* napps eval-suite apps probed on the default plan + their cf::complete seeds */
+int ocg_synth_online_apps(int64_t napps, uint64_t seed, const int32_t* cpu_caps, int32_t ncpu,
+                          const int32_t* gpu_caps, int32_t ngpu, double* probe_vals, uint8_t* probe_mask,
+                          uint64_t* seeds);
+/* joint m x n matrix (first dense_rows rows dense) as CSR: count, then fill */
+int ocg_synth_csr_count(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                        double density, int64_t dense_rows, uint64_t seed, int nthreads, int64_t* row_ptr);
+int ocg_synth_csr_fill(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                       double density, int64_t dense_rows, uint64_t seed, int nthreads, const int64_t* row_ptr,
+                       int32_t* col, float* val32, double* val64);
 
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */

@@ -127,3 +127,11 @@ def check(rc: int) -> None:
 def ptr(a):
     """Data pointer of a numpy array (or None)."""
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+_sig("ocg_ctx_flush_l2", ctypes.c_int, c_vp)
+_sig("ocg_ctx_synchronize", ctypes.c_int, c_vp)
+_sig("ocg_online_plan_create", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp,
+     c_i32, c_vp, c_dbl, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_vp))
+_sig("ocg_online_plan_run", ctypes.c_int, c_vp, ctypes.POINTER(ctypes.c_float))
+_sig("ocg_online_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_online_plan_destroy", None, c_vp)

@@ -19,7 +19,7 @@ from ._lib import lib, check, ptr
 __all__ = [
     "PowerGrid", "NcfHyper", "NcfMeta", "CapDecision", "ProbePlan", "Context", "derive_seed",
     "select_caps", "select_caps_batch", "online_complete_batch", "online_fit_batch_params", "ncf_predict",
-    "ncf_param_count", "LANE_SCALAR", "LANE_AVX2",
+    "ncf_param_count", "LANE_SCALAR", "LANE_AVX2", "OnlinePlan",
 ]
 
 LANE_SCALAR, LANE_AVX2 = _lib.LANE_SCALAR, _lib.LANE_AVX2
@@ -295,3 +295,52 @@ def ncf_predict(m: int, n: int, hyper: NcfHyper, params, app_seen, setting_seen,
     check(lib.ocg_ncf_predict(ctx.handle, m, n, ctypes.byref(h), ptr(p), ptr(a), ptr(s), ptr(r), ptr(c), len(r),
                               lane, ptr(out)))
     return out
+
+
+class OnlinePlan:
+    """Device-resident per-app batch (ocg_online_plan): inputs uploaded once,
+    the completion + selection kernel re-runnable on data already in HBM."""
+
+    def __init__(self, block_vals, block_mask, probe_vals, probe_mask, seeds, grid: PowerGrid,
+                 hyper: NcfHyper | None = None, gamma: float = 0.05, lane: int = LANE_AVX2,
+                 want_completed: bool = True, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        hyper = hyper or NcfHyper()
+        bv = np.ascontiguousarray(block_vals, np.float64)
+        bm = np.ascontiguousarray(block_mask, np.uint8)
+        pv = np.ascontiguousarray(probe_vals, np.float64)
+        pm = np.ascontiguousarray(probe_mask, np.uint8)
+        sd = np.ascontiguousarray(seeds, np.uint64)
+        self.napps, self.n = pv.shape
+        cpu, gpu = grid.arrays()
+        h = hyper.to_c()
+        self._h = ctypes.c_void_p()
+        check(lib.ocg_online_plan_create(self.ctx.handle, bv.shape[0], ptr(bv), ptr(bm), self.napps, ptr(pv), ptr(pm),
+                                         ptr(sd), ptr(cpu), len(cpu), ptr(gpu), len(gpu), ctypes.byref(h), gamma, lane,
+                                         1 if want_completed else 0, ctypes.byref(self._h)))
+
+    def run(self, timed: bool = True) -> float:
+        """Re-run the kernel; returns its CUDA-event milliseconds when timed."""
+        ms = ctypes.c_float(0.0)
+        check(lib.ocg_online_plan_run(self._h, ctypes.byref(ms) if timed else None))
+        return float(ms.value)
+
+    def results(self) -> "OnlineBatchResult":
+        n, napps = self.n, self.napps
+        out = OnlineBatchResult(np.zeros(napps, np.int32), np.zeros((napps, n)), np.zeros(napps, np.int32),
+                                np.zeros(napps), np.zeros(napps), np.zeros(napps, np.int32),
+                                np.zeros(napps, META_DTYPE))
+        check(lib.ocg_online_plan_results(self._h, ptr(out.completed), ptr(out.idx), ptr(out.saving), ptr(out.loss),
+                                          ptr(out.ncand), ptr(out.meta), ptr(out.status)))
+        return out
+
+    def close(self):
+        if self._h:
+            lib.ocg_online_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

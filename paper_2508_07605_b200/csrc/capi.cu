@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -16,7 +17,11 @@
 #include "ocg_common.cuh"
 #include "select.h"
 
+constexpr size_t kFlushBytes = size_t(256) << 20;  // > 126 MB L2
+
 struct ocg_ctx {
+    void* flush = nullptr;
+    int flush_val = 1;
     int device = 0;
     int sm_count = 0;
     int cc_major = 0, cc_minor = 0;
@@ -203,100 +208,159 @@ int prepare_batch(ocg_ctx* ctx, const BatchInputs& in, const ocg_ncf_hyper* h, o
     return OCG_OK;
 }
 
-int run_batch(ocg_ctx* ctx, const BatchInputs& in, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
-              int32_t ngpu, const ocg_ncf_hyper* h, double gamma, int lane, double* completed, int32_t* idx,
-              double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta, int32_t* status_out,
-              double* params, int64_t params_stride) {
-    if (!ctx) return fail(OCG_E_INVALID, "null context");
-    if (lane != OCG_LANE_SCALAR && lane != OCG_LANE_AVX2) return fail(OCG_E_INVALID, "unknown lane");
-    if (!status_out) return fail(OCG_E_INVALID, "status output is required");
-    ocg::BatchGeom g;
-    std::vector<double> bval;
-    std::vector<uint32_t> brc;
-    std::vector<uint8_t> bseen;
+}  // namespace
+
+// Device-resident per-app batch: inputs uploaded once, kernel re-runnable.
+struct ocg_online_plan {
+    ocg_ctx* ctx = nullptr;
+    ocg::BatchGeom g{};
+    ocg::BatchIO io{};
+    int lane = 0;
+    int64_t napps = 0, n = 0;
+    int grid = 0;
     std::vector<int32_t> hstatus;
-    int rc = prepare_batch(ctx, in, h, g, bval, brc, bseen, hstatus);
-    if (rc) return rc;
-    g.ngpu = ngpu;
-    g.e_base = cpu ? static_cast<double>(cpu[ncpu - 1] + gpu[ngpu - 1]) : 0.0;
-    g.gamma = gamma;
-    const int64_t n = in.n, napps = in.napps;
-    if (napps == 0) return OCG_OK;
-    cudaStream_t s = ctx->stream;
     DBuf<double> d_bval, d_pv, d_comp, d_sav, d_loss, d_params;
     DBuf<uint32_t> d_brc;
     DBuf<uint8_t> d_bseen, d_pm;
     DBuf<uint64_t> d_seeds;
     DBuf<int32_t> d_cpu, d_gpu, d_idx, d_ncand, d_status;
     DBuf<ocg::OcgMetaDev> d_meta;
-    OCG_CUDA(d_bval.upload(bval.data(), bval.size(), s));
-    OCG_CUDA(d_brc.upload(brc.data(), brc.size(), s));
-    OCG_CUDA(d_bseen.upload(bseen.data(), bseen.size(), s));
-    OCG_CUDA(d_pv.upload(in.probe_vals, static_cast<size_t>(napps * n), s));
-    OCG_CUDA(d_pm.upload(in.probe_mask, static_cast<size_t>(napps * n), s));
-    OCG_CUDA(d_seeds.upload(in.seeds, static_cast<size_t>(napps), s));
-    if (cpu) {
-        OCG_CUDA(d_cpu.upload(cpu, static_cast<size_t>(ncpu), s));
-        OCG_CUDA(d_gpu.upload(gpu, static_cast<size_t>(ngpu), s));
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ~ocg_online_plan() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
     }
-    OCG_CUDA(d_status.upload(hstatus.data(), hstatus.size(), s));
-    ocg::BatchIO io{};
+};
+
+namespace {
+
+int plan_create(ocg_ctx* ctx, const BatchInputs& in, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
+                int32_t ngpu, const ocg_ncf_hyper* h, double gamma, int lane, bool want_completed,
+                int64_t params_stride, ocg_online_plan** out) {
+    *out = nullptr;
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (lane != OCG_LANE_SCALAR && lane != OCG_LANE_AVX2) return fail(OCG_E_INVALID, "unknown lane");
+    auto* P = new ocg_online_plan;
+    std::unique_ptr<ocg_online_plan> guard(P);
+    P->ctx = ctx;
+    P->lane = lane;
+    std::vector<double> bval;
+    std::vector<uint32_t> brc;
+    std::vector<uint8_t> bseen;
+    int rc = prepare_batch(ctx, in, h, P->g, bval, brc, bseen, P->hstatus);
+    if (rc) return rc;
+    ocg::BatchGeom& g = P->g;
+    g.ngpu = ngpu;
+    g.e_base = cpu ? static_cast<double>(cpu[ncpu - 1] + gpu[ngpu - 1]) : 0.0;
+    g.gamma = gamma;
+    const int64_t n = in.n, napps = in.napps;
+    P->napps = napps;
+    P->n = n;
+    cudaStream_t s = ctx->stream;
+    OCG_CUDA(P->d_bval.upload(bval.data(), bval.size(), s));
+    OCG_CUDA(P->d_brc.upload(brc.data(), brc.size(), s));
+    OCG_CUDA(P->d_bseen.upload(bseen.data(), bseen.size(), s));
+    OCG_CUDA(P->d_pv.upload(in.probe_vals, static_cast<size_t>(napps * n), s));
+    OCG_CUDA(P->d_pm.upload(in.probe_mask, static_cast<size_t>(napps * n), s));
+    OCG_CUDA(P->d_seeds.upload(in.seeds, static_cast<size_t>(napps), s));
+    ocg::BatchIO& io = P->io;
     io.napps = napps;
-    io.block_val = d_bval.p;
-    io.block_rc = d_brc.p;
-    io.block_col_seen = d_bseen.p;
-    io.probe_vals = d_pv.p;
-    io.probe_mask = d_pm.p;
-    io.seeds = d_seeds.p;
-    io.cpu_caps = d_cpu.p;
-    io.gpu_caps = d_gpu.p;
-    io.status = d_status.p;
-    if (completed) {
-        OCG_CUDA(d_comp.alloc(static_cast<size_t>(napps * n)));
-        io.completed = d_comp.p;
-    }
     if (cpu) {
-        OCG_CUDA(d_idx.alloc(static_cast<size_t>(napps)));
-        OCG_CUDA(d_sav.alloc(static_cast<size_t>(napps)));
-        OCG_CUDA(d_loss.alloc(static_cast<size_t>(napps)));
-        OCG_CUDA(d_ncand.alloc(static_cast<size_t>(napps)));
-        io.sel_idx = d_idx.p;
-        io.sel_saving = d_sav.p;
-        io.sel_loss = d_loss.p;
-        io.sel_ncand = d_ncand.p;
+        OCG_CUDA(P->d_cpu.upload(cpu, static_cast<size_t>(ncpu), s));
+        OCG_CUDA(P->d_gpu.upload(gpu, static_cast<size_t>(ngpu), s));
+        OCG_CUDA(P->d_idx.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(P->d_sav.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(P->d_loss.alloc(static_cast<size_t>(napps)));
+        OCG_CUDA(P->d_ncand.alloc(static_cast<size_t>(napps)));
+        io.cpu_caps = P->d_cpu.p;
+        io.gpu_caps = P->d_gpu.p;
+        io.sel_idx = P->d_idx.p;
+        io.sel_saving = P->d_sav.p;
+        io.sel_loss = P->d_loss.p;
+        io.sel_ncand = P->d_ncand.p;
     }
-    if (meta) {
-        OCG_CUDA(d_meta.alloc(static_cast<size_t>(napps)));
-        OCG_CUDA(cudaMemsetAsync(d_meta.p, 0, sizeof(ocg::OcgMetaDev) * static_cast<size_t>(napps), s));
-        io.meta = d_meta.p;
+    OCG_CUDA(P->d_status.upload(P->hstatus.data(), P->hstatus.size(), s));
+    OCG_CUDA(P->d_meta.alloc(static_cast<size_t>(napps)));
+    OCG_CUDA(cudaMemsetAsync(P->d_meta.p, 0, sizeof(ocg::OcgMetaDev) * static_cast<size_t>(napps), s));
+    io.block_val = P->d_bval.p;
+    io.block_rc = P->d_brc.p;
+    io.block_col_seen = P->d_bseen.p;
+    io.probe_vals = P->d_pv.p;
+    io.probe_mask = P->d_pm.p;
+    io.seeds = P->d_seeds.p;
+    io.status = P->d_status.p;
+    io.meta = P->d_meta.p;
+    if (want_completed) {
+        OCG_CUDA(P->d_comp.alloc(static_cast<size_t>(napps * n)));
+        io.completed = P->d_comp.p;
     }
-    if (params) {
-        OCG_CUDA(d_params.alloc(static_cast<size_t>(napps * params_stride)));
-        io.params = d_params.p;
+    if (params_stride > 0) {
+        OCG_CUDA(P->d_params.alloc(static_cast<size_t>(napps * params_stride)));
+        io.params = P->d_params.p;
         io.params_stride = params_stride;
     }
     const size_t smem = ocg::batch_smem_bytes(g);
     if (smem > 227 * 1024) return fail(OCG_E_UNSUPPORTED, "per-app working set exceeds shared memory");
-    int per_sm = ocg::batch_max_active_per_sm(g, lane);
+    const int per_sm = ocg::batch_max_active_per_sm(g, lane);
     if (per_sm < 1) return fail(OCG_E_CUDA, "per-app kernel cannot be resident (smem " + std::to_string(smem) + ")");
-    const int64_t grid = std::min<int64_t>(napps, static_cast<int64_t>(per_sm) * ctx->sm_count);
-    OCG_CUDA(ocg::launch_app_batch(g, io, lane, static_cast<int>(grid), s));
-    std::vector<int32_t> dev_status(static_cast<size_t>(napps));
-    OCG_CUDA(d_status.download(dev_status.data(), dev_status.size(), s));
-    if (completed) OCG_CUDA(d_comp.download(completed, static_cast<size_t>(napps * n), s));
-    if (cpu) {
-        OCG_CUDA(d_idx.download(idx, static_cast<size_t>(napps), s));
-        OCG_CUDA(d_sav.download(saving, static_cast<size_t>(napps), s));
-        OCG_CUDA(d_loss.download(loss, static_cast<size_t>(napps), s));
-        OCG_CUDA(d_ncand.download(ncand, static_cast<size_t>(napps), s));
-    }
-    if (meta)
-        OCG_CUDA(d_meta.download(reinterpret_cast<ocg::OcgMetaDev*>(meta), static_cast<size_t>(napps), s));
-    if (params) OCG_CUDA(d_params.download(params, static_cast<size_t>(napps * params_stride), s));
+    P->grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(napps, 1), static_cast<int64_t>(per_sm) * ctx->sm_count));
+    OCG_CUDA(cudaEventCreate(&P->ev0));
+    OCG_CUDA(cudaEventCreate(&P->ev1));
     OCG_CUDA(cudaStreamSynchronize(s));
-    for (int64_t a = 0; a < napps; ++a)
-        status_out[a] = hstatus[a] != OCG_OK ? hstatus[a] : dev_status[a];
+    *out = guard.release();
     return OCG_OK;
+}
+
+int plan_run(ocg_online_plan* P, float* ms) {
+    if (!P) return fail(OCG_E_INVALID, "null plan");
+    if (P->napps == 0) return OCG_OK;
+    cudaStream_t s = P->ctx->stream;
+    OCG_CUDA(cudaEventRecord(P->ev0, s));
+    OCG_CUDA(ocg::launch_app_batch(P->g, P->io, P->lane, P->grid, s));
+    OCG_CUDA(cudaEventRecord(P->ev1, s));
+    if (ms) {
+        OCG_CUDA(cudaEventSynchronize(P->ev1));
+        OCG_CUDA(cudaEventElapsedTime(ms, P->ev0, P->ev1));
+    }
+    return OCG_OK;
+}
+
+int plan_results(ocg_online_plan* P, double* completed, int32_t* idx, double* saving, double* loss, int32_t* ncand,
+                 ocg_ncf_meta* meta, int32_t* status_out, double* params) {
+    if (!P) return fail(OCG_E_INVALID, "null plan");
+    const int64_t napps = P->napps, n = P->n;
+    cudaStream_t s = P->ctx->stream;
+    std::vector<int32_t> dev_status(static_cast<size_t>(napps));
+    OCG_CUDA(P->d_status.download(dev_status.data(), dev_status.size(), s));
+    if (completed && P->io.completed) OCG_CUDA(P->d_comp.download(completed, static_cast<size_t>(napps * n), s));
+    if (P->io.sel_idx) {
+        OCG_CUDA(P->d_idx.download(idx, static_cast<size_t>(napps), s));
+        OCG_CUDA(P->d_sav.download(saving, static_cast<size_t>(napps), s));
+        OCG_CUDA(P->d_loss.download(loss, static_cast<size_t>(napps), s));
+        OCG_CUDA(P->d_ncand.download(ncand, static_cast<size_t>(napps), s));
+    }
+    if (meta) OCG_CUDA(P->d_meta.download(reinterpret_cast<ocg::OcgMetaDev*>(meta), static_cast<size_t>(napps), s));
+    if (params && P->io.params)
+        OCG_CUDA(P->d_params.download(params, static_cast<size_t>(napps * P->io.params_stride), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    if (status_out)
+        for (int64_t a = 0; a < napps; ++a)
+            status_out[a] = P->hstatus[a] != OCG_OK ? P->hstatus[a] : dev_status[a];
+    return OCG_OK;
+}
+
+int run_batch(ocg_ctx* ctx, const BatchInputs& in, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
+              int32_t ngpu, const ocg_ncf_hyper* h, double gamma, int lane, double* completed, int32_t* idx,
+              double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta, int32_t* status_out,
+              double* params, int64_t params_stride) {
+    if (!status_out) return fail(OCG_E_INVALID, "status output is required");
+    ocg_online_plan* P = nullptr;
+    int rc = plan_create(ctx, in, cpu, ncpu, gpu, ngpu, h, gamma, lane, completed != nullptr,
+                         params ? params_stride : 0, &P);
+    if (rc) return rc;
+    std::unique_ptr<ocg_online_plan> guard(P);
+    if ((rc = plan_run(P, nullptr))) return rc;
+    return plan_results(P, completed, idx, saving, loss, ncand, meta, status_out, params);
 }
 
 }  // namespace
@@ -358,6 +422,7 @@ void ocg_ctx_destroy(ocg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->flush) cudaFree(ctx->flush);
     delete ctx;
 }
 
@@ -456,6 +521,42 @@ int ocg_online_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_
     BatchInputs in{d_rows, block_vals, block_mask, napps, probe_vals, probe_mask, seeds, ncpu * ngpu};
     return run_batch(ctx, in, cpu, ncpu, gpu, ngpu, hyper, gamma, lane, completed, idx, saving, loss, ncand, meta,
                      status, nullptr, 0);
+}
+
+int ocg_online_plan_create(ocg_ctx* ctx, int64_t d_rows, const double* block_vals, const uint8_t* block_mask,
+                           int64_t napps, const double* probe_vals, const uint8_t* probe_mask, const uint64_t* seeds,
+                           const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
+                           const ocg_ncf_hyper* hyper, double gamma, int lane, int want_completed,
+                           ocg_online_plan** out) {
+    if (!out) return fail(OCG_E_INVALID, "null output");
+    int rc = check_grid(cpu, ncpu, gpu, ngpu);
+    if (rc) return rc;
+    if (gamma <= 0.0 || gamma >= 1.0) return fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
+    BatchInputs in{d_rows, block_vals, block_mask, napps, probe_vals, probe_mask, seeds, ncpu * ngpu};
+    return plan_create(ctx, in, cpu, ncpu, gpu, ngpu, hyper, gamma, lane, want_completed != 0, 0, out);
+}
+
+int ocg_online_plan_run(ocg_online_plan* plan, float* kernel_ms) { return plan_run(plan, kernel_ms); }
+
+int ocg_online_plan_results(ocg_online_plan* plan, double* completed, int32_t* idx, double* saving, double* loss,
+                            int32_t* ncand, ocg_ncf_meta* meta, int32_t* status) {
+    return plan_results(plan, completed, idx, saving, loss, ncand, meta, status, nullptr);
+}
+
+void ocg_online_plan_destroy(ocg_online_plan* plan) { delete plan; }
+
+int ocg_ctx_flush_l2(ocg_ctx* ctx) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (!ctx->flush) OCG_CUDA(cudaMalloc(&ctx->flush, kFlushBytes));
+    OCG_CUDA(cudaMemsetAsync(ctx->flush, ctx->flush_val++ & 0xff, kFlushBytes, ctx->stream));
+    OCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return OCG_OK;
+}
+
+int ocg_ctx_synchronize(ocg_ctx* ctx) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    OCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return OCG_OK;
 }
 
 int ocg_online_fit_batch_params(ocg_ctx* ctx, int64_t d_rows, const double* block_vals, const uint8_t* block_mask,

@@ -1,0 +1,102 @@
+"""Synthetic inputs (host side, via the C-ABI) for benches and tests.
+
+See include/ocg.h "synthetic inputs": restatements of the reference's own
+input generators (sim::make_suite / true_perf / profile_suite) and the
+SURVEY §8d joint matrices C1-C3."""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib, check, ptr
+from .api import PowerGrid
+
+c_i32, c_i64, c_u64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
+
+
+class WorkloadSpecC(ctypes.Structure):
+    _fields_ = [("archetype", c_i32), ("kappa_c", c_dbl), ("alpha_c", c_dbl), ("kappa_g", c_dbl),
+                ("alpha_g", c_dbl), ("base_runtime_s", c_dbl), ("cpu_phase_s", c_dbl), ("noise_sigma", c_dbl),
+                ("ips_max", c_dbl), ("mem_tput_max", c_dbl), ("sm_clock_max", c_dbl)]
+
+
+lib.ocg_synth_suite.argtypes = [c_vp, c_u64, ctypes.c_int, c_dbl, c_dbl, c_vp, c_i32, c_vp, c_i32, c_vp]
+lib.ocg_synth_suite.restype = ctypes.c_int
+lib.ocg_true_perf.argtypes = [c_vp, c_i32, c_i32]
+lib.ocg_true_perf.restype = c_dbl
+lib.ocg_synth_offline_block.argtypes = [c_u64, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp]
+lib.ocg_synth_offline_block.restype = ctypes.c_int
+lib.ocg_synth_online_apps.argtypes = [c_i64, c_u64, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp]
+lib.ocg_synth_online_apps.restype = ctypes.c_int
+lib.ocg_synth_csr_count.argtypes = [c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64, c_u64, ctypes.c_int, c_vp]
+lib.ocg_synth_csr_count.restype = ctypes.c_int
+lib.ocg_synth_csr_fill.argtypes = [c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64, c_u64, ctypes.c_int, c_vp, c_vp,
+                                   c_vp, c_vp]
+lib.ocg_synth_csr_fill.restype = ctypes.c_int
+
+
+def make_suite(counts, seed: int, role: int, grid: PowerGrid, noise_sigma=0.01, cpu_phase_fraction=0.0):
+    cnt = np.asarray(counts, np.int32)
+    out = (WorkloadSpecC * int(cnt.sum()))()
+    cpu, gpu = grid.arrays()
+    check(lib.ocg_synth_suite(ptr(cnt), seed, role, noise_sigma, cpu_phase_fraction, ptr(cpu), len(cpu), ptr(gpu),
+                              len(gpu), out))
+    return list(out)
+
+
+def true_perf(spec: WorkloadSpecC, cpu_cap: int, gpu_cap: int) -> float:
+    return float(lib.ocg_true_perf(ctypes.byref(spec), cpu_cap, gpu_cap))
+
+
+def offline_block(seed: int = 42, grid: PowerGrid | None = None) -> np.ndarray:
+    grid = grid or PowerGrid.default_grid()
+    cpu, gpu = grid.arrays()
+    out = np.zeros((10, grid.n))
+    rows = c_i64()
+    check(lib.ocg_synth_offline_block(seed, ptr(cpu), len(cpu), ptr(gpu), len(gpu), ptr(out), ctypes.byref(rows)))
+    return out[: rows.value]
+
+
+def online_apps(napps: int, seed: int = 42, grid: PowerGrid | None = None):
+    """(probe_vals, probe_mask, seeds) for napps eval-suite apps."""
+    grid = grid or PowerGrid.default_grid()
+    cpu, gpu = grid.arrays()
+    pv = np.zeros((napps, grid.n))
+    pm = np.zeros((napps, grid.n), np.uint8)
+    sd = np.zeros(napps, np.uint64)
+    check(lib.ocg_synth_online_apps(napps, seed, ptr(cpu), len(cpu), ptr(gpu), len(gpu), ptr(pv), ptr(pm), ptr(sd)))
+    return pv, pm, sd
+
+
+@dataclass
+class CsrMatrix:
+    m: int
+    n: int
+    row_ptr: np.ndarray  # int64 [m+1]
+    col: np.ndarray      # int32 [nnz]
+    val: np.ndarray      # float32 or float64 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+
+def joint_csr(m: int, grid: PowerGrid, density: float, dense_rows: int, seed: int = 42, dtype=np.float32,
+              threads: int | None = None) -> CsrMatrix:
+    """SURVEY §8d synthetic joint matrix (C1: 10K x 256 @5%, C2: 1M x 4096 @2%, ...)."""
+    threads = threads or max(1, min(64, os.cpu_count() or 1))
+    cpu, gpu = grid.arrays()
+    rp = np.zeros(m + 1, np.int64)
+    check(lib.ocg_synth_csr_count(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed, threads,
+                                  ptr(rp)))
+    nnz = int(rp[-1])
+    col = np.empty(nnz, np.int32)
+    v32 = np.empty(nnz, np.float32) if dtype == np.float32 else None
+    v64 = np.empty(nnz, np.float64) if dtype == np.float64 else None
+    check(lib.ocg_synth_csr_fill(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed, threads,
+                                 ptr(rp), ptr(col), ptr(v32), ptr(v64)))
+    return CsrMatrix(m, grid.n, rp, col, v32 if v32 is not None else v64)
