@@ -23,12 +23,17 @@
 // thread that owns each parameter (owner-computes: the owner reduces its
 // gradient over the batch in sample order — the reference's accumulation
 // order — then applies Adam immediately).
+//
+// Two instantiations of one body: FixArch<8,8,32,16> (the reference default
+// NcfHyper: every layer width a compile-time constant, all layer loops
+// unrolled, shared-memory pointers resolved statically) and RtArch (any
+// other shape within the limits of ncf_batch.h, dims read at run time).
 #include <cuda_runtime.h>
 
+#include "lane_ops.cuh"
 #include "ncf_batch.h"
 #include "ocg_common.cuh"
 #include "select_dev.cuh"
-#include "lane_ops.cuh"
 
 namespace ocg {
 
@@ -37,57 +42,99 @@ namespace {
 constexpr int kCW = 8;              // compute warps
 constexpr int kCT = kCW * 32;       // compute threads
 constexpr int kThreads = kCT + 32;  // + RNG warp
-constexpr int kEPT = kMaxParams / kCT;
 
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory"); }
 
-// ---- shared-memory carve-up ---------------------------------------------
-struct Smem {
-    double* P;                   // [T] parameters
-    double* act[kMaxLayers + 1]; // act[0] = gathered inputs X; act[l+1] = layer l output
-    double* del[kMaxLayers];     // del[l]: act-grad factors, then deltas, of layer l output
-    double* ig;                  // input grads [B x stride0]
-    double* cval;                // cell values [nc]
-    uint32_t* crc;               // cell (row<<16 | col) [nc]
-    uint16_t* tset;              // train cell ids
-    uint16_t* vset;              // validation cell ids
-    uint16_t* perm[2];           // epoch permutations of train positions
-    uint32_t* draw;              // per-epoch swap targets from the RNG warp
-    uint64_t* mt;                // [312]
-    double* row;                 // [n] completed app row
-    int* s_app;                  // [32]
-    int* s_set;                  // [32]
-    double* s_y;                 // [32]
-    int* ctrl;                   // scalars
+// ---- architecture policies ------------------------------------------------
+struct RtArch {
+    static constexpr bool kStatic = false;
+    static constexpr int kEPT = kMaxParams / kCT;
+    const BatchGeom& g;
+    __device__ __forceinline__ int L() const { return g.L; }
+    __device__ __forceinline__ int dim(int l) const { return g.dims[l]; }
+    __device__ __forceinline__ int stride(int l) const { return g.stride[l]; }
+    __device__ __forceinline__ int ka() const { return g.ka; }
+    __device__ __forceinline__ int ks() const { return g.ks; }
 };
 
-__device__ inline char* carve(char*& p, size_t bytes) {
-    char* r = p;
-    p += (bytes + 15) & ~size_t(15);
+template <int KA, int KS, int H0, int H1>
+struct FixArch {
+    static constexpr bool kStatic = true;
+    static constexpr int kEPT = kFixMaxParams / kCT;
+    const BatchGeom& g;
+    __device__ __forceinline__ static constexpr int L() { return 3; }
+    __device__ __forceinline__ static constexpr int dim(int l) {
+        return l == 0 ? KA + KS : (l == 1 ? H0 : (l == 2 ? H1 : 1));
+    }
+    __device__ __forceinline__ static constexpr int stride(int l) { return dim(l) | 1; }
+    __device__ __forceinline__ static constexpr int ka() { return KA; }
+    __device__ __forceinline__ static constexpr int ks() { return KS; }
+};
+
+// ---- shared-memory carve-up ---------------------------------------------
+// Regions are kept as 32-bit byte offsets into the dynamic shared-memory
+// window and turned into pointers at the point of use, so every access is a
+// 32-bit-addressed LDS/STS and the layout costs one register per region.
+extern __shared__ __align__(16) char g_smem[];
+
+template <typename T>
+__device__ __forceinline__ T* smp(uint32_t off) {
+    return reinterpret_cast<T*>(g_smem + off);
+}
+
+struct Smem {
+    uint32_t oP;                    // [T] parameters
+    uint32_t oact[kMaxLayers + 1];  // act[0] = gathered inputs X; act[l+1] = layer l output
+    uint32_t odel[kMaxLayers];      // del[l]: act-grad factors, then deltas, of layer l output
+    uint32_t oig, ocval, ocrc, otset, ovset, operm[2], odraw, omt, orow, os_app, os_set, os_y, octrl;
+    __device__ __forceinline__ double* P() const { return smp<double>(oP); }
+    __device__ __forceinline__ double* act(int l) const { return smp<double>(oact[l]); }
+    __device__ __forceinline__ double* del(int l) const { return smp<double>(odel[l]); }
+    __device__ __forceinline__ double* ig() const { return smp<double>(oig); }        // input grads
+    __device__ __forceinline__ double* cval() const { return smp<double>(ocval); }    // cell values
+    __device__ __forceinline__ uint32_t* crc() const { return smp<uint32_t>(ocrc); }  // (row<<16 | col)
+    __device__ __forceinline__ uint16_t* tset() const { return smp<uint16_t>(otset); }  // train cell ids
+    __device__ __forceinline__ uint16_t* vset() const { return smp<uint16_t>(ovset); }  // validation ids
+    __device__ __forceinline__ uint16_t* perm(int k) const { return smp<uint16_t>(operm[k]); }
+    __device__ __forceinline__ uint32_t* draw() const { return smp<uint32_t>(odraw); }
+    __device__ __forceinline__ uint64_t* mt() const { return smp<uint64_t>(omt); }
+    __device__ __forceinline__ double* row() const { return smp<double>(orow); }  // completed app row
+    __device__ __forceinline__ int* s_app() const { return smp<int>(os_app); }
+    __device__ __forceinline__ int* s_set() const { return smp<int>(os_set); }
+    __device__ __forceinline__ double* s_y() const { return smp<double>(os_y); }
+    __device__ __forceinline__ int* ctrl() const { return smp<int>(octrl); }
+};
+
+__device__ __forceinline__ uint32_t carve(uint32_t& p, size_t bytes) {
+    const uint32_t r = p;
+    p += static_cast<uint32_t>((bytes + 15) & ~size_t(15));
     return r;
 }
 
-__device__ inline void setup_smem(Smem& S, const BatchGeom& g, char* base) {
-    char* p = base;
-    S.P = reinterpret_cast<double*>(carve(p, sizeof(double) * g.T));
-    for (int l = 0; l <= g.L; ++l)
-        S.act[l] = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[l]));
-    for (int l = 0; l < g.L; ++l)
-        S.del[l] = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[l + 1]));
-    S.ig = reinterpret_cast<double*>(carve(p, sizeof(double) * 32 * g.stride[0]));
-    S.cval = reinterpret_cast<double*>(carve(p, sizeof(double) * g.max_cells));
-    S.crc = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * g.max_cells));
-    S.tset = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
-    S.vset = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
-    S.perm[0] = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
-    S.perm[1] = reinterpret_cast<uint16_t*>(carve(p, sizeof(uint16_t) * g.max_cells));
-    S.draw = reinterpret_cast<uint32_t*>(carve(p, sizeof(uint32_t) * g.max_cells));
-    S.mt = reinterpret_cast<uint64_t*>(carve(p, sizeof(uint64_t) * 313));
-    S.row = reinterpret_cast<double*>(carve(p, sizeof(double) * g.n));
-    S.s_app = reinterpret_cast<int*>(carve(p, sizeof(int) * 32));
-    S.s_set = reinterpret_cast<int*>(carve(p, sizeof(int) * 32));
-    S.s_y = reinterpret_cast<double*>(carve(p, sizeof(double) * 32));
-    S.ctrl = reinterpret_cast<int*>(carve(p, sizeof(int) * 16));
+template <class A>
+__device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom& g) {
+    uint32_t p = 0;
+    S.oP = carve(p, sizeof(double) * g.T);
+#pragma unroll
+    for (int l = 0; l <= kMaxLayers; ++l)
+        if (l <= a.L()) S.oact[l] = carve(p, sizeof(double) * 32 * a.stride(l));
+#pragma unroll
+    for (int l = 0; l < kMaxLayers; ++l)
+        if (l < a.L()) S.odel[l] = carve(p, sizeof(double) * 32 * a.stride(l + 1));
+    S.oig = carve(p, sizeof(double) * 32 * a.stride(0));
+    S.ocval = carve(p, sizeof(double) * g.max_cells);
+    S.ocrc = carve(p, sizeof(uint32_t) * g.max_cells);
+    S.otset = carve(p, sizeof(uint16_t) * g.max_cells);
+    S.ovset = carve(p, sizeof(uint16_t) * g.max_cells);
+    S.operm[0] = carve(p, sizeof(uint16_t) * g.max_cells);
+    S.operm[1] = carve(p, sizeof(uint16_t) * g.max_cells);
+    S.odraw = carve(p, sizeof(uint32_t) * g.max_cells);
+    S.omt = carve(p, sizeof(uint64_t) * 313);
+    S.orow = carve(p, sizeof(double) * g.n);
+    S.os_app = carve(p, sizeof(int) * 32);
+    S.os_set = carve(p, sizeof(int) * 32);
+    S.os_y = carve(p, sizeof(double) * 32);
+    S.octrl = carve(p, sizeof(int) * 16);
 }
 
 enum Ctrl { kMtIdx = 0, kStop = 1, kImproved = 2, kNt = 3, kNv = 4, kNc = 5, kDiverged = 6 };
@@ -135,30 +182,32 @@ __device__ void uniform_fill(double* dst, int cnt, double lo, double hi, MtWarp&
 // forward() / forward_tape() (nnkit.cpp:74-89, :124-138) for cnt <= 32 cells
 // whose (app, setting) ids are in s_app/s_set.  Leaves layer outputs in act[],
 // and (tape) SELU derivative factors in del[].
-template <int LANE>
-__device__ void forward_chunk(const Smem& S, const BatchGeom& g, int cnt, bool tape, int warp,
-                              int lane, int ctid) {
-    const int in0 = g.dims[0];
+template <int LANE, class A>
+__device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt, bool tape,
+                                              int warp, int lane, int ctid) {
+    const int in0 = a.dim(0);
     for (int w = ctid; w < cnt * in0; w += kCT) {
         const int s = w / in0, i = w - s * in0;
-        const double v = i < g.ka ? S.P[S.s_app[s] * g.ka + i]
-                                  : S.P[g.set_off + S.s_set[s] * g.ks + (i - g.ka)];
-        S.act[0][s * g.stride[0] + i] = v;
+        const double v = i < a.ka() ? S.P()[S.s_app()[s] * a.ka() + i]
+                                    : S.P()[g.set_off + S.s_set()[s] * a.ks() + (i - a.ka())];
+        S.act(0)[s * a.stride(0) + i] = v;
     }
     bar_compute();
-    for (int l = 0; l < g.L; ++l) {
-        const int in = g.dims[l], out = g.dims[l + 1];
-        const double* W = S.P + g.off_w[l];
-        const double* b = S.P + g.off_b[l];
-        const double* ain = S.act[l] + lane * g.stride[l];
-        const bool hidden = l + 1 < g.L;
+#pragma unroll
+    for (int l = 0; l < kMaxLayers; ++l) {
+        if (l >= a.L()) break;
+        const int in = a.dim(l), out = a.dim(l + 1);
+        const double* W = S.P() + g.off_w[l];
+        const double* b = S.P() + g.off_b[l];
+        const double* ain = S.act(l) + lane * a.stride(l);
+        const bool hidden = l + 1 < a.L();
         if (lane < cnt) {
             for (int o = warp; o < out; o += kCW) {
                 const double z = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
-                double a = z, gf = 1.0;
-                if (hidden) selu_fwd(z, a, gf);
-                S.act[l + 1][lane * g.stride[l + 1] + o] = a;
-                if (tape) S.del[l][lane * g.stride[l + 1] + o] = gf;
+                double v = z, gf = 1.0;
+                if (hidden) selu_fwd(z, v, gf);
+                S.act(l + 1)[lane * a.stride(l + 1) + o] = v;
+                if (tape) S.del(l)[lane * a.stride(l + 1) + o] = gf;
             }
         }
         bar_compute();
@@ -167,29 +216,33 @@ __device__ void forward_chunk(const Smem& S, const BatchGeom& g, int cnt, bool t
 
 // backprop_sample (nnkit.cpp:184-212) deltas for a minibatch already
 // forwarded with tape; writes del[l] = deltas and ig = input gradients.
-template <int LANE>
-__device__ void backward_chunk(const Smem& S, const BatchGeom& g, int cnt, double scale, int warp,
-                               int lane) {
-    const int L = g.L;
-    if (warp == 0 && lane < cnt) {
-        const double err = dsub(S.act[L][lane * g.stride[L]], S.s_y[lane]);
-        // delta = 2*err*scale, then *= identity grad 1.0
-        S.del[L - 1][lane * g.stride[L]] = dmul(dmul(dmul(2.0, err), scale), 1.0);
-    }
-    bar_compute();
-    for (int l = L - 1; l >= 0; --l) {
-        const int in = g.dims[l], out = g.dims[l + 1];
-        const double* W = S.P + g.off_w[l];
-        const double* d = S.del[l] + lane * g.stride[l + 1];
+template <int LANE, class A>
+__device__ __forceinline__ void backward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt,
+                                               double scale, int warp, int lane) {
+    const int L = a.L();
+#pragma unroll
+    for (int l = kMaxLayers - 1; l >= 0; --l) {
+        if (l >= L) continue;
+        if (l == L - 1) {
+            if (warp == 0 && lane < cnt) {
+                const double err = dsub(S.act(l + 1)[lane * a.stride(l + 1)], S.s_y()[lane]);
+                // delta = 2*err*scale, then *= identity grad 1.0
+                S.del(l)[lane * a.stride(l + 1)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
+            }
+            bar_compute();
+        }
+        const int in = a.dim(l), out = a.dim(l + 1);
+        const double* W = S.P() + g.off_w[l];
+        const double* d = S.del(l) + lane * a.stride(l + 1);
         if (lane < cnt) {
             for (int c = warp; c < in; c += kCW) {
                 double nd = 0.0;  // matvec_t: out[c] = 0; out[c] += d[r]*w[r][c]
                 for (int r = 0; r < out; ++r) nd = LaneOps<LANE>::axpy(nd, d[r], W[r * in + c]);
                 if (l > 0) {
-                    double* gf = S.del[l - 1] + lane * g.stride[l] + c;
+                    double* gf = S.del(l > 0 ? l - 1 : 0) + lane * a.stride(l) + c;
                     *gf = dmul(nd, *gf);  // delta[o] *= activate_grad
                 } else {
-                    S.ig[lane * g.stride[0] + c] = nd;
+                    S.ig()[lane * a.stride(0) + c] = nd;
                 }
             }
         }
@@ -197,27 +250,42 @@ __device__ void backward_chunk(const Smem& S, const BatchGeom& g, int cnt, doubl
     }
 }
 
+// the network output row (act[L]) without a run-time array index
+template <class A>
+__device__ __forceinline__ const double* out_act(const Smem& S, const A& a) {
+    if constexpr (A::kStatic) return S.act(A::L());
+    switch (a.L()) {
+        case 1: return S.act(1);
+        case 2: return S.act(2);
+        case 3: return S.act(3);
+        default: return S.act(4);
+    }
+}
+
 // sequential MSE over a list of cells (cells_mse, cfcomplete.cpp:34-43)
-template <int LANE>
-__device__ double cells_mse(const Smem& S, const BatchGeom& g, const uint16_t* ids, int count,
-                            int warp, int lane, int ctid) {
+template <int LANE, class A>
+__device__ __forceinline__ double cells_mse(const Smem& S, const A& a, const BatchGeom& g, const uint16_t* ids,
+                                            int count, int warp, int lane, int ctid) {
     double acc = 0.0;  // meaningful on ctid 0 only
     for (int base = 0; base < count; base += 32) {
         const int cnt = min(32, count - base);
         if (ctid < cnt) {
             const int c = ids[base + ctid];
-            const uint32_t rc = S.crc[c];
-            S.s_app[ctid] = static_cast<int>(rc >> 16);
-            S.s_set[ctid] = static_cast<int>(rc & 0xffff);
-            S.s_y[ctid] = S.cval[c];
+            const uint32_t rc = S.crc()[c];
+            S.s_app()[ctid] = static_cast<int>(rc >> 16);
+            S.s_set()[ctid] = static_cast<int>(rc & 0xffff);
+            S.s_y()[ctid] = S.cval()[c];
         }
         bar_compute();
-        forward_chunk<LANE>(S, g, cnt, false, warp, lane, ctid);
-        if (ctid == 0)
+        forward_chunk<LANE>(S, a, g, cnt, false, warp, lane, ctid);
+        if (ctid == 0) {
+            const double* out = out_act(S, a);
+            const int so = a.stride(a.L());
             for (int s = 0; s < cnt; ++s) {
-                const double err = dsub(S.act[g.L][s * g.stride[g.L]], S.s_y[s]);
+                const double err = dsub(out[s * so], S.s_y()[s]);
                 acc = dadd(acc, dmul(err, err));
             }
+        }
         bar_compute();
     }
     return count == 0 ? 0.0 : ddiv(acc, static_cast<double>(count));
@@ -269,19 +337,57 @@ __device__ inline uint32_t describe(const BatchGeom& g, int e) {
            (static_cast<uint32_t>(kind) << 24) | (static_cast<uint32_t>(r) << 12) | static_cast<uint32_t>(c);
 }
 
-}  // namespace
+// weight / bias gradient of layer LAY summed over the batch in sample order
+template <int LANE, int LAY, class A>
+__device__ __forceinline__ double layer_grad(const Smem& S, const A& a, bool is_weight, int r, int c, int cnt) {
+    const double* dl = S.del(LAY) + r;
+    const int sd = a.stride(LAY + 1);
+    double gsum = 0.0;
+    if (is_weight) {  // outer_acc: G[r][c] += d[r] * x[c]
+        const double* al = S.act(LAY) + c;
+        const int sa = a.stride(LAY);
+        for (int s = 0; s < cnt; ++s) gsum = LaneOps<LANE>::axpy(gsum, dl[s * sd], al[s * sa]);
+    } else {  // bias: G[o] += delta[o]
+        for (int s = 0; s < cnt; ++s) gsum = dadd(gsum, dl[s * sd]);
+    }
+    return gsum;
+}
 
-template <int LANE>
-__global__ void __launch_bounds__(kThreads, 2)
-ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
-    extern __shared__ __align__(16) char smem_raw[];
+template <int LANE, class A>
+__device__ __forceinline__ double param_grad(const Smem& S, const A& a, uint32_t o, int cnt) {
+    const int kind = own_kind(o), orow = own_r(o), ocol = own_c(o);
+    if (kind >= 2) {
+        const bool w = kind == 2;
+        switch (own_layer(o)) {
+            case 0: return layer_grad<LANE, 0>(S, a, w, orow, ocol, cnt);
+            case 1: return layer_grad<LANE, 1>(S, a, w, orow, ocol, cnt);
+            case 2: return layer_grad<LANE, 2>(S, a, w, orow, ocol, cnt);
+            default: return layer_grad<LANE, 3>(S, a, w, orow, ocol, cnt);
+        }
+    }
+    double gsum = 0.0;
+    const int st0 = a.stride(0);
+    if (kind == 0) {  // app-embedding scatter (cfcomplete.cpp:171-172)
+        for (int s = 0; s < cnt; ++s)
+            if (S.s_app()[s] == orow) gsum = dadd(gsum, S.ig()[s * st0 + ocol]);
+    } else {  // setting-embedding scatter (:173-174)
+        for (int s = 0; s < cnt; ++s)
+            if (S.s_set()[s] == orow) gsum = dadd(gsum, S.ig()[s * st0 + a.ka() + ocol]);
+    }
+    return gsum;
+}
+
+template <int LANE, class ARCH>
+__device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO& io) {
+    const ARCH a{g};
+    constexpr int kEPT = ARCH::kEPT;
     Smem S;
-    setup_smem(S, g, smem_raw);
+    setup_smem(S, a, g);
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const bool is_rng = warp == kCW;
     const int ctid = tid;  // valid for compute threads
-    MtWarp mt{S.mt, S.ctrl + kMtIdx};
+    MtWarp mt{S.mt(), S.ctrl() + kMtIdx};
 
     // owned parameters (compile-time indexed so moments stay in registers)
     uint32_t own[kEPT];
@@ -300,17 +406,17 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
         const double* prow = io.probe_vals + app * g.n;
         const uint8_t* pmask = io.probe_mask + app * g.n;
         const int D = g.m - 1;
-        if (tid < 16) S.ctrl[tid] = 0;
+        if (tid < 16) S.ctrl()[tid] = 0;
         __syncthreads();
         if (tid == 0) {
-            S.ctrl[kMtIdx] = 312;
+            S.ctrl()[kMtIdx] = 312;
             int napp = 0;
             for (int j = 0; j < g.n; ++j) napp += pmask[j] != 0;
-            S.ctrl[kNc] = g.block_nnz + napp;
+            S.ctrl()[kNc] = g.block_nnz + napp;
         }
         for (int q = tid; q < g.block_nnz; q += kThreads) {
-            S.cval[q] = io.block_val[q];
-            S.crc[q] = io.block_rc[q];
+            S.cval()[q] = io.block_val[q];
+            S.crc()[q] = io.block_rc[q];
         }
         if (tid < 32) {  // app row cells in column order (ballot compaction)
             int base = g.block_nnz;
@@ -320,15 +426,15 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
                 const unsigned bal = __ballot_sync(0xffffffffu, obs);
                 if (obs) {
                     const int pos = base + __popc(bal & ((1u << lane) - 1));
-                    S.cval[pos] = prow[j];
-                    S.crc[pos] = (static_cast<uint32_t>(D) << 16) | static_cast<uint32_t>(j);
+                    S.cval()[pos] = prow[j];
+                    S.crc()[pos] = (static_cast<uint32_t>(D) << 16) | static_cast<uint32_t>(j);
                 }
                 base += __popc(bal);
             }
         }
-        for (int j = tid; j < g.n; j += kThreads) S.row[j] = prow[j];
+        for (int j = tid; j < g.n; j += kThreads) S.row()[j] = prow[j];
         __syncthreads();
-        const int nc = S.ctrl[kNc];
+        const int nc = S.ctrl()[kNc];
         const int napp_obs = nc - g.block_nnz;
 
         int status = OCG_OK;
@@ -346,43 +452,41 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
             // ------------- init + split (RNG warp) -----------------------
             if (is_rng) {
                 mt.seed(derive_seed_h(seed, g.fit_tag_mix, 0), lane);
-                const double ba = dsqrt(ddiv(6.0, static_cast<double>(g.m + g.ka)));
-                uniform_fill(S.P, g.m * g.ka, -ba, ba, mt, lane);
-                const double bs = dsqrt(ddiv(6.0, static_cast<double>(g.n + g.ks)));
-                uniform_fill(S.P + g.set_off, g.n * g.ks, -bs, bs, mt, lane);
-                for (int l = 0; l < g.L; ++l) {
-                    const double bw = dsqrt(ddiv(6.0, static_cast<double>(g.dims[l] + g.dims[l + 1])));
-                    uniform_fill(S.P + g.off_w[l], g.dims[l] * g.dims[l + 1], -bw, bw, mt, lane);
-                    for (int q = lane; q < g.dims[l + 1]; q += 32) S.P[g.off_b[l] + q] = 0.0;
+                const double ba = dsqrt(ddiv(6.0, static_cast<double>(g.m + a.ka())));
+                uniform_fill(S.P(), g.m * a.ka(), -ba, ba, mt, lane);
+                const double bs = dsqrt(ddiv(6.0, static_cast<double>(g.n + a.ks())));
+                uniform_fill(S.P() + g.set_off, g.n * a.ks(), -bs, bs, mt, lane);
+                for (int l = 0; l < a.L(); ++l) {
+                    const double bw = dsqrt(ddiv(6.0, static_cast<double>(a.dim(l) + a.dim(l + 1))));
+                    uniform_fill(S.P() + g.off_w[l], a.dim(l) * a.dim(l + 1), -bw, bw, mt, lane);
+                    for (int q = lane; q < a.dim(l + 1); q += 32) S.P()[g.off_b[l] + q] = 0.0;
                 }
                 // validation split: order = shuffled iota(nc)
-                uint16_t* order = S.perm[1];
+                uint16_t* order = S.perm(1);
                 for (int q = lane; q < nc; q += 32) order[q] = static_cast<uint16_t>(q);
                 __syncwarp();
-                shuffle_warp(order, nc, S.draw, mt, lane);
+                shuffle_warp(order, nc, S.draw(), mt, lane);
                 const int val_count = static_cast<int>(g.val_fraction * static_cast<double>(nc));
-                int nv = 0, nt = 0;
                 for (int q = lane; q < nc; q += 32) {
-                    if (q < val_count) S.vset[q] = order[q];
-                    else S.tset[q - val_count] = order[q];
+                    if (q < val_count) S.vset()[q] = order[q];
+                    else S.tset()[q - val_count] = order[q];
                 }
-                nv = val_count;
-                nt = nc - val_count;
+                int nv = val_count, nt = nc - val_count;
                 __syncwarp();
                 if (nt == 0) {  // std::swap(train, val)
-                    for (int q = lane; q < nv; q += 32) S.tset[q] = S.vset[q];
+                    for (int q = lane; q < nv; q += 32) S.tset()[q] = S.vset()[q];
                     nt = nv;
                     nv = 0;
                 }
                 if (lane == 0) {
-                    S.ctrl[kNt] = nt;
-                    S.ctrl[kNv] = nv;
+                    S.ctrl()[kNt] = nt;
+                    S.ctrl()[kNv] = nv;
                 }
                 __syncwarp();
             }
             __syncthreads();
-            const int nt = S.ctrl[kNt], nv = S.ctrl[kNv];
-            const uint16_t* mon = nv == 0 ? S.tset : S.vset;
+            const int nt = S.ctrl()[kNt], nv = S.ctrl()[kNv];
+            const uint16_t* mon = nv == 0 ? S.tset() : S.vset();
             const int nmon = nv == 0 ? nt : nv;
 
             double init_train = 0.0, best_val = 0.0;
@@ -390,15 +494,15 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
 #pragma unroll
                 for (int k = 0; k < kEPT; ++k) {
                     M1[k] = V1[k] = 0.0;
-                    if (own_valid(own[k])) BEST[k] = S.P[ctid + k * kCT];
+                    if (own_valid(own[k])) BEST[k] = S.P()[ctid + k * kCT];
                 }
-                init_train = cells_mse<LANE>(S, g, S.tset, nt, warp, lane, ctid);
-                best_val = cells_mse<LANE>(S, g, mon, nmon, warp, lane, ctid);
+                init_train = cells_mse<LANE>(S, a, g, S.tset(), nt, warp, lane, ctid);
+                best_val = cells_mse<LANE>(S, a, g, mon, nmon, warp, lane, ctid);
             } else {
                 // epoch-0 permutation of train positions
-                for (int q = lane; q < nt; q += 32) S.perm[0][q] = static_cast<uint16_t>(q);
+                for (int q = lane; q < nt; q += 32) S.perm(0)[q] = static_cast<uint16_t>(q);
                 __syncwarp();
-                shuffle_warp(S.perm[0], nt, S.draw, mt, lane);
+                shuffle_warp(S.perm(0), nt, S.draw(), mt, lane);
             }
             __syncthreads();
 
@@ -406,26 +510,26 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
             double b1p = 1.0, b2p = 1.0;
             bool diverged = false;
             for (; epoch < g.max_epochs; ++epoch) {
-                const uint16_t* perm = S.perm[epoch & 1];
+                const uint16_t* perm = S.perm(epoch & 1);
                 if (is_rng) {
-                    uint16_t* nxt = S.perm[(epoch + 1) & 1];
+                    uint16_t* nxt = S.perm((epoch + 1) & 1);
                     for (int q = lane; q < nt; q += 32) nxt[q] = perm[q];
                     __syncwarp();
-                    shuffle_warp(nxt, nt, S.draw, mt, lane);
+                    shuffle_warp(nxt, nt, S.draw(), mt, lane);
                 } else {
                     for (int start = 0; start < nt; start += g.batch) {
                         const int cnt = min(g.batch, nt - start);
                         const double scale = ddiv(1.0, static_cast<double>(cnt));
                         if (ctid < cnt) {
-                            const int c = S.tset[perm[start + ctid]];
-                            const uint32_t rc = S.crc[c];
-                            S.s_app[ctid] = static_cast<int>(rc >> 16);
-                            S.s_set[ctid] = static_cast<int>(rc & 0xffff);
-                            S.s_y[ctid] = S.cval[c];
+                            const int c = S.tset()[perm[start + ctid]];
+                            const uint32_t rc = S.crc()[c];
+                            S.s_app()[ctid] = static_cast<int>(rc >> 16);
+                            S.s_set()[ctid] = static_cast<int>(rc & 0xffff);
+                            S.s_y()[ctid] = S.cval()[c];
                         }
                         bar_compute();
-                        forward_chunk<LANE>(S, g, cnt, true, warp, lane, ctid);
-                        backward_chunk<LANE>(S, g, cnt, scale, warp, lane);
+                        forward_chunk<LANE>(S, a, g, cnt, true, warp, lane, ctid);
+                        backward_chunk<LANE>(S, a, g, cnt, scale, warp, lane);
                         // AdamState::step (nnkit.cpp:239-251): dense over every block
                         b1p = dmul(b1p, b1);
                         b2p = dmul(b2p, b2);
@@ -434,32 +538,16 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
                         for (int k = 0; k < kEPT; ++k) {
                             const uint32_t o = own[k];
                             if (!own_valid(o)) continue;
-                            const int e = ctid + k * kCT, kind = own_kind(o), lay = own_layer(o);
-                            const int orow = own_r(o), ocol = own_c(o);
-                            double gsum = 0.0;
-                            if (kind == 2) {  // outer_acc: G[r][c] += d[r] * x[c]
-                                const double* dl = S.del[lay] + orow;
-                                const double* al = S.act[lay] + ocol;
-                                const int sd = g.stride[lay + 1], sa = g.stride[lay];
-                                for (int s = 0; s < cnt; ++s) gsum = LaneOps<LANE>::axpy(gsum, dl[s * sd], al[s * sa]);
-                            } else if (kind == 3) {  // bias: G[o] += delta[o]
-                                const double* dl = S.del[lay] + orow;
-                                const int sd = g.stride[lay + 1];
-                                for (int s = 0; s < cnt; ++s) gsum = dadd(gsum, dl[s * sd]);
-                            } else if (kind == 0) {  // app-embedding scatter (:171-172)
-                                for (int s = 0; s < cnt; ++s)
-                                    if (S.s_app[s] == orow) gsum = dadd(gsum, S.ig[s * g.stride[0] + ocol]);
-                            } else {  // setting-embedding scatter (:173-174)
-                                for (int s = 0; s < cnt; ++s)
-                                    if (S.s_set[s] == orow) gsum = dadd(gsum, S.ig[s * g.stride[0] + g.ka + ocol]);
-                            }
-                            double p = S.P[e];
-                            LaneOps<LANE>::adam(p, M1[k], V1[k], gsum, lr, b1, omb1, b2, omb2, eps, mc, vc, own_vec(o));
-                            S.P[e] = p;
+                            const int e = ctid + k * kCT;
+                            const double gsum = param_grad<LANE>(S, a, o, cnt);
+                            double p = S.P()[e];
+                            LaneOps<LANE>::adam(p, M1[k], V1[k], gsum, lr, b1, omb1, b2, omb2, eps, mc, vc,
+                                                own_vec(o));
+                            S.P()[e] = p;
                         }
                         bar_compute();
                     }
-                    const double vl = cells_mse<LANE>(S, g, mon, nmon, warp, lane, ctid);
+                    const double vl = cells_mse<LANE>(S, a, g, mon, nmon, warp, lane, ctid);
                     if (ctid == 0) {
                         int improved = 0, stop = 0, div = 0;
                         if (!isfinite(vl)) {
@@ -472,21 +560,21 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
                         } else if (++stale > g.patience) {
                             stop = 1;
                         }
-                        S.ctrl[kImproved] = improved;
-                        S.ctrl[kStop] = stop;
-                        S.ctrl[kDiverged] = div;
+                        S.ctrl()[kImproved] = improved;
+                        S.ctrl()[kStop] = stop;
+                        S.ctrl()[kDiverged] = div;
                     }
                 }
                 __syncthreads();
-                const bool stop = S.ctrl[kStop] != 0;
-                if (S.ctrl[kDiverged]) {
+                const bool stop = S.ctrl()[kStop] != 0;
+                if (S.ctrl()[kDiverged]) {
                     diverged = true;
                     break;
                 }
-                if (!is_rng && S.ctrl[kImproved]) {
+                if (!is_rng && S.ctrl()[kImproved]) {
 #pragma unroll
                     for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) BEST[k] = S.P[ctid + k * kCT];
+                        if (own_valid(own[k])) BEST[k] = S.P()[ctid + k * kCT];
                 }
                 if (stop) {
                     ++epoch;
@@ -500,15 +588,15 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
                 if (!is_rng) {
 #pragma unroll
                     for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) S.P[ctid + k * kCT] = BEST[k];
+                        if (own_valid(own[k])) S.P()[ctid + k * kCT] = BEST[k];
                 }
                 __syncthreads();
                 double final_train = 0.0;
-                if (!is_rng) final_train = cells_mse<LANE>(S, g, S.tset, nt, warp, lane, ctid);
+                if (!is_rng) final_train = cells_mse<LANE>(S, a, g, S.tset(), nt, warp, lane, ctid);
                 if (tid == 0) {
                     for (int q = g.off_w[0]; q < g.T; ++q)  // check_finite (nnkit.cpp:106-113)
-                        if (!isfinite(S.P[q])) {
-                            S.ctrl[kDiverged] = 2;
+                        if (!isfinite(S.P()[q])) {
+                            S.ctrl()[kDiverged] = 2;
                             break;
                         }
                     if (io.meta) {
@@ -523,25 +611,25 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
                 }
                 if (io.params) {
                     __syncthreads();
-                    for (int q = tid; q < g.T; q += kThreads) io.params[app * io.params_stride + q] = S.P[q];
+                    for (int q = tid; q < g.T; q += kThreads) io.params[app * io.params_stride + q] = S.P()[q];
                 }
                 __syncthreads();
-                if (S.ctrl[kDiverged] == 2) status = OCG_E_LOGIC;
+                if (S.ctrl()[kDiverged] == 2) status = OCG_E_LOGIC;
                 else if (cold) status = OCG_E_COLD;
                 // ------------ impute the app's missing cells ---------------
                 if (status == OCG_OK && !is_rng) {
                     for (int j0 = 0; j0 < g.n; j0 += 32) {
                         if (ctid < 32) {
                             const int j = j0 + ctid;
-                            S.s_app[ctid] = D;
-                            S.s_set[ctid] = j < g.n ? j : 0;
+                            S.s_app()[ctid] = D;
+                            S.s_set()[ctid] = j < g.n ? j : 0;
                         }
                         bar_compute();
                         const int cnt = min(32, g.n - j0);
-                        forward_chunk<LANE>(S, g, cnt, false, warp, lane, ctid);
+                        forward_chunk<LANE>(S, a, g, cnt, false, warp, lane, ctid);
                         if (ctid < cnt && pmask[j0 + ctid] == 0) {
-                            const double v = S.act[g.L][ctid * g.stride[g.L]];
-                            S.row[j0 + ctid] = v < 0.01 ? 0.01 : (1.25 < v ? 1.25 : v);  // std::clamp
+                            const double v = out_act(S, a)[ctid * a.stride(a.L())];
+                            S.row()[j0 + ctid] = v < 0.01 ? 0.01 : (1.25 < v ? 1.25 : v);  // std::clamp
                         }
                         bar_compute();
                     }
@@ -553,7 +641,7 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
         if (warp == 0) {
             SelResult r{};
             if (status == OCG_OK && io.cpu_caps != nullptr) {
-                r = select_row_warp(S.row, g.n, io.cpu_caps, io.gpu_caps, g.ngpu, g.e_base, g.gamma, lane);
+                r = select_row_warp(S.row(), g.n, io.cpu_caps, io.gpu_caps, g.ngpu, g.e_base, g.gamma, lane);
                 if (r.idx < 0) status = OCG_E_LOGIC;
             }
             if (lane == 0) {
@@ -565,9 +653,22 @@ ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
             }
         }
         if (io.completed)
-            for (int j = tid; j < g.n; j += kThreads) io.completed[app * g.n + j] = S.row[j];
+            for (int j = tid; j < g.n; j += kThreads) io.completed[app * g.n + j] = S.row()[j];
         __syncthreads();
     }
+}
+
+}  // namespace
+
+template <int LANE>
+__global__ void __launch_bounds__(kThreads, 2) ncf_app_batch_kernel(BatchGeom g, BatchIO io) {
+    app_batch_body<LANE, RtArch>(g, io);
+}
+
+// reference-default architecture: app/setting dim 8, hidden {32, 16}
+template <int LANE>
+__global__ void __launch_bounds__(kThreads, 2) ncf_app_batch_kernel_k8(BatchGeom g, BatchIO io) {
+    app_batch_body<LANE, FixArch<8, 8, 32, 16>>(g, io);
 }
 
 size_t batch_smem_bytes(const BatchGeom& g) {
@@ -592,29 +693,32 @@ size_t batch_smem_bytes(const BatchGeom& g) {
 
 int batch_threads() { return kThreads; }
 
-cudaError_t launch_app_batch(const BatchGeom& g, const BatchIO& io, int lane, int grid,
-                             cudaStream_t stream) {
+bool batch_is_fixed_k8(const BatchGeom& g) {
+    return g.L == 3 && g.ka == 8 && g.ks == 8 && g.dims[1] == 32 && g.dims[2] == 16 && g.T <= kFixMaxParams;
+}
+
+namespace {
+using KernelFn = void (*)(BatchGeom, BatchIO);
+KernelFn pick(const BatchGeom& g, int lane) {
+    if (batch_is_fixed_k8(g)) return lane == 0 ? ncf_app_batch_kernel_k8<0> : ncf_app_batch_kernel_k8<1>;
+    return lane == 0 ? ncf_app_batch_kernel<0> : ncf_app_batch_kernel<1>;
+}
+}  // namespace
+
+cudaError_t launch_app_batch(const BatchGeom& g, const BatchIO& io, int lane, int grid, cudaStream_t stream) {
     const size_t smem = batch_smem_bytes(g);
-    if (lane == 0) {
-        cudaFuncSetAttribute(ncf_app_batch_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        ncf_app_batch_kernel<0><<<grid, kThreads, smem, stream>>>(g, io);
-    } else {
-        cudaFuncSetAttribute(ncf_app_batch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        ncf_app_batch_kernel<1><<<grid, kThreads, smem, stream>>>(g, io);
-    }
+    const KernelFn k = pick(g, lane);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<grid, kThreads, smem, stream>>>(g, io);
     return cudaGetLastError();
 }
 
 int batch_max_active_per_sm(const BatchGeom& g, int lane) {
     int n = 0;
     const size_t smem = batch_smem_bytes(g);
-    if (lane == 0) {
-        cudaFuncSetAttribute(ncf_app_batch_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ncf_app_batch_kernel<0>, kThreads, smem);
-    } else {
-        cudaFuncSetAttribute(ncf_app_batch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ncf_app_batch_kernel<1>, kThreads, smem);
-    }
+    const KernelFn k = pick(g, lane);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kThreads, smem);
     return n;
 }
 

@@ -12,6 +12,7 @@ namespace ocg {
 constexpr int kMaxLayers = 4;      // MLP layers (hidden + output)
 constexpr int kMaxWidth = 64;      // widest MLP layer / input
 constexpr int kMaxParams = 2048;   // parameters of one app's model (8 per compute thread)
+constexpr int kFixMaxParams = 1536; // same, reference-default architecture kernel (6 per thread)
 constexpr int kMaxCells = 16384;   // observed cells of one app's matrix
 constexpr int kMaxBatch = 32;      // minibatch size (one sample per lane)
 
@@ -58,6 +59,7 @@ struct BatchIO {
 };
 
 size_t batch_smem_bytes(const BatchGeom& g);
+bool batch_is_fixed_k8(const BatchGeom& g);
 int batch_threads();
 int batch_max_active_per_sm(const BatchGeom& g, int lane);
 cudaError_t launch_app_batch(const BatchGeom& g, const BatchIO& io, int lane, int grid, cudaStream_t stream);
