@@ -151,6 +151,39 @@ int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* hyp
                     const int64_t* rows, const int64_t* cols, int64_t count, int lane,
                     double* out);
 
+/* ---- ALS completion + selection (joint mode) -------
+ * No reference counterpart: the reference's CF is NCF only.  Semantics are
+ * defined by the CPU oracle (oracle/ocg_oracle.c, ocgo_als_fit): weighted-
+ * lambda ALS P ~ U V^T of rank k over the observed CSR entries, then
+ * cf::complete-style imputation (observed verbatim, clamp(u_i.v_j, 0.01,
+ * 1.25) elsewhere) fused with policy::select_caps (policy.cpp:17-64) per row.
+ * FP32 factors, FP64 selection arithmetic.  Parity vs the reference:
+ * unpinned (vs the oracle: within tolerance; selections exact given the
+ * completed rows). */
+typedef struct {
+    int32_t rank;   /* 8, 16 or 32 */
+    float lambda;   /* weighted-lambda regularisation */
+    int32_t sweeps; /* row + column half-sweeps per fit */
+    uint64_t seed;  /* V initialisation (ocgo_als_init_value) */
+} ocg_als_hyper;
+
+typedef struct ocg_als_plan ocg_als_plan;
+/* CSR input: row_ptr[m+1] (int64), col[nnz] (int32, ascending per row),
+ * val[nnz] (FP32 normalized performance).  on_device=0: host buffers are
+ * copied; on_device=1: device pointers are used in place (must outlive the
+ * plan).  Columns follow PowerGrid::settings() of (cpu_caps x gpu_caps). */
+int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const int32_t* col, const float* val,
+                        int on_device, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
+                        int32_t ngpu, const ocg_als_hyper* hyper, double gamma, ocg_als_plan** out);
+/* one full step on device data: CSC build, fit, fused imputation+selection.
+ * total_ms / phase_ms[4] (CSC, row sweeps, column sweeps, select): CUDA-event
+ * times on the context stream (either may be NULL = asynchronous). */
+int ocg_als_plan_run(ocg_als_plan* plan, float* total_ms, float* phase_ms);
+int ocg_als_plan_results(ocg_als_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand,
+                         float* U, float* V);
+int ocg_als_plan_completed_rows(ocg_als_plan* plan, int64_t row0, int64_t nrows, double* out);
+void ocg_als_plan_destroy(ocg_als_plan* plan);
+
 /* ---- synthetic inputs (benches/tests; host only, no GPU needed) --------
  * Restatements of the reference's input generators so benches never need
  * the reference: sim::make_suite (simnode.cpp:192-244), sim::true_perf

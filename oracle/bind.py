@@ -102,6 +102,10 @@ class Port:
         L.ocgo_ncf_fit.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_u64, c_vp, c_vp, c_vp, c_vp]
         L.ocgo_ncf_predict.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]
         L.ocgo_set_lane.argtypes = [ctypes.c_int]
+        L.ocgo_als_fit.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_dbl, c_i32, c_u64, c_vp,
+                                   c_vp]
+        L.ocgo_als_init_value.restype = c_dbl
+        L.ocgo_als_init_value.argtypes = [c_u64, c_i64, c_i32, c_i32]
 
     def set_lane(self, lane):
         """0: reference scalar lane FP order, 1: AVX2/FMA lane."""
@@ -154,6 +158,35 @@ class Port:
         rc = self.L.ocgo_ncf_predict(m, n, ctypes.byref(h), P(params), P(aseen), P(sseen), P(rows), P(cols),
                                      len(rows), P(out))
         return rc, out
+
+
+def csc_of(m, n, row_ptr, col, val):
+    """Stable CSC mirror (rows ascending inside a column) of a CSR matrix."""
+    rows = np.repeat(np.arange(m, dtype=np.int32), np.diff(row_ptr))
+    order = np.argsort(col, kind="stable")
+    cp = np.zeros(n + 1, np.int64)
+    cp[1:] = np.cumsum(np.bincount(col, minlength=n))
+    return cp, rows[order].astype(np.int32), np.ascontiguousarray(val[order], np.float32)
+
+
+def als_fit(port, m, n, row_ptr, col, val, k, lam, sweeps, seed):
+    """FP64 ALS oracle (no reference counterpart)."""
+    val = np.ascontiguousarray(val, np.float32)
+    cp, crow, cval = csc_of(m, n, row_ptr, col, val)
+    U, V = np.zeros((m, k)), np.zeros((n, k))
+    rc = port.L.ocgo_als_fit(m, n, P(row_ptr), P(col), P(val), P(cp), P(crow), P(cval), k, lam, sweeps, seed,
+                             P(U), P(V))
+    assert rc == 0, port.err()
+    return U, V
+
+
+def als_completed_rows(U, V, row_ptr, col, val, rows):
+    """oracle completed rows: observed verbatim (FP32 value widened), else clamp(u.v)."""
+    out = np.clip(U[rows] @ V.T, 0.01, 1.25)
+    for r, i in enumerate(rows):
+        s, e = row_ptr[i], row_ptr[i + 1]
+        out[r, col[s:e]] = val[s:e].astype(np.float64)
+    return out
 
 
 class Ref:

@@ -510,3 +510,83 @@ int ocgo_ncf_predict(int64_t m, int64_t n, const ocgo_hyper* h, const double* P,
     }
     return E_OK;
 }
+
+/* ------------------------------------------------------------------ als --
+ * ALS matrix factorisation P ~ U V^T.  NO REFERENCE COUNTERPART: the
+ * reference's only CF is NCF, so this oracle defines the semantics the GPU
+ * path is checked against ("parity unpinned" vs the reference).
+ *   init   V[j][0] = 1, V[j][f>0] = 0.01*(2u-1), u = splitmix64 stream
+ *          (ocgo_als_init_value); U unused until the first row sweep
+ *   sweep  rows:    u_i = (sum_j v_j v_j^T + lambda n_i I)^-1 sum_j r_ij v_j
+ *          columns: v_j = (sum_i u_i u_i^T + lambda n_j I)^-1 sum_i r_ij u_i
+ *          (weighted-lambda regularisation; empty row/col -> zero factor)
+ *   solve  Cholesky (lower), forward + back substitution
+ * FP64 throughout (the GPU runs FP32; tests compare within tolerance). */
+double ocgo_als_init_value(uint64_t seed, int64_t j, int32_t f, int32_t k) {
+    if (f == 0) return 1.0;
+    const uint64_t h = splitmix64(seed ^ splitmix64((uint64_t)(j * k + f)));
+    const double u = (double)(h >> 11) * 0x1.0p-53;
+    return 0.01 * (2.0 * u - 1.0);
+}
+
+static void chol_solve(double* A, double* b, int k) {
+    for (int c = 0; c < k; ++c) {
+        double d = A[c * k + c];
+        for (int q = 0; q < c; ++q) d -= A[c * k + q] * A[c * k + q];
+        d = sqrt(d);
+        A[c * k + c] = d;
+        for (int r = c + 1; r < k; ++r) {
+            double s = A[r * k + c];
+            for (int q = 0; q < c; ++q) s -= A[r * k + q] * A[c * k + q];
+            A[r * k + c] = s / d;
+        }
+    }
+    for (int c = 0; c < k; ++c) { /* L y = b */
+        double s = b[c];
+        for (int q = 0; q < c; ++q) s -= A[c * k + q] * b[q];
+        b[c] = s / A[c * k + c];
+    }
+    for (int c = k - 1; c >= 0; --c) { /* L^T x = y */
+        double s = b[c];
+        for (int q = c + 1; q < k; ++q) s -= A[q * k + c] * b[q];
+        b[c] = s / A[c * k + c];
+    }
+}
+
+static void als_half(int64_t nrows, const int64_t* ptr, const int32_t* idx, const float* val, const double* Y,
+                     double* X, int k, double lambda) {
+    double A[64 * 64], b[64];
+    for (int64_t i = 0; i < nrows; ++i) {
+        const int64_t cnt = ptr[i + 1] - ptr[i];
+        if (cnt == 0) {
+            for (int f = 0; f < k; ++f) X[i * k + f] = 0.0;
+            continue;
+        }
+        memset(A, 0, sizeof(double) * (size_t)(k * k));
+        memset(b, 0, sizeof(double) * (size_t)k);
+        for (int64_t q = ptr[i]; q < ptr[i + 1]; ++q) {
+            const double* y = Y + (int64_t)idx[q] * k;
+            const double r = val[q];
+            for (int a = 0; a < k; ++a) {
+                b[a] += r * y[a];
+                for (int c = 0; c <= a; ++c) A[a * k + c] += y[a] * y[c];
+            }
+        }
+        for (int a = 0; a < k; ++a) A[a * k + a] += lambda * (double)cnt;
+        chol_solve(A, b, k);
+        for (int f = 0; f < k; ++f) X[i * k + f] = b[f];
+    }
+}
+
+int ocgo_als_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const float* val,
+                 const int64_t* col_ptr, const int32_t* row_idx, const float* cval, int32_t k, double lambda,
+                 int32_t sweeps, uint64_t seed, double* U, double* V) {
+    if (k <= 0 || k > 64) return fail(E_INVALID, "als: rank must be in [1, 64]");
+    for (int64_t j = 0; j < n; ++j)
+        for (int32_t f = 0; f < k; ++f) V[j * k + f] = ocgo_als_init_value(seed, j, f, k);
+    for (int32_t s = 0; s < sweeps; ++s) {
+        als_half(m, row_ptr, col, val, V, U, k, lambda);
+        als_half(n, col_ptr, row_idx, cval, U, V, k, lambda);
+    }
+    return E_OK;
+}

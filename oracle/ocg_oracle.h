@@ -57,6 +57,12 @@ int ocgo_ncf_predict(int64_t m, int64_t n, const ocgo_hyper* h, const double* pa
                      const uint8_t* app_seen, const uint8_t* setting_seen, const int64_t* rows,
                      const int64_t* cols, int64_t count, double* out);
 
+/* ALS (no reference counterpart; semantics defined in ocg_oracle.c) */
+double ocgo_als_init_value(uint64_t seed, int64_t j, int32_t f, int32_t k);
+int ocgo_als_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const float* val,
+                 const int64_t* col_ptr, const int32_t* row_idx, const float* cval, int32_t k, double lambda,
+                 int32_t sweeps, uint64_t seed, double* U, double* V);
+
 #ifdef __cplusplus
 }
 #endif

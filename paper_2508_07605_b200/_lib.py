@@ -135,3 +135,17 @@ _sig("ocg_online_plan_create", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_v
 _sig("ocg_online_plan_run", ctypes.c_int, c_vp, ctypes.POINTER(ctypes.c_float))
 _sig("ocg_online_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_online_plan_destroy", None, c_vp)
+
+
+class AlsHyperC(ctypes.Structure):
+    """ocg_als_hyper."""
+
+    _fields_ = [("rank", c_i32), ("lambda_", ctypes.c_float), ("sweeps", c_i32), ("seed", c_u64)]
+
+
+_sig("ocg_als_plan_create", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i32, c_vp, c_i32,
+     c_vp, c_dbl, ctypes.POINTER(c_vp))
+_sig("ocg_als_plan_run", ctypes.c_int, c_vp, c_vp, c_vp)
+_sig("ocg_als_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_als_plan_completed_rows", ctypes.c_int, c_vp, c_i64, c_i64, c_vp)
+_sig("ocg_als_plan_destroy", None, c_vp)

@@ -1,0 +1,88 @@
+"""ALS completion + selection (joint mode) through the C-ABI (include/ocg.h).
+
+No reference counterpart (the reference's CF is NCF only); semantics are the
+CPU oracle's (oracle/ocg_oracle.c: ocgo_als_fit)."""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import lib, check, ptr
+from .api import Context, PowerGrid, default_context
+
+
+@dataclass
+class AlsHyper:
+    rank: int = 32
+    lam: float = 0.003
+    sweeps: int = 10
+    seed: int = 42
+
+    def to_c(self):
+        h = _lib.AlsHyperC()
+        h.rank, h.lambda_, h.sweeps, h.seed = self.rank, self.lam, self.sweeps, self.seed
+        return h
+
+
+class AlsPlan:
+    """One joint completion problem resident on the device.
+
+    csr: (m, row_ptr, col, val) host numpy arrays, or device addresses when
+    ``on_device`` (ints; the caller keeps the buffers alive)."""
+
+    def __init__(self, m, row_ptr, col, val, grid: PowerGrid, hyper: AlsHyper | None = None, gamma: float = 0.05,
+                 on_device: bool = False, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.m, self.n = int(m), grid.n
+        self.hyper = hyper or AlsHyper()
+        cpu, gpu = grid.arrays()
+        h = self.hyper.to_c()
+        self._h = ctypes.c_void_p()
+        if on_device:
+            args = (ctypes.c_void_p(row_ptr), ctypes.c_void_p(col), ctypes.c_void_p(val))
+        else:
+            self._keep = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
+                          np.ascontiguousarray(val, np.float32))
+            args = tuple(ptr(a) for a in self._keep)
+        check(lib.ocg_als_plan_create(self.ctx.handle, self.m, *args, 1 if on_device else 0, ptr(cpu), len(cpu),
+                                      ptr(gpu), len(gpu), ctypes.byref(h), gamma, ctypes.byref(self._h)))
+
+    def run(self, timed: bool = True):
+        """One step (CSC build + fit + fused imputation/selection).
+        Returns (total_ms, [csc_ms, row_sweeps_ms, col_sweeps_ms, select_ms])."""
+        tot = ctypes.c_float(0)
+        ph = (ctypes.c_float * 4)()
+        check(lib.ocg_als_plan_run(self._h, ctypes.byref(tot) if timed else None, ph if timed else None))
+        return float(tot.value), [float(x) for x in ph]
+
+    def results(self):
+        m = self.m
+        idx, nc = np.zeros(m, np.int32), np.zeros(m, np.int32)
+        sv, lo = np.zeros(m), np.zeros(m)
+        check(lib.ocg_als_plan_results(self._h, ptr(idx), ptr(sv), ptr(lo), ptr(nc), None, None))
+        return idx, sv, lo, nc
+
+    def factors(self):
+        U = np.zeros((self.m, self.hyper.rank), np.float32)
+        V = np.zeros((self.n, self.hyper.rank), np.float32)
+        check(lib.ocg_als_plan_results(self._h, None, None, None, None, ptr(U), ptr(V)))
+        return U, V
+
+    def completed_rows(self, row0: int, nrows: int) -> np.ndarray:
+        out = np.zeros((nrows, self.n))
+        check(lib.ocg_als_plan_completed_rows(self._h, row0, nrows, ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ocg_als_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,44 @@
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ocg {
+
+cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);
+// mode 0: solve items in place (X); mode 1: write reduced Gram+rhs to Gout
+cudaError_t launch_als_gram_solve(int k, int64_t nitems, const int64_t* ptr, const int32_t* idx, const float* val,
+                                  const float* Y, float* X, float* Gout, float lambda, int wpi, int mode,
+                                  int sm_count, cudaStream_t s);
+cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const int64_t* counts, const float* G, float* X,
+                                       float lambda, int sm_count, cudaStream_t s);
+cudaError_t launch_expand_rows(int64_t m, const int64_t* ptr, int32_t* rowid, int sm_count, cudaStream_t s);
+cudaError_t launch_gather_csc(int64_t nnz, const int32_t* perm, const int32_t* rowid, const float* val, int32_t* crow,
+                              float* cval, cudaStream_t s);
+cudaError_t launch_col_ptr(int64_t nnz, int64_t n, const int32_t* skeys, int64_t* cptr, cudaStream_t s);
+
+// fused completion + Algorithm-2 selection over all rows (als_select.cu)
+struct AlsSelectArgs {
+    int64_t m, n;
+    int k;
+    const float* U;
+    const float* V;   // n x K
+    const float* Vt;  // K x n (transposed copy)
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const float* val;
+    const int32_t* cpu_caps;
+    const int32_t* gpu_caps;
+    int ngpu;
+    double e_base, gamma;
+    int32_t* idx;
+    double* saving;
+    double* loss;
+    int32_t* ncand;
+    double* completed;  // optional m x n completed rows (tests), else nullptr
+};
+cudaError_t launch_als_select(const AlsSelectArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_transpose(int64_t n, int k, const float* V, float* Vt, cudaStream_t s);
+
+}  // namespace ocg

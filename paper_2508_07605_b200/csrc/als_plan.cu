@@ -1,0 +1,312 @@
+// Host orchestration of the ALS completion + selection path (C-ABI in
+// include/ocg.h).  One step = build the CSC mirror of the CSR input on the
+// device (stable radix sort by column -> rows stay ascending inside a column,
+// so the column Gram reduction order is fixed), V init, `sweeps` x (row
+// half-sweep, column half-sweep), then the fused imputation + selection pass.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ocg.h"
+#include "als.h"
+#include "ocg_common.cuh"
+
+// from capi.cu
+int ocg_internal_fail(int code, const std::string& msg);
+cudaStream_t ocg_internal_stream(ocg_ctx* ctx);
+int ocg_internal_sm_count(ocg_ctx* ctx);
+
+namespace {
+
+#define ALS_CUDA(call)                                                                                    \
+    do {                                                                                                  \
+        cudaError_t e_ = (call);                                                                          \
+        if (e_ != cudaSuccess) return ocg_internal_fail(OCG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+struct Buf {
+    T* p = nullptr;
+    bool own = true;
+    ~Buf() {
+        if (p && own) cudaFree(p);
+    }
+    cudaError_t alloc(size_t n) { return n ? cudaMalloc(&p, sizeof(T) * n) : cudaSuccess; }
+};
+
+__global__ void iota_kernel(int64_t n, int32_t* out) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = static_cast<int32_t>(q);
+}
+
+int bits_for(int64_t n) {
+    int b = 1;
+    while ((int64_t(1) << b) < n + 1) ++b;
+    return b;
+}
+
+}  // namespace
+
+struct ocg_als_plan {
+    ocg_ctx* ctx = nullptr;
+    int64_t m = 0, n = 0, nnz = 0;
+    int k = 32, sweeps = 10;
+    float lambda = 0.05f;
+    uint64_t seed = 0;
+    double gamma = 0.05, e_base = 0.0;
+    int ngpu = 1;
+    // CSR (owned copies unless created from device pointers)
+    Buf<int64_t> row_ptr;
+    Buf<int32_t> col;
+    Buf<float> val;
+    // CSC mirror + scratch
+    Buf<int64_t> col_ptr;
+    Buf<int32_t> crow, rowid, keys_out, perm_in, perm_out;
+    Buf<float> cval;
+    Buf<uint8_t> sort_tmp;
+    size_t sort_tmp_bytes = 0;
+    // factors + outputs
+    Buf<float> U, V, Vt;
+    Buf<int32_t> cpu, gpu, idx, ncand;
+    Buf<double> saving, loss;
+    cudaEvent_t ev[6] = {};
+    ~ocg_als_plan() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+static int als_build_csc(ocg_als_plan* P) {
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const int sm = ocg_internal_sm_count(P->ctx);
+    ALS_CUDA(ocg::launch_expand_rows(P->m, P->row_ptr.p, P->rowid.p, sm, s));
+    if (P->nnz > 0) {
+        iota_kernel<<<static_cast<unsigned>((P->nnz + 255) / 256), 256, 0, s>>>(P->nnz, P->perm_in.p);
+        ALS_CUDA(cudaGetLastError());
+        size_t bytes = P->sort_tmp_bytes;
+        ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, P->col.p, P->keys_out.p, P->perm_in.p,
+                                                 P->perm_out.p, P->nnz, 0, bits_for(P->n), s));
+        ALS_CUDA(ocg::launch_gather_csc(P->nnz, P->perm_out.p, P->rowid.p, P->val.p, P->crow.p, P->cval.p, s));
+    }
+    ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
+    return OCG_OK;
+}
+
+static int als_alloc(ocg_als_plan* P) {
+    ALS_CUDA(P->col_ptr.alloc(static_cast<size_t>(P->n + 1)));
+    ALS_CUDA(P->crow.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->cval.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->rowid.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->keys_out.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->perm_in.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->perm_out.alloc(static_cast<size_t>(P->nnz)));
+    size_t bytes = 0;
+    ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P->col.p, P->keys_out.p, P->perm_in.p, P->perm_out.p,
+                                             P->nnz, 0, bits_for(P->n)));
+    P->sort_tmp_bytes = bytes;
+    ALS_CUDA(P->sort_tmp.alloc(bytes));
+    ALS_CUDA(P->U.alloc(static_cast<size_t>(P->m * P->k)));
+    ALS_CUDA(P->V.alloc(static_cast<size_t>(P->n * P->k)));
+    ALS_CUDA(P->Vt.alloc(static_cast<size_t>(P->n * P->k)));
+    ALS_CUDA(P->idx.alloc(static_cast<size_t>(P->m)));
+    ALS_CUDA(P->ncand.alloc(static_cast<size_t>(P->m)));
+    ALS_CUDA(P->saving.alloc(static_cast<size_t>(P->m)));
+    ALS_CUDA(P->loss.alloc(static_cast<size_t>(P->m)));
+    for (auto& e : P->ev) ALS_CUDA(cudaEventCreate(&e));
+    return OCG_OK;
+}
+
+static int als_check(int64_t m, int64_t n, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
+                     const ocg_als_hyper* h, double gamma) {
+    if (!h) return ocg_internal_fail(OCG_E_INVALID, "als: null hyperparameters");
+    if (h->rank != 8 && h->rank != 16 && h->rank != 32)
+        return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: rank must be 8, 16 or 32");
+    if (h->lambda <= 0.0f || h->sweeps <= 0) return ocg_internal_fail(OCG_E_INVALID, "als: bad hyperparameters");
+    if (m <= 0 || n <= 0) return ocg_internal_fail(OCG_E_INVALID, "als: empty matrix");
+    if (gamma <= 0.0 || gamma >= 1.0) return ocg_internal_fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
+    if (static_cast<int64_t>(ncpu) * ngpu != n) return ocg_internal_fail(OCG_E_INVALID, "row length does not cover the grid");
+    if (ncpu + ngpu > 512) return ocg_internal_fail(OCG_E_UNSUPPORTED, "grid too large");
+    (void)cpu;
+    (void)gpu;
+    return OCG_OK;
+}
+
+extern "C" {
+
+int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const int32_t* col, const float* val,
+                        int on_device, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
+                        const ocg_als_hyper* h, double gamma, ocg_als_plan** out) {
+    if (!ctx || !out) return ocg_internal_fail(OCG_E_INVALID, "null context/output");
+    *out = nullptr;
+    const int64_t n = static_cast<int64_t>(ncpu) * ngpu;
+    int rc = als_check(m, n, cpu, ncpu, gpu, ngpu, h, gamma);
+    if (rc) return rc;
+    auto P = std::make_unique<ocg_als_plan>();
+    P->ctx = ctx;
+    P->m = m;
+    P->n = n;
+    P->k = h->rank;
+    P->sweeps = h->sweeps;
+    P->lambda = h->lambda;
+    P->seed = h->seed;
+    P->gamma = gamma;
+    P->ngpu = ngpu;
+    P->e_base = static_cast<double>(cpu[ncpu - 1] + gpu[ngpu - 1]);
+    cudaStream_t s = ocg_internal_stream(ctx);
+    if (on_device) {
+        ALS_CUDA(cudaMemcpy(&P->nnz, row_ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        P->row_ptr.p = const_cast<int64_t*>(row_ptr);
+        P->row_ptr.own = false;
+        P->col.p = const_cast<int32_t*>(col);
+        P->col.own = false;
+        P->val.p = const_cast<float*>(val);
+        P->val.own = false;
+    } else {
+        P->nnz = row_ptr[m];
+        ALS_CUDA(P->row_ptr.alloc(static_cast<size_t>(m + 1)));
+        ALS_CUDA(P->col.alloc(static_cast<size_t>(P->nnz)));
+        ALS_CUDA(P->val.alloc(static_cast<size_t>(P->nnz)));
+        ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, s));
+        ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
+        ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
+    }
+    if (P->nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: nnz >= 2^31");
+    if ((rc = als_alloc(P.get()))) return rc;
+    ALS_CUDA(P->cpu.alloc(static_cast<size_t>(ncpu)));
+    ALS_CUDA(P->gpu.alloc(static_cast<size_t>(ngpu)));
+    ALS_CUDA(cudaMemcpyAsync(P->cpu.p, cpu, sizeof(int32_t) * ncpu, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(P->gpu.p, gpu, sizeof(int32_t) * ngpu, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaStreamSynchronize(s));
+    *out = P.release();
+    return OCG_OK;
+}
+
+// phase_ms (optional, 4 floats): CSC build, row half-sweeps, column half-sweeps, select
+int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const int sm = ocg_internal_sm_count(P->ctx);
+    ALS_CUDA(cudaEventRecord(P->ev[0], s));
+    int rc = als_build_csc(P);
+    if (rc) return rc;
+    ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
+    ALS_CUDA(cudaEventRecord(P->ev[1], s));
+    float row_ms = 0.f, col_ms = 0.f;
+    for (int it = 0; it < P->sweeps; ++it) {
+        ALS_CUDA(cudaEventRecord(P->ev[2], s));
+        ALS_CUDA(ocg::launch_als_gram_solve(P->k, P->m, P->row_ptr.p, P->col.p, P->val.p, P->V.p, P->U.p, nullptr,
+                                            P->lambda, 1, 0, sm, s));
+        ALS_CUDA(cudaEventRecord(P->ev[3], s));
+        ALS_CUDA(ocg::launch_als_gram_solve(P->k, P->n, P->col_ptr.p, P->crow.p, P->cval.p, P->U.p, P->V.p, nullptr,
+                                            P->lambda, 8, 0, sm, s));
+        ALS_CUDA(cudaEventRecord(P->ev[4], s));
+        if (phase_ms) {
+            float a = 0, b = 0;
+            ALS_CUDA(cudaEventSynchronize(P->ev[4]));
+            ALS_CUDA(cudaEventElapsedTime(&a, P->ev[2], P->ev[3]));
+            ALS_CUDA(cudaEventElapsedTime(&b, P->ev[3], P->ev[4]));
+            row_ms += a;
+            col_ms += b;
+        }
+    }
+    ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
+    ALS_CUDA(cudaEventRecord(P->ev[2], s));
+    ocg::AlsSelectArgs a{};
+    a.m = P->m;
+    a.n = P->n;
+    a.k = P->k;
+    a.U = P->U.p;
+    a.V = P->V.p;
+    a.Vt = P->Vt.p;
+    a.row_ptr = P->row_ptr.p;
+    a.col = P->col.p;
+    a.val = P->val.p;
+    a.cpu_caps = P->cpu.p;
+    a.gpu_caps = P->gpu.p;
+    a.ngpu = P->ngpu;
+    a.e_base = P->e_base;
+    a.gamma = P->gamma;
+    a.idx = P->idx.p;
+    a.saving = P->saving.p;
+    a.loss = P->loss.p;
+    a.ncand = P->ncand.p;
+    a.completed = nullptr;
+    ALS_CUDA(ocg::launch_als_select(a, sm, s));
+    ALS_CUDA(cudaEventRecord(P->ev[5], s));
+    if (total_ms || phase_ms) {
+        ALS_CUDA(cudaEventSynchronize(P->ev[5]));
+        if (total_ms) ALS_CUDA(cudaEventElapsedTime(total_ms, P->ev[0], P->ev[5]));
+        if (phase_ms) {
+            ALS_CUDA(cudaEventElapsedTime(&phase_ms[0], P->ev[0], P->ev[1]));
+            phase_ms[1] = row_ms;
+            phase_ms[2] = col_ms;
+            ALS_CUDA(cudaEventElapsedTime(&phase_ms[3], P->ev[2], P->ev[5]));
+        }
+    }
+    return OCG_OK;
+}
+
+int ocg_als_plan_results(ocg_als_plan* P, int32_t* idx, double* saving, double* loss, int32_t* ncand, float* U,
+                         float* V) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const size_t m = static_cast<size_t>(P->m);
+    if (idx) ALS_CUDA(cudaMemcpyAsync(idx, P->idx.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    if (saving) ALS_CUDA(cudaMemcpyAsync(saving, P->saving.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (loss) ALS_CUDA(cudaMemcpyAsync(loss, P->loss.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (ncand) ALS_CUDA(cudaMemcpyAsync(ncand, P->ncand.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    if (U) ALS_CUDA(cudaMemcpyAsync(U, P->U.p, sizeof(float) * m * P->k, cudaMemcpyDeviceToHost, s));
+    if (V) ALS_CUDA(cudaMemcpyAsync(V, P->V.p, sizeof(float) * P->n * P->k, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+// completed rows [row0, row0+nrows) as the selection saw them (FP64), for tests
+int ocg_als_plan_completed_rows(ocg_als_plan* P, int64_t row0, int64_t nrows, double* out) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    if (row0 < 0 || nrows < 0 || row0 + nrows > P->m) return ocg_internal_fail(OCG_E_RANGE, "row range");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    Buf<double> d;
+    Buf<int32_t> di, dn;
+    Buf<double> ds, dl;
+    ALS_CUDA(d.alloc(static_cast<size_t>(nrows * P->n)));
+    ALS_CUDA(di.alloc(static_cast<size_t>(nrows)));
+    ALS_CUDA(dn.alloc(static_cast<size_t>(nrows)));
+    ALS_CUDA(ds.alloc(static_cast<size_t>(nrows)));
+    ALS_CUDA(dl.alloc(static_cast<size_t>(nrows)));
+    ocg::AlsSelectArgs a{};
+    a.m = nrows;
+    a.n = P->n;
+    a.k = P->k;
+    a.U = P->U.p + row0 * P->k;
+    a.V = P->V.p;
+    a.Vt = P->Vt.p;
+    // the rows' CSR slice: row_ptr offsets stay absolute, so pass shifted pointers
+    a.row_ptr = P->row_ptr.p + row0;
+    a.col = P->col.p;
+    a.val = P->val.p;
+    a.cpu_caps = P->cpu.p;
+    a.gpu_caps = P->gpu.p;
+    a.ngpu = P->ngpu;
+    a.e_base = P->e_base;
+    a.gamma = P->gamma;
+    a.idx = di.p;
+    a.saving = ds.p;
+    a.loss = dl.p;
+    a.ncand = dn.p;
+    a.completed = d.p;
+    ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
+    ALS_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double) * nrows * P->n, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+void ocg_als_plan_destroy(ocg_als_plan* P) { delete P; }
+
+}  // extern "C"

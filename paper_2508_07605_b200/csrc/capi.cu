@@ -210,6 +210,10 @@ int prepare_batch(ocg_ctx* ctx, const BatchInputs& in, const ocg_ncf_hyper* h, o
 
 }  // namespace
 
+int ocg_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+cudaStream_t ocg_internal_stream(ocg_ctx* ctx) { return ctx->stream; }
+int ocg_internal_sm_count(ocg_ctx* ctx) { return ctx->sm_count; }
+
 // Device-resident per-app batch: inputs uploaded once, kernel re-runnable.
 struct ocg_online_plan {
     ocg_ctx* ctx = nullptr;

@@ -1,0 +1,123 @@
+"""ALS completion + fused selection on the GPU vs the FP64 CPU oracle.
+
+ALS has no reference counterpart (parity vs the reference: unpinned); the
+oracle (oracle/ocg_oracle.c) defines it.  Bars:
+  * factors / predictions: FP32 GPU vs FP64 oracle within PRED_RTOL;
+  * selection: bit-exact w.r.t. the completed rows the kernel used
+    (oracle select_caps on the GPU's completed rows);
+  * end-to-end decisions: identical to the oracle's wherever the row's
+    selection margin exceeds the prediction tolerance."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PRED_RTOL = 2e-3  # FP32 ALS vs FP64 oracle, relative, on imputed cells
+
+
+def _problem(m, nc, ng, density, dense_rows, seed):
+    from paper_2508_07605_b200 import PowerGrid, synth
+
+    grid = PowerGrid.spanning(nc, ng)
+    return grid, synth.joint_csr(m, grid, density, dense_rows, seed=seed)
+
+
+@pytest.mark.parametrize("k", [8, 16, 32])
+def test_als_factors_and_predictions_match_oracle(ctx, port, k):
+    from oracle import bind
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(1500, 8, 16, 0.15, 4, seed=3)
+    hyp = AlsHyper(rank=k, lam=0.003, sweeps=6, seed=11)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+    plan.run()
+    Ug, Vg = plan.factors()
+    Uo, Vo = bind.als_fit(port, A.m, A.n, A.row_ptr, A.col, A.val, k, 0.003, 6, 11)
+    Pg = np.clip(Ug.astype(np.float64) @ Vg.T.astype(np.float64), 0.01, 1.25)
+    Po = np.clip(Uo @ Vo.T, 0.01, 1.25)
+    rel = np.abs(Pg - Po) / Po
+    assert np.quantile(rel, 0.999) < PRED_RTOL, (rel.max(), np.quantile(rel, 0.999))
+
+
+@pytest.mark.parametrize("n_grid", [(8, 16), (16, 16), (64, 64)])
+def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid):
+    """The fused kernel's decision == policy::select_caps on the very rows it
+    completed (bit-exact: index, saving, loss, candidates)."""
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    m = 700 if n_grid[0] < 64 else 200
+    grid, A = _problem(m, *n_grid, 0.05, 2, seed=5)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, AlsHyper(rank=16, sweeps=4), 0.05, ctx=ctx)
+    plan.run()
+    idx, sav, loss, nc = plan.results()
+    rows = plan.completed_rows(0, A.m)
+    # observed cells verbatim
+    i = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    np.testing.assert_array_equal(rows[i, A.col], A.val.astype(np.float64))
+    assert ((rows >= 0.01) & (rows <= 1.25)).all()
+    cpu, gpu = grid.arrays()
+    rc, i2, s2, l2, n2 = port.select_caps(rows, cpu, gpu, 0.05)
+    assert rc == 0
+    np.testing.assert_array_equal(idx, i2)
+    np.testing.assert_array_equal(sav, s2)
+    np.testing.assert_array_equal(loss, l2)
+    np.testing.assert_array_equal(nc, n2)
+
+
+def test_als_selection_ties_and_clamps(ctx, port):
+    """Rows engineered to hit the clamp floor/ceiling and exact saving ties."""
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+    from paper_2508_07605_b200 import PowerGrid
+
+    grid = PowerGrid.spanning(4, 8)
+    n = grid.n
+    rng = np.random.default_rng(0)
+    m = 400
+    dense = rng.choice([0.01, 0.5, 0.9, 1.0, 1.25], size=(m, n))
+    mask = rng.random((m, n)) < 0.7
+    mask[:, -1] = True
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(mask.sum(1))
+    ii, jj = np.nonzero(mask)
+    col, val = jj.astype(np.int32), dense[ii, jj].astype(np.float32)
+    plan = AlsPlan(m, rp, col, val, grid, AlsHyper(rank=8, sweeps=3), 0.1, ctx=ctx)
+    plan.run()
+    idx, sav, loss, nc = plan.results()
+    rows = plan.completed_rows(0, m)
+    cpu, gpu = grid.arrays()
+    rc, i2, s2, l2, n2 = port.select_caps(rows, cpu, gpu, 0.1)
+    np.testing.assert_array_equal(idx, i2)
+    np.testing.assert_array_equal(sav, s2)
+    np.testing.assert_array_equal(loss, l2)
+    np.testing.assert_array_equal(nc, n2)
+
+
+def test_als_end_to_end_decisions_match_oracle_where_margin_allows(ctx, port):
+    from oracle import bind
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(2000, 16, 16, 0.05, 2, seed=9)
+    hyp = AlsHyper(rank=16, lam=0.003, sweeps=8, seed=2)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+    plan.run()
+    idx, sav, loss, nc = plan.results()
+    Uo, Vo = bind.als_fit(port, A.m, A.n, A.row_ptr, A.col, A.val, 16, 0.003, 8, 2)
+    rows_o = bind.als_completed_rows(Uo, Vo, A.row_ptr, A.col, A.val, np.arange(A.m))
+    cpu, gpu = grid.arrays()
+    rc, io_, so, lo, no = port.select_caps(rows_o, cpu, gpu, 0.05)
+    # margin: relative gap between the best and the runner-up valid saving, and
+    # the distance of any cell from the validity threshold
+    E = cpu[-1] + gpu[-1]
+    caps = np.add.outer(cpu, gpu).ravel().astype(np.float64)
+    sav_all = (E - caps[None, :] / rows_o) / E
+    loss_all = 1.0 - rows_o / rows_o[:, -1:]
+    valid = loss_all <= 0.05
+    s_sorted = np.sort(np.where(valid, sav_all, -np.inf), axis=1)
+    gap = s_sorted[:, -1] - s_sorted[:, -2]
+    thr_gap = np.min(np.abs(loss_all - 0.05), axis=1)
+    tol = 4 * PRED_RTOL
+    safe = (gap > tol) & (thr_gap > tol)
+    assert safe.mean() > 0.5
+    np.testing.assert_array_equal(idx[safe], io_[safe])
+    agree = (idx == io_).mean()
+    assert agree > 0.9, agree
