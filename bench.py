@@ -222,7 +222,111 @@ def workload_c0xn(args, d: Dist):
     return out, ("c0xn", per_gpu)
 
 
-WORKLOADS = {"c0xn": workload_c0xn}
+JOINT = {  # SURVEY §8d joint configs
+    "c1": dict(m=10_000, grid=(16, 16), density=0.05, dense_rows=10, rank=8),
+    "c2": dict(m=1_000_000, grid=(64, 64), density=0.02, dense_rows=1000, rank=32),
+}
+
+
+def _joint_matrix(name, rank, world):
+    from paper_2508_07605_b200 import PowerGrid, synth
+
+    c = JOINT[name]
+    grid = PowerGrid.spanning(*c["grid"])
+    A = synth.joint_csr(c["m"], grid, c["density"], c["dense_rows"], seed=42)
+    return c, grid, A
+
+
+def workload_joint(args, d: Dist):
+    """ALS completion + fused imputation + Algorithm-2 selection of a joint matrix."""
+    import torch
+
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    cfg, grid, A = _joint_matrix(args.workload, d.rank, d.world)
+    m, n, nnz = A.m, grid.n, A.nnz
+    ctx = ocg.Context(d.local)
+    hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
+    # device-resident inputs (value) ...
+    dev = torch.device("cuda", d.local)
+    t_rp = torch.from_numpy(A.row_ptr).to(dev)
+    t_col = torch.from_numpy(A.col).to(dev)
+    t_val = torch.from_numpy(A.val).to(dev)
+    torch.cuda.synchronize(dev)
+    plan = AlsPlan(m, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, hyp, args.gamma, on_device=True,
+                   ctx=ctx)
+    for _ in range(args.warmup):
+        plan.run(timed=True)
+    d.barrier()
+    tot_ms, phases = 0.0, [0.0, 0.0, 0.0, 0.0]
+    with Clocks(d.local) as clk:
+        for _ in range(args.steps):
+            ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+            ms, ph = plan.run(timed=True)
+            tot_ms += ms
+            phases = [a + b for a, b in zip(phases, ph)]
+    d.barrier()
+    t_dev = d.max(tot_ms / 1e3)
+    idx, sav, loss, ncand = plan.results()
+    assert (idx >= 0).all() and (ncand >= 1).all()
+    plan.close()
+    del t_rp, t_col, t_val
+    # ... and end to end through the public API with host buffers
+    e2e_t = 0.0
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        p2 = AlsPlan(m, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+        p2.run(timed=False)
+        r2 = p2.results()
+        p2.close()
+        e2e_t += time.perf_counter() - t0
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_t = d.max(e2e_t / e2e_steps)
+    assert np.array_equal(r2[0], idx)
+    cells = m * n
+    k = cfg["rank"]
+    # roofline of the Gram kernels (K3, SURVEY §8d): per observation 8 B
+    # (index + value) + 4k B gathered factor row, per item 4k B factor out +
+    # 8 B row pointer.  Row and column half-sweeps launch once per sweep each.
+    row_bytes = nnz * (8 + 4 * k) + m * (4 * k + 8)
+    col_bytes = nnz * (8 + 4 * k) + n * (4 * k + 8)
+    row_ms = phases[1] / args.steps / args.sweeps
+    col_ms = phases[2] / args.steps / args.sweeps
+    dom = "row" if row_ms >= col_ms else "col"
+    bytes_l, ms_l = (row_bytes, row_ms) if dom == "row" else (col_bytes, col_ms)
+    achieved = bytes_l / (ms_l / 1e3) / 1e9
+    out = {
+        "metric": "CF-completed matrix cells/sec",
+        "value": cells * args.steps / t_dev,
+        "unit": "cells/s",
+        "selections_per_sec": m * args.steps / t_dev,
+        "ms_per_step": t_dev * 1e3 / args.steps,
+        "e2e": {"value": cells / e2e_t, "unit": "cells/s", "h2d_bytes_per_step": int(A.row_ptr.nbytes + A.col.nbytes +
+                                                                                      A.val.nbytes),
+                "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes),
+                "selections_per_sec": m / e2e_t},
+        "dtype": "f32 factors / f64 selection",
+        "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "observed": nnz,
+                   "density": nnz / (m * n), "offline_dense_rows": cfg["dense_rows"], "solver": "als",
+                   "sweeps": args.sweeps, "lambda": args.als_lambda, "gamma": args.gamma,
+                   "l2": "inputs (CSR %.0f MB) larger than L2, and L2 flushed before every timed step" %
+                         ((A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) / 1e6)},
+        "phases_ms_per_step": {"csc_build": phases[0] / args.steps, "row_half_sweeps": phases[1] / args.steps,
+                               "col_half_sweeps": phases[2] / args.steps, "impute_select": phases[3] / args.steps},
+        "scaling": "strong",
+        "gpu_launches": args.steps * (6 + 2 * args.sweeps + 2),
+        "roofline": {"bound": "hbm", "kernel": f"als_gram_solve ({dom} half-sweep)", "achieved": achieved,
+                     "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "frac": achieved / PEAKS["hbm_gbs"],
+                     "traffic": None,
+                     "bytes_def": "gather-counted: nnz*(8+4k) + items*(4k+8) per launch (SURVEY 8d K3)",
+                     "launch_ms": ms_l},
+        "clocks": clk.summary(),
+    }
+    return out, (args.workload, m)
+
+
+WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint}
 
 
 # -------------------------------------------------------- reference (CPU)
@@ -292,7 +396,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c0xn")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--sweeps", type=int, default=10, help="ALS sweeps per fit (c1/c2)")
+    ap.add_argument("--als-lambda", type=float, default=0.003)
+    ap.add_argument("--gamma", type=float, default=0.05)
     ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")
     ap.add_argument("--lane", type=int, default=1, help="c0xn: reference FP lane (0 scalar, 1 avx2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
