@@ -4,19 +4,27 @@
 // semantics are defined by oracle/ocg_oracle.c (ocgo_als_fit) — weighted-
 // lambda ALS, u_i = (sum_j v_j v_j^T + lambda n_i I)^-1 sum_j r_ij v_j.
 //
-// als_gram_solve_kernel: one ITEM (a row for the row half-sweep, a column for
-// the column half-sweep) is owned by WPI warps.  Each warp streams 32
-// observations at a time: the (index, value) pairs are read coalesced, the 32
-// gathered factor rows (K floats each, 128 B at K=32) are staged in shared
-// memory, and every lane accumulates a (K/8) x (K/4) block of the K x K Gram
-// in registers (all loads are conflict-free 16-byte LDS within one staged
-// row).  The WPI partial Grams are reduced in a fixed order in shared memory
-// (deterministic), lambda*n is added to the diagonal, and one warp factors
-// the system with a register-resident right-looking Cholesky (lane l owns row
-// l) followed by forward/back substitution.  MODE_GRAM instead writes the
-// reduced Gram + rhs to global memory (multi-GPU: allreduced over ranks, then
-// als_solve_from_gram_kernel).
+// Work unit = SEGMENT: at most kSeg consecutive observations of one ITEM (a
+// row for the row half-sweep, a column for the column half-sweep).  Segments
+// make the work uniform: C2's plan columns hold ~1M observations and its dense
+// rows 4096, against ~80 for a typical row.
+//
+// als_seg_gram_kernel: one warp per segment.  The warp streams its
+// observations 32 at a time: (index, value) pairs are read coalesced, the 32
+// gathered factor rows (K floats, 128 B at K=32) are copied global->shared
+// with cp.async into a double-buffered stage (the next chunk's gathers are in
+// flight while the current chunk is accumulated), and every lane accumulates
+// a (K/8) x (K/4) block of the K x K Gram in registers (conflict-free 16-byte
+// LDS inside one staged row).  A single-segment item is solved right there
+// (fused K3+K4); otherwise the partial Gram + rhs goes to a slot in a global
+// buffer and als_reduce_solve_kernel sums the item's partials in segment order
+// (deterministic) and solves.  The solve is a compact left-looking Cholesky on
+// the Gram in shared memory (lane l owns row l) + forward/back substitution.
+// MODE 1 writes the reduced Gram + rhs + count instead of solving
+// (multi-GPU: allreduced over ranks, then als_solve_from_gram_kernel).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "als.h"
 #include "ocg_common.cuh"
@@ -27,213 +35,281 @@ namespace {
 
 template <int K>
 struct GramShape {
-    static constexpr int RB = K / 8;  // rows per lane block
-    static constexpr int CB = K / 4;  // cols per lane block
-    static constexpr int GS = K + 1;  // padded Gram row stride (floats)
-    static constexpr int TS = K + 4;  // staged-row stride (floats), keeps 16-byte alignment
+    static constexpr int RB = K / 8;           // rows per lane block
+    static constexpr int CB = K / 4;           // cols per lane block
+    static constexpr int GS = K + 4;           // Gram row stride (floats): 16-byte rows
+    static constexpr int TS = K;               // staged-row stride (floats): conflict-free as is
+    static constexpr int GSZ = K * K + K + 1;  // global Gram record: K*K, rhs K, count
 };
 
-// Cholesky-solve A x = b on one warp; lane l < K owns row l of A (in smem G,
-// row stride GS) and b_l.  Returns x_l.  A is overwritten with L.
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Solve (G + diag_add I) x = b on one warp.  G: K x GS shared (full
+// symmetric); lane l < K holds b_l; returns x_l.  G's lower triangle is
+// overwritten with L.  Left-looking: column c needs only finished columns,
+// so the code stays compact (no fully unrolled K x K update).
 template <int K>
-__device__ __forceinline__ float chol_solve_warp(float* G, float* colb, float b, float diag_add, int lane) {
+__device__ __noinline__ float chol_solve_warp(float* G, float b, float diag_add, int lane) {
     constexpr int GS = GramShape<K>::GS;
-    float a[K];
-#pragma unroll
-    for (int m = 0; m < K; ++m) a[m] = lane < K ? G[lane * GS + m] : 0.0f;
-    if (lane < K) a[lane] += diag_add;
-    // right-looking factorisation, column c per step
-#pragma unroll
+    float* Gl = G + lane * GS;
+    if (lane < K) Gl[lane] += diag_add;
+    __syncwarp();
     for (int c = 0; c < K; ++c) {
-        if (lane == c) {
-            a[c] = sqrtf(a[c]);
-            colb[c] = a[c];
+        const float* Gc = G + c * GS;
+        float s = (lane >= c && lane < K) ? Gl[c] : 0.0f;
+        int q = 0;
+        for (; q + 4 <= c; q += 4) {
+            const float4 a = *reinterpret_cast<const float4*>(Gl + q);
+            const float4 w = *reinterpret_cast<const float4*>(Gc + q);
+            s = fmaf(-a.x, w.x, s);
+            s = fmaf(-a.y, w.y, s);
+            s = fmaf(-a.z, w.z, s);
+            s = fmaf(-a.w, w.w, s);
         }
+        for (; q < c; ++q) s = fmaf(-Gl[q], Gc[q], s);
+        if (lane == c) G[c * GS + c] = sqrtf(s);
         __syncwarp();
-        const float d = colb[c];
-        if (lane > c && lane < K) {
-            a[c] = a[c] / d;
-            colb[lane] = a[c];
-        }
-        __syncwarp();
-        if (lane > c && lane < K) {
-#pragma unroll
-            for (int m = c + 1; m < K; ++m)
-                if (m <= lane) a[m] = fmaf(-a[c], colb[m], a[m]);
-        }
+        if (lane > c && lane < K) Gl[c] = s / Gc[c];
         __syncwarp();
     }
     // L y = b
     float y = b;
-#pragma unroll
     for (int c = 0; c < K; ++c) {
-        if (lane == c) {
-            y = y / a[c];
-            colb[c] = y;
-        }
-        __syncwarp();
-        const float yc = colb[c];
-        if (lane > c && lane < K) y = fmaf(-a[c], yc, y);
-        __syncwarp();
+        if (lane == c) y = y / Gl[c];
+        const float yc = __shfl_sync(0xffffffffu, y, c);
+        if (lane > c && lane < K) y = fmaf(-Gl[c], yc, y);
     }
-    // L^T x = y : needs L[c][l] -> stage L in G
-    if (lane < K) {
-#pragma unroll
-        for (int m = 0; m < K; ++m)
-            if (m <= lane) G[lane * GS + m] = a[m];
-    }
-    __syncwarp();
-#pragma unroll
+    // L^T x = y
     for (int c = K - 1; c >= 0; --c) {
-        if (lane == c) {
-            y = y / a[c];
-            colb[c] = y;
-        }
-        __syncwarp();
-        const float xc = colb[c];
+        if (lane == c) y = y / Gl[c];
+        const float xc = __shfl_sync(0xffffffffu, y, c);
         if (lane < c) y = fmaf(-G[c * GS + lane], xc, y);
-        __syncwarp();
     }
     return y;
 }
 
-// Accumulate one warp's share of an item's Gram (register blocks) and rhs.
-template <int K>
-__device__ __forceinline__ void gram_accumulate(const int32_t* __restrict__ idx, const float* __restrict__ val,
-                                                int64_t beg, int64_t end, int64_t step_chunks, int64_t first_chunk,
-                                                const float* __restrict__ Y, float* stage, float* rstage,
-                                                float (&acc)[GramShape<K>::RB][GramShape<K>::CB], float& bacc,
-                                                int lane) {
-    constexpr int RB = GramShape<K>::RB, CB = GramShape<K>::CB, TS = GramShape<K>::TS;
-    constexpr int PER = 32 / K > 0 ? 32 / K : 1;  // observations loaded per instruction
-    const int bi = lane >> 2, bj = lane & 3;
-    for (int64_t base = beg + first_chunk * 32; base < end; base += step_chunks * 32) {
-        const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
-        int j = 0;
-        float r = 0.0f;
-        if (lane < cnt) {
-            j = __ldg(idx + base + lane);
-            r = __ldg(val + base + lane);
+template <int N>
+__device__ __forceinline__ void load_vec(float (&dst)[N], const float* src) {
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < N; q += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(src + q);
+            dst[q] = v.x;
+            dst[q + 1] = v.y;
+            dst[q + 2] = v.z;
+            dst[q + 3] = v.w;
         }
-        rstage[lane] = r;
-        // gather the cnt factor rows into the stage (coalesced K-float rows)
-#pragma unroll 8
-        for (int o0 = 0; o0 < 32; o0 += PER) {
-            const int o = o0 + lane / K;
-            const int f = lane % K;
-            const int jo = __shfl_sync(0xffffffffu, j, o);
-            if (o < cnt) stage[o * TS + f] = __ldg(Y + static_cast<int64_t>(jo) * K + f);
-        }
-        __syncwarp();
-        for (int o = 0; o < cnt; ++o) {
-            const float* row = stage + o * TS;
-            float x[RB], yv[CB];
+    } else {
 #pragma unroll
-            for (int q = 0; q < RB; ++q) x[q] = row[bi * RB + q];
-#pragma unroll
-            for (int q = 0; q < CB; ++q) yv[q] = row[bj * CB + q];
-#pragma unroll
-            for (int p = 0; p < RB; ++p)
-#pragma unroll
-                for (int q = 0; q < CB; ++q) acc[p][q] = fmaf(x[p], yv[q], acc[p][q]);
-            if (lane < K) bacc = fmaf(rstage[o], row[lane], bacc);
-        }
-        __syncwarp();
+        for (int q = 0; q < N; ++q) dst[q] = src[q];
     }
 }
 
 }  // namespace
 
-template <int K, int WPI, int MODE>
-__global__ void __launch_bounds__(256) als_gram_solve_kernel(int64_t nitems, const int64_t* __restrict__ ptr,
-                                                             const int32_t* __restrict__ idx,
-                                                             const float* __restrict__ val,
-                                                             const float* __restrict__ Y, float* __restrict__ X,
-                                                             float* __restrict__ Gout, float lambda) {
+// Segment table of one CSR-like side: item i with cnt observations owns
+// nseg = max(1, ceil(cnt / kSeg)) consecutive segments from seg_first[i]
+// (exclusive prefix sum of nseg, computed with cub on the host side).
+// nmulti[i] = nseg[i] if the item needs partial Grams (nseg > 1), else 0; its
+// exclusive prefix sum pfirst[] places an item's partials contiguously.
+__global__ void seg_count_kernel(int64_t nitems, const int64_t* __restrict__ ptr, int32_t* __restrict__ nseg,
+                                 int32_t* __restrict__ nmulti, int force_partials) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nitems) return;
+    const int64_t cnt = ptr[i + 1] - ptr[i];
+    const int32_t ns = cnt == 0 ? 1 : static_cast<int32_t>((cnt + kSeg - 1) / kSeg);
+    nseg[i] = ns;
+    nmulti[i] = (ns > 1 || force_partials) ? ns : 0;
+}
+
+__global__ void seg_fill_kernel(int64_t nitems, const int64_t* __restrict__ ptr, const int32_t* __restrict__ nseg,
+                                const int32_t* __restrict__ first, int32_t* __restrict__ seg_item,
+                                int64_t* __restrict__ seg_beg, int32_t* __restrict__ total) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nitems) return;
+    const int32_t f = first[i];
+    if (i == nitems - 1) *total = f + nseg[i];
+    for (int32_t s = 0; s < nseg[i]; ++s) {
+        seg_item[f + s] = static_cast<int32_t>(i);
+        seg_beg[f + s] = ptr[i] + static_cast<int64_t>(s) * kSeg;
+    }
+}
+
+// MODE 0: fused solve of single-segment items, partials for the rest.
+// MODE 1: partials for every segment (multi-GPU column side).
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) als_seg_gram_kernel(const int32_t* __restrict__ total_segs,
+                                                           const int32_t* __restrict__ seg_item,
+                                                           const int64_t* __restrict__ seg_beg,
+                                                           const int32_t* __restrict__ nseg_of,
+                                                           const int32_t* __restrict__ first,
+                                                           const int32_t* __restrict__ pfirst,
+                                                           const int64_t* __restrict__ ptr,
+                                                           const int32_t* __restrict__ idx,
+                                                           const float* __restrict__ val,
+                                                           const float* __restrict__ Y, float* __restrict__ X,
+                                                           float* __restrict__ partial, float lambda) {
     constexpr int RB = GramShape<K>::RB, CB = GramShape<K>::CB, GS = GramShape<K>::GS, TS = GramShape<K>::TS;
-    constexpr int WARPS = 8;
-    constexpr int ITEMS_PER_CTA = WARPS / WPI;
-    static_assert(32 * TS >= K * GS, "Gram aliases the item's first stage buffer");
-    __shared__ __align__(16) float stage_all[WARPS][32 * TS];
-    __shared__ float rstage_all[WARPS][32];
-    __shared__ float rhs_all[ITEMS_PER_CTA][WPI][K];
-    __shared__ float colb_all[ITEMS_PER_CTA][K];
+    constexpr int GSZ = GramShape<K>::GSZ;
+    constexpr int PER = 32 / K;  // observations gathered per cp.async instruction
+    static_assert(K * GS <= 2 * 32 * TS, "Gram aliases the double stage");
+    extern __shared__ __align__(16) float dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = warp / WPI, sub = warp % WPI;
-    float* stage = stage_all[warp];
-    float* rstage = rstage_all[warp];
-    float* G = stage_all[slot * WPI];  // free once the item's sub-0 warp finished accumulating
-    float* colb = colb_all[slot];
+    float* stage = dyn + warp * (2 * 32 * TS + 64);  // [2][32][TS] + rstage[2][32]
+    float* rstage = stage + 2 * 32 * TS;
     const int bi = lane >> 2, bj = lane & 3;
-    for (int64_t item0 = static_cast<int64_t>(blockIdx.x) * ITEMS_PER_CTA; item0 < nitems;
-         item0 += static_cast<int64_t>(gridDim.x) * ITEMS_PER_CTA) {
-        const int64_t item = item0 + slot;
-        const bool live = item < nitems;
-        const int64_t beg = live ? ptr[item] : 0, end = live ? ptr[item + 1] : 0;
+    const int f = lane % K, osub = lane / K;
+    const int32_t nsegs = *total_segs;
+    for (int32_t sg = blockIdx.x * 8 + warp; sg < nsegs; sg += gridDim.x * 8) {
+        const int32_t item = seg_item[sg];
+        const int64_t beg = seg_beg[sg];
+        const int64_t iend = ptr[item + 1];
+        const int64_t end = beg + kSeg < iend ? beg + kSeg : iend;
         float acc[RB][CB];
 #pragma unroll
         for (int p = 0; p < RB; ++p)
 #pragma unroll
             for (int q = 0; q < CB; ++q) acc[p][q] = 0.0f;
         float bacc = 0.0f;
-        if (live) gram_accumulate<K>(idx, val, beg, end, WPI, sub, Y, stage, rstage, acc, bacc, lane);
-        // deterministic reduction of the WPI partial Grams: sub 0 writes, others add in order
-        for (int s = 0; s < WPI; ++s) {
-            if (sub == s && live) {
+        // chunk pipeline: the gathers of chunk t+1 are issued before chunk t is accumulated
+        auto issue = [&](int64_t base, int buf) {
+            const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
+            int j = 0;
+            float r = 0.0f;
+            if (lane < cnt) {
+                j = __ldg(idx + base + lane);
+                r = __ldg(val + base + lane);
+            }
+            rstage[buf * 32 + lane] = r;
+            float* st = stage + buf * 32 * TS;
+#pragma unroll
+            for (int t = 0; t < 32 / PER; ++t) {
+                const int o = t * PER + osub;
+                const int jo = __shfl_sync(0xffffffffu, j, o);
+                if (o < cnt) cp_async4(st + o * TS + f, Y + static_cast<int64_t>(jo) * K + f);
+            }
+            cp_async_commit();
+        };
+        int buf = 0;
+        if (beg < end) issue(beg, 0);
+        for (int64_t base = beg; base < end; base += 32) {
+            const int cnt = static_cast<int>(end - base < 32 ? end - base : 32);
+            if (base + 32 < end) {
+                issue(base + 32, buf ^ 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncwarp();
+            const float* st = stage + buf * 32 * TS;
+            const float* rs = rstage + buf * 32;
+            for (int o = 0; o < cnt; ++o) {
+                const float* row = st + o * TS;
+                float xv[RB], yv[CB];
+                load_vec(xv, row + bi * RB);
+                load_vec(yv, row + bj * CB);
 #pragma unroll
                 for (int p = 0; p < RB; ++p)
 #pragma unroll
-                    for (int q = 0; q < CB; ++q) {
-                        float* g = G + (bi * RB + p) * GS + bj * CB + q;
-                        *g = s == 0 ? acc[p][q] : *g + acc[p][q];
-                    }
-                if (lane < K) rhs_all[slot][s][lane] = bacc;
+                    for (int q = 0; q < CB; ++q) acc[p][q] = fmaf(xv[p], yv[q], acc[p][q]);
+                if (lane < K) bacc = fmaf(rs[o], row[lane], bacc);
             }
-            if (WPI > 1) __syncthreads();
-            else __syncwarp();
+            __syncwarp();
+            buf ^= 1;
         }
-        if (sub == 0 && live) {
-            float b = 0.0f;
-            if (lane < K)
-                for (int s = 0; s < WPI; ++s) b += rhs_all[slot][s][lane];
-            const int64_t cnt = end - beg;
-            if (MODE == 1) {  // write Gram + rhs for the cross-rank allreduce
-                float* out = Gout + item * (K * K + K);
-                for (int e = lane; e < K * K; e += 32) out[e] = G[(e / K) * GS + (e % K)];
-                if (lane < K) out[K * K + lane] = b;
-            } else if (cnt == 0) {
-                if (lane < K) X[item * K + lane] = 0.0f;
+        const bool single = MODE == 0 && nseg_of[item] == 1;
+        if (single) {
+            // Gram -> shared (aliases the drained stage), solve, write the factor
+            float* G = stage;
+#pragma unroll
+            for (int p = 0; p < RB; ++p)
+#pragma unroll
+                for (int q = 0; q < CB; ++q) G[(bi * RB + p) * GS + bj * CB + q] = acc[p][q];
+            __syncwarp();
+            const int64_t cnt = iend - ptr[item];
+            if (cnt == 0) {
+                if (lane < K) X[static_cast<int64_t>(item) * K + lane] = 0.0f;
             } else {
-                const float x = chol_solve_warp<K>(G, colb, b, lambda * static_cast<float>(cnt), lane);
-                if (lane < K) X[item * K + lane] = x;
+                const float x = chol_solve_warp<K>(G, bacc, lambda * static_cast<float>(cnt), lane);
+                if (lane < K) X[static_cast<int64_t>(item) * K + lane] = x;
             }
+            __syncwarp();
+        } else {
+            float* out = partial + static_cast<int64_t>(pfirst[item] + (sg - first[item])) * GSZ;
+#pragma unroll
+            for (int p = 0; p < RB; ++p)
+#pragma unroll
+                for (int q = 0; q < CB; ++q) out[(bi * RB + p) * K + bj * CB + q] = acc[p][q];
+            if (lane < K) out[K * K + lane] = bacc;
         }
-        if (WPI > 1) __syncthreads();
-        else __syncwarp();
     }
 }
 
-// Solve from a (possibly allreduced) Gram + rhs buffer; cnt per item from ptr.
+// Sum an item's segment partials in segment order; MODE 0 solves, MODE 1
+// writes the reduced record (Gram, rhs, count) to Gout[item].
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) als_reduce_solve_kernel(int64_t nitems, const int64_t* __restrict__ ptr,
+                                                               const int32_t* __restrict__ nseg_of,
+                                                               const int32_t* __restrict__ first,
+                                                               const float* __restrict__ partial,
+                                                               float* __restrict__ X, float* __restrict__ Gout,
+                                                               float lambda) {
+    constexpr int GS = GramShape<K>::GS, GSZ = GramShape<K>::GSZ;
+    __shared__ __align__(16) float G[K * GS];
+    __shared__ float rhs[K];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int32_t ns = nseg_of[item];
+        if (MODE == 0 && ns == 1) continue;  // solved by the segment kernel
+        const float* base = partial + static_cast<int64_t>(first[item]) * GSZ;  // first = pfirst here
+        for (int e = tid; e < K * K + K; e += 256) {
+            float s = 0.0f;
+            for (int32_t q = 0; q < ns; ++q) s += base[static_cast<int64_t>(q) * GSZ + e];
+            if (e < K * K) G[(e / K) * GS + (e % K)] = s;
+            else rhs[e - K * K] = s;
+        }
+        __syncthreads();
+        const int64_t cnt = ptr[item + 1] - ptr[item];
+        if (MODE == 1) {
+            float* out = Gout + item * GSZ;
+            for (int e = tid; e < K * K; e += 256) out[e] = G[(e / K) * GS + (e % K)];
+            if (tid < K) out[K * K + tid] = rhs[tid];
+            if (tid == 0) out[K * K + K] = static_cast<float>(cnt);
+        } else if (tid < 32) {
+            const float x = chol_solve_warp<K>(G, lane < K ? rhs[lane] : 0.0f, lambda * static_cast<float>(cnt), lane);
+            if (lane < K) X[item * K + lane] = x;
+        }
+        __syncthreads();
+    }
+}
+
+// Solve from a (possibly allreduced) Gram record buffer (count in the record).
 template <int K>
-__global__ void __launch_bounds__(256) als_solve_from_gram_kernel(int64_t nitems, const int64_t* __restrict__ counts,
-                                                                  const float* __restrict__ Gin, float* __restrict__ X,
-                                                                  float lambda) {
-    constexpr int GS = GramShape<K>::GS;
-    __shared__ float gram_all[8][K * GS];
-    __shared__ float colb_all[8][K];
+__global__ void __launch_bounds__(256) als_solve_from_gram_kernel(int64_t nitems, const float* __restrict__ Gin,
+                                                                  float* __restrict__ X, float lambda) {
+    constexpr int GS = GramShape<K>::GS, GSZ = GramShape<K>::GSZ;
+    __shared__ __align__(16) float gram_all[8][K * GS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + warp; item < nitems;
          item += static_cast<int64_t>(gridDim.x) * 8) {
-        const float* in = Gin + item * (K * K + K);
+        const float* in = Gin + item * GSZ;
         float* G = gram_all[warp];
         for (int e = lane; e < K * K; e += 32) G[(e / K) * GS + (e % K)] = in[e];
         const float b = lane < K ? in[K * K + lane] : 0.0f;
+        const float cnt = in[K * K + K];
         __syncwarp();
-        const int64_t cnt = counts[item];
-        if (cnt == 0) {
+        if (cnt == 0.0f) {
             if (lane < K) X[item * K + lane] = 0.0f;
         } else {
-            const float x = chol_solve_warp<K>(G, colb_all[warp], b, lambda * static_cast<float>(cnt), lane);
+            const float x = chol_solve_warp<K>(G, b, lambda * cnt, lane);
             if (lane < K) X[item * K + lane] = x;
         }
         __syncwarp();
@@ -287,45 +363,68 @@ cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStrea
     return cudaGetLastError();
 }
 
-template <int K>
-static cudaError_t launch_gs(int64_t nitems, const int64_t* ptr, const int32_t* idx, const float* val,
-                             const float* Y, float* X, float* Gout, float lambda, int wpi, int mode, int sm_count,
+cudaError_t launch_seg_count(int64_t nitems, const int64_t* ptr, int32_t* nseg, int32_t* nmulti, int force_partials,
                              cudaStream_t s) {
-    const int per_cta = 8 / wpi;
-    int64_t blocks = (nitems + per_cta - 1) / per_cta;
-    const int64_t cap = static_cast<int64_t>(sm_count) * 16;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    const unsigned b = static_cast<unsigned>(blocks);
-    if (wpi == 1 && mode == 0) als_gram_solve_kernel<K, 1, 0><<<b, 256, 0, s>>>(nitems, ptr, idx, val, Y, X, Gout, lambda);
-    else if (wpi == 8 && mode == 0) als_gram_solve_kernel<K, 8, 0><<<b, 256, 0, s>>>(nitems, ptr, idx, val, Y, X, Gout, lambda);
-    else if (wpi == 1 && mode == 1) als_gram_solve_kernel<K, 1, 1><<<b, 256, 0, s>>>(nitems, ptr, idx, val, Y, X, Gout, lambda);
-    else if (wpi == 8 && mode == 1) als_gram_solve_kernel<K, 8, 1><<<b, 256, 0, s>>>(nitems, ptr, idx, val, Y, X, Gout, lambda);
-    else return cudaErrorInvalidValue;
+    seg_count_kernel<<<static_cast<unsigned>((nitems + 255) / 256), 256, 0, s>>>(nitems, ptr, nseg, nmulti,
+                                                                                  force_partials);
     return cudaGetLastError();
 }
 
-cudaError_t launch_als_gram_solve(int k, int64_t nitems, const int64_t* ptr, const int32_t* idx, const float* val,
-                                  const float* Y, float* X, float* Gout, float lambda, int wpi, int mode,
-                                  int sm_count, cudaStream_t s) {
+cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* nseg, const int32_t* first,
+                            int32_t* seg_item, int64_t* seg_beg, int32_t* total, cudaStream_t s) {
+    seg_fill_kernel<<<static_cast<unsigned>((nitems + 255) / 256), 256, 0, s>>>(nitems, ptr, nseg, first, seg_item,
+                                                                                 seg_beg, total);
+    return cudaGetLastError();
+}
+
+size_t als_gram_record_floats(int k) { return static_cast<size_t>(k) * k + k + 1; }
+
+template <int K>
+static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+    constexpr int TS = GramShape<K>::TS;
+    const size_t smem = sizeof(float) * 8 * (2 * 32 * TS + 64);
+    int64_t blocks = (h.max_segs + 7) / 8;
+    const int64_t cap = static_cast<int64_t>(sm_count) * 32;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 8)));
+    if (mode == 0) {
+        cudaFuncSetAttribute(als_seg_gram_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        als_seg_gram_kernel<K, 0><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X, h.partial,
+            h.lambda);
+        als_reduce_solve_kernel<K, 0><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.pfirst, h.partial, h.X,
+                                                                 nullptr, h.lambda);
+    } else {
+        cudaFuncSetAttribute(als_seg_gram_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X, h.partial,
+            h.lambda);
+        als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.pfirst, h.partial, nullptr,
+                                                             h.gram_out, h.lambda);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
     switch (k) {
-        case 8: return launch_gs<8>(nitems, ptr, idx, val, Y, X, Gout, lambda, wpi, mode, sm_count, s);
-        case 16: return launch_gs<16>(nitems, ptr, idx, val, Y, X, Gout, lambda, wpi, mode, sm_count, s);
-        case 32: return launch_gs<32>(nitems, ptr, idx, val, Y, X, Gout, lambda, wpi, mode, sm_count, s);
+        case 8: return launch_half_k<8>(h, mode, sm_count, s);
+        case 16: return launch_half_k<16>(h, mode, sm_count, s);
+        case 32: return launch_half_k<32>(h, mode, sm_count, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const int64_t* counts, const float* G, float* X,
-                                       float lambda, int sm_count, cudaStream_t s) {
+cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
+                                       cudaStream_t s) {
     int64_t blocks = (nitems + 7) / 8;
     if (blocks > sm_count * 16) blocks = sm_count * 16;
     if (blocks < 1) blocks = 1;
     const unsigned b = static_cast<unsigned>(blocks);
     switch (k) {
-        case 8: als_solve_from_gram_kernel<8><<<b, 256, 0, s>>>(nitems, counts, G, X, lambda); break;
-        case 16: als_solve_from_gram_kernel<16><<<b, 256, 0, s>>>(nitems, counts, G, X, lambda); break;
-        case 32: als_solve_from_gram_kernel<32><<<b, 256, 0, s>>>(nitems, counts, G, X, lambda); break;
+        case 8: als_solve_from_gram_kernel<8><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
+        case 16: als_solve_from_gram_kernel<16><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
+        case 32: als_solve_from_gram_kernel<32><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -6,13 +6,38 @@
 
 namespace ocg {
 
+constexpr int kSeg = 1024;  // observations per ALS work segment
+
+// One half-sweep: solve X (items x K) from Y given the item-major sparse matrix
+struct AlsHalf {
+    int64_t nitems;
+    int32_t max_segs;           // host upper bound (grid sizing)
+    const int32_t* total_segs;  // device scalar: actual segment count
+    const int64_t* ptr;
+    const int32_t* idx;
+    const float* val;
+    const int32_t* seg_item;
+    const int64_t* seg_beg;
+    const int32_t* nseg;   // per item
+    const int32_t* first;   // per item: first segment
+    const int32_t* pfirst;  // per item: first partial-Gram slot (items with >1 segment)
+    const float* Y;
+    float* X;
+    float* partial;   // partial-Gram slots x (K*K + K + 1)
+    float* gram_out;  // mode 1: nitems x (K*K + K + 1)
+    float lambda;
+};
+
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);
-// mode 0: solve items in place (X); mode 1: write reduced Gram+rhs to Gout
-cudaError_t launch_als_gram_solve(int k, int64_t nitems, const int64_t* ptr, const int32_t* idx, const float* val,
-                                  const float* Y, float* X, float* Gout, float lambda, int wpi, int mode,
-                                  int sm_count, cudaStream_t s);
-cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const int64_t* counts, const float* G, float* X,
-                                       float lambda, int sm_count, cudaStream_t s);
+cudaError_t launch_seg_count(int64_t nitems, const int64_t* ptr, int32_t* nseg, int32_t* nmulti, int force_partials,
+                             cudaStream_t s);
+cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* nseg, const int32_t* first,
+                            int32_t* seg_item, int64_t* seg_beg, int32_t* total, cudaStream_t s);
+size_t als_gram_record_floats(int k);
+// mode 0: solve in place; mode 1: write reduced Gram records to gram_out
+cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
+cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
+                                       cudaStream_t s);
 cudaError_t launch_expand_rows(int64_t m, const int64_t* ptr, int32_t* rowid, int sm_count, cudaStream_t s);
 cudaError_t launch_gather_csc(int64_t nnz, const int32_t* perm, const int32_t* rowid, const float* val, int32_t* crow,
                               float* cval, cudaStream_t s);

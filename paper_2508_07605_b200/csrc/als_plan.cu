@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstring>
@@ -71,6 +72,15 @@ struct ocg_als_plan {
     Buf<float> cval;
     Buf<uint8_t> sort_tmp;
     size_t sort_tmp_bytes = 0;
+    // segment tables (index 0: rows over CSR, 1: columns over CSC)
+    struct Side {
+        Buf<int32_t> nseg, first, nmulti, pfirst, seg_item, total;
+        Buf<int64_t> seg_beg;
+        Buf<float> partial;
+        int32_t max_segs = 0;
+    } side[2];
+    Buf<uint8_t> scan_tmp;
+    size_t scan_tmp_bytes = 0;
     // factors + outputs
     Buf<float> U, V, Vt;
     Buf<int32_t> cpu, gpu, idx, ncand;
@@ -95,7 +105,40 @@ static int als_build_csc(ocg_als_plan* P) {
         ALS_CUDA(ocg::launch_gather_csc(P->nnz, P->perm_out.p, P->rowid.p, P->val.p, P->crow.p, P->cval.p, s));
     }
     ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
+    for (int sd = 0; sd < 2; ++sd) {
+        auto& S = P->side[sd];
+        const int64_t items = sd == 0 ? P->m : P->n;
+        const int64_t* ptr = sd == 0 ? P->row_ptr.p : P->col_ptr.p;
+        ALS_CUDA(ocg::launch_seg_count(items, ptr, S.nseg.p, S.nmulti.p, 0, s));
+        size_t b = P->scan_tmp_bytes;
+        ALS_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, b, S.nseg.p, S.first.p, items, s));
+        b = P->scan_tmp_bytes;
+        ALS_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, b, S.nmulti.p, S.pfirst.p, items, s));
+        ALS_CUDA(ocg::launch_seg_fill(items, ptr, S.nseg.p, S.first.p, S.seg_item.p, S.seg_beg.p, S.total.p, s));
+    }
     return OCG_OK;
+}
+
+static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
+    auto& S = P->side[sd];
+    ocg::AlsHalf h{};
+    h.nitems = sd == 0 ? P->m : P->n;
+    h.max_segs = S.max_segs;
+    h.total_segs = S.total.p;
+    h.ptr = sd == 0 ? P->row_ptr.p : P->col_ptr.p;
+    h.idx = sd == 0 ? P->col.p : P->crow.p;
+    h.val = sd == 0 ? P->val.p : P->cval.p;
+    h.seg_item = S.seg_item.p;
+    h.seg_beg = S.seg_beg.p;
+    h.nseg = S.nseg.p;
+    h.first = S.first.p;
+    h.pfirst = S.pfirst.p;
+    h.Y = sd == 0 ? P->V.p : P->U.p;
+    h.X = sd == 0 ? P->U.p : P->V.p;
+    h.partial = S.partial.p;
+    h.gram_out = nullptr;
+    h.lambda = P->lambda;
+    return h;
 }
 
 static int als_alloc(ocg_als_plan* P) {
@@ -111,6 +154,27 @@ static int als_alloc(ocg_als_plan* P) {
                                              P->nnz, 0, bits_for(P->n)));
     P->sort_tmp_bytes = bytes;
     ALS_CUDA(P->sort_tmp.alloc(bytes));
+    for (int sd = 0; sd < 2; ++sd) {
+        auto& S = P->side[sd];
+        const int64_t items = sd == 0 ? P->m : P->n;
+        const int64_t ms = items + P->nnz / ocg::kSeg + 1;
+        if (ms >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: too many segments");
+        S.max_segs = static_cast<int32_t>(ms);
+        ALS_CUDA(S.nseg.alloc(static_cast<size_t>(items)));
+        ALS_CUDA(S.first.alloc(static_cast<size_t>(items)));
+        ALS_CUDA(S.total.alloc(1));
+        ALS_CUDA(S.seg_item.alloc(static_cast<size_t>(ms)));
+        ALS_CUDA(S.seg_beg.alloc(static_cast<size_t>(ms)));
+        // partial Grams only for items with >1 segment: sum of their nseg <= 2*nnz/kSeg
+        const int64_t mp = std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
+        ALS_CUDA(S.nmulti.alloc(static_cast<size_t>(items)));
+        ALS_CUDA(S.pfirst.alloc(static_cast<size_t>(items)));
+        ALS_CUDA(S.partial.alloc(static_cast<size_t>(mp) * ocg::als_gram_record_floats(P->k)));
+        size_t b = 0;
+        ALS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, S.nseg.p, S.first.p, items));
+        P->scan_tmp_bytes = std::max(P->scan_tmp_bytes, b);
+    }
+    ALS_CUDA(P->scan_tmp.alloc(P->scan_tmp_bytes));
     ALS_CUDA(P->U.alloc(static_cast<size_t>(P->m * P->k)));
     ALS_CUDA(P->V.alloc(static_cast<size_t>(P->n * P->k)));
     ALS_CUDA(P->Vt.alloc(static_cast<size_t>(P->n * P->k)));
@@ -200,11 +264,9 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     float row_ms = 0.f, col_ms = 0.f;
     for (int it = 0; it < P->sweeps; ++it) {
         ALS_CUDA(cudaEventRecord(P->ev[2], s));
-        ALS_CUDA(ocg::launch_als_gram_solve(P->k, P->m, P->row_ptr.p, P->col.p, P->val.p, P->V.p, P->U.p, nullptr,
-                                            P->lambda, 1, 0, sm, s));
+        ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 0), 0, sm, s));
         ALS_CUDA(cudaEventRecord(P->ev[3], s));
-        ALS_CUDA(ocg::launch_als_gram_solve(P->k, P->n, P->col_ptr.p, P->crow.p, P->cval.p, P->U.p, P->V.p, nullptr,
-                                            P->lambda, 8, 0, sm, s));
+        ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 1), 0, sm, s));
         ALS_CUDA(cudaEventRecord(P->ev[4], s));
         if (phase_ms) {
             float a = 0, b = 0;
