@@ -59,7 +59,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int K>
 __device__ __noinline__ float chol_solve_warp(float* G, float b, float diag_add, int lane) {
     constexpr int GS = GramShape<K>::GS;
-    float* Gl = G + lane * GS;
+    float* Gl = G + (lane < K ? lane : K - 1) * GS;  // lanes >= K read a valid row, results unused
     if (lane < K) Gl[lane] += diag_add;
     __syncwarp();
     for (int c = 0; c < K; ++c) {
