@@ -353,7 +353,52 @@ def reference_c0xn(napps: int, threads: int, lane: int = 1):
     return secs, idx, sav, grid.n
 
 
+def reference_joint(workload: str, threads: int, nprob: int, max_epochs: int = 1, lane: int = 1):
+    """The reference's cf::complete + select_caps on row samples of the joint matrix.
+
+    Each problem = 1 dense row + (m_s - 1) rows taken at a stride through the
+    C1/C2 matrix (all n settings), completed by the reference's NCF with
+    app_dim = setting_dim = rank and max_epochs capped, then every row
+    selected.  Returns (cells/s, description)."""
+    import ctypes
+
+    from oracle import bind
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+
+    c = JOINT[workload]
+    grid = ocg.PowerGrid.spanning(*c["grid"])
+    m, n = c["m"], grid.n
+    m_s = 128 if n > 1024 else 256
+    vals = np.zeros((nprob, m_s, n))
+    mask = np.zeros((nprob, m_s, n), np.uint8)
+    stride = m // m_s
+    for p in range(nprob):
+        rows = np.concatenate([[p % c["dense_rows"]],
+                               (c["dense_rows"] + p * 7919 + np.arange(1, m_s) * stride) % (m - c["dense_rows"])
+                               + c["dense_rows"]])
+        vals[p], mask[p] = synth.joint_rows_dense(m, grid, c["density"], c["dense_rows"], rows, seed=42)
+    ref = bind.Ref()
+    ref.force_lane(lane)
+    h = bind._hyper(bind.RefHyper, app_dim=c["rank"], setting_dim=c["rank"], max_epochs=max_epochs)
+    seeds = np.arange(nprob, dtype=np.uint64) + 1
+    sel = np.zeros((nprob, m_s), np.int32)
+    cpu, gpu = grid.arrays()
+    secs = ref.L.ref_complete_select_batch(nprob, m_s, bind.P(cpu), len(cpu), bind.P(gpu), len(gpu), bind.P(vals),
+                                           bind.P(mask), ctypes.byref(h), bind.P(seeds), 0.05, threads, bind.P(sel))
+    assert (sel >= 0).all(), "reference sample failed"
+    desc = (f"{nprob} problems of {m_s} rows x {n} settings sampled from {workload} (1 dense + strided rows), "
+            f"reference cf::complete (NCF rank {c['rank']}, max_epochs={max_epochs}) + select_caps per row, "
+            f"AVX2 lane, {threads} threads. UPPER BOUND on the reference's {workload} rate: its fit runs to early "
+            f"stopping (hundreds of epochs) and its per-epoch cost grows with m (dense Adam over (m+n)k params)")
+    return nprob * m_s * n / secs, desc, secs
+
+
 def cpu_baseline(workload: str, threads: int):
+    if workload in JOINT:
+        v, desc, secs = reference_joint(workload, threads, nprob=2 * threads)
+        return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
+                "seconds": secs}
     if workload == "c0xn":
         napps = max(threads * 8, 16)
         secs, _, _, n = reference_c0xn(napps, threads)
@@ -384,6 +429,26 @@ def run_reference(args, d: Dist):
                 "config": {"workload": "c0xn", "apps_per_step": napps},
                 "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
                                  "sample": f"{napps} apps per step, cf::complete + select_caps, AVX2 lane"},
+                "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    if args.workload in JOINT:
+        for _ in range(args.warmup):
+            reference_joint(args.workload, threads, nprob=threads)
+        tot, vals = 0.0, []
+        for _ in range(args.steps):
+            v, desc, secs = reference_joint(args.workload, threads, nprob=2 * threads)
+            vals.append(v)
+            tot += secs
+        v = float(np.mean(vals))
+        line = {"impl": "reference", "metric": "CF-completed matrix cells/sec", "value": v, "unit": "cells/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8d generators, seed 42)",
+                "config": {"workload": args.workload, "apps": JOINT[args.workload]["m"],
+                           "rank": JOINT[args.workload]["rank"]},
+                "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
+                                 "sample": desc},
                 "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return

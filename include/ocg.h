@@ -213,6 +213,12 @@ int ocg_synth_csr_fill(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const i
                        double density, int64_t dense_rows, uint64_t seed, int nthreads, const int64_t* row_ptr,
                        int32_t* col, float* val32, double* val64);
 
+/* selected rows of the same joint matrix as dense values + mask (values as
+ * the FP32 CSR carries them, widened) — CPU-baseline samples */
+int ocg_synth_rows_dense(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                         double density, int64_t dense_rows, uint64_t seed, const int64_t* rows, int64_t nrows,
+                         double* values, uint8_t* mask);
+
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */
 double ocg_debug_exp_host(double x);                                       /* same code, host build */

@@ -217,6 +217,9 @@ class Ref:
         L.ref_online_batch.argtypes = [c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_sz, c_dbl, c_vp,
                                        ctypes.c_int, c_vp, c_vp]
         L.ref_force_lane.argtypes = [ctypes.c_int]
+        L.ref_complete_select_batch.restype = c_dbl
+        L.ref_complete_select_batch.argtypes = [c_sz, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_dbl,
+                                                ctypes.c_int, c_vp]
 
     def err(self):
         return self.L.ref_last_error().decode()

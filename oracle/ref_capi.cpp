@@ -435,4 +435,42 @@ double ref_online_batch(size_t d_rows, const int* cpu, size_t ncpu, const int* g
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// nprob independent joint problems (each m x n, dense values + mask): per
+// problem cf::complete (cfcomplete.cpp:198-213) then policy::select_caps on
+// every completed row.  Problems are spread over `threads` std::threads.
+// Returns wall seconds.
+double ref_complete_select_batch(size_t nprob, size_t m, const int* cpu, size_t ncpu, const int* gpu, size_t ngpu,
+                                 const double* values, const uint8_t* mask, const ref_ncf_hyper* h,
+                                 const uint64_t* seeds, double gamma, int threads, int32_t* sel_idx) {
+    const auto grid = make_grid(cpu, ncpu, gpu, ngpu);
+    const size_t n = grid.settings().size();
+    const auto hy = to_hyper(h);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    const int nt = std::max(1, threads);
+    for (int t = 0; t < nt; ++t) {
+        pool.emplace_back([&, t] {
+            for (size_t p = static_cast<size_t>(t); p < nprob; p += static_cast<size_t>(nt)) {
+                try {
+                    const auto pm = make_matrix(m, grid, values + p * m * n, mask + p * m * n);
+                    const auto done = cf::complete(pm, hy, seeds[p]);
+                    const policy::SelectionConfig cfg{grid, gamma};
+                    const auto settings = grid.settings();
+                    std::vector<double> row(n);
+                    for (size_t i = 0; i < m; ++i) {
+                        for (size_t j = 0; j < n; ++j) row[j] = done.value(i, j);
+                        const auto d = policy::select_caps(row, cfg);
+                        sel_idx[p * m + i] = static_cast<int32_t>(
+                            std::find(settings.begin(), settings.end(), d.setting) - settings.begin());
+                    }
+                } catch (...) {
+                    for (size_t i = 0; i < m; ++i) sel_idx[p * m + i] = -1;
+                }
+            }
+        });
+    }
+    for (auto& th : pool) th.join();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 }  // extern "C"

@@ -281,4 +281,28 @@ int ocg_synth_csr_fill(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_
     return OCG_OK;
 }
 
+// selected rows of the joint matrix as dense values + mask (nrows x n)
+int ocg_synth_rows_dense(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu, double density,
+                         int64_t dense_rows, uint64_t seed, const int64_t* rows, int64_t nrows, double* values,
+                         uint8_t* mask) {
+    const Grid g{cpu, ncpu, gpu, ngpu};
+    const auto specs = joint_specs(m, seed, g);
+    const auto plan = default_plan(g);
+    std::vector<uint8_t> in_plan(static_cast<size_t>(g.n()), 0);
+    for (auto j : plan) in_plan[j] = 1;
+    const double p = bernoulli_p(m, g.n(), density, dense_rows, static_cast<int64_t>(plan.size()));
+    const int64_t n = g.n();
+    std::memset(mask, 0, static_cast<size_t>(nrows * n));
+    std::memset(values, 0, sizeof(double) * static_cast<size_t>(nrows * n));
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = rows[r];
+        if (i < 0 || i >= m) return OCG_E_RANGE;
+        gen_row(i, dense_rows, g, in_plan, p, specs[i], seed, [&](int64_t j, double v) {
+            values[r * n + j] = static_cast<double>(static_cast<float>(v));  // as the FP32 CSR carries it
+            mask[r * n + j] = 1;
+        });
+    }
+    return OCG_OK;
+}
+
 }  // extern "C"

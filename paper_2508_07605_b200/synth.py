@@ -39,6 +39,21 @@ lib.ocg_synth_csr_fill.argtypes = [c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64
 lib.ocg_synth_csr_fill.restype = ctypes.c_int
 
 
+lib.ocg_synth_rows_dense.argtypes = [c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64, c_u64, c_vp, c_i64, c_vp, c_vp]
+lib.ocg_synth_rows_dense.restype = ctypes.c_int
+
+
+def joint_rows_dense(m: int, grid: PowerGrid, density: float, dense_rows: int, rows, seed: int = 42):
+    """Selected rows of joint_csr(...) as dense (values, mask)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cpu, gpu = grid.arrays()
+    vals = np.zeros((len(rows), grid.n))
+    mask = np.zeros((len(rows), grid.n), np.uint8)
+    check(lib.ocg_synth_rows_dense(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed, ptr(rows),
+                                   len(rows), ptr(vals), ptr(mask)))
+    return vals, mask
+
+
 def make_suite(counts, seed: int, role: int, grid: PowerGrid, noise_sigma=0.01, cpu_phase_fraction=0.0):
     cnt = np.asarray(counts, np.int32)
     out = (WorkloadSpecC * int(cnt.sum()))()
