@@ -230,99 +230,132 @@ JOINT = {  # SURVEY §8d joint configs
 
 def _joint_matrix(name, rank, world):
     from paper_2508_07605_b200 import PowerGrid, synth
+    from paper_2508_07605_b200.dist import shard_rows
 
     c = JOINT[name]
     grid = PowerGrid.spanning(*c["grid"])
-    A = synth.joint_csr(c["m"], grid, c["density"], c["dense_rows"], seed=42)
+    r0, r1 = shard_rows(c["m"], world, rank)
+    A = synth.joint_csr(c["m"], grid, c["density"], c["dense_rows"], seed=42, rows=(r0, r1))
     return c, grid, A
 
 
 def workload_joint(args, d: Dist):
-    """ALS completion + fused imputation + Algorithm-2 selection of a joint matrix."""
+    """ALS completion + fused imputation + Algorithm-2 selection of a joint matrix.
+    N=1: the fused single-GPU plan; N>1: rows sharded over ranks, column Gram
+    records allreduced with NCCL each column half-sweep (paper_2508_07605_b200.dist)."""
     import torch
 
     import paper_2508_07605_b200 as ocg
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+    from paper_2508_07605_b200.dist import GpuAlsBackend, ShardedAlsDriver
 
     cfg, grid, A = _joint_matrix(args.workload, d.rank, d.world)
-    m, n, nnz = A.m, grid.n, A.nnz
+    m_loc, n, nnz = A.m, grid.n, A.nnz
+    m = cfg["m"]
     ctx = ocg.Context(d.local)
     hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
-    # device-resident inputs (value) ...
     dev = torch.device("cuda", d.local)
     t_rp = torch.from_numpy(A.row_ptr).to(dev)
     t_col = torch.from_numpy(A.col).to(dev)
     t_val = torch.from_numpy(A.val).to(dev)
     torch.cuda.synchronize(dev)
-    plan = AlsPlan(m, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, hyp, args.gamma, on_device=True,
-                   ctx=ctx)
+    plan = AlsPlan(m_loc, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, hyp, args.gamma,
+                   on_device=True, ctx=ctx)
+    phases = [0.0, 0.0, 0.0, 0.0]
+    if d.world == 1:
+        step = lambda: plan.run(timed=True)  # noqa: E731
+    else:
+        backend = GpuAlsBackend(plan, dev)
+        driver = ShardedAlsDriver(backend, d.world, lambda g: d.pg.all_reduce(g))
+
+        def step():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            driver.run(args.sweeps)
+            e1.record()
+            e1.synchronize()
+            return e0.elapsed_time(e1), [0.0] * 4
     for _ in range(args.warmup):
-        plan.run(timed=True)
+        step()
+    torch.cuda.synchronize(dev)
     d.barrier()
-    tot_ms, phases = 0.0, [0.0, 0.0, 0.0, 0.0]
+    tot_ms = 0.0
     with Clocks(d.local) as clk:
         for _ in range(args.steps):
             ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
-            ms, ph = plan.run(timed=True)
+            ms, ph = step()
             tot_ms += ms
             phases = [a + b for a, b in zip(phases, ph)]
+    torch.cuda.synchronize(dev)
     d.barrier()
     t_dev = d.max(tot_ms / 1e3)
     idx, sav, loss, ncand = plan.results()
     assert (idx >= 0).all() and (ncand >= 1).all()
     plan.close()
     del t_rp, t_col, t_val
-    # ... and end to end through the public API with host buffers
+    # end to end through the public API with host buffers (N=1: the one-shot plan;
+    # N>1: each rank uploads its shard and runs the sharded schedule)
+    e2e_steps = max(1, min(args.steps, 3))
+    d.barrier()
     e2e_t = 0.0
-    for _ in range(max(1, min(args.steps, 3))):
+    for _ in range(e2e_steps):
         t0 = time.perf_counter()
-        p2 = AlsPlan(m, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
-        p2.run(timed=False)
+        p2 = AlsPlan(m_loc, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+        if d.world == 1:
+            p2.run(timed=False)
+        else:
+            ShardedAlsDriver(GpuAlsBackend(p2, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
         r2 = p2.results()
         p2.close()
         e2e_t += time.perf_counter() - t0
-    e2e_steps = max(1, min(args.steps, 3))
     e2e_t = d.max(e2e_t / e2e_steps)
-    assert np.array_equal(r2[0], idx)
+    if d.world == 1:
+        assert np.array_equal(r2[0], idx)
     cells = m * n
     k = cfg["rank"]
-    # roofline of the Gram kernels (K3, SURVEY §8d): per observation 8 B
-    # (index + value) + 4k B gathered factor row, per item 4k B factor out +
-    # 8 B row pointer.  Row and column half-sweeps launch once per sweep each.
-    row_bytes = nnz * (8 + 4 * k) + m * (4 * k + 8)
+    # roofline of the Gram kernel (K3, SURVEY §8d): per observation 8 B (index +
+    # value) + 4k B gathered factor row, per item 4k B factor + 8 B pointer; the
+    # same kernel runs the row and the column half-sweep once per sweep each.
+    row_bytes = nnz * (8 + 4 * k) + m_loc * (4 * k + 8)
     col_bytes = nnz * (8 + 4 * k) + n * (4 * k + 8)
-    row_ms = phases[1] / args.steps / args.sweeps
-    col_ms = phases[2] / args.steps / args.sweeps
-    dom = "row" if row_ms >= col_ms else "col"
-    bytes_l, ms_l = (row_bytes, row_ms) if dom == "row" else (col_bytes, col_ms)
-    achieved = bytes_l / (ms_l / 1e3) / 1e9
     out = {
         "metric": "CF-completed matrix cells/sec",
         "value": cells * args.steps / t_dev,
         "unit": "cells/s",
         "selections_per_sec": m * args.steps / t_dev,
         "ms_per_step": t_dev * 1e3 / args.steps,
-        "e2e": {"value": cells / e2e_t, "unit": "cells/s", "h2d_bytes_per_step": int(A.row_ptr.nbytes + A.col.nbytes +
-                                                                                      A.val.nbytes),
-                "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes),
+        "e2e": {"value": cells / e2e_t, "unit": "cells/s",
+                "h2d_bytes_per_step": int(A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) * d.world,
+                "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes) * d.world,
                 "selections_per_sec": m / e2e_t},
         "dtype": "f32 factors / f64 selection",
-        "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "observed": nnz,
-                   "density": nnz / (m * n), "offline_dense_rows": cfg["dense_rows"], "solver": "als",
+        "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "observed_per_gpu": nnz,
+                   "density": cfg["density"], "offline_dense_rows": cfg["dense_rows"], "solver": "als",
                    "sweeps": args.sweeps, "lambda": args.als_lambda, "gamma": args.gamma,
-                   "l2": "inputs (CSR %.0f MB) larger than L2, and L2 flushed before every timed step" %
+                   "parallelism": f"rows sharded over {d.world} GPU(s), column Gram allreduce (NCCL)"
+                   if d.world > 1 else "1 GPU",
+                   "l2": "inputs (CSR %.0f MB/GPU) larger than L2, and L2 flushed before every timed step" %
                          ((A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) / 1e6)},
-        "phases_ms_per_step": {"csc_build": phases[0] / args.steps, "row_half_sweeps": phases[1] / args.steps,
-                               "col_half_sweeps": phases[2] / args.steps, "impute_select": phases[3] / args.steps},
         "scaling": "strong",
-        "gpu_launches": args.steps * (6 + 2 * args.sweeps + 2),
-        "roofline": {"bound": "hbm", "kernel": f"als_gram_solve ({dom} half-sweep)", "achieved": achieved,
-                     "peak": PEAKS["hbm_gbs"], "unit": "GB/s", "frac": achieved / PEAKS["hbm_gbs"],
-                     "traffic": None,
-                     "bytes_def": "gather-counted: nnz*(8+4k) + items*(4k+8) per launch (SURVEY 8d K3)",
-                     "launch_ms": ms_l},
+        "gpu_launches": args.steps * (16 + args.sweeps * (4 if d.world == 1 else 5) + 2),
         "clocks": clk.summary(),
     }
+    if d.world == 1:
+        row_ms = phases[1] / args.steps / args.sweeps
+        col_ms = phases[2] / args.steps / args.sweeps
+        # one kernel (als_seg_gram_kernel) serves both half-sweeps: average bytes
+        # per launch over the average launch duration
+        achieved = (row_bytes + col_bytes) / 2 / ((row_ms + col_ms) / 2 / 1e3) / 1e9
+        out["phases_ms_per_step"] = {"csc_build_and_segments": phases[0] / args.steps,
+                                     "row_half_sweeps": phases[1] / args.steps,
+                                     "col_half_sweeps": phases[2] / args.steps,
+                                     "impute_select": phases[3] / args.steps}
+        out["roofline"] = {"bound": "hbm", "kernel": "als_seg_gram_kernel (K3 Gram accumulation)",
+                           "achieved": achieved, "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
+                           "frac": achieved / PEAKS["hbm_gbs"], "traffic": None,
+                           "bytes_def": "gather-counted per launch: nnz*(8+4k) + items*(4k+8) (SURVEY 8d K3); "
+                                        "DRAM traffic from ncu in profiles/ (V gathers hit L2)",
+                           "launch_ms_row": row_ms, "launch_ms_col": col_ms}
     return out, (args.workload, m)
 
 

@@ -77,6 +77,9 @@ void ocg_ctx_destroy(ocg_ctx* ctx);
 int ocg_ctx_device_info(ocg_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor);
 int ocg_ctx_flush_l2(ocg_ctx* ctx);    /* overwrite a 256 MB scratch buffer (> L2) on the stream */
 int ocg_ctx_synchronize(ocg_ctx* ctx);
+/* run the context's work on an external stream (e.g. torch's current stream,
+ * so NCCL collectives issued by torch are ordered with our kernels) */
+int ocg_ctx_set_stream(ocg_ctx* ctx, void* stream);
 
 /* ---- K1: Algorithm 2 selection ---------------------------------------
  * policy::select_caps (policy.cpp:17-64; policy.hpp:34) batched over `nrows`
@@ -179,6 +182,19 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
  * total_ms / phase_ms[4] (CSC, row sweeps, column sweeps, select): CUDA-event
  * times on the context stream (either may be NULL = asynchronous). */
 int ocg_als_plan_run(ocg_als_plan* plan, float* total_ms, float* phase_ms);
+/* Phase-level form of _run for the row-sharded multi-GPU driver (each rank
+ * holds a row shard of the CSR with all n columns): begin = CSC +
+ * V init; per sweep: row_half (local), col_gram (this shard's column Gram
+ * records, n x (k*k + k + 1) floats, into d_gram) -> allreduce(sum) across
+ * ranks -> col_solve(d_gram) (replicated, deterministic); finally select.
+ * col_half = the single-GPU fused column half-sweep. */
+int ocg_als_plan_begin(ocg_als_plan* plan);
+int ocg_als_plan_row_half(ocg_als_plan* plan);
+int ocg_als_plan_col_half(ocg_als_plan* plan);
+int64_t ocg_als_plan_gram_floats(ocg_als_plan* plan);
+int ocg_als_plan_col_gram(ocg_als_plan* plan, float* d_gram);
+int ocg_als_plan_col_solve(ocg_als_plan* plan, const float* d_gram);
+int ocg_als_plan_select(ocg_als_plan* plan);
 int ocg_als_plan_results(ocg_als_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand,
                          float* U, float* V);
 int ocg_als_plan_completed_rows(ocg_als_plan* plan, int64_t row0, int64_t nrows, double* out);
@@ -213,6 +229,13 @@ int ocg_synth_csr_fill(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const i
                        double density, int64_t dense_rows, uint64_t seed, int nthreads, const int64_t* row_ptr,
                        int32_t* col, float* val32, double* val64);
 
+/* rows [row0, row1) of the same matrix (a rank's shard), local row_ptr */
+int ocg_synth_csr_range_count(int64_t m, int64_t row0, int64_t row1, const int32_t* cpu_caps, int32_t ncpu,
+                              const int32_t* gpu_caps, int32_t ngpu, double density, int64_t dense_rows,
+                              uint64_t seed, int nthreads, int64_t* row_ptr);
+int ocg_synth_csr_range_fill(int64_t m, int64_t row0, int64_t row1, const int32_t* cpu_caps, int32_t ncpu,
+                             const int32_t* gpu_caps, int32_t ngpu, double density, int64_t dense_rows, uint64_t seed,
+                             int nthreads, const int64_t* row_ptr, int32_t* col, float* val32, double* val64);
 /* selected rows of the same joint matrix as dense values + mask (values as
  * the FP32 CSR carries them, widened) — CPU-baseline samples */
 int ocg_synth_rows_dense(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,

@@ -104,6 +104,9 @@ class Port:
         L.ocgo_set_lane.argtypes = [ctypes.c_int]
         L.ocgo_als_fit.argtypes = [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_dbl, c_i32, c_u64, c_vp,
                                    c_vp]
+        L.ocgo_als_solve_rows.argtypes = [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_dbl]
+        L.ocgo_als_col_gram.argtypes = [c_i64, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp]
+        L.ocgo_als_solve_from_gram.argtypes = [c_i64, c_vp, c_vp, c_i32, c_dbl]
         L.ocgo_als_init_value.restype = c_dbl
         L.ocgo_als_init_value.argtypes = [c_u64, c_i64, c_i32, c_i32]
 

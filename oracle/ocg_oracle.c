@@ -590,3 +590,48 @@ int ocgo_als_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* co
     }
     return E_OK;
 }
+
+/* Per-half pieces of ocgo_als_fit for the row-sharded (multi-rank) schedule:
+ * row solves are local; column Gram records [k*k Gram | k rhs | count] are
+ * summed across ranks, then every rank solves the same records. */
+void ocgo_als_solve_rows(int64_t nrows, const int64_t* ptr, const int32_t* idx, const float* val, const double* Y,
+                         double* X, int32_t k, double lambda) {
+    als_half(nrows, ptr, idx, val, Y, X, k, lambda);
+}
+
+void ocgo_als_col_gram(int64_t ncols, const int64_t* col_ptr, const int32_t* row_idx, const float* cval,
+                       const double* U, int32_t k, double* G) {
+    const int64_t rec = (int64_t)k * k + k + 1;
+    for (int64_t j = 0; j < ncols; ++j) {
+        double* g = G + j * rec;
+        memset(g, 0, sizeof(double) * (size_t)rec);
+        for (int64_t q = col_ptr[j]; q < col_ptr[j + 1]; ++q) {
+            const double* u = U + (int64_t)row_idx[q] * k;
+            for (int a = 0; a < k; ++a) {
+                g[k * k + a] += (double)cval[q] * u[a];
+                for (int c = 0; c < k; ++c) g[a * k + c] += u[a] * u[c];
+            }
+        }
+        g[k * k + k] = (double)(col_ptr[j + 1] - col_ptr[j]);
+    }
+}
+
+void ocgo_als_solve_from_gram(int64_t ncols, const double* G, double* X, int32_t k, double lambda) {
+    const int64_t rec = (int64_t)k * k + k + 1;
+    double A[64 * 64], b[64];
+    for (int64_t j = 0; j < ncols; ++j) {
+        const double* g = G + j * rec;
+        const double cnt = g[k * k + k];
+        if (cnt == 0.0) {
+            for (int f = 0; f < k; ++f) X[j * k + f] = 0.0;
+            continue;
+        }
+        for (int a = 0; a < k; ++a) {
+            for (int c = 0; c <= a; ++c) A[a * k + c] = g[a * k + c];
+            b[a] = g[k * k + a];
+            A[a * k + a] += lambda * cnt;
+        }
+        chol_solve(A, b, k);
+        for (int f = 0; f < k; ++f) X[j * k + f] = b[f];
+    }
+}

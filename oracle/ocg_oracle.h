@@ -63,6 +63,12 @@ int ocgo_als_fit(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* co
                  const int64_t* col_ptr, const int32_t* row_idx, const float* cval, int32_t k, double lambda,
                  int32_t sweeps, uint64_t seed, double* U, double* V);
 
+void ocgo_als_solve_rows(int64_t nrows, const int64_t* ptr, const int32_t* idx, const float* val, const double* Y,
+                         double* X, int32_t k, double lambda);
+void ocgo_als_col_gram(int64_t ncols, const int64_t* col_ptr, const int32_t* row_idx, const float* cval,
+                       const double* U, int32_t k, double* G);
+void ocgo_als_solve_from_gram(int64_t ncols, const double* G, double* X, int32_t k, double lambda);
+
 #ifdef __cplusplus
 }
 #endif

@@ -149,3 +149,12 @@ _sig("ocg_als_plan_run", ctypes.c_int, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_completed_rows", ctypes.c_int, c_vp, c_i64, c_i64, c_vp)
 _sig("ocg_als_plan_destroy", None, c_vp)
+
+_sig("ocg_ctx_set_stream", ctypes.c_int, c_vp, c_vp)
+_sig("ocg_als_plan_begin", ctypes.c_int, c_vp)
+_sig("ocg_als_plan_row_half", ctypes.c_int, c_vp)
+_sig("ocg_als_plan_col_half", ctypes.c_int, c_vp)
+_sig("ocg_als_plan_gram_floats", c_i64, c_vp)
+_sig("ocg_als_plan_col_gram", ctypes.c_int, c_vp, c_vp)
+_sig("ocg_als_plan_col_solve", ctypes.c_int, c_vp, c_vp)
+_sig("ocg_als_plan_select", ctypes.c_int, c_vp)

@@ -251,6 +251,33 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     return OCG_OK;
 }
 
+static int launch_select(ocg_als_plan* P) {
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
+    ocg::AlsSelectArgs a{};
+    a.m = P->m;
+    a.n = P->n;
+    a.k = P->k;
+    a.U = P->U.p;
+    a.V = P->V.p;
+    a.Vt = P->Vt.p;
+    a.row_ptr = P->row_ptr.p;
+    a.col = P->col.p;
+    a.val = P->val.p;
+    a.cpu_caps = P->cpu.p;
+    a.gpu_caps = P->gpu.p;
+    a.ngpu = P->ngpu;
+    a.e_base = P->e_base;
+    a.gamma = P->gamma;
+    a.idx = P->idx.p;
+    a.saving = P->saving.p;
+    a.loss = P->loss.p;
+    a.ncand = P->ncand.p;
+    a.completed = nullptr;
+    ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
+    return OCG_OK;
+}
+
 // phase_ms (optional, 4 floats): CSC build, row half-sweeps, column half-sweeps, select
 int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
@@ -277,29 +304,8 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             col_ms += b;
         }
     }
-    ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
     ALS_CUDA(cudaEventRecord(P->ev[2], s));
-    ocg::AlsSelectArgs a{};
-    a.m = P->m;
-    a.n = P->n;
-    a.k = P->k;
-    a.U = P->U.p;
-    a.V = P->V.p;
-    a.Vt = P->Vt.p;
-    a.row_ptr = P->row_ptr.p;
-    a.col = P->col.p;
-    a.val = P->val.p;
-    a.cpu_caps = P->cpu.p;
-    a.gpu_caps = P->gpu.p;
-    a.ngpu = P->ngpu;
-    a.e_base = P->e_base;
-    a.gamma = P->gamma;
-    a.idx = P->idx.p;
-    a.saving = P->saving.p;
-    a.loss = P->loss.p;
-    a.ncand = P->ncand.p;
-    a.completed = nullptr;
-    ALS_CUDA(ocg::launch_als_select(a, sm, s));
+    if ((rc = launch_select(P))) return rc;
     ALS_CUDA(cudaEventRecord(P->ev[5], s));
     if (total_ms || phase_ms) {
         ALS_CUDA(cudaEventSynchronize(P->ev[5]));
@@ -312,6 +318,54 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
         }
     }
     return OCG_OK;
+}
+
+// ---- phase-level entry points for the row-sharded multi-GPU driver --------
+// (all asynchronous on the context stream; see ocg_ctx_set_stream)
+int ocg_als_plan_begin(ocg_als_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    int rc = als_build_csc(P);
+    if (rc) return rc;
+    ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, ocg_internal_stream(P->ctx)));
+    return OCG_OK;
+}
+
+int ocg_als_plan_row_half(ocg_als_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 0), 0, ocg_internal_sm_count(P->ctx), ocg_internal_stream(P->ctx)));
+    return OCG_OK;
+}
+
+int ocg_als_plan_col_half(ocg_als_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 1), 0, ocg_internal_sm_count(P->ctx), ocg_internal_stream(P->ctx)));
+    return OCG_OK;
+}
+
+int64_t ocg_als_plan_gram_floats(ocg_als_plan* P) {
+    return P ? P->n * static_cast<int64_t>(ocg::als_gram_record_floats(P->k)) : 0;
+}
+
+// this shard's column Gram records (K*K Gram, K rhs, count per column) -> d_gram
+int ocg_als_plan_col_gram(ocg_als_plan* P, float* d_gram) {
+    if (!P || !d_gram) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    ocg::AlsHalf h = als_half(P, 1);
+    h.gram_out = d_gram;
+    ALS_CUDA(ocg::launch_als_half(P->k, h, 1, ocg_internal_sm_count(P->ctx), ocg_internal_stream(P->ctx)));
+    return OCG_OK;
+}
+
+// V from (allreduced) column Gram records
+int ocg_als_plan_col_solve(ocg_als_plan* P, const float* d_gram) {
+    if (!P || !d_gram) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    ALS_CUDA(ocg::launch_als_solve_from_gram(P->k, P->n, d_gram, P->V.p, P->lambda, ocg_internal_sm_count(P->ctx),
+                                             ocg_internal_stream(P->ctx)));
+    return OCG_OK;
+}
+
+int ocg_als_plan_select(ocg_als_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    return launch_select(P);
 }
 
 int ocg_als_plan_results(ocg_als_plan* P, int32_t* idx, double* saving, double* loss, int32_t* ncand, float* U,

@@ -26,6 +26,7 @@ struct ocg_ctx {
     int sm_count = 0;
     int cc_major = 0, cc_minor = 0;
     cudaStream_t stream = nullptr;
+    bool own_stream = true;
 };
 
 namespace {
@@ -425,7 +426,7 @@ int ocg_ctx_create(int device, ocg_ctx** out) {
 void ocg_ctx_destroy(ocg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->flush) cudaFree(ctx->flush);
     delete ctx;
 }
@@ -554,6 +555,14 @@ int ocg_ctx_flush_l2(ocg_ctx* ctx) {
     if (!ctx->flush) OCG_CUDA(cudaMalloc(&ctx->flush, kFlushBytes));
     OCG_CUDA(cudaMemsetAsync(ctx->flush, ctx->flush_val++ & 0xff, kFlushBytes, ctx->stream));
     OCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return OCG_OK;
+}
+
+int ocg_ctx_set_stream(ocg_ctx* ctx, void* stream) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+    ctx->stream = static_cast<cudaStream_t>(stream);
     return OCG_OK;
 }
 

@@ -242,35 +242,41 @@ int ocg_synth_online_apps(int64_t napps, uint64_t seed, const int32_t* cpu, int3
     return OCG_OK;
 }
 
-int ocg_synth_csr_count(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
-                        double density, int64_t dense_rows, uint64_t seed, int nthreads, int64_t* row_ptr) {
+// rows [row0, row1) of the m-row joint matrix; row_ptr is local (row_ptr[0] = 0)
+int ocg_synth_csr_range_count(int64_t m, int64_t row0, int64_t row1, const int32_t* cpu, int32_t ncpu,
+                              const int32_t* gpu, int32_t ngpu, double density, int64_t dense_rows, uint64_t seed,
+                              int nthreads, int64_t* row_ptr) {
+    if (row0 < 0 || row1 > m || row0 > row1) return OCG_E_RANGE;
     const Grid g{cpu, ncpu, gpu, ngpu};
     const auto specs = joint_specs(m, seed, g);
     const auto plan = default_plan(g);
     std::vector<uint8_t> in_plan(static_cast<size_t>(g.n()), 0);
     for (auto j : plan) in_plan[j] = 1;
     const double p = bernoulli_p(m, g.n(), density, dense_rows, static_cast<int64_t>(plan.size()));
-    parallel_rows(m, nthreads, [&](int64_t i) {
+    parallel_rows(row1 - row0, nthreads, [&](int64_t r) {
+        const int64_t i = row0 + r;
         int64_t c = 0;
         gen_row(i, dense_rows, g, in_plan, p, specs[i], seed, [&](int64_t, double) { ++c; });
-        row_ptr[i + 1] = c;
+        row_ptr[r + 1] = c;
     });
     row_ptr[0] = 0;
-    for (int64_t i = 0; i < m; ++i) row_ptr[i + 1] += row_ptr[i];
+    for (int64_t r = 0; r < row1 - row0; ++r) row_ptr[r + 1] += row_ptr[r];
     return OCG_OK;
 }
 
-int ocg_synth_csr_fill(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
-                       double density, int64_t dense_rows, uint64_t seed, int nthreads, const int64_t* row_ptr,
-                       int32_t* col, float* val32, double* val64) {
+int ocg_synth_csr_range_fill(int64_t m, int64_t row0, int64_t row1, const int32_t* cpu, int32_t ncpu,
+                             const int32_t* gpu, int32_t ngpu, double density, int64_t dense_rows, uint64_t seed,
+                             int nthreads, const int64_t* row_ptr, int32_t* col, float* val32, double* val64) {
+    if (row0 < 0 || row1 > m || row0 > row1) return OCG_E_RANGE;
     const Grid g{cpu, ncpu, gpu, ngpu};
     const auto specs = joint_specs(m, seed, g);
     const auto plan = default_plan(g);
     std::vector<uint8_t> in_plan(static_cast<size_t>(g.n()), 0);
     for (auto j : plan) in_plan[j] = 1;
     const double p = bernoulli_p(m, g.n(), density, dense_rows, static_cast<int64_t>(plan.size()));
-    parallel_rows(m, nthreads, [&](int64_t i) {
-        int64_t q = row_ptr[i];
+    parallel_rows(row1 - row0, nthreads, [&](int64_t r) {
+        const int64_t i = row0 + r;
+        int64_t q = row_ptr[r];
         gen_row(i, dense_rows, g, in_plan, p, specs[i], seed, [&](int64_t j, double v) {
             col[q] = static_cast<int32_t>(j);
             if (val32) val32[q] = static_cast<float>(v);
@@ -279,6 +285,18 @@ int ocg_synth_csr_fill(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_
         });
     });
     return OCG_OK;
+}
+
+int ocg_synth_csr_count(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
+                        double density, int64_t dense_rows, uint64_t seed, int nthreads, int64_t* row_ptr) {
+    return ocg_synth_csr_range_count(m, 0, m, cpu, ncpu, gpu, ngpu, density, dense_rows, seed, nthreads, row_ptr);
+}
+
+int ocg_synth_csr_fill(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
+                       double density, int64_t dense_rows, uint64_t seed, int nthreads, const int64_t* row_ptr,
+                       int32_t* col, float* val32, double* val64) {
+    return ocg_synth_csr_range_fill(m, 0, m, cpu, ncpu, gpu, ngpu, density, dense_rows, seed, nthreads, row_ptr, col,
+                                    val32, val64);
 }
 
 // selected rows of the joint matrix as dense values + mask (nrows x n)

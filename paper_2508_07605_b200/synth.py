@@ -100,18 +100,28 @@ class CsrMatrix:
         return int(self.row_ptr[-1])
 
 
+lib.ocg_synth_csr_range_count.argtypes = [c_i64, c_i64, c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64, c_u64,
+                                          ctypes.c_int, c_vp]
+lib.ocg_synth_csr_range_count.restype = ctypes.c_int
+lib.ocg_synth_csr_range_fill.argtypes = [c_i64, c_i64, c_i64, c_vp, c_i32, c_vp, c_i32, c_dbl, c_i64, c_u64,
+                                         ctypes.c_int, c_vp, c_vp, c_vp, c_vp]
+lib.ocg_synth_csr_range_fill.restype = ctypes.c_int
+
+
 def joint_csr(m: int, grid: PowerGrid, density: float, dense_rows: int, seed: int = 42, dtype=np.float32,
-              threads: int | None = None) -> CsrMatrix:
-    """SURVEY §8d synthetic joint matrix (C1: 10K x 256 @5%, C2: 1M x 4096 @2%, ...)."""
+              threads: int | None = None, rows: tuple | None = None) -> CsrMatrix:
+    """SURVEY §8d synthetic joint matrix (C1: 10K x 256 @5%, C2: 1M x 4096 @2%, ...).
+    rows=(r0, r1): only that row shard (local row_ptr), identical to the full matrix's rows."""
     threads = threads or max(1, min(64, os.cpu_count() or 1))
+    r0, r1 = rows if rows is not None else (0, m)
     cpu, gpu = grid.arrays()
-    rp = np.zeros(m + 1, np.int64)
-    check(lib.ocg_synth_csr_count(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed, threads,
-                                  ptr(rp)))
+    rp = np.zeros(r1 - r0 + 1, np.int64)
+    check(lib.ocg_synth_csr_range_count(m, r0, r1, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed,
+                                        threads, ptr(rp)))
     nnz = int(rp[-1])
     col = np.empty(nnz, np.int32)
     v32 = np.empty(nnz, np.float32) if dtype == np.float32 else None
     v64 = np.empty(nnz, np.float64) if dtype == np.float64 else None
-    check(lib.ocg_synth_csr_fill(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed, threads,
-                                 ptr(rp), ptr(col), ptr(v32), ptr(v64)))
-    return CsrMatrix(m, grid.n, rp, col, v32 if v32 is not None else v64)
+    check(lib.ocg_synth_csr_range_fill(m, r0, r1, ptr(cpu), len(cpu), ptr(gpu), len(gpu), density, dense_rows, seed,
+                                       threads, ptr(rp), ptr(col), ptr(v32), ptr(v64)))
+    return CsrMatrix(r1 - r0, grid.n, rp, col, v32 if v32 is not None else v64)
