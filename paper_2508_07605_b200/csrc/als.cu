@@ -243,7 +243,10 @@ __global__ void __launch_bounds__(256) als_seg_gram_kernel(const int32_t* __rest
             }
             __syncwarp();
         } else {
-            float* out = partial + static_cast<int64_t>(pfirst[item] + (sg - first[item])) * GSZ;
+            // MODE 1 keeps every segment's partial (slot = segment index); MODE 0
+            // only multi-segment items' (compact slots from pfirst)
+            const int64_t slot = MODE == 1 ? sg : pfirst[item] + (sg - first[item]);
+            float* out = partial + slot * GSZ;
 #pragma unroll
             for (int p = 0; p < RB; ++p)
 #pragma unroll
@@ -400,7 +403,7 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
         als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
             h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X, h.partial,
             h.lambda);
-        als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.pfirst, h.partial, nullptr,
+        als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.first, h.partial, nullptr,
                                                              h.gram_out, h.lambda);
     }
     return cudaGetLastError();
