@@ -55,16 +55,20 @@ __device__ __forceinline__ void cp_async_wait() {
 // Solve (G + diag_add I) x = b on one warp.  G: K x GS shared (full
 // symmetric); lane l < K holds b_l; returns x_l.  G's lower triangle is
 // overwritten with L.  Left-looking: column c needs only finished columns,
-// so the code stays compact (no fully unrolled K x K update).
+// so the code stays compact (no fully unrolled K x K update).  The diagonal
+// pivot is broadcast with a shuffle and every lane scales by rsqrt(pivot), so
+// a column costs one shuffle + one warp barrier and no division; lane l keeps
+// 1/L[l][l] for the substitutions.
 template <int K>
 __device__ __noinline__ float chol_solve_warp(float* G, float b, float diag_add, int lane) {
     constexpr int GS = GramShape<K>::GS;
     float* Gl = G + (lane < K ? lane : K - 1) * GS;  // lanes >= K read a valid row, results unused
     if (lane < K) Gl[lane] += diag_add;
     __syncwarp();
+    float inv_diag = 1.0f;
     for (int c = 0; c < K; ++c) {
         const float* Gc = G + c * GS;
-        float s = (lane >= c && lane < K) ? Gl[c] : 0.0f;
+        float s = Gl[c];
         int q = 0;
         for (; q + 4 <= c; q += 4) {
             const float4 a = *reinterpret_cast<const float4*>(Gl + q);
@@ -75,21 +79,22 @@ __device__ __noinline__ float chol_solve_warp(float* G, float b, float diag_add,
             s = fmaf(-a.w, w.w, s);
         }
         for (; q < c; ++q) s = fmaf(-Gl[q], Gc[q], s);
-        if (lane == c) G[c * GS + c] = sqrtf(s);
-        __syncwarp();
-        if (lane > c && lane < K) Gl[c] = s / Gc[c];
+        const float piv = __shfl_sync(0xffffffffu, s, c);  // L[c][c]^2
+        const float r = rsqrtf(piv);
+        if (lane == c) inv_diag = r;
+        if (lane >= c && lane < K) Gl[c] = s * r;  // lane c: sqrt(piv); below: L[l][c]
         __syncwarp();
     }
     // L y = b
     float y = b;
     for (int c = 0; c < K; ++c) {
-        if (lane == c) y = y / Gl[c];
+        if (lane == c) y *= inv_diag;
         const float yc = __shfl_sync(0xffffffffu, y, c);
         if (lane > c && lane < K) y = fmaf(-Gl[c], yc, y);
     }
     // L^T x = y
     for (int c = K - 1; c >= 0; --c) {
-        if (lane == c) y = y / Gl[c];
+        if (lane == c) y *= inv_diag;
         const float xc = __shfl_sync(0xffffffffu, y, c);
         if (lane < c) y = fmaf(-G[c * GS + lane], xc, y);
     }
