@@ -64,18 +64,37 @@ __device__ double valid_threshold(double p_base, double gamma) {
     return x;
 }
 
-struct RowBest {
-    float t;      // FP32 estimate of c_sum/p of the best so far
-    int j;        // column (-1: none)
-    double s, p;  // exact saving and completed value of the best
-    int sum;
-    int ncand;
+// exact state of a lane's best cell for one row (shared memory; touched only
+// on the rare exact-evaluation path)
+struct BestExact {
+    double s, p;  // exact saving and completed value
+    int j, sum;   // column (-1: none), c+g
 };
+
+// Rare path: FP64 evaluation of one cell (policy.cpp:37-38) and the 4-key
+// compare against the lane's current best.  Kept out of line so the unrolled
+// hot loop stays small.
+__device__ __noinline__ void exact_update(BestExact* b, double pd, int cs, int j, double e_base) {
+    const double e_pred = ddiv(static_cast<double>(cs), pd);
+    const double s = ddiv(dsub(e_base, e_pred), e_base);
+    bool better;
+    if (b->j < 0) better = true;
+    else if (s != b->s) better = s > b->s;
+    else if (pd != b->p) better = pd > b->p;
+    else if (cs != b->sum) better = cs < b->sum;
+    else better = j < b->j;
+    if (better) {
+        b->s = s;
+        b->p = pd;
+        b->j = j;
+        b->sum = cs;
+    }
+}
 
 }  // namespace
 
 template <int K>
-__global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
+__global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
     static_assert(K % 4 == 0 && K <= 32, "rank");
     __shared__ __align__(16) float Ut[K][kRows];
     __shared__ double pbase_s[kRows], pthr_s[kRows];
@@ -84,6 +103,7 @@ __global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
     extern __shared__ __align__(16) float dyn[];
     float (*Vt)[K][kTC] = reinterpret_cast<float (*)[K][kTC]>(dyn);                      // [2][K][kTC]
     float (*obs)[kRPW][kTC] = reinterpret_cast<float (*)[kRPW][kTC]>(dyn + 2 * K * kTC);  // [8][kRPW][kTC]
+    BestExact* bex = reinterpret_cast<BestExact*>(dyn + 2 * K * kTC + 8 * kRPW * kTC);     // [8][kRPW][32]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t n = a.n;
     const int ntiles = static_cast<int>((n + kTC - 1) / kTC);
@@ -123,18 +143,23 @@ __global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
         }
         __syncthreads();
         const int r0 = warp * kRPW;
-        RowBest best[kRPW];
-        bool obs_cut[kRPW];  // 0.01 (clamped floor) is valid for this row
+        float tbest[kRPW];   // FP32 estimate of c_sum/p of the lane's best, per row
+        int ncand[kRPW];
+        bool lo_ok[kRPW], hi_ok[kRPW];  // clamp floor 0.01 / ceiling 1.25 valid for this row
         int64_t cursor[kRPW], rend[kRPW];
         float fthr[kRPW];
+        BestExact* myb = bex + (warp * kRPW) * 32 + lane;  // row q at myb[q * 32]
 #pragma unroll
         for (int q = 0; q < kRPW; ++q) {
-            best[q] = RowBest{INFINITY, -1, 0.0, 0.0, 0, 0};
+            tbest[q] = INFINITY;
+            ncand[q] = 0;
+            myb[q * 32] = BestExact{0.0, 0.0, -1, 0};
             const int64_t i = rb + r0 + q;
             cursor[q] = i < a.m ? a.row_ptr[i] : 0;
             rend[q] = i < a.m ? a.row_ptr[i + 1] : 0;
             fthr[q] = fthr_s[r0 + q];
-            obs_cut[q] = 0.01 >= pthr_s[r0 + q];
+            lo_ok[q] = 0.01 >= pthr_s[r0 + q];
+            hi_ok[q] = 1.25 >= pthr_s[r0 + q];
         }
         // ---- prefetch tile 0 ---------------------------------------------
         auto load_tile = [&](int t, int buf) {
@@ -193,7 +218,8 @@ __global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) acc[q][u] = fmaf(us[q], vs[u], acc[q][u]);
             }
-            // selection epilogue on the 16 cells
+            // selection epilogue on the 16 cells (branch-free hot path; the
+            // exact FP64 path runs only for cells within the band of the best)
             int ci = static_cast<int>((c0 + lane * 4) / a.ngpu);
             int gi = static_cast<int>(c0 + lane * 4 - static_cast<int64_t>(ci) * a.ngpu);
 #pragma unroll
@@ -203,55 +229,29 @@ __global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
                     gi = 0;
                     ++ci;
                 }
-                if (j >= n) continue;
-                const int cs = caps_s[ci] + caps_s[ncpu + gi];
+                const bool jin = j < n;
+                const int cs = jin ? caps_s[ci] + caps_s[ncpu + gi] : 1;
+                const float csf = static_cast<float>(cs);
 #pragma unroll
                 for (int q = 0; q < kRPW; ++q) {
-                    if (rb + r0 + q >= a.m) continue;
+                    const bool live = jin && (rb + r0 + q < a.m);
                     const float ov = obs[warp][q][lane * 4 + u];
                     const bool is_obs = ov > 0.0f;
                     const float pf = is_obs ? ov : acc[q][u];
-                    // completed value (double) and exact validity without a division
-                    bool valid;
-                    float pe;  // FP32 stand-in for the band test
-                    if (is_obs) {
-                        valid = pf >= fthr[q];
-                        pe = pf;
-                    } else if (pf < 0.01f || static_cast<double>(pf) < 0.01) {
-                        valid = obs_cut[q];
-                        pe = 0.01f;
-                    } else if (pf > 1.25f) {
-                        valid = 1.25 >= pthr_s[r0 + q];
-                        pe = 1.25f;
-                    } else {
-                        valid = pf >= fthr[q];
-                        pe = pf;
+                    // clamp(p, 0.01, 1.25) in the double domain: float p <= 0.01f <=> (double)p < 0.01
+                    const bool lo = !is_obs && pf <= 0.01f;
+                    const bool hi = !is_obs && pf > 1.25f;
+                    const float pe = lo ? 0.01f : (hi ? 1.25f : pf);
+                    const bool valid = live && (lo ? lo_ok[q] : (hi ? hi_ok[q] : pf >= fthr[q]));
+                    if (a.completed && live)
+                        a.completed[(rb + r0 + q) * n + j] = lo ? 0.01 : (hi ? 1.25 : static_cast<double>(pf));
+                    ncand[q] += valid ? 1 : 0;
+                    const float tf = __fdividef(csf, pe);
+                    if (valid && tf <= tbest[q] * kBand) {
+                        const double pd = lo ? 0.01 : (hi ? 1.25 : static_cast<double>(pf));
+                        exact_update(myb + q * 32, pd, cs, static_cast<int>(j), a.e_base);
+                        tbest[q] = fminf(tbest[q], tf);
                     }
-                    if (a.completed) {
-                        double pd = is_obs ? static_cast<double>(pf) : fmin(fmax(static_cast<double>(pf), 0.01), 1.25);
-                        a.completed[(rb + r0 + q) * n + j] = pd;
-                    }
-                    if (!valid) continue;
-                    ++best[q].ncand;
-                    const float tf = static_cast<float>(cs) / pe;
-                    if (tf > best[q].t * kBand) continue;
-                    // exact FP64 evaluation (policy.cpp:37-38) and 4-key compare
-                    const double pd = is_obs ? static_cast<double>(pf) : fmin(fmax(static_cast<double>(pf), 0.01), 1.25);
-                    const double e_pred = ddiv(static_cast<double>(cs), pd);
-                    const double s = ddiv(dsub(a.e_base, e_pred), a.e_base);
-                    bool better;
-                    if (best[q].j < 0) better = true;
-                    else if (s != best[q].s) better = s > best[q].s;
-                    else if (pd != best[q].p) better = pd > best[q].p;
-                    else if (cs != best[q].sum) better = cs < best[q].sum;
-                    else better = j < best[q].j;
-                    if (better) {
-                        best[q].j = static_cast<int>(j);
-                        best[q].s = s;
-                        best[q].p = pd;
-                        best[q].sum = cs;
-                    }
-                    best[q].t = fminf(best[q].t, tf);
                 }
             }
         }
@@ -259,8 +259,9 @@ __global__ void __launch_bounds__(256) als_select_kernel(AlsSelectArgs a) {
 #pragma unroll
         for (int q = 0; q < kRPW; ++q) {
             const int64_t i = rb + r0 + q;
-            SelResult sr{best[q].j, best[q].s, 0.0, best[q].p, best[q].sum, 0};
-            const SelResult w = sel_warp_reduce(sr, best[q].j >= 0, best[q].ncand);
+            const BestExact b = myb[q * 32];
+            SelResult sr{b.j, b.s, 0.0, b.p, b.sum, 0};
+            const SelResult w = sel_warp_reduce(sr, b.j >= 0, ncand[q]);
             if (lane == 0 && i < a.m) {
                 a.idx[i] = w.idx;
                 a.saving[i] = w.saving;
@@ -285,7 +286,8 @@ cudaError_t launch_als_select(const AlsSelectArgs& a, int sm_count, cudaStream_t
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const unsigned b = static_cast<unsigned>(blocks);
-    const size_t smem = sizeof(float) * (2 * static_cast<size_t>(a.k) * kTC + 8 * kRPW * kTC);
+    const size_t smem = sizeof(float) * (2 * static_cast<size_t>(a.k) * kTC + 8 * kRPW * kTC) +
+                        sizeof(BestExact) * 8 * kRPW * 32;
     switch (a.k) {
         case 8:
             cudaFuncSetAttribute(als_select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
