@@ -93,8 +93,8 @@ __device__ __noinline__ void exact_update(BestExact* b, double pd, int cs, int j
 
 }  // namespace
 
-template <int K>
-__global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
+template <int K, bool WRITE_COMPLETED>
+__global__ void __launch_bounds__(256, 2) als_select_kernel(AlsSelectArgs a) {
     static_assert(K % 4 == 0 && K <= 32, "rank");
     __shared__ __align__(16) float Ut[K][kRows];
     __shared__ double pbase_s[kRows], pthr_s[kRows];
@@ -146,7 +146,10 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
         float tbest[kRPW];   // FP32 estimate of c_sum/p of the lane's best, per row
         int ncand[kRPW];
         bool lo_ok[kRPW], hi_ok[kRPW];  // clamp floor 0.01 / ceiling 1.25 valid for this row
-        int64_t cursor[kRPW], rend[kRPW];
+        const int32_t* rcol[kRPW];  // the row's CSR columns / values (32-bit cursors)
+        const float* rval[kRPW];
+        int cursor[kRPW], rend[kRPW];
+        bool rowlive[kRPW];
         float fthr[kRPW];
         BestExact* myb = bex + (warp * kRPW) * 32 + lane;  // row q at myb[q * 32]
 #pragma unroll
@@ -155,8 +158,12 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
             ncand[q] = 0;
             myb[q * 32] = BestExact{0.0, 0.0, -1, 0};
             const int64_t i = rb + r0 + q;
-            cursor[q] = i < a.m ? a.row_ptr[i] : 0;
-            rend[q] = i < a.m ? a.row_ptr[i + 1] : 0;
+            rowlive[q] = i < a.m;
+            const int64_t rbeg = rowlive[q] ? a.row_ptr[i] : 0;
+            rcol[q] = a.col + rbeg;
+            rval[q] = a.val + rbeg;
+            cursor[q] = 0;
+            rend[q] = rowlive[q] ? static_cast<int>(a.row_ptr[i + 1] - rbeg) : 0;
             fthr[q] = fthr_s[r0 + q];
             lo_ok[q] = 0.01 >= pthr_s[r0 + q];
             hi_ok[q] = 1.25 >= pthr_s[r0 + q];
@@ -189,13 +196,14 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
                 o4[lane] = make_float4(-1.f, -1.f, -1.f, -1.f);
             }
             __syncwarp();
+            const int c0i = static_cast<int>(c0);
 #pragma unroll
             for (int q = 0; q < kRPW; ++q) {
                 while (cursor[q] < rend[q]) {
-                    const int64_t e = cursor[q] + lane;
-                    const int32_t c = e < rend[q] ? a.col[e] : INT32_MAX;
-                    const bool in = c < c0 + kTC;
-                    if (in) obs[warp][q][c - c0] = a.val[e];
+                    const int e = cursor[q] + lane;
+                    const int c = e < rend[q] ? __ldg(rcol[q] + e) : INT32_MAX;
+                    const bool in = c < c0i + kTC;
+                    if (in) obs[warp][q][c - c0i] = __ldg(rval[q] + e);
                     const unsigned bal = __ballot_sync(0xffffffffu, in);
                     cursor[q] += __popc(bal);
                     if (bal != 0xffffffffu) break;
@@ -220,11 +228,12 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
             }
             // selection epilogue on the 16 cells (branch-free hot path; the
             // exact FP64 path runs only for cells within the band of the best)
-            int ci = static_cast<int>((c0 + lane * 4) / a.ngpu);
-            int gi = static_cast<int>(c0 + lane * 4 - static_cast<int64_t>(ci) * a.ngpu);
+            const int jb = c0i + lane * 4;
+            int ci = jb / a.ngpu;
+            int gi = jb - ci * a.ngpu;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int64_t j = c0 + lane * 4 + u;
+                const int j = jb + u;
                 if (u > 0 && ++gi == a.ngpu) {
                     gi = 0;
                     ++ci;
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
                 const float csf = static_cast<float>(cs);
 #pragma unroll
                 for (int q = 0; q < kRPW; ++q) {
-                    const bool live = jin && (rb + r0 + q < a.m);
+                    const bool live = jin && rowlive[q];
                     const float ov = obs[warp][q][lane * 4 + u];
                     const bool is_obs = ov > 0.0f;
                     const float pf = is_obs ? ov : acc[q][u];
@@ -243,13 +252,13 @@ __global__ void __launch_bounds__(256, 3) als_select_kernel(AlsSelectArgs a) {
                     const bool hi = !is_obs && pf > 1.25f;
                     const float pe = lo ? 0.01f : (hi ? 1.25f : pf);
                     const bool valid = live && (lo ? lo_ok[q] : (hi ? hi_ok[q] : pf >= fthr[q]));
-                    if (a.completed && live)
+                    if (WRITE_COMPLETED && live)
                         a.completed[(rb + r0 + q) * n + j] = lo ? 0.01 : (hi ? 1.25 : static_cast<double>(pf));
                     ncand[q] += valid ? 1 : 0;
                     const float tf = __fdividef(csf, pe);
                     if (valid && tf <= tbest[q] * kBand) {
                         const double pd = lo ? 0.01 : (hi ? 1.25 : static_cast<double>(pf));
-                        exact_update(myb + q * 32, pd, cs, static_cast<int>(j), a.e_base);
+                        exact_update(myb + q * 32, pd, cs, j, a.e_base);
                         tbest[q] = fminf(tbest[q], tf);
                     }
                 }
@@ -288,19 +297,15 @@ cudaError_t launch_als_select(const AlsSelectArgs& a, int sm_count, cudaStream_t
     const unsigned b = static_cast<unsigned>(blocks);
     const size_t smem = sizeof(float) * (2 * static_cast<size_t>(a.k) * kTC + 8 * kRPW * kTC) +
                         sizeof(BestExact) * 8 * kRPW * 32;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<b, 256, smem, s>>>(a);
+    };
+    const bool wc = a.completed != nullptr;
     switch (a.k) {
-        case 8:
-            cudaFuncSetAttribute(als_select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            als_select_kernel<8><<<b, 256, smem, s>>>(a);
-            break;
-        case 16:
-            cudaFuncSetAttribute(als_select_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            als_select_kernel<16><<<b, 256, smem, s>>>(a);
-            break;
-        case 32:
-            cudaFuncSetAttribute(als_select_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            als_select_kernel<32><<<b, 256, smem, s>>>(a);
-            break;
+        case 8: wc ? go(als_select_kernel<8, true>) : go(als_select_kernel<8, false>); break;
+        case 16: wc ? go(als_select_kernel<16, true>) : go(als_select_kernel<16, false>); break;
+        case 32: wc ? go(als_select_kernel<32, true>) : go(als_select_kernel<32, false>); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
