@@ -72,17 +72,19 @@ __device__ __noinline__ float chol_solve_warp(float* G, float b, float diag_add,
     float inv_diag = 1.0f;
     for (int c = 0; c < K; ++c) {
         const float* Gc = G + c * GS;
-        float s = Gl[c];
+        // four independent partial sums: no serial FFMA dependency chain
+        float s0 = Gl[c], s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
         int q = 0;
         for (; q + 4 <= c; q += 4) {
             const float4 a = *reinterpret_cast<const float4*>(Gl + q);
             const float4 w = *reinterpret_cast<const float4*>(Gc + q);
-            s = fmaf(-a.x, w.x, s);
-            s = fmaf(-a.y, w.y, s);
-            s = fmaf(-a.z, w.z, s);
-            s = fmaf(-a.w, w.w, s);
+            s0 = fmaf(-a.x, w.x, s0);
+            s1 = fmaf(-a.y, w.y, s1);
+            s2 = fmaf(-a.z, w.z, s2);
+            s3 = fmaf(-a.w, w.w, s3);
         }
-        for (; q < c; ++q) s = fmaf(-Gl[q], Gc[q], s);
+        for (; q < c; ++q) s0 = fmaf(-Gl[q], Gc[q], s0);
+        const float s = (s0 + s1) + (s2 + s3);
         const float piv = __shfl_sync(0xffffffffu, s, c);  // L[c][c]^2
         const float r = rsqrtf(piv);
         if (lane == c) inv_diag = r;
