@@ -242,6 +242,18 @@ int ocg_synth_rows_dense(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const
                          double density, int64_t dense_rows, uint64_t seed, const int64_t* rows, int64_t nrows,
                          double* values, uint8_t* mask);
 
+/* ---- probe ingest ----------------------------------
+ * pred::predict_perf (predictor.cpp:151-157) for `count` counter samples
+ * (count x 7 doubles in CounterSample field order, core.hpp:62-70):
+ * validate_counters, standardize with (mean7, std7), MLP forward
+ * (dims[0..n_layers], acts: 0 selu / 1 relu / 2 identity; params = per layer
+ * W (out x in, row-major) then b — the reference's model-file order,
+ * nnkit.cpp:306-330), clamp to [0.01, 1.25].  FP64, lane-exact.
+ * has_stats = 0 -> OCG_E_MISSING (missing_artifact_error, :152-153). */
+int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
+                           const double* params, const double* mean7, const double* std7, int has_stats,
+                           const double* counters, int64_t count, int lane, double* out);
+
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */
 double ocg_debug_exp_host(double x);                                       /* same code, host build */

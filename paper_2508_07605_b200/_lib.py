@@ -158,3 +158,6 @@ _sig("ocg_als_plan_gram_floats", c_i64, c_vp)
 _sig("ocg_als_plan_col_gram", ctypes.c_int, c_vp, c_vp)
 _sig("ocg_als_plan_col_solve", ctypes.c_int, c_vp, c_vp)
 _sig("ocg_als_plan_select", ctypes.c_int, c_vp)
+
+_sig("ocg_predict_perf_batch", ctypes.c_int, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i64,
+     ctypes.c_int, c_vp)

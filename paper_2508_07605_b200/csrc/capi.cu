@@ -16,6 +16,7 @@
 #include "ncf_infer.h"
 #include "ocg_common.cuh"
 #include "select.h"
+#include "predictor.h"
 
 constexpr size_t kFlushBytes = size_t(256) << 20;  // > 126 MB L2
 
@@ -626,6 +627,54 @@ int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* h, 
     OCG_CUDA(ocg::launch_ncf_predict(g, dp.p, dr.p, dc.p, count, dout.p, lane, s));
     OCG_CUDA(dout.download(out, static_cast<size_t>(count), s));
     OCG_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
+                           const double* params, const double* mean7, const double* std7, int has_stats,
+                           const double* counters, int64_t count, int lane, double* out) {
+    if (!ctx) return fail(OCG_E_INVALID, "null context");
+    // predict_perf (predictor.cpp:151-153): stats first
+    if (!has_stats) return fail(OCG_E_MISSING, "predictor model lacks feature standardization stats");
+    if (n_layers < 1 || n_layers > ocg::kPredMaxLayers) return fail(OCG_E_UNSUPPORTED, "predictor: layer count");
+    if (dims[0] != 7) return fail(OCG_E_INVALID, "forward: input dimension mismatch");
+    if (dims[n_layers] != 1) return fail(OCG_E_INVALID, "predictor: output dimension must be 1");
+    ocg::PredGeom g{};
+    g.L = n_layers;
+    int off = 0;
+    for (int l = 0; l <= n_layers; ++l) {
+        if (dims[l] <= 0 || dims[l] > ocg::kPredMaxWidth) return fail(OCG_E_UNSUPPORTED, "predictor: layer width");
+        g.dims[l] = static_cast<int>(dims[l]);
+    }
+    for (int l = 0; l < n_layers; ++l) {
+        if (acts[l] < 0 || acts[l] > 2) return fail(OCG_E_INVALID, "unknown activation");
+        g.acts[l] = acts[l];
+        g.off_w[l] = off;
+        off += g.dims[l] * g.dims[l + 1];
+        g.off_b[l] = off;
+        off += g.dims[l + 1];
+    }
+    g.T = off;
+    for (int q = 0; q < 7; ++q) {
+        g.mean[q] = mean7[q];
+        g.std[q] = std7[q];
+    }
+    if (ocg::predictor_smem_bytes(g) > 200 * 1024) return fail(OCG_E_UNSUPPORTED, "predictor too large");
+    if (count == 0) return OCG_OK;
+    cudaStream_t s = ctx->stream;
+    DBuf<double> dp, dc, dout;
+    DBuf<int> dbad;
+    OCG_CUDA(dp.upload(params, static_cast<size_t>(g.T), s));
+    OCG_CUDA(dc.upload(counters, static_cast<size_t>(count) * 7, s));
+    OCG_CUDA(dout.alloc(static_cast<size_t>(count)));
+    OCG_CUDA(dbad.alloc(1));
+    OCG_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), s));
+    OCG_CUDA(ocg::launch_predict_perf(g, dp.p, dc.p, count, dout.p, dbad.p, lane, ctx->sm_count, s));
+    int bad = 0;
+    OCG_CUDA(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    OCG_CUDA(dout.download(out, static_cast<size_t>(count), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    if (bad) return fail(OCG_E_INVALID, "invalid counter sample (non-finite, negative or activity outside [0,1])");
     return OCG_OK;
 }
 

@@ -1,0 +1,56 @@
+"""Probe ingest: pred::predict_perf (predictor.cpp:151-157) batched on the GPU.
+
+PredictorModel reads the reference's own predictor model file (nnkit model
+JSON + feature_stats, predictor.cpp:292-316)."""
+from __future__ import annotations
+
+import ctypes
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import check, lib, ptr
+from .api import LANE_AVX2, Context, default_context
+
+_ACT = {"selu": 0, "relu": 1, "identity": 2}
+
+
+@dataclass
+class PredictorModel:
+    dims: list
+    acts: list
+    params: np.ndarray  # per layer W (out x in row-major) then b
+    mean: np.ndarray
+    std: np.ndarray
+    has_stats: bool
+
+    @staticmethod
+    def from_json(text: str) -> "PredictorModel":
+        """pred::predictor_from_json (predictor.cpp:302-316) / nn::model_from_json (nnkit.cpp:332-365)."""
+        doc = json.loads(text)
+        if doc.get("format_version") != 1:
+            raise ValueError("model file: unsupported format_version")
+        dims = [int(d) for d in doc["architecture"]["dims"]]
+        acts = [_ACT[a] for a in doc["architecture"]["activations"]]
+        parts = []
+        for layer in doc["layers"]:
+            parts.append(np.asarray(layer["weights"], np.float64).ravel())
+            parts.append(np.asarray(layer["biases"], np.float64).ravel())
+        fs = doc.get("feature_stats")
+        mean = np.asarray(fs["mean"] if fs else [0.0] * 7, np.float64)
+        std = np.asarray(fs["std"] if fs else [1.0] * 7, np.float64)
+        return PredictorModel(dims, acts, np.concatenate(parts), mean, std, fs is not None)
+
+
+def predict_perf_batch(model: PredictorModel, counters, lane: int = LANE_AVX2,
+                       ctx: Context | None = None) -> np.ndarray:
+    """Normalized-performance estimates for counter samples (count x 7, CounterSample field order)."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(counters, np.float64).reshape(-1, 7)
+    dims = np.asarray(model.dims, np.int64)
+    acts = np.asarray(model.acts, np.int32)
+    out = np.zeros(len(c))
+    check(lib.ocg_predict_perf_batch(ctx.handle, len(acts), ptr(dims), ptr(acts), ptr(model.params), ptr(model.mean),
+                                     ptr(model.std), 1 if model.has_stats else 0, ptr(c), len(c), lane, ptr(out)))
+    return out

@@ -185,6 +185,43 @@ def golden_c0(ref: bind.Ref):
     return apps
 
 
+def golden_predictor(ref: bind.Ref, pred_json: str):
+    """pred::predict_perf on counters of the eval suite at every default-grid setting (+ CPU-phase counters)."""
+    import ctypes
+
+    specs = (bind.RefSpec * 20)()
+    cpu, gpu = np.asarray(DEFAULT_CPU, np.int32), np.asarray(DEFAULT_GPU, np.int32)
+    assert ref.L.ref_make_suite(5, 5, 5, 5, 42, 0.01, 1, 0.2, bind.P(cpu), 5, bind.P(gpu), 4, specs) == 0
+    rows = []
+    for sp in specs:
+        for c in DEFAULT_CPU:
+            for g in DEFAULT_GPU:
+                v = np.zeros(7)
+                ref.L.ref_sample_counters(ctypes.byref(sp), c, g, bind.P(v))
+                rows.append(v)
+    counters = np.array(rows)
+    # extremes: zero activity, saturated activity, huge throughput
+    extra = counters[:8].copy()
+    extra[0, 5] = extra[0, 6] = 0.0
+    extra[1, 5] = extra[1, 6] = 1.0
+    extra[2, 2] *= 50.0
+    extra[3, 4] = 0.0
+    counters = np.vstack([counters, extra])
+    out = {"counters": counters}
+    for lane in (0, 1):
+        ref.force_lane(lane)
+        o = np.zeros(len(counters))
+        rc = ref.L.ref_predict_perf(pred_json.encode(), bind.P(counters), len(counters), bind.P(o))
+        assert rc == 0, ref.err()
+        out[f"lane{lane}"] = o
+    ref.force_lane(1)
+    bad = counters[:1].copy()
+    bad[0, 2] = -1.0
+    rc_bad = ref.L.ref_predict_perf(pred_json.encode(), bind.P(bad), 1, bind.P(np.zeros(1)))
+    np.savez_compressed(OUT / "predictor.npz", **out)
+    return {"predict_rc_negative_ips": rc_bad}
+
+
 def main():
     bind.build(ref=True)
     ref = bind.Ref()
@@ -196,6 +233,7 @@ def main():
     golden["c0_apps"] = c0
     dense = np.load(OUT / "c0.npz")["dense"]
     golden["fit_cases"] = golden_fit(ref, dense)
+    golden.update(golden_predictor(ref, (OUT / "predictor.json").read_text()))
     # cf::complete seeds used by run_open_online for the 20 eval apps
     specs = ["ev_gpu_sensitive_%d", "ev_cpu_sensitive_%d", "ev_both_sensitive_%d", "ev_insensitive_%d"]
     ids = [s % k for s in specs for k in range(5)]

@@ -108,3 +108,14 @@ def test_oracle_vs_reference_random_fits(port, ref, lane):
     finally:
         ref.force_lane(1)
         port.set_lane(0)
+
+
+def test_predictor_model_json_parse():
+    """PredictorModel.from_json reads the reference's predictor file (predictor.cpp:302-316)."""
+    from conftest import GOLD
+    from paper_2508_07605_b200.predictor import PredictorModel
+
+    m = PredictorModel.from_json((GOLD / "predictor.json").read_text())
+    assert m.dims[0] == 7 and m.dims[-1] == 1 and m.has_stats
+    assert len(m.params) == sum(a * b + b for a, b in zip(m.dims[:-1], m.dims[1:]))
+    assert len(m.acts) == len(m.dims) - 1
