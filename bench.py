@@ -2,7 +2,7 @@
 """bench.py — B200 online CF completion + selection (OPEN online phase).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c0xn]
+                  [--workload c2|c1|c0xn|ingest]
 
 One JSON line on rank 0.  For N>1 launch with
 torch.distributed.run; each rank takes an equal shard of the units (weak
@@ -16,6 +16,9 @@ synthetic input:
   c0xn  the reference's own online semantics at scale: N independent apps,
         each cf::complete'd against the paper-scale offline block + selected
         (bit-exact NCF, one CTA per app)
+  ingest  probe ingest (SURVEY §8a row a3): pred::predict_perf over every
+        (app, setting) counter sample of 20K eval apps on the C2 64x64 grid
+        (81.9M samples, the C2 probe count), bit-exact FP64
 
 --impl reference times the reference's own CPU implementation of the path
 (oracle/_ref, compiled from the unmodified reference sources) on this host's
@@ -222,6 +225,113 @@ def workload_c0xn(args, d: Dist):
     return out, ("c0xn", per_gpu)
 
 
+def _simt_peaks():
+    """Measured FP64/FP32 SIMT peaks (tools/simt_peak.cu on a B200, profiles/simt_peak.json)."""
+    try:
+        return json.loads((ROOT / "profiles" / "simt_peak.json").read_text()), "measured (tools/simt_peak.cu)"
+    except Exception:
+        return {"fp64_tflops": 37.0, "fp32_tflops": 74.5}, "nominal (no measured SIMT peak)"
+
+
+PRED_MODEL = ROOT / "tests" / "golden" / "predictor.json"  # a predictor trained by the reference (make_golden.py)
+INGEST_APPS = 20_000  # x 4096 settings = 81.9M counter samples per GPU
+
+
+def _ingest_counters(apps: int, rank: int):
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+
+    grid = ocg.PowerGrid.spanning(64, 64)
+    specs = synth.make_suite([apps * (rank + 1) // 4] * 4, 42, 1, grid, 0.01, 0.2)
+    lo = apps * rank // 4
+    mine = [specs[a * (apps * (rank + 1) // 4) + lo + i] for a in range(4) for i in range(apps // 4)]
+    return grid, synth.counters(mine, grid)
+
+
+def workload_ingest(args, d: Dist):
+    """Batched pred::predict_perf (predictor.cpp:151-157) over the C2 probe volume, bit-exact FP64."""
+    import ctypes
+
+    import torch
+
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200.predictor import Predictor, PredictorModel
+
+    grid, counters = _ingest_counters(INGEST_APPS, d.rank)
+    count = len(counters)
+    dev = torch.device("cuda", d.local)
+    torch.cuda.set_device(dev)
+    ctx = ocg.Context(d.local)
+    stream = torch.cuda.current_stream(dev)
+    ocg._lib.check(ocg._lib.lib.ocg_ctx_set_stream(ctx.handle, ctypes.c_void_p(stream.cuda_stream)))
+    model = PredictorModel.from_json(PRED_MODEL.read_text())
+    pred = Predictor(model, ctx)
+    c_dev = torch.from_numpy(counters).to(dev)
+    out = torch.empty(count, dtype=torch.float64, device=dev)
+    for _ in range(args.warmup):
+        pred.run_device(c_dev.data_ptr(), count, out.data_ptr(), args.lane)
+    torch.cuda.synchronize()
+    d.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(d.local) as clk:
+        for e0, e1 in ev:  # 4.6 GB of counters per step: inputs larger than L2
+            e0.record(stream)
+            pred.run_device(c_dev.data_ptr(), count, out.data_ptr(), args.lane)
+            e1.record(stream)
+        torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    d.barrier()
+    t_dev = d.max(ms / 1e3)
+    res_dev = out.cpu().numpy()
+    # e2e: host counters in, host estimates out, through the public API
+    e2e_t = 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = pred(counters, args.lane)
+        e2e_t += time.perf_counter() - t0
+    e2e_t = d.max(e2e_t)
+    assert np.array_equal(res, res_dev)
+    total = count * d.world * args.steps
+    dims = model.dims
+    flops = 2 * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1)) + sum(dims[1:]) + 14
+    peaks, src = _simt_peaks()
+    achieved = flops * count * args.steps / (ms / 1e3) / 1e12
+    out_line = {
+        "metric": "probe performance estimates/sec",
+        "value": total / t_dev,
+        "unit": "estimates/s",
+        "ms_per_step": t_dev * 1e3 / args.steps,
+        "e2e": {"value": total / e2e_t, "unit": "estimates/s", "h2d_bytes_per_step": int(counters.nbytes),
+                "d2h_bytes_per_step": int(res.nbytes)},
+        "dtype": "f64",
+        "config": {"workload": "ingest", "samples_per_gpu": count, "apps_per_gpu": INGEST_APPS,
+                   "settings": grid.n, "architecture": dims, "lane": "avx2" if args.lane else "scalar",
+                   "model": "tests/golden/predictor.json (trained by the reference)",
+                   "l2": "inputs (4.6 GB counters) larger than L2"},
+        "scaling": "weak",
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["fp64_tflops"], "traffic": None,
+                     "note": f"algorithmic {flops} flop/sample (2*MACs + biases + standardize); peak {src}"},
+        "clocks": clk.summary(),
+    }
+    return out_line, ("ingest", count)
+
+
+def reference_ingest(samples: int, threads: int, lane: int = 1):
+    """pred::predict_perf of the reference (oracle/_ref) over the first `samples` ingest counters."""
+    from oracle import bind
+
+    ref = bind.Ref()
+    ref.force_lane(lane)
+    _, counters = _ingest_counters(max(4, samples // 4096 + 4), 0)
+    c = np.ascontiguousarray(counters[:samples])
+    out = np.zeros(len(c))
+    secs = ref.L.ref_predict_perf_mt(PRED_MODEL.read_text().encode(), bind.P(c), len(c), threads, bind.P(out))
+    assert secs > 0, ref.err()
+    return len(c) / secs, secs, len(c)
+
+
 JOINT = {  # SURVEY §8d joint configs
     "c1": dict(m=10_000, grid=(16, 16), density=0.05, dense_rows=10, rank=8),
     "c2": dict(m=1_000_000, grid=(64, 64), density=0.02, dense_rows=1000, rank=32),
@@ -359,7 +469,7 @@ def workload_joint(args, d: Dist):
     return out, (args.workload, m)
 
 
-WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint}
+WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "ingest": workload_ingest}
 
 
 # -------------------------------------------------------- reference (CPU)
@@ -432,6 +542,11 @@ def cpu_baseline(workload: str, threads: int):
         v, desc, secs = reference_joint(workload, threads, nprob=2 * threads)
         return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
                 "seconds": secs}
+    if workload == "ingest":
+        v, secs, n = reference_ingest(400_000 * threads, threads)
+        return {"value": v, "unit": "estimates/s", "cores": threads, "kind": "reference",
+                "sample": f"first {n} ingest counter samples, pred::predict_perf (oracle/_ref, AVX2 lane, "
+                          f"{threads} threads)", "seconds": secs}
     if workload == "c0xn":
         napps = max(threads * 8, 16)
         secs, _, _, n = reference_c0xn(napps, threads)
@@ -463,6 +578,25 @@ def run_reference(args, d: Dist):
                 "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
                                  "sample": f"{napps} apps per step, cf::complete + select_caps, AVX2 lane"},
                 "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    if args.workload == "ingest":
+        for _ in range(args.warmup):
+            reference_ingest(20_000 * threads, threads)
+        tot, cnt = 0.0, 0
+        for _ in range(args.steps):
+            v, secs, n = reference_ingest(200_000 * threads, threads)
+            tot += secs
+            cnt += n
+        v = cnt / tot
+        line = {"impl": "reference", "metric": "probe performance estimates/sec", "value": v, "unit": "estimates/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (sim::sample_counters of eval apps, C2 grid)",
+                "config": {"workload": "ingest", "samples_per_step": cnt // args.steps},
+                "cpu_baseline": {"value": v, "unit": "estimates/s", "cores": threads, "kind": "reference",
+                                 "sample": f"{cnt // args.steps} samples per step, pred::predict_perf, AVX2 lane"},
+                "e2e": {"value": v, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
     if args.workload in JOINT:
@@ -499,7 +633,7 @@ def main():
     ap.add_argument("--als-lambda", type=float, default=0.003)
     ap.add_argument("--gamma", type=float, default=0.05)
     ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")
-    ap.add_argument("--lane", type=int, default=1, help="c0xn: reference FP lane (0 scalar, 1 avx2)")
+    ap.add_argument("--lane", type=int, default=1, help="c0xn/ingest: reference FP lane (0 scalar, 1 avx2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -222,6 +222,11 @@ int ocg_synth_offline_block(uint64_t seed, const int32_t* cpu_caps, int32_t ncpu
 int ocg_synth_online_apps(int64_t napps, uint64_t seed, const int32_t* cpu_caps, int32_t ncpu,
                           const int32_t* gpu_caps, int32_t ngpu, double* probe_vals, uint8_t* probe_mask,
                           uint64_t* seeds);
+/* sim::sample_counters (simnode.cpp:98-110; cpu_phase != 0: sample_counters_cpu_phase
+ * :112-123) of every spec at every grid setting (lexicographic order):
+ * nspecs x ncpu*ngpu x 7 doubles in CounterSample field order */
+int ocg_synth_counters(const ocg_workload_spec* specs, int64_t nspecs, const int32_t* cpu_caps, int32_t ncpu,
+                       const int32_t* gpu_caps, int32_t ngpu, int cpu_phase, int nthreads, double* out);
 /* joint m x n matrix (first dense_rows rows dense) as CSR: count, then fill */
 int ocg_synth_csr_count(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
                         double density, int64_t dense_rows, uint64_t seed, int nthreads, int64_t* row_ptr);
@@ -253,6 +258,22 @@ int ocg_synth_rows_dense(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const
 int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
                            const double* params, const double* mean7, const double* std7, int has_stats,
                            const double* counters, int64_t count, int lane, double* out);
+
+/* A loaded predictor (pred::PredictorModel, predictor.hpp:60-68) resident on
+ * the context's device: create validates + uploads once, run streams counter
+ * batches through it.  run flags: OCG_PRED_DEVICE_PTRS -> counters/out are
+ * device pointers on the context's device (no host copies); OCG_PRED_GENERIC
+ * -> use the any-architecture kernel even for the reference architecture
+ * (7-64-64-1 SELU, which otherwise runs the thread-per-sample kernel).
+ * run is synchronous (it reports invalid counters, like validate_counters). */
+typedef struct ocg_predictor ocg_predictor;
+enum { OCG_PRED_DEVICE_PTRS = 1, OCG_PRED_GENERIC = 2 };
+int ocg_predictor_create(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
+                         const double* params, const double* mean7, const double* std7, int has_stats,
+                         ocg_predictor** out);
+int ocg_predictor_run(ocg_predictor* pred, const double* counters, int64_t count, int lane, double* out,
+                      uint32_t flags);
+int ocg_predictor_destroy(ocg_predictor* pred);
 
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */

@@ -209,6 +209,8 @@ class Ref:
         L.ref_ncf_complete.argtypes = [c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_u64, c_vp]
         L.ref_ncf_predict.argtypes = [ctypes.c_char_p, c_vp, c_vp, c_sz, c_vp]
         L.ref_predict_perf.argtypes = [ctypes.c_char_p, c_vp, c_sz, c_vp]
+        L.ref_predict_perf_mt.argtypes = [ctypes.c_char_p, c_vp, c_sz, ctypes.c_int, c_vp]
+        L.ref_predict_perf_mt.restype = c_dbl
         L.ref_make_suite.argtypes = [c_i32, c_i32, c_i32, c_i32, c_u64, c_dbl, c_i32, c_dbl, c_vp, c_sz, c_vp, c_sz,
                                      c_vp]
         L.ref_true_perf.restype = c_dbl

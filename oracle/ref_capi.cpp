@@ -8,6 +8,7 @@
 // comment; nothing here re-implements reference arithmetic.
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -252,6 +253,36 @@ int ref_predict_perf(const char* json, const double* counters, size_t count, dou
         return 0;
     } catch (...) {
         return map_exception();
+    }
+}
+
+// the same over `threads` host threads (contiguous sample ranges); returns the
+// wall seconds of the prediction loop (model parse excluded), <0 on error
+double ref_predict_perf_mt(const char* json, const double* counters, size_t count, int threads, double* out) {
+    try {
+        const auto model = pred::predictor_from_json(json);
+        std::atomic<int> bad{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                const size_t lo = count * t / threads, hi = count * (t + 1) / threads;
+                try {
+                    for (size_t k = lo; k < hi; ++k) {
+                        const double* c = counters + 7 * k;
+                        CounterSample s{c[0], c[1], c[2], c[3], c[4], c[5], c[6]};
+                        out[k] = pred::predict_perf(model, s);
+                    }
+                } catch (...) {
+                    bad = 1;
+                }
+            });
+        for (auto& th : pool) th.join();
+        const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return bad ? -1.0 : secs;
+    } catch (...) {
+        map_exception();
+        return -1.0;
     }
 }
 

@@ -159,5 +159,10 @@ _sig("ocg_als_plan_col_gram", ctypes.c_int, c_vp, c_vp)
 _sig("ocg_als_plan_col_solve", ctypes.c_int, c_vp, c_vp)
 _sig("ocg_als_plan_select", ctypes.c_int, c_vp)
 
+_sig("ocg_predictor_create", ctypes.c_int, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,
+     ctypes.POINTER(c_vp))
+_sig("ocg_predictor_run", ctypes.c_int, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, ctypes.c_uint32)
+_sig("ocg_predictor_destroy", ctypes.c_int, c_vp)
+OCG_PRED_DEVICE_PTRS, OCG_PRED_GENERIC = 1, 2
 _sig("ocg_predict_perf_batch", ctypes.c_int, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i64,
      ctypes.c_int, c_vp)

@@ -630,16 +630,25 @@ int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* h, 
     return OCG_OK;
 }
 
-int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
-                           const double* params, const double* mean7, const double* std7, int has_stats,
-                           const double* counters, int64_t count, int lane, double* out) {
-    if (!ctx) return fail(OCG_E_INVALID, "null context");
+struct ocg_predictor {
+    ocg_ctx* ctx = nullptr;
+    ocg::PredGeom g{};
+    DBuf<double> params;
+    DBuf<int> bad;
+};
+
+int ocg_predictor_create(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
+                         const double* params, const double* mean7, const double* std7, int has_stats,
+                         ocg_predictor** out) {
+    if (!ctx || !out || !dims || !acts || !params || !mean7 || !std7) return fail(OCG_E_INVALID, "null argument");
+    *out = nullptr;
     // predict_perf (predictor.cpp:151-153): stats first
     if (!has_stats) return fail(OCG_E_MISSING, "predictor model lacks feature standardization stats");
     if (n_layers < 1 || n_layers > ocg::kPredMaxLayers) return fail(OCG_E_UNSUPPORTED, "predictor: layer count");
     if (dims[0] != 7) return fail(OCG_E_INVALID, "forward: input dimension mismatch");
     if (dims[n_layers] != 1) return fail(OCG_E_INVALID, "predictor: output dimension must be 1");
-    ocg::PredGeom g{};
+    auto p = std::make_unique<ocg_predictor>();
+    ocg::PredGeom& g = p->g;
     g.L = n_layers;
     int off = 0;
     for (int l = 0; l <= n_layers; ++l) {
@@ -660,22 +669,59 @@ int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, 
         g.std[q] = std7[q];
     }
     if (ocg::predictor_smem_bytes(g) > 200 * 1024) return fail(OCG_E_UNSUPPORTED, "predictor too large");
-    if (count == 0) return OCG_OK;
+    p->ctx = ctx;
     cudaStream_t s = ctx->stream;
-    DBuf<double> dp, dc, dout;
-    DBuf<int> dbad;
-    OCG_CUDA(dp.upload(params, static_cast<size_t>(g.T), s));
-    OCG_CUDA(dc.upload(counters, static_cast<size_t>(count) * 7, s));
-    OCG_CUDA(dout.alloc(static_cast<size_t>(count)));
-    OCG_CUDA(dbad.alloc(1));
-    OCG_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), s));
-    OCG_CUDA(ocg::launch_predict_perf(g, dp.p, dc.p, count, dout.p, dbad.p, lane, ctx->sm_count, s));
+    OCG_CUDA(p->params.upload(params, static_cast<size_t>(g.T), s));
+    OCG_CUDA(p->bad.alloc(1));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    *out = p.release();
+    return OCG_OK;
+}
+
+int ocg_predictor_run(ocg_predictor* pred, const double* counters, int64_t count, int lane, double* out,
+                      uint32_t flags) {
+    if (!pred) return fail(OCG_E_INVALID, "null predictor");
+    if (count < 0) return fail(OCG_E_INVALID, "negative count");
+    if (lane != OCG_LANE_SCALAR && lane != OCG_LANE_AVX2) return fail(OCG_E_INVALID, "unknown kernel lane");
+    if (count == 0) return OCG_OK;
+    if (!counters || !out) return fail(OCG_E_INVALID, "null buffer");
+    ocg_ctx* ctx = pred->ctx;
+    cudaStream_t s = ctx->stream;
+    const bool on_dev = flags & OCG_PRED_DEVICE_PTRS;
+    DBuf<double> dc, dout;
+    const double* c = counters;
+    double* o = out;
+    if (!on_dev) {
+        OCG_CUDA(dc.upload(counters, static_cast<size_t>(count) * 7, s));
+        OCG_CUDA(dout.alloc(static_cast<size_t>(count)));
+        c = dc.p;
+        o = dout.p;
+    }
+    OCG_CUDA(cudaMemsetAsync(pred->bad.p, 0, sizeof(int), s));
+    OCG_CUDA(ocg::launch_predict_perf(pred->g, pred->params.p, c, count, o, pred->bad.p, lane, ctx->sm_count, s,
+                                      !(flags & OCG_PRED_GENERIC)));
     int bad = 0;
-    OCG_CUDA(cudaMemcpyAsync(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    OCG_CUDA(dout.download(out, static_cast<size_t>(count), s));
+    OCG_CUDA(cudaMemcpyAsync(&bad, pred->bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (!on_dev) OCG_CUDA(dout.download(out, static_cast<size_t>(count), s));
     OCG_CUDA(cudaStreamSynchronize(s));
     if (bad) return fail(OCG_E_INVALID, "invalid counter sample (non-finite, negative or activity outside [0,1])");
     return OCG_OK;
+}
+
+int ocg_predictor_destroy(ocg_predictor* pred) {
+    delete pred;
+    return OCG_OK;
+}
+
+int ocg_predict_perf_batch(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, const int32_t* acts,
+                           const double* params, const double* mean7, const double* std7, int has_stats,
+                           const double* counters, int64_t count, int lane, double* out) {
+    ocg_predictor* p = nullptr;
+    int rc = ocg_predictor_create(ctx, n_layers, dims, acts, params, mean7, std7, has_stats, &p);
+    if (rc != OCG_OK) return rc;
+    rc = ocg_predictor_run(p, counters, count, lane, out, 0);
+    ocg_predictor_destroy(p);
+    return rc;
 }
 
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out) {

@@ -80,12 +80,13 @@ struct LaneOps<1> {
 
 
 // SELU value and derivative from one exp (nnkit.cpp:27-45)
-__device__ __forceinline__ void selu_fwd(double z, double& a, double& gf) {
+template <class Tab = ExpTabConst>
+__device__ __forceinline__ void selu_fwd(double z, double& a, double& gf, Tab tab = Tab{}) {
     if (z > 0) {
         a = dmul(kLambda, z);
         gf = kLambda;
     } else {
-        const double e = glibc_exp(z);
+        const double e = glibc_exp_with(z, tab);
         a = dmul(kLA, dsub(e, 1.0));
         gf = dmul(kLA, e);
     }

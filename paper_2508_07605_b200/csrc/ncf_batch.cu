@@ -86,7 +86,7 @@ struct Smem {
     uint32_t oP;                    // [T] parameters
     uint32_t oact[kMaxLayers + 1];  // act[0] = gathered inputs X; act[l+1] = layer l output
     uint32_t odel[kMaxLayers];      // del[l]: act-grad factors, then deltas, of layer l output
-    uint32_t oig, ocval, ocrc, otset, ovset, operm[2], odraw, omt, orow, os_app, os_set, os_y, octrl;
+    uint32_t oig, ocval, ocrc, otset, ovset, operm[2], odraw, omt, orow, os_app, os_set, os_y, octrl, otab;
     __device__ __forceinline__ double* P() const { return smp<double>(oP); }
     __device__ __forceinline__ double* act(int l) const { return smp<double>(oact[l]); }
     __device__ __forceinline__ double* del(int l) const { return smp<double>(odel[l]); }
@@ -103,6 +103,8 @@ struct Smem {
     __device__ __forceinline__ int* s_set() const { return smp<int>(os_set); }
     __device__ __forceinline__ double* s_y() const { return smp<double>(os_y); }
     __device__ __forceinline__ int* ctrl() const { return smp<int>(octrl); }
+    // glibc exp table: SELU's exp runs on per-lane (divergent) arguments
+    __device__ __forceinline__ ExpTabPtr tab() const { return ExpTabPtr{smp<uint64_t>(otab)}; }
 };
 
 __device__ __forceinline__ uint32_t carve(uint32_t& p, size_t bytes) {
@@ -135,6 +137,7 @@ __device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom&
     S.os_set = carve(p, sizeof(int) * 32);
     S.os_y = carve(p, sizeof(double) * 32);
     S.octrl = carve(p, sizeof(int) * 16);
+    S.otab = carve(p, sizeof(uint64_t) * 256);
 }
 
 enum Ctrl { kMtIdx = 0, kStop = 1, kImproved = 2, kNt = 3, kNv = 4, kNc = 5, kDiverged = 6 };
@@ -205,7 +208,7 @@ __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const B
             for (int o = warp; o < out; o += kCW) {
                 const double z = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
                 double v = z, gf = 1.0;
-                if (hidden) selu_fwd(z, v, gf);
+                if (hidden) selu_fwd(z, v, gf, S.tab());
                 S.act(l + 1)[lane * a.stride(l + 1) + o] = v;
                 if (tape) S.del(l)[lane * a.stride(l + 1) + o] = gf;
             }
@@ -388,6 +391,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
     const bool is_rng = warp == kCW;
     const int ctid = tid;  // valid for compute threads
     MtWarp mt{S.mt(), S.ctrl() + kMtIdx};
+    for (int e = tid; e < 256; e += blockDim.x) smp<uint64_t>(S.otab)[e] = exp_tab(e);  // first app's sync publishes it
 
     // owned parameters (compile-time indexed so moments stay in registers)
     uint32_t own[kEPT];
@@ -688,6 +692,7 @@ size_t batch_smem_bytes(const BatchGeom& g) {
     add(sizeof(int) * 32);
     add(sizeof(double) * 32);
     add(sizeof(int) * 16);
+    add(sizeof(uint64_t) * 256);
     return b;
 }
 

@@ -19,7 +19,10 @@ struct PredGeom {
 };
 
 size_t predictor_smem_bytes(const PredGeom& g);
+bool predictor_is_fixed(const PredGeom& g);
+// allow_fixed: the reference architecture (7-64-64-1) runs the thread-per-sample
+// kernel, anything else (and allow_fixed=false) the warp-per-sample one
 cudaError_t launch_predict_perf(const PredGeom& g, const double* params, const double* counters, int64_t count,
-                                double* out, int* bad, int lane, int sm_count, cudaStream_t s);
+                                double* out, int* bad, int lane, int sm_count, cudaStream_t s, bool allow_fixed = true);
 
 }  // namespace ocg

@@ -185,6 +185,34 @@ int ocg_synth_suite(const int32_t counts[4], uint64_t seed, int role, double noi
     return OCG_OK;
 }
 
+int ocg_synth_counters(const ocg_workload_spec* specs, int64_t nspecs, const int32_t* cpu, int32_t ncpu,
+                       const int32_t* gpu, int32_t ngpu, int cpu_phase, int nthreads, double* out) {
+    if (!specs || !cpu || !gpu || !out || ncpu <= 0 || ngpu <= 0 || nspecs < 0) return OCG_E_INVALID;
+    const int64_t n = static_cast<int64_t>(ncpu) * ngpu;
+    parallel_rows(nspecs, nthreads, [&](int64_t a) {
+        const ocg_workload_spec& w = specs[a];
+        for (int32_t i = 0; i < ncpu; ++i)
+            for (int32_t j = 0; j < ngpu; ++j) {
+                const double fc = knee(cpu[i], w.kappa_c, w.alpha_c), fg = knee(gpu[j], w.kappa_g, w.alpha_g);
+                double* c = out + (a * n + static_cast<int64_t>(i) * ngpu + j) * 7;
+                c[0] = cpu[i];
+                c[1] = gpu[j];
+                c[2] = w.ips_max * fc;
+                c[3] = w.mem_tput_max * std::pow(fc, 0.8);
+                if (cpu_phase) {
+                    c[4] = 0.3 * w.sm_clock_max;  // idle clock floor
+                    c[5] = 0.02;
+                    c[6] = 0.05;
+                } else {
+                    c[4] = w.sm_clock_max * std::sqrt(std::min(1.0, gpu[j] / w.kappa_g));
+                    c[5] = fg;
+                    c[6] = std::min(1.0, 0.9 * fg + 0.1);
+                }
+            }
+    });
+    return OCG_OK;
+}
+
 double ocg_true_perf(const ocg_workload_spec* w, int32_t cpu_cap, int32_t gpu_cap) {
     return true_perf(*w, cpu_cap, gpu_cap);
 }

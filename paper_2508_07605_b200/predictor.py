@@ -10,7 +10,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import check, lib, ptr
+from ._lib import OCG_PRED_DEVICE_PTRS, OCG_PRED_GENERIC, check, lib, ptr
 from .api import LANE_AVX2, Context, default_context
 
 _ACT = {"selu": 0, "relu": 1, "identity": 2}
@@ -54,3 +54,42 @@ def predict_perf_batch(model: PredictorModel, counters, lane: int = LANE_AVX2,
     check(lib.ocg_predict_perf_batch(ctx.handle, len(acts), ptr(dims), ptr(acts), ptr(model.params), ptr(model.mean),
                                      ptr(model.std), 1 if model.has_stats else 0, ptr(c), len(c), lane, ptr(out)))
     return out
+
+
+class Predictor:
+    """A PredictorModel resident on the context's device (ocg_predictor_*)."""
+
+    def __init__(self, model: PredictorModel, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.model = model
+        dims = np.asarray(model.dims, np.int64)
+        acts = np.asarray(model.acts, np.int32)
+        h = ctypes.c_void_p()
+        check(lib.ocg_predictor_create(self.ctx.handle, len(acts), ptr(dims), ptr(acts), ptr(model.params),
+                                       ptr(model.mean), ptr(model.std), 1 if model.has_stats else 0,
+                                       ctypes.byref(h)))
+        self.handle = h
+
+    def __call__(self, counters, lane: int = LANE_AVX2, generic: bool = False) -> np.ndarray:
+        c = np.ascontiguousarray(counters, np.float64).reshape(-1, 7)
+        out = np.zeros(len(c))
+        check(lib.ocg_predictor_run(self.handle, ptr(c), len(c), lane, ptr(out), OCG_PRED_GENERIC if generic else 0))
+        return out
+
+    def run_device(self, counters_ptr: int, count: int, out_ptr: int, lane: int = LANE_AVX2,
+                   generic: bool = False) -> None:
+        """counters/out: device addresses (e.g. torch tensor data_ptr()) on the context's device."""
+        flags = OCG_PRED_DEVICE_PTRS | (OCG_PRED_GENERIC if generic else 0)
+        check(lib.ocg_predictor_run(self.handle, ctypes.c_void_p(counters_ptr), count, lane, ctypes.c_void_p(out_ptr),
+                                    flags))
+
+    def close(self):
+        if self.handle:
+            lib.ocg_predictor_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -60,7 +60,22 @@ def make_suite(counts, seed: int, role: int, grid: PowerGrid, noise_sigma=0.01, 
     cpu, gpu = grid.arrays()
     check(lib.ocg_synth_suite(ptr(cnt), seed, role, noise_sigma, cpu_phase_fraction, ptr(cpu), len(cpu), ptr(gpu),
                               len(gpu), out))
-    return list(out)
+    return out
+
+
+lib.ocg_synth_counters.argtypes = [c_vp, c_i64, c_vp, c_i32, c_vp, c_i32, ctypes.c_int, ctypes.c_int, c_vp]
+lib.ocg_synth_counters.restype = ctypes.c_int
+
+
+def counters(specs, grid: PowerGrid, cpu_phase: bool = False, threads: int | None = None) -> np.ndarray:
+    """sim::sample_counters of every spec at every setting: (len(specs) * grid.n, 7)."""
+    threads = threads or max(1, min(64, os.cpu_count() or 1))
+    arr = specs if isinstance(specs, ctypes.Array) else (WorkloadSpecC * len(specs))(*specs)
+    cpu, gpu = grid.arrays()
+    out = np.empty((len(arr) * grid.n, 7))
+    check(lib.ocg_synth_counters(arr, len(arr), ptr(cpu), len(cpu), ptr(gpu), len(gpu), int(cpu_phase), threads,
+                                 ptr(out)))
+    return out
 
 
 def true_perf(spec: WorkloadSpecC, cpu_cap: int, gpu_cap: int) -> float:

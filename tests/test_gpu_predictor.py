@@ -20,11 +20,28 @@ def model():
 
 @pytest.mark.parametrize("lane", [0, 1])
 def test_predict_perf_bit_exact(ctx, model, lane):
-    from paper_2508_07605_b200.predictor import predict_perf_batch
+    from paper_2508_07605_b200.predictor import Predictor, predict_perf_batch
 
     g = np.load(GOLD / "predictor.npz")
     out = predict_perf_batch(model, g["counters"], lane, ctx)
     np.testing.assert_array_equal(out, g[f"lane{lane}"])
+    p = Predictor(model, ctx)  # both kernels: thread-per-sample (reference arch) and warp-per-sample (any arch)
+    np.testing.assert_array_equal(p(g["counters"], lane), g[f"lane{lane}"])
+    np.testing.assert_array_equal(p(g["counters"], lane, generic=True), g[f"lane{lane}"])
+
+
+def test_predict_perf_device_pointers(ctx, model):
+    import torch
+
+    from paper_2508_07605_b200.predictor import Predictor
+
+    g = np.load(GOLD / "predictor.npz")
+    dev = torch.device("cuda", 0)
+    c = torch.from_numpy(g["counters"]).to(dev)
+    out = torch.zeros(len(c), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    Predictor(model, ctx).run_device(c.data_ptr(), len(c), out.data_ptr(), 1)
+    np.testing.assert_array_equal(out.cpu().numpy(), g["lane1"])
 
 
 def test_predict_perf_large_batch_consistent(ctx, model):

@@ -59,3 +59,33 @@ def test_joint_csr_shape_and_density():
         c = a.col[a.row_ptr[i]:a.row_ptr[i + 1]]
         assert (np.diff(c) > 0).all()
     assert ((a.val >= 0.01) & (a.val <= 1.25)).all()
+
+
+def test_counters_match_reference_golden():
+    """synth.counters == sim::sample_counters as the reference computed them (tests/golden/predictor.npz)."""
+    from conftest import GOLD
+    from paper_2508_07605_b200 import PowerGrid, synth
+
+    grid = PowerGrid.default_grid()
+    specs = synth.make_suite([5, 5, 5, 5], 42, 1, grid, 0.01, 0.2)
+    c = synth.counters(specs, grid)
+    g = np.load(GOLD / "predictor.npz")["counters"]
+    np.testing.assert_array_equal(c, g[: len(c)])
+
+
+def test_counters_cpu_phase_vs_reference(ref):
+    from oracle.bind import P
+    from paper_2508_07605_b200 import PowerGrid, synth
+
+    grid = PowerGrid.spanning(8, 8)
+    specs = synth.make_suite([3, 3, 3, 3], 9, 1, grid, 0.01, 0.2)
+    cpu, gpu = grid.arrays()
+    mine = synth.counters(specs, grid, cpu_phase=True)
+    assert mine.shape == (12 * 64, 7)
+    assert (mine[:, 5] == 0.02).all() and (mine[:, 4] > 0).all()
+    mine = synth.counters(specs, grid)
+    for a in (0, 5, 11):
+        for j in (0, 17, 63):
+            v = np.zeros(7)
+            ref.L.ref_sample_counters(ctypes.byref(specs[a]), int(cpu[j // 8]), int(gpu[j % 8]), P(v))
+            np.testing.assert_array_equal(mine[a * 64 + j], v)
