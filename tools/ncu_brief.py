@@ -23,9 +23,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=20)
+    ap.add_argument("--kernel", type=int, default=0, help="index of the launch in the report")
     a = ap.parse_args()
     rows = list(csv.reader(io.StringIO(ncu(a.rep, "--page", "raw", "--csv"))))
-    h, units, v = rows[0], rows[1], rows[2]
+    h, units, v = rows[0], rows[1], rows[2 + a.kernel]
     print("kernel:", v[h.index("Kernel Name")][:100])
     for k in KEYS:
         if k in h:
@@ -36,8 +37,10 @@ def main():
     print("  stall samples:")
     for k, x in sorted(st, key=lambda t: -t[1])[:8]:
         print(f"    {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):24s} {100 * x / tot:5.1f}%")
-    src = list(csv.reader(io.StringIO(ncu(a.rep, "--page", "source", "--csv", "--print-source", "sass"))))[1:]
-    hh, body = src[0], src[1:]
+    src = list(csv.reader(io.StringIO(ncu(a.rep, "--page", "source", "--csv", "--print-source", "sass"))))
+    starts = [i for i, r in enumerate(src) if r and r[0] == "Kernel Name"] + [len(src)]
+    sect = src[starts[a.kernel] + 1: starts[a.kernel + 1]]
+    hh, body = sect[0], [r for r in sect[1:] if len(r) == len(sect[0])]
     ia, isrc = hh.index("Address"), hh.index("Source")
     iss, iex = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Instructions Executed")
     tot = sum(float(r[iss] or 0) for r in body) or 1
