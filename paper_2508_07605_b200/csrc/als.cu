@@ -519,17 +519,29 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     if (blocks < 1) blocks = 1;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 8)));
     if (mode == 0) {
-        cudaFuncSetAttribute(als_seg_gram_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        als_seg_gram_kernel<K, 0><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
-            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X, h.partial,
-            h.lambda);
+        if (K == 32 && h.Yh) {
+            const cudaError_t e = launch_als_mma_gram(h, 0, sm_count, s);
+            if (e != cudaSuccess) return e;
+        } else {
+            cudaFuncSetAttribute(als_seg_gram_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            als_seg_gram_kernel<K, 0><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+                h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
+                h.partial, h.lambda);
+        }
         als_reduce_solve_kernel<K, 0><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.pfirst, h.partial, h.X,
                                                                  nullptr, h.lambda);
     } else {
-        cudaFuncSetAttribute(als_seg_gram_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
-            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X, h.partial,
-            h.lambda);
+        if (K == 32 && h.Yh) {
+            const cudaError_t e = launch_als_mma_gram(h, 1, sm_count, s);
+            if (e != cudaSuccess) return e;
+        } else {
+            cudaFuncSetAttribute(als_seg_gram_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+                h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
+                h.partial, h.lambda);
+        }
         als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.first, h.partial, nullptr,
                                                              h.gram_out, h.lambda);
     }

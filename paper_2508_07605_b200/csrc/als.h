@@ -26,6 +26,10 @@ struct AlsHalf {
     float* partial;   // partial-Gram slots x (K*K + K + 1)
     float* gram_out;  // mode 1: nitems x (K*K + K + 1)
     float lambda;
+    // rank-32 tensor-core path (als_mma.cu): Y packed as fp16 hi/lo rows
+    const uint4* Yh = nullptr;
+    const unsigned* ymax = nullptr;  // max |Y| (float bits) the packing scale came from
+    const unsigned* vmax = nullptr;  // max |val|
 };
 
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);
@@ -36,6 +40,10 @@ cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* n
 size_t als_gram_record_floats(int k);
 // mode 0: solve in place; mode 1: write reduced Gram records to gram_out
 cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
+// rank-32 tensor-core Gram (+ fused single-segment solve) + the packing of a factor matrix it gathers (als_mma.cu)
+cudaError_t launch_als_mma_gram(const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
+cudaError_t launch_als_pack(int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count, cudaStream_t s);
+cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int sm_count, cudaStream_t s);
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                        cudaStream_t s);
 cudaError_t launch_expand_rows(int64_t m, const int64_t* ptr, int32_t* rowid, int sm_count, cudaStream_t s);

@@ -83,6 +83,10 @@ struct ocg_als_plan {
     size_t scan_tmp_bytes = 0;
     // factors + outputs
     Buf<float> U, V, Vt;
+    // rank 32: factors packed as fp16 hi/lo rows for the tensor-core Gram + the
+    // max |.| each packing scale came from ([0] U, [1] V, [2] observed values)
+    Buf<uint4> Uh, Vh;
+    Buf<unsigned> maxbits;
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
     cudaEvent_t ev[6] = {};
@@ -138,7 +142,22 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     h.partial = S.partial.p;
     h.gram_out = nullptr;
     h.lambda = P->lambda;
+    if (P->k == 32) {
+        h.Yh = sd == 0 ? P->Vh.p : P->Uh.p;
+        h.ymax = P->maxbits.p + (sd == 0 ? 1 : 0);
+        h.vmax = P->maxbits.p + 2;
+    }
     return h;
+}
+
+// after a half-sweep (or V init): repack the factor the next half gathers
+static int als_pack(ocg_als_plan* P, int sd) {
+    if (P->k != 32) return OCG_OK;
+    const int64_t rows = sd == 0 ? P->m : P->n;
+    ALS_CUDA(ocg::launch_als_pack(rows, sd == 0 ? P->U.p : P->V.p, P->maxbits.p + (sd == 0 ? 0 : 1),
+                                  sd == 0 ? P->Uh.p : P->Vh.p, ocg_internal_sm_count(P->ctx),
+                                  ocg_internal_stream(P->ctx)));
+    return OCG_OK;
 }
 
 static int als_alloc(ocg_als_plan* P) {
@@ -179,6 +198,11 @@ static int als_alloc(ocg_als_plan* P) {
     ALS_CUDA(P->U.alloc(static_cast<size_t>(P->m * P->k)));
     ALS_CUDA(P->V.alloc(static_cast<size_t>(P->n * P->k)));
     ALS_CUDA(P->Vt.alloc(static_cast<size_t>(P->n * P->k)));
+    if (P->k == 32) {
+        ALS_CUDA(P->Uh.alloc(static_cast<size_t>(P->m * 8)));
+        ALS_CUDA(P->Vh.alloc(static_cast<size_t>(P->n * 8)));
+        ALS_CUDA(P->maxbits.alloc(3));
+    }
     ALS_CUDA(P->idx.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->ncand.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->saving.alloc(static_cast<size_t>(P->m)));
@@ -243,6 +267,8 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     }
     if (P->nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: nnz >= 2^31");
     if ((rc = als_alloc(P.get()))) return rc;
+    if (P->k == 32)
+        ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(ctx), s));
     ALS_CUDA(P->cpu.alloc(static_cast<size_t>(ncpu)));
     ALS_CUDA(P->gpu.alloc(static_cast<size_t>(ngpu)));
     ALS_CUDA(cudaMemcpyAsync(P->cpu.p, cpu, sizeof(int32_t) * ncpu, cudaMemcpyHostToDevice, s));
@@ -288,13 +314,16 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     int rc = als_build_csc(P);
     if (rc) return rc;
     ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
+    if ((rc = als_pack(P, 1))) return rc;
     ALS_CUDA(cudaEventRecord(P->ev[1], s));
     float row_ms = 0.f, col_ms = 0.f;
     for (int it = 0; it < P->sweeps; ++it) {
         ALS_CUDA(cudaEventRecord(P->ev[2], s));
         ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 0), 0, sm, s));
+        if ((rc = als_pack(P, 0))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[3], s));
         ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 1), 0, sm, s));
+        if ((rc = als_pack(P, 1))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[4], s));
         if (phase_ms) {
             float a = 0, b = 0;
@@ -328,19 +357,19 @@ int ocg_als_plan_begin(ocg_als_plan* P) {
     int rc = als_build_csc(P);
     if (rc) return rc;
     ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, ocg_internal_stream(P->ctx)));
-    return OCG_OK;
+    return als_pack(P, 1);
 }
 
 int ocg_als_plan_row_half(ocg_als_plan* P) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
     ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 0), 0, ocg_internal_sm_count(P->ctx), ocg_internal_stream(P->ctx)));
-    return OCG_OK;
+    return als_pack(P, 0);
 }
 
 int ocg_als_plan_col_half(ocg_als_plan* P) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
     ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 1), 0, ocg_internal_sm_count(P->ctx), ocg_internal_stream(P->ctx)));
-    return OCG_OK;
+    return als_pack(P, 1);
 }
 
 int64_t ocg_als_plan_gram_floats(ocg_als_plan* P) {
@@ -361,7 +390,7 @@ int ocg_als_plan_col_solve(ocg_als_plan* P, const float* d_gram) {
     if (!P || !d_gram) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     ALS_CUDA(ocg::launch_als_solve_from_gram(P->k, P->n, d_gram, P->V.p, P->lambda, ocg_internal_sm_count(P->ctx),
                                              ocg_internal_stream(P->ctx)));
-    return OCG_OK;
+    return als_pack(P, 1);
 }
 
 int ocg_als_plan_select(ocg_als_plan* P) {

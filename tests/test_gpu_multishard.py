@@ -7,7 +7,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_two_shard_schedule_matches_oracle(ctx, port):
+@pytest.mark.parametrize("k", [16, 32])  # 32: tensor-core Gram records (MODE 1)
+def test_two_shard_schedule_matches_oracle(ctx, port, k):
     import torch
 
     from oracle import bind
@@ -16,7 +17,7 @@ def test_two_shard_schedule_matches_oracle(ctx, port):
     from paper_2508_07605_b200.dist import GpuAlsBackend, shard_rows
 
     grid = PowerGrid.spanning(8, 16)
-    m, k, sweeps = 2000, 16, 5
+    m, sweeps = 2000, 5
     hyp = AlsHyper(rank=k, lam=0.003, sweeps=sweeps, seed=3)
     A = synth.joint_csr(m, grid, 0.1, 4, seed=21)
     dev = torch.device("cuda", 0)

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:als_seg_gram -c 2 -f \
+ncu --set full --clock-control none --import-source on -k regex:"als_(seg|mma)_gram" -c 2 -f \
     -o gpurun_out/c2_gram python bench.py --steps 1 --warmup 0 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:als_select -c 1 -f \
     -o gpurun_out/c2_select python bench.py --steps 1 --warmup 0 --no-cpu-baseline > /dev/null 2>&1
