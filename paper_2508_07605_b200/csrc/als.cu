@@ -131,14 +131,28 @@ __device__ __forceinline__ void load_vec(float (&dst)[N], const float* src) {
 // (exclusive prefix sum of nseg, computed with cub on the host side).
 // nmulti[i] = nseg[i] if the item needs partial Grams (nseg > 1), else 0; its
 // exclusive prefix sum pfirst[] places an item's partials contiguously.
+// Items with nseg > 1 are also appended (in any order) to multi_list /
+// *multi_count (zeroed by the caller) so the reduce pass visits only them.
 __global__ void seg_count_kernel(int64_t nitems, const int64_t* __restrict__ ptr, int32_t* __restrict__ nseg,
-                                 int32_t* __restrict__ nmulti, int force_partials) {
+                                 int32_t* __restrict__ nmulti, int force_partials, int32_t* __restrict__ multi_list,
+                                 int32_t* __restrict__ multi_count) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nitems) return;
     const int64_t cnt = ptr[i + 1] - ptr[i];
     const int32_t ns = cnt == 0 ? 1 : static_cast<int32_t>((cnt + kSeg - 1) / kSeg);
     nseg[i] = ns;
     nmulti[i] = (ns > 1 || force_partials) ? ns : 0;
+    if (ns > 1 && multi_list) multi_list[atomicAdd(multi_count, 1)] = static_cast<int32_t>(i);
+}
+
+// column side: segment sort key = row of its first observation (the L2 band
+// its factor gathers touch); padding slots sort last
+__global__ void seg_key_kernel(int32_t max_segs, const int32_t* __restrict__ total, const int64_t* __restrict__ seg_beg,
+                               const int32_t* __restrict__ idx, int32_t* __restrict__ key, int32_t* __restrict__ id) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= max_segs) return;
+    key[s] = s < *total ? idx[seg_beg[s]] : 0x7fffffff;
+    id[s] = s;
 }
 
 __global__ void seg_fill_kernel(int64_t nitems, const int64_t* __restrict__ ptr, const int32_t* __restrict__ nseg,
@@ -385,8 +399,11 @@ __global__ void __launch_bounds__(256, 3) als_seg_gram_kernel(const int32_t* __r
 
 // Sum an item's segment partials in segment order; MODE 0 solves, MODE 1
 // writes the reduced record (Gram, rhs, count) to Gout[item].
+// MODE 0 visits only the listed (multi-segment) items when list != nullptr.
 template <int K, int MODE>
-__global__ void __launch_bounds__(256) als_reduce_solve_kernel(int64_t nitems, const int64_t* __restrict__ ptr,
+__global__ void __launch_bounds__(256) als_reduce_solve_kernel(int64_t nitems, const int32_t* __restrict__ list,
+                                                               const int32_t* __restrict__ list_count,
+                                                               const int64_t* __restrict__ ptr,
                                                                const int32_t* __restrict__ nseg_of,
                                                                const int32_t* __restrict__ first,
                                                                const float* __restrict__ partial,
@@ -396,7 +413,9 @@ __global__ void __launch_bounds__(256) als_reduce_solve_kernel(int64_t nitems, c
     __shared__ __align__(16) float G[K * GS];
     __shared__ float rhs[K];
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
         const int32_t ns = nseg_of[item];
         if (MODE == 0 && ns == 1) continue;  // solved by the segment kernel
         const float* base = partial + static_cast<int64_t>(first[item]) * GSZ;  // first = pfirst here
@@ -494,9 +513,20 @@ cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStrea
 }
 
 cudaError_t launch_seg_count(int64_t nitems, const int64_t* ptr, int32_t* nseg, int32_t* nmulti, int force_partials,
-                             cudaStream_t s) {
+                             int32_t* multi_list, int32_t* multi_count, cudaStream_t s) {
+    if (multi_count) {
+        const cudaError_t e = cudaMemsetAsync(multi_count, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return e;
+    }
     seg_count_kernel<<<static_cast<unsigned>((nitems + 255) / 256), 256, 0, s>>>(nitems, ptr, nseg, nmulti,
-                                                                                  force_partials);
+                                                                                  force_partials, multi_list,
+                                                                                  multi_count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg_key(int32_t max_segs, const int32_t* total, const int64_t* seg_beg, const int32_t* idx,
+                           int32_t* key, int32_t* id, cudaStream_t s) {
+    seg_key_kernel<<<static_cast<unsigned>((max_segs + 255) / 256), 256, 0, s>>>(max_segs, total, seg_beg, idx, key, id);
     return cudaGetLastError();
 }
 
@@ -529,8 +559,9 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
                 h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
                 h.partial, h.lambda);
         }
-        als_reduce_solve_kernel<K, 0><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.pfirst, h.partial, h.X,
-                                                                 nullptr, h.lambda);
+        if (K == 32 && h.Yh && h.multi_list) return launch_als_reduce_solve32(h, sm_count, s);
+        als_reduce_solve_kernel<K, 0><<<rblocks, 256, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.ptr, h.nseg,
+                                                                 h.pfirst, h.partial, h.X, nullptr, h.lambda);
     } else {
         if (K == 32 && h.Yh) {
             const cudaError_t e = launch_als_mma_gram(h, 1, sm_count, s);
@@ -542,8 +573,8 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
                 h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
                 h.partial, h.lambda);
         }
-        als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, h.ptr, h.nseg, h.first, h.partial, nullptr,
-                                                             h.gram_out, h.lambda);
+        als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, nullptr, nullptr, h.ptr, h.nseg, h.first,
+                                                                 h.partial, nullptr, h.gram_out, h.lambda);
     }
     return cudaGetLastError();
 }

@@ -30,11 +30,19 @@ struct AlsHalf {
     const uint4* Yh = nullptr;
     const unsigned* ymax = nullptr;  // max |Y| (float bits) the packing scale came from
     const unsigned* vmax = nullptr;  // max |val|
+    const uint32_t* valh = nullptr;  // observed values packed (fp16 hi, fp16 lo) of val * 2^ev
+    // optional: multi-segment items (MODE 0 reduce visits only these) and a
+    // processing order of the segments (column side: sorted by first row)
+    const int32_t* multi_list = nullptr;
+    const int32_t* multi_count = nullptr;
+    const int32_t* seg_order = nullptr;
 };
 
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);
 cudaError_t launch_seg_count(int64_t nitems, const int64_t* ptr, int32_t* nseg, int32_t* nmulti, int force_partials,
-                             cudaStream_t s);
+                             int32_t* multi_list, int32_t* multi_count, cudaStream_t s);
+cudaError_t launch_seg_key(int32_t max_segs, const int32_t* total, const int64_t* seg_beg, const int32_t* idx,
+                           int32_t* key, int32_t* id, cudaStream_t s);
 cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* nseg, const int32_t* first,
                             int32_t* seg_item, int64_t* seg_beg, int32_t* total, cudaStream_t s);
 size_t als_gram_record_floats(int k);
@@ -42,7 +50,9 @@ size_t als_gram_record_floats(int k);
 cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
 // rank-32 tensor-core Gram (+ fused single-segment solve) + the packing of a factor matrix it gathers (als_mma.cu)
 cudaError_t launch_als_mma_gram(const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
+cudaError_t launch_als_reduce_solve32(const AlsHalf& h, int sm_count, cudaStream_t s);
 cudaError_t launch_als_pack(int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count, cudaStream_t s);
+cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vmax, uint32_t* out, cudaStream_t s);
 cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int sm_count, cudaStream_t s);
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                        cudaStream_t s);

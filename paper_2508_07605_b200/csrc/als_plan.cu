@@ -74,7 +74,11 @@ struct ocg_als_plan {
     size_t sort_tmp_bytes = 0;
     // segment tables (index 0: rows over CSR, 1: columns over CSC)
     struct Side {
-        Buf<int32_t> nseg, first, nmulti, pfirst, seg_item, total;
+        Buf<int32_t> nseg, first, nmulti, pfirst, seg_item, total;  // total: [0] segments, [1] multi items
+        Buf<int32_t> multi_list;
+        Buf<int32_t> seg_order, seg_key, seg_key_out, seg_id;  // column side: processing order
+        Buf<uint8_t> order_tmp;
+        size_t order_tmp_bytes = 0;
         Buf<int64_t> seg_beg;
         Buf<float> partial;
         int32_t max_segs = 0;
@@ -87,6 +91,7 @@ struct ocg_als_plan {
     // max |.| each packing scale came from ([0] U, [1] V, [2] observed values)
     Buf<uint4> Uh, Vh;
     Buf<unsigned> maxbits;
+    Buf<uint32_t> valh;  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
     cudaEvent_t ev[6] = {};
@@ -106,19 +111,27 @@ static int als_build_csc(ocg_als_plan* P) {
         size_t bytes = P->sort_tmp_bytes;
         ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, P->col.p, P->keys_out.p, P->perm_in.p,
                                                  P->perm_out.p, P->nnz, 0, bits_for(P->n), s));
-        ALS_CUDA(ocg::launch_gather_csc(P->nnz, P->perm_out.p, P->rowid.p, P->val.p, P->crow.p, P->cval.p, s));
+        // rank 32: the column side gathers the packed values (same 4-byte moves)
+        const float* cv = P->k == 32 ? reinterpret_cast<const float*>(P->valh.p) : P->val.p;
+        ALS_CUDA(ocg::launch_gather_csc(P->nnz, P->perm_out.p, P->rowid.p, cv, P->crow.p, P->cval.p, s));
     }
     ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
     for (int sd = 0; sd < 2; ++sd) {
         auto& S = P->side[sd];
         const int64_t items = sd == 0 ? P->m : P->n;
         const int64_t* ptr = sd == 0 ? P->row_ptr.p : P->col_ptr.p;
-        ALS_CUDA(ocg::launch_seg_count(items, ptr, S.nseg.p, S.nmulti.p, 0, s));
+        ALS_CUDA(ocg::launch_seg_count(items, ptr, S.nseg.p, S.nmulti.p, 0, S.multi_list.p, S.total.p + 1, s));
         size_t b = P->scan_tmp_bytes;
         ALS_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, b, S.nseg.p, S.first.p, items, s));
         b = P->scan_tmp_bytes;
         ALS_CUDA(cub::DeviceScan::ExclusiveSum(P->scan_tmp.p, b, S.nmulti.p, S.pfirst.p, items, s));
         ALS_CUDA(ocg::launch_seg_fill(items, ptr, S.nseg.p, S.first.p, S.seg_item.p, S.seg_beg.p, S.total.p, s));
+        if (S.seg_order.p) {
+            ALS_CUDA(ocg::launch_seg_key(S.max_segs, S.total.p, S.seg_beg.p, P->crow.p, S.seg_key.p, S.seg_id.p, s));
+            size_t ob = S.order_tmp_bytes;
+            ALS_CUDA(cub::DeviceRadixSort::SortPairs(S.order_tmp.p, ob, S.seg_key.p, S.seg_key_out.p, S.seg_id.p,
+                                                     S.seg_order.p, S.max_segs, 0, 31, s));
+        }
     }
     return OCG_OK;
 }
@@ -137,12 +150,16 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     h.nseg = S.nseg.p;
     h.first = S.first.p;
     h.pfirst = S.pfirst.p;
+    h.multi_list = S.multi_list.p;
+    h.multi_count = S.total.p + 1;
+    h.seg_order = S.seg_order.p;
     h.Y = sd == 0 ? P->V.p : P->U.p;
     h.X = sd == 0 ? P->U.p : P->V.p;
     h.partial = S.partial.p;
     h.gram_out = nullptr;
     h.lambda = P->lambda;
     if (P->k == 32) {
+        h.valh = sd == 0 ? P->valh.p : reinterpret_cast<const uint32_t*>(P->cval.p);
         h.Yh = sd == 0 ? P->Vh.p : P->Uh.p;
         h.ymax = P->maxbits.p + (sd == 0 ? 1 : 0);
         h.vmax = P->maxbits.p + 2;
@@ -181,7 +198,19 @@ static int als_alloc(ocg_als_plan* P) {
         S.max_segs = static_cast<int32_t>(ms);
         ALS_CUDA(S.nseg.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.first.alloc(static_cast<size_t>(items)));
-        ALS_CUDA(S.total.alloc(1));
+        ALS_CUDA(S.total.alloc(2));
+        ALS_CUDA(S.multi_list.alloc(static_cast<size_t>(items)));
+        if (sd == 1 && P->k == 32) {
+            ALS_CUDA(S.seg_order.alloc(static_cast<size_t>(ms)));
+            ALS_CUDA(S.seg_key.alloc(static_cast<size_t>(ms)));
+            ALS_CUDA(S.seg_key_out.alloc(static_cast<size_t>(ms)));
+            ALS_CUDA(S.seg_id.alloc(static_cast<size_t>(ms)));
+            size_t ob = 0;
+            ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, ob, S.seg_key.p, S.seg_key_out.p, S.seg_id.p,
+                                                     S.seg_order.p, static_cast<int>(ms), 0, 31));
+            S.order_tmp_bytes = ob;
+            ALS_CUDA(S.order_tmp.alloc(ob));
+        }
         ALS_CUDA(S.seg_item.alloc(static_cast<size_t>(ms)));
         ALS_CUDA(S.seg_beg.alloc(static_cast<size_t>(ms)));
         // partial Grams only for items with >1 segment: sum of their nseg <= 2*nnz/kSeg
@@ -267,8 +296,11 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     }
     if (P->nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: nnz >= 2^31");
     if ((rc = als_alloc(P.get()))) return rc;
-    if (P->k == 32)
+    if (P->k == 32) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(ctx), s));
+        ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
+        ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
+    }
     ALS_CUDA(P->cpu.alloc(static_cast<size_t>(ncpu)));
     ALS_CUDA(P->gpu.alloc(static_cast<size_t>(ngpu)));
     ALS_CUDA(cudaMemcpyAsync(P->cpu.p, cpu, sizeof(int32_t) * ncpu, cudaMemcpyHostToDevice, s));
