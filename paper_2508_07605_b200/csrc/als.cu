@@ -537,7 +537,8 @@ cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* n
     return cudaGetLastError();
 }
 
-size_t als_gram_record_floats(int k) { return static_cast<size_t>(k) * k + k + 1; }
+// rank 32 (tensor-core path): packed lower-triangle record of als_mma.cu
+size_t als_gram_record_floats(int k) { return k == 32 ? als_record_floats32() : static_cast<size_t>(k) * k + k + 1; }
 
 template <int K>
 static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
@@ -549,30 +550,19 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     if (blocks < 1) blocks = 1;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 8)));
     if (mode == 0) {
-        if (K == 32 && h.Yh) {
-            const cudaError_t e = launch_als_mma_gram(h, 0, sm_count, s);
-            if (e != cudaSuccess) return e;
-        } else {
-            cudaFuncSetAttribute(als_seg_gram_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            als_seg_gram_kernel<K, 0><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
-                h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
-                h.partial, h.lambda);
-        }
-        if (K == 32 && h.Yh && h.multi_list) return launch_als_reduce_solve32(h, sm_count, s);
+        cudaFuncSetAttribute(als_seg_gram_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        als_seg_gram_kernel<K, 0><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
+            h.partial, h.lambda);
         als_reduce_solve_kernel<K, 0><<<rblocks, 256, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.ptr, h.nseg,
                                                                  h.pfirst, h.partial, h.X, nullptr, h.lambda);
     } else {
-        if (K == 32 && h.Yh) {
-            const cudaError_t e = launch_als_mma_gram(h, 1, sm_count, s);
-            if (e != cudaSuccess) return e;
-        } else {
-            cudaFuncSetAttribute(als_seg_gram_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-            als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
-                h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
-                h.partial, h.lambda);
-        }
+        cudaFuncSetAttribute(als_seg_gram_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        als_seg_gram_kernel<K, 1><<<static_cast<unsigned>(blocks), 256, smem, s>>>(
+            h.total_segs, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.idx, h.val, h.Y, h.X,
+            h.partial, h.lambda);
         als_reduce_solve_kernel<K, 1><<<rblocks, 256, 0, s>>>(h.nitems, nullptr, nullptr, h.ptr, h.nseg, h.first,
                                                                  h.partial, nullptr, h.gram_out, h.lambda);
     }
@@ -580,6 +570,7 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
 }
 
 cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+    if (k == 32 && h.Yh) return launch_als_mma_half(h, mode, sm_count, s);
     switch (k) {
         case 8: return launch_half_k<8>(h, mode, sm_count, s);
         case 16: return launch_half_k<16>(h, mode, sm_count, s);
@@ -590,6 +581,7 @@ cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cud
 
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                        cudaStream_t s) {
+    if (k == 32) return launch_als_solve_records(nitems, G, X, lambda, sm_count, s);
     int64_t blocks = (nitems + 7) / 8;
     if (blocks > sm_count * 16) blocks = sm_count * 16;
     if (blocks < 1) blocks = 1;

@@ -1,29 +1,32 @@
-// ALS K3 Gram accumulation on the tensor cores (rank 32) + register-resident
-// Cholesky (K4), fused per segment.
+// ALS rank-32 half-sweep on B200: K3 Gram accumulation on the tensor cores,
+// K4 batched Cholesky with one system per lane.
 //
 // Semantics: oracle/ocg_oracle.c ocgo_als_fit (weighted-lambda ALS; no
-// reference counterpart).  Same work decomposition as the
-// SIMT kernel in als.cu (warp per <= kSeg-observation segment, single-segment
-// items solved in place, multi-segment items reduced in segment order by
-// als_reduce_solve_kernel), different arithmetic:
+// reference counterpart): x_i = (G_i + lambda n_i I)^-1 b_i,
+// G_i = sum_j y_j y_j^T and b_i = sum_j r_ij y_j over item i's observations.
 //
-// * Factor rows are gathered as FP16 hi/lo pairs, written once per half-sweep
+// K3 als_mma_gram32_kernel: warp per <= kSeg-observation segment.
+// * Factor rows are gathered as FP16 hi/lo pairs written once per half-sweep
 //   by als_pack_kernel: y*s = hi + lo (hi = fp16(y*s), lo = fp16(y*s - hi)),
-//   s = 2^e a power-of-two scale from the factor matrix's max |y| (so y*s <=
-//   2^14 and lo stays a normal fp16 for every entry that matters).  The packed
-//   row is 8 x 16 B: chunk g = {hi[4g..4g+3], lo[4g..4g+3]}.
-// * Gram = H^T H + H^T L + L^T H (the L^T L term is below 2^-22 relative) with
-//   mma.sync m16n8k16 f16 -> f32.  A lane loads ONE 16-byte chunk g of four
-//   observation rows and byte-permutes them into the B fragments of all four
-//   n-tiles (MMA column 8j+g <-> factor dim 4g+j); the A fragments of the two
-//   m-tiles are the same registers.  Per 16 observations: 6 MMAs for the
-//   lower tiles of H^T H, 8 for S = H^T L (full; G = HH + S + S^T), 4 for the
-//   rhs (B = [r_hi, r_lo, 0..]).  That replaces 18 FFMA/observation/lane.
-// * Epilogue: fragments -> shared (natural dim order, mirrored), lane l builds
-//   row l of G + lambda*n*I in registers, then a fully unrolled left-looking
-//   Cholesky (row c of L broadcast from shared with LDS.128) with the forward
-//   substitution folded into the factorisation loop, and a column-oriented
-//   back substitution.
+//   s = 2^e from the factor matrix's max |y| (y*s <= 2^14, lo stays normal for
+//   every entry that matters).  Packed row = 8 x 16 B, chunk g = {hi[4g..4g+3],
+//   lo[4g..4g+3]}.  Observed values are packed the same way once per plan.
+// * G = H^T H + H^T L + L^T H (L^T L is below 2^-22 relative) with mma.sync
+//   m16n8k16 f16 -> f32 on the 6 lower tiles (in MMA index space) of the
+//   32x32 Gram: a lane loads ONE 16-byte chunk g of four observation rows and
+//   byte-permutes it into the B fragments of all four n-tiles (MMA column
+//   8j+g <-> factor dim 4g+j); the A fragments of the two m-tiles are the same
+//   registers.  rhs: (H + L)^T [r_hi r_lo].  22 MMAs per 16 observations.
+// * Output: one RECORD per segment (als_rec layout below), unscaled FP32,
+//   written straight from the accumulator fragments.
+// Reduce (multi-segment items): records summed in segment order into the
+// item's first slot (deterministic).
+// K4 als_solve_records_kernel: 32 items per warp, ONE ITEM PER LANE: the
+// records are staged in shared memory (row stride 612 floats = 4 mod 32
+// banks, so 16-byte loads of 8 lanes at the same offset are conflict-free)
+// and each lane runs a left-looking Cholesky + two substitutions on its own
+// system -- no idle lanes, no shuffles (a lane-per-row Cholesky wastes 2/3 of
+// its FMAs on the upper triangle and serialises 64 shuffles per system).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -133,84 +136,37 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return y;
 }
 
-// Gram / L rows in shared memory: 32 floats per row, 16-byte chunk cc of row a
-// stored at chunk cc ^ (a & 7) so that 8 lanes reading 8 different rows' same
-// chunk (LDS.128) hit 8 different bank groups; broadcasts of one row and
-// column reads (lane = column) stay conflict-free.
-__device__ __forceinline__ int gidx(int a, int b) { return a * K + ((((b >> 2) ^ a) & 7) << 2) + (b & 3); }
+// ---- record layout (floats): padded lower triangle, row i at T(i) with its
+// length rounded up to 4 (16-byte aligned rows), rhs at 576, count at 608.
+constexpr int kRec = 612;
+constexpr int kRhs = 576;
+constexpr int kCnt = 608;
+__host__ __device__ constexpr int tri_off(int i) { return 4 * ((i >> 2) + 1) * (2 * (i >> 2) + (i & 3)); }
+static_assert(tri_off(32) == kRhs, "record layout");
 
-// Solve A x = b on one warp; lane l holds row l of A (SPD) in a[] and b_l.
-// L overwrites a[] (lane l: row l of L, entries above the diagonal are
-// garbage); Ls (32 x 32 swizzled, warp-private) mirrors L row-wise so row c
-// can be broadcast.  The forward substitution L y = b rides along in the
-// factorisation loop (t); the back substitution is column-oriented.
-__device__ __forceinline__ float chol_solve_regs(float (&a)[K], float b, float* Ls, int lane) {
-    float inv = 0.0f;
-    float t = b;  // b_l - sum_{q<c} L[l][q] y_q; lanes < c hold y_l
-#pragma unroll
-    for (int c = 0; c < K; ++c) {
-        float s0 = a[c], s1 = 0.0f, s2 = 0.0f, s3 = 0.0f;
-#pragma unroll
-        for (int q = 0; q + 4 <= c; q += 4) {
-            const float4 w = *reinterpret_cast<const float4*>(Ls + gidx(c, q));
-            s0 = fmaf(-a[q], w.x, s0);
-            s1 = fmaf(-a[q + 1], w.y, s1);
-            s2 = fmaf(-a[q + 2], w.z, s2);
-            s3 = fmaf(-a[q + 3], w.w, s3);
-        }
-#pragma unroll
-        for (int q = c & ~3; q < c; ++q) s0 = fmaf(-a[q], Ls[gidx(c, q)], s0);
-        const float s = (s0 + s1) + (s2 + s3);
-        const float piv = __shfl_sync(0xffffffffu, s, c);
-        const float tc = __shfl_sync(0xffffffffu, t, c);
-        const float r = rsqrt_ftz(piv);
-        a[c] = s * r;  // L[l][c] (lane c: the diagonal)
-        Ls[gidx(lane, c)] = a[c];
-        inv = lane == c ? r : inv;
-        const float yc = tc * r;  // y_c
-        t = lane == c ? yc : (lane > c ? fmaf(-a[c], yc, t) : t);
-        __syncwarp();
-    }
-    // L^T x = y (lane l holds y_l in t)
-    float y = t;
-#pragma unroll
-    for (int c = K - 1; c >= 0; --c) {
-        const float lc = Ls[gidx(c, lane)];  // L[c][l]
-        const float xc = __shfl_sync(0xffffffffu, y * inv, c);
-        if (lane == c) y = xc;
-        else if (lane < c) y = fmaf(-lc, xc, y);
-    }
-    return y;
-}
-
-// MODE 0: fused solve of single-segment items, partial records for the rest.
-// MODE 1: partial records for every segment (multi-GPU column side).
+// K3.  MODE 0 and 1 are identical here (every segment writes its record to
+// slot = segment id); the difference is in the reduce step.
 //
 // Gathers: 8 lanes copy one 128-byte factor row with 16-byte cp.async (rows
 // past the chunk are zero-filled); 16-byte chunk c of stage row o sits at
 // chunk c ^ (o & 7), which makes the fragment loads conflict-free.  (One TMA
 // bulk copy per row was measured 1.4x slower: per-operation cost of the
-// bulk-copy unit at 128 B.)  Observed values arrive pre-packed as (fp16 hi,
-// fp16 lo) of val * 2^ev (als_pack_vals_kernel).
-// Pipelining: a segment's first chunk is gathered into stage buffer 1 while
-// the previous segment is in its Cholesky (which only uses buffer 0), its
-// metadata two segments ahead, and every chunk's (index, value) pair one chunk
-// ahead of its gather.
-template <int MODE>
+// bulk-copy unit at 128 B.)
+// Pipelining: a segment's first chunk is gathered while the previous
+// segment's record is written, its metadata two segments ahead, and every
+// chunk's (index, value) pair one chunk ahead of its gather.
 __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
-    const int64_t* __restrict__ seg_beg, const int32_t* __restrict__ nseg_of, const int32_t* __restrict__ first,
-    const int32_t* __restrict__ pfirst, const int64_t* __restrict__ ptr, int64_t nitems, const int32_t* __restrict__ idx,
+    const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, int64_t nitems, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
-    const unsigned* __restrict__ vmax, float* __restrict__ X, float* __restrict__ partial, float lambda) {
+    const unsigned* __restrict__ vmax, float* __restrict__ rec) {
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
     uint4* stage = dyn4 + warp * kStageU4;  // [2][32][8] uint4
     uint32_t* rstage = reinterpret_cast<uint32_t*>(stage + 2 * 32 * 8);  // [2][32] packed r
-    float* Gs = reinterpret_cast<float*>(stage);  // epilogue: Gram / L (inside buffer 0)
     const int ey = als_scale_exp(*ymax), ev = als_scale_exp(*vmax);
-    const float s2 = ldexpf(1.0f, 2 * ey), inv_s2 = ldexpf(1.0f, -2 * ey), inv_sv = ldexpf(1.0f, -(ey + ev));
+    const float inv_s2 = ldexpf(1.0f, -2 * ey), inv_sv = ldexpf(1.0f, -(ey + ev));
     const int32_t nsegs = *total_segs;
     const int64_t nnz = ptr[nitems];
     const int32_t stride = gridDim.x * kWarps;
@@ -260,13 +216,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
     int32_t nitem = nwk < nsegs ? seg_item[nsg] : 0;
     int64_t nbeg = nwk < nsegs ? seg_beg[nsg] : 0;
     while (true) {
-        // per-segment scalars + the next segment's end / first indices (in flight over this segment)
-        const int32_t nseg_item = nseg_of[item];
-        const int64_t item_beg = ptr[item];
-        const int64_t item_end = ptr[item + 1];
-        int64_t slot = 0;
-        if (MODE == 1) slot = sg;
-        else if (nseg_item > 1) slot = pfirst[item] + (sg - first[item]);
+        // the next segment's end / first indices and the one after's metadata: in flight over this segment
         int64_t nend = 0;
         int j0n = 0;
         uint32_t r0n = 0u;
@@ -289,6 +239,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
         int jn = 0;
         uint32_t rn = 0u;
         if (beg + 32 < end) ldidx(beg + 32, end, jn, rn);
+        if (beg >= end) cp_async_wait<0>();  // empty item: its (zero-fill) gather must land before buffer 1 is reused
         int buf = 1;
         for (int64_t base = beg; base < end; base += 32) {
             const int cnt = min32(end - base);
@@ -352,8 +303,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
             __syncwarp();
             buf ^= 1;
         }
-        // ---- epilogue: lower tiles -> shared (natural dims, mirrored), rows into registers.
-        // Element e of tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)).
+        // both buffers drained: gather the next segment's first chunk while the record is written
+        if (nwk < nsegs) issue(1, min32(nend - nbeg), j0n, r0n);
+        // ---- record: element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1))
+        // -> natural dims (pi(M), pi(N)); every unordered pair is owned by exactly one (M >= N) element.
+        float* out = rec + static_cast<int64_t>(sg) * kRec;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             const int i = q < 2 ? 0 : 1, j = q < 2 ? q : q - 2;
@@ -362,46 +316,20 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
                 const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
                 if (M >= N) {
                     const int a = pi_dim(M), b = pi_dim(N);
-                    Gs[gidx(a, b)] = acc[q][e];
-                    Gs[gidx(b, a)] = acc[q][e];
+                    const int hi = a > b ? a : b, lo = a > b ? b : a;
+                    out[tri_off(hi) + lo] = acc[q][e] * inv_s2;
                 }
             }
         }
-        float* rhs = reinterpret_cast<float*>(rstage);  // buffer 0's r slots (drained)
         if (t == 0) {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                rhs[4 * g + 2 * i] = racc[i][0] + racc[i][1];
-                rhs[4 * g + 2 * i + 1] = racc[i][2] + racc[i][3];
-            }
+            float4 rv;
+            rv.x = (racc[0][0] + racc[0][1]) * inv_sv;  // dim 4g
+            rv.y = (racc[0][2] + racc[0][3]) * inv_sv;  // dim 4g+1
+            rv.z = (racc[1][0] + racc[1][1]) * inv_sv;  // dim 4g+2
+            rv.w = (racc[1][2] + racc[1][3]) * inv_sv;  // dim 4g+3
+            *reinterpret_cast<float4*>(out + kRhs + 4 * g) = rv;
         }
-        const bool single = MODE == 0 && nseg_item == 1;
-        const int64_t cnt_item = item_end - item_beg;
-        __syncwarp();
-        if (single && cnt_item > 0) Gs[gidx(lane, lane)] += lambda * static_cast<float>(cnt_item) * s2;
-        __syncwarp();
-        float row[K];
-#pragma unroll
-        for (int c = 0; c < K; c += 4) {
-            const float4 gv = *reinterpret_cast<const float4*>(Gs + gidx(lane, c));
-            row[c] = gv.x * inv_s2;
-            row[c + 1] = gv.y * inv_s2;
-            row[c + 2] = gv.z * inv_s2;
-            row[c + 3] = gv.w * inv_s2;
-        }
-        const float b = rhs[lane] * inv_sv;
-        __syncwarp();  // Gs / rhs dead: buffer 1 takes the next segment's first chunk, buffer 0 the L mirror
-        if (nwk < nsegs) issue(1, min32(nend - nbeg), j0n, r0n);
-        if (single) {
-            const float x = cnt_item > 0 ? chol_solve_regs(row, b, Gs, lane) : 0.0f;
-            X[static_cast<int64_t>(item) * K + lane] = x;
-        } else {
-            float* out = partial + slot * GSZ;
-#pragma unroll
-            for (int c = 0; c < K; ++c) out[lane * K + c] = row[c];  // records are only 4-byte aligned
-            out[K * K + lane] = b;
-        }
-        __syncwarp();
+        if (lane == 0) out[kCnt] = static_cast<float>(end - beg);
         if (nwk >= nsegs) break;
         wk = nwk;
         sg = nsg;
@@ -425,88 +353,230 @@ __global__ void als_pack_vals_kernel(int64_t n, const float* __restrict__ val, c
     out[q] = pack_h2(h, __float2half_rn(y - __half2float(h)));
 }
 
-cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vmax, uint32_t* out, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    als_pack_vals_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, val, vmax, out);
-    return cudaGetLastError();
-}
-
-// Multi-segment items: sum the partial records in segment order
-// (deterministic), then one warp solves with the register Cholesky.
-__global__ void __launch_bounds__(256) als_reduce_solve32_kernel(const int32_t* __restrict__ list,
+// Sum each multi-segment item's segment records in segment order.  list ==
+// nullptr: every item, result to out[item] (multi-GPU Gram records); else the
+// listed items, result to rec[first[item]] in place.
+__global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems, const int32_t* __restrict__ list,
                                                                  const int32_t* __restrict__ list_count,
-                                                                 const int64_t* __restrict__ ptr,
                                                                  const int32_t* __restrict__ nseg_of,
-                                                                 const int32_t* __restrict__ pfirst,
-                                                                 const float* __restrict__ partial,
-                                                                 float* __restrict__ X, float lambda) {
-    __shared__ __align__(16) float Gs[K * K];
-    __shared__ float rhs[K];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int32_t nwork = *list_count;
-    for (int32_t w = blockIdx.x; w < nwork; w += gridDim.x) {
-        const int32_t item = list[w];
+                                                                 const int32_t* __restrict__ first,
+                                                                 float* __restrict__ rec, float* __restrict__ out) {
+    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
+    const int c = threadIdx.x;  // float4 chunk of the record
+    if (c >= kRec / 4) return;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
         const int32_t ns = nseg_of[item];
-        const float* base = partial + static_cast<int64_t>(pfirst[item]) * GSZ;
-        for (int e = tid; e < K * K + K; e += 256) {
-            float s = 0.0f;
-            for (int32_t q = 0; q < ns; ++q) s += base[static_cast<int64_t>(q) * GSZ + e];
-            if (e < K * K) Gs[gidx(e / K, e % K)] = s;
-            else rhs[e - K * K] = s;
+        const float4* src = reinterpret_cast<const float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c;
+        float4 s = src[0];
+        for (int32_t q = 1; q < ns; ++q) {
+            const float4 v = src[static_cast<int64_t>(q) * (kRec / 4)];
+            s.x += v.x;
+            s.y += v.y;
+            s.z += v.z;
+            s.w += v.w;
         }
-        __syncthreads();
-        if (tid < 32) {
-            const int64_t cnt = ptr[item + 1] - ptr[item];
-            if (cnt > 0) Gs[gidx(lane, lane)] += lambda * static_cast<float>(cnt);
-            __syncwarp();
-            float row[K];
-#pragma unroll
-            for (int c = 0; c < K; c += 4) {
-                const float4 gv = *reinterpret_cast<const float4*>(Gs + gidx(lane, c));
-                row[c] = gv.x;
-                row[c + 1] = gv.y;
-                row[c + 2] = gv.z;
-                row[c + 3] = gv.w;
-            }
-            const float b = rhs[lane];
-            __syncwarp();
-            X[static_cast<int64_t>(item) * K + lane] = cnt > 0 ? chol_solve_regs(row, b, Gs, lane) : 0.0f;
-        }
-        __syncthreads();
+        float4* dst = list ? reinterpret_cast<float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c
+                           : reinterpret_cast<float4*>(out + item * kRec) + c;
+        *dst = s;
     }
 }
 
-cudaError_t launch_als_reduce_solve32(const AlsHalf& h, int sm_count, cudaStream_t s) {
-    const int64_t cap = static_cast<int64_t>(sm_count) * 8;
-    const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, cap)));
-    als_reduce_solve32_kernel<<<blocks, 256, 0, s>>>(h.multi_list, h.multi_count, h.ptr, h.nseg, h.pfirst, h.partial,
-                                                     h.X, h.lambda);
-    return cudaGetLastError();
+// K4: 16 items per warp, TWO LANES PER ITEM (lane = 2*item + parity): the
+// item's record is staged in shared memory and the lane pair runs a
+// left-looking Cholesky of G + lambda*cnt*I in place, lane p computing the
+// rows i == p (mod 2) of each column (row K of the record is the rhs, so the
+// forward substitution rides along: L[K][j] = y_j).  Both lanes then run the
+// back substitution.  Record of item i at slot first[i] (first == nullptr:
+// slot i).  Two lanes per item instead of one halve the shared memory per
+// warp (39 KB), so 5 warps share an SM.
+constexpr int kSys = 16;
+constexpr int kSolveSmem = kSys * kRec * 4;
+__global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
+                                                               const float* __restrict__ rec, float* __restrict__ X,
+                                                               float lambda) {
+    extern __shared__ __align__(16) float srec[];
+    const int lane = threadIdx.x, sys = lane >> 1, par = lane & 1;
+    float* S = srec + sys * kRec;
+    const int64_t nbatch = (nitems + kSys - 1) / kSys;
+    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+        const int64_t i0 = bt * kSys;
+        const int nb = static_cast<int>(nitems - i0 < kSys ? nitems - i0 : kSys);
+        // stage: the warp copies record r with coalesced 16-byte cp.async
+        const int64_t myslot = lane < nb ? (first ? static_cast<int64_t>(first[i0 + lane]) : i0 + lane) : 0;
+        for (int r = 0; r < nb; ++r) {
+            const int64_t slot = __shfl_sync(0xffffffffu, myslot, r);
+            const float4* src = reinterpret_cast<const float4*>(rec + slot * kRec);
+            float4* dst = reinterpret_cast<float4*>(srec + r * kRec);
+            for (int c = lane; c < kRec / 4; c += 32) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + c) : "memory");
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        const bool live = sys < nb;
+        const float cnt = live ? S[kCnt] : 1.0f;
+        const float diag = lambda * cnt;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            // row j of L (columns < j) -> registers (both lanes: broadcast)
+            float rj[K];
+            const float* Rj = S + tri_off(j);
+#pragma unroll
+            for (int q = 0; q + 4 <= j; q += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(Rj + q);
+                rj[q] = v.x;
+                rj[q + 1] = v.y;
+                rj[q + 2] = v.z;
+                rj[q + 3] = v.w;
+            }
+#pragma unroll
+            for (int q = j & ~3; q < j; ++q) rj[q] = Rj[q];
+            float d0 = Rj[j] + diag, d1 = 0.0f;
+#pragma unroll
+            for (int q = 0; q < j; ++q) {
+                if (q & 1) d1 = fmaf(-rj[q], rj[q], d1);
+                else d0 = fmaf(-rj[q], rj[q], d0);
+            }
+            const float r = rsqrt_ftz(d0 + d1);
+            // rows i > j with i == par (mod 2), two per iteration (independent chains)
+            int i = j + 1 + ((j + 1 + par) & 1);
+            int off = tri_off(i);
+#pragma unroll 1
+            for (; i + 2 <= K; i += 4) {
+                const int off2 = off + 4 * ((i >> 2) + 1) + 4 * (((i + 1) >> 2) + 1);
+                const float* Ra = S + off;
+                const float* Rb = S + off2;
+                float a0 = Ra[j], a1 = 0.0f, b0 = Rb[j], b1 = 0.0f;
+#pragma unroll
+                for (int q = 0; q + 4 <= j; q += 4) {
+                    const float4 va = *reinterpret_cast<const float4*>(Ra + q);
+                    const float4 vb = *reinterpret_cast<const float4*>(Rb + q);
+                    a0 = fmaf(-va.x, rj[q], a0);
+                    b0 = fmaf(-vb.x, rj[q], b0);
+                    a1 = fmaf(-va.y, rj[q + 1], a1);
+                    b1 = fmaf(-vb.y, rj[q + 1], b1);
+                    a0 = fmaf(-va.z, rj[q + 2], a0);
+                    b0 = fmaf(-vb.z, rj[q + 2], b0);
+                    a1 = fmaf(-va.w, rj[q + 3], a1);
+                    b1 = fmaf(-vb.w, rj[q + 3], b1);
+                }
+#pragma unroll
+                for (int q = j & ~3; q < j; ++q) {
+                    a0 = fmaf(-Ra[q], rj[q], a0);
+                    b0 = fmaf(-Rb[q], rj[q], b0);
+                }
+                S[off + j] = (a0 + a1) * r;
+                S[off2 + j] = (b0 + b1) * r;
+                off = off2 + 4 * (((i + 2) >> 2) + 1) + 4 * (((i + 3) >> 2) + 1);
+            }
+            if (i <= K) {
+                const float* Ra = S + off;
+                float a0 = Ra[j], a1 = 0.0f;
+#pragma unroll
+                for (int q = 0; q + 4 <= j; q += 4) {
+                    const float4 va = *reinterpret_cast<const float4*>(Ra + q);
+                    a0 = fmaf(-va.x, rj[q], a0);
+                    a1 = fmaf(-va.y, rj[q + 1], a1);
+                    a0 = fmaf(-va.z, rj[q + 2], a0);
+                    a1 = fmaf(-va.w, rj[q + 3], a1);
+                }
+#pragma unroll
+                for (int q = j & ~3; q < j; ++q) a0 = fmaf(-Ra[q], rj[q], a0);
+                S[off + j] = (a0 + a1) * r;
+            }
+            __syncwarp();
+            if (par == 0) S[tri_off(j) + j] = r;  // the diagonal slot keeps 1 / L[j][j]
+        }
+        __syncwarp();
+        // L^T x = y (y = row K of the factorised record), column-oriented, both lanes
+        float y[K];
+#pragma unroll
+        for (int q = 0; q < K; q += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(S + kRhs + q);
+            y[q] = v.x;
+            y[q + 1] = v.y;
+            y[q + 2] = v.z;
+            y[q + 3] = v.w;
+        }
+#pragma unroll
+        for (int q = K - 1; q >= 0; --q) {
+            const float* Rq = S + tri_off(q);
+            y[q] *= Rq[q];
+#pragma unroll
+            for (int i = 0; i + 4 <= q; i += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(Rq + i);
+                y[i] = fmaf(-v.x, y[q], y[i]);
+                y[i + 1] = fmaf(-v.y, y[q], y[i + 1]);
+                y[i + 2] = fmaf(-v.z, y[q], y[i + 2]);
+                y[i + 3] = fmaf(-v.w, y[q], y[i + 3]);
+            }
+#pragma unroll
+            for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
+        }
+        if (live) {
+            // lane pair writes the 128-byte row: parity p stores float4 chunks p, p+2, ...
+            float4* xo = reinterpret_cast<float4*>(X + (i0 + sys) * K);
+            const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q)
+                if ((q & 1) == par)
+                    xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
+                                  : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        }
+        __syncwarp();
+    }
 }
 
 size_t als_mma_smem_bytes() { return sizeof(uint4) * kWarps * kStageU4; }
 
-cudaError_t launch_als_mma_gram(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+static cudaError_t launch_solve(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
+                                int sm_count, cudaStream_t s) {
+    cudaFuncSetAttribute(als_solve_records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
+    const int64_t nbatch = (nitems + kSys - 1) / kSys;
+    int64_t blocks = nbatch;
+    const int64_t cap = static_cast<int64_t>(sm_count) * 5;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    als_solve_records_kernel<<<static_cast<unsigned>(blocks), 32, kSolveSmem, s>>>(nitems, first, rec, X, lambda);
+    return cudaGetLastError();
+}
+
+// one rank-32 half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
+// -> per-item Gram records in h.gram_out (mode 1, multi-GPU column side)
+cudaError_t launch_als_mma_half(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
     const size_t smem = als_mma_smem_bytes();
     int64_t blocks = (h.max_segs + kWarps - 1) / kWarps;
     const int64_t cap = static_cast<int64_t>(sm_count) * 3;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (mode == 0) {
-        cudaFuncSetAttribute(als_mma_gram32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        als_mma_gram32_kernel<0><<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-            h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.nitems, h.idx, h.valh, h.Yh,
-            h.ymax, h.vmax,
-            h.X, h.partial, h.lambda);
-    } else {
-        cudaFuncSetAttribute(als_mma_gram32_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        als_mma_gram32_kernel<1><<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-            h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.nseg, h.first, h.pfirst, h.ptr, h.nitems, h.idx, h.valh, h.Yh,
-            h.ymax, h.vmax,
-            h.X, h.partial, h.lambda);
+    cudaFuncSetAttribute(als_mma_gram32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    als_mma_gram32_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.nitems, h.idx, h.valh, h.Yh, h.ymax, h.vmax,
+        h.partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
+    if (mode == 1) {
+        als_reduce_records_kernel<<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
+                                                          h.gram_out);
+        return cudaGetLastError();
     }
-    return cudaGetLastError();
+    als_reduce_records_kernel<<<rblocks, 160, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.nseg, h.first,
+                                                      h.partial, nullptr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_solve(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s);
 }
+
+cudaError_t launch_als_solve_records(int64_t nitems, const float* G, float* X, float lambda, int sm_count,
+                                     cudaStream_t s) {
+    return launch_solve(nitems, nullptr, G, X, lambda, sm_count, s);
+}
+
+size_t als_record_floats32() { return kRec; }
 
 // max |X| -> *maxbits (zeroed here), then X -> packed hi/lo rows
 cudaError_t launch_als_pack(int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count, cudaStream_t s) {
@@ -528,6 +598,12 @@ cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int 
     if (blocks > sm_count * 8) blocks = sm_count * 8;
     if (blocks < 1) blocks = 1;
     als_absmax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(count, x, maxbits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vmax, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    als_pack_vals_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, val, vmax, out);
     return cudaGetLastError();
 }
 

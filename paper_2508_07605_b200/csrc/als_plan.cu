@@ -215,7 +215,8 @@ static int als_alloc(ocg_als_plan* P) {
         ALS_CUDA(S.seg_beg.alloc(static_cast<size_t>(ms)));
         // partial Grams only for items with >1 segment: sum of their nseg <= 2*nnz/kSeg
         // (the column side may also run in MODE 1 — every segment keeps a slot)
-        const int64_t mp = sd == 1 ? ms : std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
+        // (rank 32: every segment writes a record, slot = segment id)
+        const int64_t mp = (sd == 1 || P->k == 32) ? ms : std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
         ALS_CUDA(S.nmulti.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.pfirst.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.partial.alloc(static_cast<size_t>(mp) * ocg::als_gram_record_floats(P->k)));
