@@ -155,7 +155,7 @@ static_assert(tri_off(32) == kRhs, "record layout");
 // Pipelining: a segment's first chunk is gathered while the previous
 // segment's record is written, its metadata two segments ahead, and every
 // chunk's (index, value) pair one chunk ahead of its gather.
-__global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
+__global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, int64_t nitems, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
@@ -211,18 +211,26 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
         ldidx(beg, end, j, r);
         issue(1, min32(end - beg), j, r);
     }
+    int ja = 0, jb = 0;  // index queue: chunks 1 and 2 of the current segment
+    uint32_t ra = 0u, rb = 0u;
+    ldidx(beg + 32, end, ja, ra);
+    ldidx(beg + 64, end, jb, rb);
     int32_t nwk = wk + stride;
     int32_t nsg = nwk < nsegs ? seg_of(nwk) : 0;
     int32_t nitem = nwk < nsegs ? seg_item[nsg] : 0;
     int64_t nbeg = nwk < nsegs ? seg_beg[nsg] : 0;
     while (true) {
         // the next segment's end / first indices and the one after's metadata: in flight over this segment
+        // (its first three chunks' indices: chunk 0 is gathered during this
+        // segment's record write, chunks 1-2 seed the next index queue)
         int64_t nend = 0;
-        int j0n = 0;
-        uint32_t r0n = 0u;
+        int j0n = 0, j1n = 0, j2n = 0;
+        uint32_t r0n = 0u, r1n = 0u, r2n = 0u;
         if (nwk < nsegs) {
             nend = min(nbeg + kSeg, ptr[nitem + 1]);
             ldidx(nbeg, nnz, j0n, r0n);  // speculative: masked to the segment when issued
+            ldidx(nbeg + 32, nnz, j1n, r1n);
+            ldidx(nbeg + 64, nnz, j2n, r2n);
         }
         const int32_t nnwk = nwk + stride;
         const int32_t nnsg = nnwk < nsegs ? seg_of(nnwk) : 0;
@@ -236,16 +244,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
             for (int q = 0; q < 6; ++q) acc[q][e] = 0.0f;
             racc[0][e] = racc[1][e] = 0.0f;
         }
-        int jn = 0;
-        uint32_t rn = 0u;
-        if (beg + 32 < end) ldidx(beg + 32, end, jn, rn);
         if (beg >= end) cp_async_wait<0>();  // empty item: its (zero-fill) gather must land before buffer 1 is reused
         int buf = 1;
         for (int64_t base = beg; base < end; base += 32) {
             const int cnt = min32(end - base);
             if (base + 32 < end) {
-                issue(buf ^ 1, min32(end - base - 32), jn, rn);
-                if (base + 64 < end) ldidx(base + 64, end, jn, rn);
+                // index queue (ja: chunk t+1, jb: chunk t+2); chunk t+3's load has two iterations to land
+                issue(buf ^ 1, min32(end - base - 32), ja, ra);
+                ja = jb;
+                ra = rb;
+                if (base + 96 < end) ldidx(base + 96, end, jb, rb);
                 cp_async_wait<1>();
             } else {
                 cp_async_wait<0>();
@@ -305,9 +313,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
         }
         // both buffers drained: gather the next segment's first chunk while the record is written
         if (nwk < nsegs) issue(1, min32(nend - nbeg), j0n, r0n);
-        // ---- record: element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1))
-        // -> natural dims (pi(M), pi(N)); every unordered pair is owned by exactly one (M >= N) element.
-        float* out = rec + static_cast<int64_t>(sg) * kRec;
+        // ---- record, assembled in buffer 0 then stored with 16-byte coalesced writes.
+        // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) -> natural
+        // dims (pi(M), pi(N)); every unordered pair is owned by exactly one (M >= N) element.
+        float* rs_ = reinterpret_cast<float*>(stage);
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             const int i = q < 2 ? 0 : 1, j = q < 2 ? q : q - 2;
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
                 if (M >= N) {
                     const int a = pi_dim(M), b = pi_dim(N);
                     const int hi = a > b ? a : b, lo = a > b ? b : a;
-                    out[tri_off(hi) + lo] = acc[q][e] * inv_s2;
+                    rs_[tri_off(hi) + lo] = acc[q][e] * inv_s2;
                 }
             }
         }
@@ -327,9 +336,21 @@ __global__ void __launch_bounds__(kWarps * 32, 3) als_mma_gram32_kernel(
             rv.y = (racc[0][2] + racc[0][3]) * inv_sv;  // dim 4g+1
             rv.z = (racc[1][0] + racc[1][1]) * inv_sv;  // dim 4g+2
             rv.w = (racc[1][2] + racc[1][3]) * inv_sv;  // dim 4g+3
-            *reinterpret_cast<float4*>(out + kRhs + 4 * g) = rv;
+            *reinterpret_cast<float4*>(rs_ + kRhs + 4 * g) = rv;
         }
-        if (lane == 0) out[kCnt] = static_cast<float>(end - beg);
+        if (lane == 0) rs_[kCnt] = static_cast<float>(end - beg);
+        __syncwarp();
+        {
+            float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
+            const float4* src = reinterpret_cast<const float4*>(rs_);
+#pragma unroll
+            for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots carry stale values, never read
+        }
+        __syncwarp();
+        ja = j1n;
+        ra = r1n;
+        jb = j2n;
+        rb = r2n;
         if (nwk >= nsegs) break;
         wk = nwk;
         sg = nsg;
