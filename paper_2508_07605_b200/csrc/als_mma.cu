@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
     }
 }
 
-// K4: 16 items per warp, TWO LANES PER ITEM (lane = 2*item + parity): the
+// K4: 16 items per warp, TWO LANES PER ITEM (lane = 16*parity + item): the
 // item's record is staged in shared memory and the lane pair runs a
 // left-looking Cholesky of G + lambda*cnt*I in place, lane p computing the
 // rows i == p (mod 2) of each column (row K of the record is the rhs, so the
@@ -417,7 +417,10 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
                                                                const float* __restrict__ rec, float* __restrict__ X,
                                                                float lambda) {
     extern __shared__ __align__(16) float srec[];
-    const int lane = threadIdx.x, sys = lane >> 1, par = lane & 1;
+    // lane = 16 * parity + item: the 8 lanes of a 16-byte shared-memory phase
+    // are 8 different items at the same record offset (stride 153 x 16 B: 8
+    // distinct bank groups)
+    const int lane = threadIdx.x, sys = lane & 15, par = lane >> 4;
     float* S = srec + sys * kRec;
     const int64_t nbatch = (nitems + kSys - 1) / kSys;
     for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
@@ -537,15 +540,13 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
 #pragma unroll
             for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
         }
-        if (live) {
-            // lane pair writes the 128-byte row: parity p stores float4 chunks p, p+2, ...
+        if (live && par == 0) {  // both lanes hold x; parity 0 writes the 128-byte row
             float4* xo = reinterpret_cast<float4*>(X + (i0 + sys) * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
             for (int q = 0; q < K / 4; ++q)
-                if ((q & 1) == par)
-                    xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
-                                  : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+                xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
+                              : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
         }
         __syncwarp();
     }
