@@ -84,6 +84,9 @@ struct AlsSelectArgs {
     double* completed;  // optional m x n completed rows (tests), else nullptr
 };
 cudaError_t launch_als_select(const AlsSelectArgs& a, int sm_count, cudaStream_t s);
+// rank 32 on the tensor cores (als_select_mma.cu); Vsel: n x 8 uint4 scratch
+cudaError_t launch_als_select_mma(const AlsSelectArgs& a, uint4* Vsel, const unsigned* umax, const unsigned* vmax,
+                                  int sm_count, cudaStream_t s);
 cudaError_t launch_transpose(int64_t n, int k, const float* V, float* Vt, cudaStream_t s);
 
 }  // namespace ocg

@@ -91,7 +91,8 @@ struct ocg_als_plan {
     // max |.| each packing scale came from ([0] U, [1] V, [2] observed values)
     Buf<uint4> Uh, Vh;
     Buf<unsigned> maxbits;
-    Buf<uint32_t> valh;  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
+    Buf<uint32_t> valh;
+    Buf<uint4> Vsel;  // V in the tensor-core selection layout  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
     cudaEvent_t ev[6] = {};
@@ -232,6 +233,7 @@ static int als_alloc(ocg_als_plan* P) {
         ALS_CUDA(P->Uh.alloc(static_cast<size_t>(P->m * 8)));
         ALS_CUDA(P->Vh.alloc(static_cast<size_t>(P->n * 8)));
         ALS_CUDA(P->maxbits.alloc(3));
+        ALS_CUDA(P->Vsel.alloc(static_cast<size_t>(P->n * 8)));
     }
     ALS_CUDA(P->idx.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->ncand.alloc(static_cast<size_t>(P->m)));
@@ -313,7 +315,7 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
 
 static int launch_select(ocg_als_plan* P) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
-    ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
+    if (P->k != 32) ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
     ocg::AlsSelectArgs a{};
     a.m = P->m;
     a.n = P->n;
@@ -334,7 +336,10 @@ static int launch_select(ocg_als_plan* P) {
     a.loss = P->loss.p;
     a.ncand = P->ncand.p;
     a.completed = nullptr;
-    ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
+    if (P->k == 32)
+        ALS_CUDA(ocg::launch_als_select_mma(a, P->Vsel.p, P->maxbits.p, P->maxbits.p + 1, ocg_internal_sm_count(P->ctx), s));
+    else
+        ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
     return OCG_OK;
 }
 
@@ -480,7 +485,10 @@ int ocg_als_plan_completed_rows(ocg_als_plan* P, int64_t row0, int64_t nrows, do
     a.loss = dl.p;
     a.ncand = dn.p;
     a.completed = d.p;
-    ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
+    if (P->k == 32)
+        ALS_CUDA(ocg::launch_als_select_mma(a, P->Vsel.p, P->maxbits.p, P->maxbits.p + 1, ocg_internal_sm_count(P->ctx), s));
+    else
+        ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
     ALS_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double) * nrows * P->n, cudaMemcpyDeviceToHost, s));
     ALS_CUDA(cudaStreamSynchronize(s));
     return OCG_OK;

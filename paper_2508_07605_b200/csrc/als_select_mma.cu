@@ -1,0 +1,437 @@
+// Rank-32 fused ALS imputation + Algorithm-2 selection on the tensor cores.
+//
+// Same contract as als_select_kernel (als_select.cu): for every row i the
+// completed row is p_ij = r_ij (observed, verbatim) or clamp(u_i . v_j, 0.01,
+// 1.25) (cf::complete semantics, cfcomplete.cpp:198-213), and
+// policy::select_caps (policy.cpp:17-64) picks the setting, bit-exact given
+// the completed row.  What changes is how u_i . v_j is formed and how the
+// epilogue is organised:
+//
+// * The m x n product is a GEMM with K = 32.  U and V are split into FP16
+//   hi/lo pairs (power-of-two scales su, sv; als_pack*), and
+//   u.v * su*sv = Uh.Vh + Uh.Vl + Ul.Vh  (the Ul.Vl term is below 2^-21
+//   relative) runs as mma.sync m16n8k16 f16 -> f32: 6 MMAs per 16x8 cell
+//   tile (2 k-steps x 3).  The completed value of an unobserved cell is the
+//   FP32 accumulator times 2^-(eu+ev) (exact).
+// * A warp owns 16 rows; a CTA (8 warps, 128 rows) streams V in 256-column
+//   tiles (32 KB, cp.async double buffer) stored per column as 8 x 16 B
+//   chunks ordered so that one LDS.128 yields a lane's B fragments for both
+//   k-steps (hi or lo); hi/lo chunk halves swap on odd columns so the 8 lanes
+//   of a shared-memory phase hit 8 different bank groups.
+// * Each lane holds 2 rows x 64 columns of a tile in the accumulator layout
+//   (rows g, g+8; columns 8nt + 2t + e).  Observed cells are skipped through
+//   a per-tile bit mask (bits permuted so a lane's 64 bits are two words) and
+//   evaluated afterwards from the CSR entries (observed pass); the two passes
+//   feed the same per-row selection state.
+// * Per unobserved cell the epilogue is branch-free FP32: validity
+//   loss <= gamma as an exact compare against the row's FP32 threshold, the
+//   candidate count, and the 2^-18 band test of c_sum/p against the lane's
+//   best (as a multiply); only cells inside the band take the out-of-line
+//   FP64 path (exact saving + the 4-key order).
+// * The baseline p_base = p_{i,n-1} is produced first by the same MMA
+//   sequence on the tile holding column n-1, so thresholds use the very value
+//   the row completes to.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "als.h"
+#include "ocg_common.cuh"
+#include "select_dev.cuh"
+
+namespace ocg {
+
+namespace {
+
+constexpr int K = 32;
+constexpr int kW = 8;          // warps per CTA
+constexpr int kTile = 256;     // V columns per tile
+constexpr int kNT = kTile / 8;  // n-tiles per tile
+constexpr float kBand = 1.0f + 0x1p-18f;
+
+struct BestX {
+    double s, p;
+    int j, sum;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
+    return static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
+}
+// (a, b) -> packed hi pair and lo pair of a*s, b*s
+__device__ __forceinline__ void split2(float a, float b, float s, uint32_t& hi, uint32_t& lo) {
+    const float ya = a * s, yb = b * s;
+    const __half ha = __float2half_rn(ya), hb = __float2half_rn(yb);
+    hi = pack_h2(ha, hb);
+    lo = pack_h2(__float2half_rn(ya - __half2float(ha)), __float2half_rn(yb - __half2float(hb)));
+}
+
+__device__ __forceinline__ int scale_exp(unsigned maxbits) {
+    const float mx = __uint_as_float(maxbits);
+    if (!(mx > 0.0f) || !isfinite(mx)) return 0;
+    int e;
+    frexpf(mx, &e);
+    const int x = 14 - e;
+    return x < -60 ? -60 : (x > 60 ? 60 : x);
+}
+
+// loss(p) = fl(1 - fl(p / p_base)) <= gamma, exactly as policy.cpp:34-35
+__device__ __forceinline__ bool valid_exact(double p, double p_base, double gamma) {
+    return !(dsub(1.0, ddiv(p, p_base)) > gamma);
+}
+__device__ __forceinline__ double next_up(double x) { return u2d(d2u(x) + 1); }
+__device__ __forceinline__ double next_down(double x) { return u2d(d2u(x) - 1); }
+__device__ double valid_threshold(double p_base, double gamma) {
+    double x = dmul(p_base, dsub(1.0, gamma));
+    if (valid_exact(x, p_base, gamma)) {
+        for (int it = 0; it < 64; ++it) {
+            const double y = next_down(x);
+            if (!valid_exact(y, p_base, gamma)) break;
+            x = y;
+        }
+    } else {
+        for (int it = 0; it < 64 && !valid_exact(x, p_base, gamma); ++it) x = next_up(x);
+    }
+    return x;
+}
+
+// FP64 evaluation of one cell (policy.cpp:37-38) + the 4-key compare
+__device__ __noinline__ void exact_update(BestX* b, double pd, int cs, int j, double e_base) {
+    const double e_pred = ddiv(static_cast<double>(cs), pd);
+    const double s = ddiv(dsub(e_base, e_pred), e_base);
+    bool better;
+    if (b->j < 0) better = true;
+    else if (s != b->s) better = s > b->s;
+    else if (pd != b->p) better = pd > b->p;
+    else if (cs != b->sum) better = cs < b->sum;
+    else better = j < b->j;
+    if (better) {
+        b->s = s;
+        b->p = pd;
+        b->j = j;
+        b->sum = cs;
+    }
+}
+
+// V (n x 32 f32) -> per column 8 x 16 B: chunk t of the hi (lo) half holds dims
+// {2t, 2t+1, 2t+8, 2t+9, 2t+16, 2t+17, 2t+24, 2t+25}; hi chunks sit at
+// positions 0-3 on even columns and 4-7 on odd columns (lo the other half)
+__global__ void pack_vsel_kernel(int64_t n, const float* __restrict__ V, const unsigned* __restrict__ vmaxbits,
+                                 uint4* __restrict__ out) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (column, t)
+    if (q >= n * 4) return;
+    const int64_t c = q >> 2;
+    const int t = static_cast<int>(q & 3);
+    const float s = ldexpf(1.0f, scale_exp(*vmaxbits));
+    const float* v = V + c * K;
+    const int d[8] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9, 2 * t + 16, 2 * t + 17, 2 * t + 24, 2 * t + 25};
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split2(v[d[2 * u]], v[d[2 * u + 1]], s, hi[u], lo[u]);
+    const int odd = static_cast<int>(c & 1);
+    out[c * 8 + t + 4 * odd] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    out[c * 8 + t + 4 * (1 - odd)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+}  // namespace
+
+struct AlsSelMmaArgs {
+    AlsSelectArgs a;
+    const uint4* Vsel;         // packed V (pack_vsel_kernel)
+    const unsigned* umax;      // max |U| bits
+    const unsigned* vmax;      // max |V| bits
+};
+
+template <bool WRITE_COMPLETED>
+__global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArgs P) {
+    const AlsSelectArgs& a = P.a;
+    extern __shared__ __align__(16) uint4 sdyn[];
+    uint4* Vs = sdyn;                                                   // [2][kTile][8]
+    int32_t* csum = reinterpret_cast<int32_t*>(Vs + 2 * kTile * 8);     // [2][kTile]
+    uint32_t* maskw = reinterpret_cast<uint32_t*>(csum + 2 * kTile);    // [kW][16][8]
+    BestX* bx = reinterpret_cast<BestX*>(maskw + kW * 16 * 8);          // [kW][32 lanes][2 rows]
+    int32_t* caps = reinterpret_cast<int32_t*>(bx + kW * 32 * 2);       // [ncpu + ngpu]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int64_t n = a.n;
+    const int ngpu = a.ngpu, ncpu = static_cast<int>(n / ngpu);
+    const int ntiles = static_cast<int>((n + kTile - 1) / kTile);
+    for (int e = tid; e < ncpu + ngpu; e += blockDim.x) caps[e] = e < ncpu ? a.cpu_caps[e] : a.gpu_caps[e - ncpu];
+    const int eu = scale_exp(*P.umax), ev = scale_exp(*P.vmax);
+    const float su = ldexpf(1.0f, eu), inv_s = ldexpf(1.0f, -(eu + ev));
+    uint32_t* mymask = maskw + warp * 16 * 8;
+    BestX* myb = bx + (warp * 32 + lane) * 2;
+
+    auto load_tile = [&](int tt, int buf) {
+        const int64_t c0 = static_cast<int64_t>(tt) * kTile;
+        for (int e = tid; e < kTile * 8; e += blockDim.x) {
+            const int64_t c = c0 + e / 8;
+            uint4* dst = Vs + buf * kTile * 8 + e;
+            if (c < n) cp_async16(dst, P.Vsel + c * 8 + (e & 7));
+            else *dst = make_uint4(0u, 0u, 0u, 0u);
+        }
+        for (int e = tid; e < kTile; e += blockDim.x) {
+            const int64_t j = c0 + e;
+            int cs = 1;
+            if (j < n) {
+                const int ci = static_cast<int>(j / ngpu);
+                cs = caps[ci] + caps[ncpu + static_cast<int>(j - static_cast<int64_t>(ci) * ngpu)];
+            }
+            csum[buf * kTile + e] = cs;
+        }
+        cp_async_commit();
+    };
+
+    for (int64_t rb = static_cast<int64_t>(blockIdx.x) * (kW * 16); rb < a.m;
+         rb += static_cast<int64_t>(gridDim.x) * (kW * 16)) {
+        __syncthreads();  // previous block's tile buffers are free
+        load_tile(0, 0);
+        const int64_t r0 = rb + warp * 16;
+        const int64_t rowg[2] = {r0 + g, r0 + g + 8};
+        const bool live[2] = {rowg[0] < a.m, rowg[1] < a.m};
+        // A fragments (rows g, g+8; k-step ks: dims 16ks + {2t,2t+1} / {2t+8,2t+9})
+        uint32_t ah[2][4], al[2][4];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            float2 v[2][2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const float* u = a.U + (live[q] ? rowg[q] : 0) * K + 16 * ks + 2 * t;
+                v[q][0] = live[q] ? *reinterpret_cast<const float2*>(u) : make_float2(0.f, 0.f);
+                v[q][1] = live[q] ? *reinterpret_cast<const float2*>(u + 8) : make_float2(0.f, 0.f);
+            }
+            split2(v[0][0].x, v[0][0].y, su, ah[ks][0], al[ks][0]);  // row g,   k 2t..
+            split2(v[1][0].x, v[1][0].y, su, ah[ks][1], al[ks][1]);  // row g+8, k 2t..
+            split2(v[0][1].x, v[0][1].y, su, ah[ks][2], al[ks][2]);  // row g,   k 2t+8..
+            split2(v[1][1].x, v[1][1].y, su, ah[ks][3], al[ks][3]);  // row g+8, k 2t+8..
+        }
+        auto mma_cell = [&](float (&d)[4], const uint4& bh, const uint4& bl) {
+            d[0] = d[1] = d[2] = d[3] = 0.0f;
+            mma16816(d, ah[0][0], ah[0][1], ah[0][2], ah[0][3], bh.x, bh.y);
+            mma16816(d, ah[0][0], ah[0][1], ah[0][2], ah[0][3], bl.x, bl.y);
+            mma16816(d, al[0][0], al[0][1], al[0][2], al[0][3], bh.x, bh.y);
+            mma16816(d, ah[1][0], ah[1][1], ah[1][2], ah[1][3], bh.z, bh.w);
+            mma16816(d, ah[1][0], ah[1][1], ah[1][2], ah[1][3], bl.z, bl.w);
+            mma16816(d, al[1][0], al[1][1], al[1][2], al[1][3], bh.z, bh.w);
+        };
+        // ---- baseline p_{i,n-1}: the n-tile holding column n-1, same MMA sequence
+        double pbase[2];
+        {
+            const int64_t cb = (n - 1) & ~static_cast<int64_t>(7);  // n-tile base column
+            const int64_t col = cb + g;                              // this lane's B column
+            uint4 bh = make_uint4(0u, 0u, 0u, 0u), bl = bh;
+            if (col < n) {
+                const int odd = static_cast<int>(col & 1);
+                bh = P.Vsel[col * 8 + t + 4 * odd];
+                bl = P.Vsel[col * 8 + t + 4 * (1 - odd)];
+            }
+            float d[4];
+            mma_cell(d, bh, bl);
+            const int jl = static_cast<int>((n - 1) - cb);  // 0..7: column within the n-tile
+            const int src = jl >> 1;                                 // lane t of the quad holding it
+            const float v0 = (jl & 1) ? d[1] : d[0], v1 = (jl & 1) ? d[3] : d[2];
+            float pb[2];
+            pb[0] = __shfl_sync(0xffffffffu, v0, (lane & ~3) | src) * inv_s;
+            pb[1] = __shfl_sync(0xffffffffu, v1, (lane & ~3) | src) * inv_s;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                double p = 1.0;
+                if (live[q]) {
+                    const int64_t e = a.row_ptr[rowg[q] + 1] - 1;  // baseline = last column n-1
+                    if (e >= a.row_ptr[rowg[q]] && a.col[e] == n - 1) p = static_cast<double>(a.val[e]);
+                    else p = pb[q] <= 0.01f ? 0.01 : (pb[q] > 1.25f ? 1.25 : static_cast<double>(pb[q]));
+                }
+                pbase[q] = p;
+            }
+        }
+        float fthr[2], lov[2], tbest[2], tband[2];
+        int ncand[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double thr = valid_threshold(pbase[q], a.gamma);
+            float f = static_cast<float>(thr);
+            if (static_cast<double>(f) < thr) f = __uint_as_float(__float_as_uint(f) + 1u);
+            fthr[q] = f;                                  // float p valid <=> p >= fthr
+            lov[q] = 0.01 >= thr ? INFINITY : -INFINITY;  // cells clamped to 0.01: valid iff 0.01 >= thr
+            tbest[q] = INFINITY;
+            tband[q] = INFINITY;
+            ncand[q] = 0;
+            myb[q] = BestX{0.0, 0.0, -1, 0};
+        }
+        // mask owner: lane r < 16 walks row r0 + r's CSR entries tile by tile
+        int64_t mbeg = 0;
+        int mcur = 0, mend = 0;
+        if (lane < 16 && r0 + lane < a.m) {
+            mbeg = a.row_ptr[r0 + lane];
+            mend = static_cast<int>(a.row_ptr[r0 + lane + 1] - mbeg);
+        }
+        // ---- dense pass over the tiles (unobserved cells)
+        for (int tt = 0; tt < ntiles; ++tt) {
+            const int buf = tt & 1;
+            const int64_t c0 = static_cast<int64_t>(tt) * kTile;
+            // observed-cell mask of this tile: column cc -> word 2*((cc&7)>>1) + (cc>>7),
+            // bit (((cc>>3)&15)<<1) | (cc&1)  (a lane's 64 bits are 2 words per row)
+            __syncwarp();  // every lane has read the previous tile's mask words
+            if (lane < 16) {
+                uint32_t* mw = mymask + lane * 8;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) mw[w] = 0u;
+                while (mcur < mend) {
+                    const int64_t c = a.col[mbeg + mcur];
+                    if (c >= c0 + kTile) break;
+                    const int cc = static_cast<int>(c - c0);
+                    mw[2 * ((cc & 7) >> 1) + (cc >> 7)] |= 1u << ((((cc >> 3) & 15) << 1) | (cc & 1));
+                    ++mcur;
+                }
+            }
+            cp_async_wait_all();
+            __syncthreads();  // tile tt landed, masks written
+            if (tt + 1 < ntiles) load_tile(tt + 1, buf ^ 1);
+            const uint4* vt = Vs + buf * kTile * 8;
+            const int32_t* cst = csum + buf * kTile;
+            uint32_t mk[2][2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint2 w = *reinterpret_cast<const uint2*>(mymask + (g + 8 * q) * 8 + 2 * t);
+                mk[q][0] = w.x;
+                mk[q][1] = w.y;
+            }
+            const int64_t nleft = n - c0;  // columns of this tile that exist
+#pragma unroll 4
+            for (int nt = 0; nt < kNT; ++nt) {
+                const int cc = nt * 8;
+                const int odd = g & 1;
+                const uint4 bh = vt[(cc + g) * 8 + t + 4 * odd];
+                const uint4 bl = vt[(cc + g) * 8 + t + 4 * (1 - odd)];
+                float d[4];
+                mma_cell(d, bh, bl);
+                const int2 cs2 = *reinterpret_cast<const int2*>(cst + cc + 2 * t);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int jc = cc + 2 * t + e;
+                    const bool jin = jc < nleft;
+                    const int cs = e ? cs2.y : cs2.x;
+                    const float csf = static_cast<float>(cs);
+                    const int bit = ((nt & 15) << 1) | e;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const float pf = d[2 * q + e] * inv_s;
+                        const bool ob = (mk[q][nt >> 4] >> bit) & 1u;
+                        const bool use = live[q] && jin && !ob;
+                        const bool lo = pf <= 0.01f;
+                        const float pc = fminf(pf, 1.25f);
+                        const float pv = lo ? lov[q] : pc;
+                        const bool valid = use && pv >= fthr[q];
+                        ncand[q] += valid ? 1 : 0;
+                        const float pe = fmaxf(pc, 0.01f);
+                        if (WRITE_COMPLETED && use)
+                            a.completed[rowg[q] * n + c0 + jc] = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
+                        if (valid && csf <= tband[q] * pe) {
+                            const double pd = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
+                            exact_update(myb + q, pd, cs, static_cast<int>(c0) + jc, a.e_base);
+                            tbest[q] = fminf(tbest[q], __fdividef(csf, pe));
+                            tband[q] = tbest[q] * kBand;
+                        }
+                    }
+                }
+            }
+        }
+        // ---- observed pass + per-row merge.  Row r = r0 + rr: its dense state is in the
+        // quad g = rr & 7 (q = rr >> 3); the whole warp walks its CSR entries.
+#pragma unroll 1
+        for (int rr = 0; rr < 16; ++rr) {
+            const int64_t i = r0 + rr;
+            if (i >= a.m) break;
+            const int qq = rr >> 3, src = (rr & 7) * 4;
+            const float my_tb = qq ? tbest[1] : tbest[0];
+            float tb = fminf(my_tb, __shfl_xor_sync(0xffffffffu, my_tb, 1));
+            tb = fminf(tb, __shfl_xor_sync(0xffffffffu, tb, 2));
+            tb = __shfl_sync(0xffffffffu, tb, src);
+            const float fth = __shfl_sync(0xffffffffu, qq ? fthr[1] : fthr[0], src);
+            const double pb = __shfl_sync(0xffffffffu, qq ? pbase[1] : pbase[0], src);
+            float tbd = tb * kBand;
+            const int64_t rbeg = a.row_ptr[i];
+            const int rl = static_cast<int>(a.row_ptr[i + 1] - rbeg);
+            BestX ob{0.0, 0.0, -1, 0};
+            int oc = 0;
+            for (int e = lane; e < rl; e += 32) {
+                const int j = a.col[rbeg + e];
+                const float v = a.val[rbeg + e];
+                const int ci = j / ngpu;
+                const int cs = caps[ci] + caps[ncpu + (j - ci * ngpu)];
+                const bool valid = v >= fth;
+                oc += valid ? 1 : 0;
+                if (WRITE_COMPLETED) a.completed[i * n + j] = static_cast<double>(v);
+                if (valid && static_cast<float>(cs) <= tbd * v) {
+                    exact_update(&ob, static_cast<double>(v), cs, j, a.e_base);
+                    tbd = fminf(tbd, __fdividef(static_cast<float>(cs), v) * kBand);
+                }
+            }
+            // merge the quad's dense candidate into its lanes' observed candidate
+            if ((lane >> 2) == (rr & 7)) {
+                const BestX db = myb[qq];
+                oc += qq ? ncand[1] : ncand[0];
+                if (db.j >= 0) {
+                    bool better;
+                    if (ob.j < 0) better = true;
+                    else if (db.s != ob.s) better = db.s > ob.s;
+                    else if (db.p != ob.p) better = db.p > ob.p;
+                    else if (db.sum != ob.sum) better = db.sum < ob.sum;
+                    else better = db.j < ob.j;
+                    if (better) ob = db;
+                }
+            }
+            SelResult sr{ob.j, ob.s, 0.0, ob.p, ob.sum, 0};
+            const SelResult w = sel_warp_reduce(sr, ob.j >= 0, oc);
+            if (lane == 0) {
+                a.idx[i] = w.idx;
+                a.saving[i] = w.saving;
+                a.loss[i] = w.idx >= 0 ? dsub(1.0, ddiv(w.perf, pb)) : 0.0;
+                a.ncand[i] = w.ncand;
+            }
+        }
+    }
+}
+
+size_t als_select_mma_smem() {
+    return sizeof(uint4) * 2 * kTile * 8 + sizeof(int32_t) * 2 * kTile + sizeof(uint32_t) * kW * 16 * 8 +
+           sizeof(BestX) * kW * 32 * 2 + sizeof(int32_t) * 512;
+}
+
+// V -> packed select layout; U's and V's scales come from the Gram packing
+// (maxbits[0] = max |U|, maxbits[1] = max |V|, refreshed after every half-sweep)
+cudaError_t launch_als_select_mma(const AlsSelectArgs& a, uint4* Vsel, const unsigned* umax, const unsigned* vmax,
+                                  int sm_count, cudaStream_t s) {
+    if (a.k != K) return cudaErrorInvalidValue;
+    if (static_cast<int64_t>(a.n / a.ngpu) + a.ngpu > 512) return cudaErrorInvalidValue;
+    pack_vsel_kernel<<<static_cast<unsigned>((a.n * 4 + 255) / 256), 256, 0, s>>>(a.n, a.V, vmax, Vsel);
+    AlsSelMmaArgs P{a, Vsel, umax, vmax};
+    const size_t smem = als_select_mma_smem();
+    int64_t blocks = (a.m + kW * 16 - 1) / (kW * 16);
+    const int64_t cap = static_cast<int64_t>(sm_count) * 2;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<static_cast<unsigned>(blocks), kW * 32, smem, s>>>(P);
+    };
+    if (a.completed) go(als_select_mma_kernel<true>);
+    else go(als_select_mma_kernel<false>);
+    return cudaGetLastError();
+}
+
+}  // namespace ocg

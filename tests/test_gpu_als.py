@@ -39,15 +39,16 @@ def test_als_factors_and_predictions_match_oracle(ctx, port, k):
     assert np.quantile(rel, 0.999) < PRED_RTOL, (rel.max(), np.quantile(rel, 0.999))
 
 
-@pytest.mark.parametrize("n_grid", [(8, 16), (16, 16), (64, 64)])
-def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid):
+@pytest.mark.parametrize("rank", [16, 32])  # 32: tensor-core imputation + selection
+@pytest.mark.parametrize("n_grid", [(8, 16), (16, 16), (64, 64), (10, 30)])
+def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid, rank):
     """The fused kernel's decision == policy::select_caps on the very rows it
     completed (bit-exact: index, saving, loss, candidates)."""
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
 
     m = 700 if n_grid[0] < 64 else 200
     grid, A = _problem(m, *n_grid, 0.05, 2, seed=5)
-    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, AlsHyper(rank=16, sweeps=4), 0.05, ctx=ctx)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, AlsHyper(rank=rank, sweeps=4), 0.05, ctx=ctx)
     plan.run()
     idx, sav, loss, nc = plan.results()
     rows = plan.completed_rows(0, A.m)
@@ -64,7 +65,8 @@ def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid):
     np.testing.assert_array_equal(nc, n2)
 
 
-def test_als_selection_ties_and_clamps(ctx, port):
+@pytest.mark.parametrize("rank", [8, 32])
+def test_als_selection_ties_and_clamps(ctx, port, rank):
     """Rows engineered to hit the clamp floor/ceiling and exact saving ties."""
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
     from paper_2508_07605_b200 import PowerGrid
@@ -80,7 +82,7 @@ def test_als_selection_ties_and_clamps(ctx, port):
     rp[1:] = np.cumsum(mask.sum(1))
     ii, jj = np.nonzero(mask)
     col, val = jj.astype(np.int32), dense[ii, jj].astype(np.float32)
-    plan = AlsPlan(m, rp, col, val, grid, AlsHyper(rank=8, sweeps=3), 0.1, ctx=ctx)
+    plan = AlsPlan(m, rp, col, val, grid, AlsHyper(rank=rank, sweeps=3), 0.1, ctx=ctx)
     plan.run()
     idx, sav, loss, nc = plan.results()
     rows = plan.completed_rows(0, m)
@@ -92,16 +94,17 @@ def test_als_selection_ties_and_clamps(ctx, port):
     np.testing.assert_array_equal(nc, n2)
 
 
-def test_als_end_to_end_decisions_match_oracle_where_margin_allows(ctx, port):
+@pytest.mark.parametrize("rank", [16, 32])
+def test_als_end_to_end_decisions_match_oracle_where_margin_allows(ctx, port, rank):
     from oracle import bind
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
 
     grid, A = _problem(2000, 16, 16, 0.05, 2, seed=9)
-    hyp = AlsHyper(rank=16, lam=0.003, sweeps=8, seed=2)
+    hyp = AlsHyper(rank=rank, lam=0.003, sweeps=8, seed=2)
     plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
     plan.run()
     idx, sav, loss, nc = plan.results()
-    Uo, Vo = bind.als_fit(port, A.m, A.n, A.row_ptr, A.col, A.val, 16, 0.003, 8, 2)
+    Uo, Vo = bind.als_fit(port, A.m, A.n, A.row_ptr, A.col, A.val, rank, 0.003, 8, 2)
     rows_o = bind.als_completed_rows(Uo, Vo, A.row_ptr, A.col, A.val, np.arange(A.m))
     cpu, gpu = grid.arrays()
     rc, io_, so, lo, no = port.select_caps(rows_o, cpu, gpu, 0.05)
