@@ -403,21 +403,30 @@ def workload_joint(args, d: Dist):
     assert (idx >= 0).all() and (ncand >= 1).all()
     plan.close()
     del t_rp, t_col, t_val
-    # end to end through the public API with host buffers (N=1: the one-shot plan;
-    # N>1: each rank uploads its shard and runs the sharded schedule)
+    # end to end through the public API with host buffers: a plan created once
+    # (device allocations are not the workload), then per step the CSR is
+    # uploaded from pinned host memory (ocg_als_plan_upload), the plan runs
+    # from scratch and the decisions are read back to the host.
+    # N>1: each rank uploads its shard and runs the sharded schedule.
+    pin = [torch.from_numpy(x).pin_memory() for x in (A.row_ptr, A.col, A.val)]
+    p2 = AlsPlan(m_loc, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+    if d.world == 1:
+        p2.run(timed=False)  # warm (module load, first-touch)
     e2e_steps = max(1, min(args.steps, 3))
     d.barrier()
     e2e_t = 0.0
     for _ in range(e2e_steps):
+        ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+        torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        p2 = AlsPlan(m_loc, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+        p2.upload(*(int(x.data_ptr()) for x in pin))
         if d.world == 1:
             p2.run(timed=False)
         else:
             ShardedAlsDriver(GpuAlsBackend(p2, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
         r2 = p2.results()
-        p2.close()
         e2e_t += time.perf_counter() - t0
+    p2.close()
     e2e_t = d.max(e2e_t / e2e_steps)
     if d.world == 1:
         assert np.array_equal(r2[0], idx)

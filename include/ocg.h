@@ -178,6 +178,12 @@ typedef struct ocg_als_plan ocg_als_plan;
 int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const int32_t* col, const float* val,
                         int on_device, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
                         int32_t ngpu, const ocg_als_hyper* hyper, double gamma, ocg_als_plan** out);
+/* new observations for an existing plan (streaming refits, end-to-end
+ * timing): host CSR with the plan's m and nnz, copied asynchronously on the
+ * context stream into the plan's own device buffers (pinned host memory makes
+ * the copy overlap-capable); the next _run completes it from scratch.
+ * OCG_E_INVALID if nnz differs or the plan was created on device pointers. */
+int ocg_als_plan_upload(ocg_als_plan* plan, const int64_t* row_ptr, const int32_t* col, const float* val);
 /* one full step on device data: CSC build, fit, fused imputation+selection.
  * total_ms / phase_ms[4] (CSC, row sweeps, column sweeps, select): CUDA-event
  * times on the context stream (either may be NULL = asynchronous). */
@@ -185,7 +191,9 @@ int ocg_als_plan_run(ocg_als_plan* plan, float* total_ms, float* phase_ms);
 /* Phase-level form of _run for the row-sharded multi-GPU driver (each rank
  * holds a row shard of the CSR with all n columns): begin = CSC +
  * V init; per sweep: row_half (local), col_gram (this shard's column Gram
- * records, n x (k*k + k + 1) floats, into d_gram) -> allreduce(sum) across
+ * records, n x ocg_als_plan_gram_floats/n floats: k*k + k + 1 at rank 8/16,
+ * the 612-float packed lower-triangle record at rank 32, into d_gram) ->
+ * allreduce(sum) across
  * ranks -> col_solve(d_gram) (replicated, deterministic); finally select.
  * col_half = the single-GPU fused column half-sweep. */
 int ocg_als_plan_begin(ocg_als_plan* plan);

@@ -146,6 +146,7 @@ class AlsHyperC(ctypes.Structure):
 _sig("ocg_als_plan_create", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i32, c_vp, c_i32,
      c_vp, c_dbl, ctypes.POINTER(c_vp))
 _sig("ocg_als_plan_run", ctypes.c_int, c_vp, c_vp, c_vp)
+_sig("ocg_als_plan_upload", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_completed_rows", ctypes.c_int, c_vp, c_i64, c_i64, c_vp)
 _sig("ocg_als_plan_destroy", None, c_vp)

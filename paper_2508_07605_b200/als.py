@@ -50,6 +50,18 @@ class AlsPlan:
         check(lib.ocg_als_plan_create(self.ctx.handle, self.m, *args, 1 if on_device else 0, ptr(cpu), len(cpu),
                                       ptr(gpu), len(gpu), ctypes.byref(h), gamma, ctypes.byref(self._h)))
 
+    def upload(self, row_ptr, col, val):
+        """New observations (same m and nnz) from host memory: numpy arrays, or
+        host addresses (ints, e.g. pinned buffers) the caller keeps alive until
+        the next run completes."""
+        if isinstance(row_ptr, int):
+            args = (ctypes.c_void_p(row_ptr), ctypes.c_void_p(col), ctypes.c_void_p(val))
+        else:
+            self._keep = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
+                          np.ascontiguousarray(val, np.float32))
+            args = tuple(ptr(a) for a in self._keep)
+        check(lib.ocg_als_plan_upload(self._h, *args))
+
     def run(self, timed: bool = True):
         """One step (CSC build + fit + fused imputation/selection).
         Returns (total_ms, [csc_ms, row_sweeps_ms, col_sweeps_ms, select_ms])."""

@@ -313,6 +313,21 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     return OCG_OK;
 }
 
+int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* col, const float* val) {
+    if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (row_ptr[P->m] != P->nnz) return ocg_internal_fail(OCG_E_INVALID, "als upload: nnz differs from the plan's");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
+    if (P->k == 32) {
+        ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
+        ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
+    }
+    return OCG_OK;
+}
+
 static int launch_select(ocg_als_plan* P) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
     if (P->k != 32) ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));

@@ -126,3 +126,27 @@ def test_als_end_to_end_decisions_match_oracle_where_margin_allows(ctx, port, ra
     np.testing.assert_array_equal(idx[safe], io_[safe])
     agree = (idx == io_).mean()
     assert agree > 0.9, agree
+
+
+def test_als_upload_refit_matches_fresh_plan(ctx):
+    """ocg_als_plan_upload + run == a plan created on the new data (streaming refit)."""
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(900, 8, 16, 0.08, 2, seed=13)
+    hyp = AlsHyper(rank=32, sweeps=3)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+    plan.run()
+    rng = np.random.default_rng(1)
+    val2 = np.clip(A.val * rng.uniform(0.9, 1.1, A.val.shape), 0.01, 1.25).astype(np.float32)
+    plan.upload(A.row_ptr, A.col, val2)
+    plan.run()
+    got = plan.results()
+    fresh = AlsPlan(A.m, A.row_ptr, A.col, val2, grid, hyp, 0.05, ctx=ctx)
+    fresh.run()
+    want = fresh.results()
+    for g_, w_ in zip(got, want):
+        np.testing.assert_array_equal(g_, w_)
+    rp2 = A.row_ptr.copy()
+    rp2[-1] -= 1  # nnz differs from the plan's
+    with pytest.raises(Exception):
+        plan.upload(rp2, A.col[:-1], val2[:-1])
