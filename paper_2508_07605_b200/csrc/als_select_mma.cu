@@ -47,6 +47,7 @@ constexpr int kW = 8;          // warps per CTA
 constexpr int kTile = 256;     // V columns per tile
 constexpr int kNT = kTile / 8;  // n-tiles per tile
 constexpr float kBand = 1.0f + 0x1p-18f;
+constexpr int kList = 96;      // observed columns kept in shared memory per row (longer rows: global)
 
 struct BestX {
     double s, p;
@@ -160,11 +161,14 @@ template <bool WRITE_COMPLETED>
 __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArgs P) {
     const AlsSelectArgs& a = P.a;
     extern __shared__ __align__(16) uint4 sdyn[];
-    uint4* Vs = sdyn;                                                   // [2][kTile][8]
-    int32_t* csum = reinterpret_cast<int32_t*>(Vs + 2 * kTile * 8);     // [2][kTile]
-    uint32_t* maskw = reinterpret_cast<uint32_t*>(csum + 2 * kTile);    // [kW][16][8]
-    BestX* bx = reinterpret_cast<BestX*>(maskw + kW * 16 * 8);          // [kW][32 lanes][2 rows]
-    int32_t* caps = reinterpret_cast<int32_t*>(bx + kW * 32 * 2);       // [ncpu + ngpu]
+    uint4* Vs = sdyn;                                                     // [2][kTile][8]
+    float* csum = reinterpret_cast<float*>(Vs + 2 * kTile * 8);           // [2][kTile] c+g per column
+    uint32_t* maskw = reinterpret_cast<uint32_t*>(csum + 2 * kTile);      // [kW][16][8]
+    BestX* bx = reinterpret_cast<BestX*>(maskw + kW * 16 * 8);            // [kW][32 lanes][2 rows]
+    BestX* obest = bx + kW * 32 * 2;                                      // [kW][16 rows] observed best
+    int32_t* ocnt = reinterpret_cast<int32_t*>(obest + kW * 16);          // [kW][16] valid observed
+    int32_t* caps = ocnt + kW * 16;                                       // [512]
+    uint16_t* olist = reinterpret_cast<uint16_t*>(caps + 512);            // [kW][16][kList] columns
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t = lane & 3;
     const int64_t n = a.n;
@@ -175,6 +179,10 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
     const float su = ldexpf(1.0f, eu), inv_s = ldexpf(1.0f, -(eu + ev));
     uint32_t* mymask = maskw + warp * 16 * 8;
     BestX* myb = bx + (warp * 32 + lane) * 2;
+    BestX* myob = obest + warp * 16;
+    int32_t* myoc = ocnt + warp * 16;
+    uint16_t* mylist = olist + warp * 16 * kList;
+    __syncthreads();  // caps
 
     auto load_tile = [&](int tt, int buf) {
         const int64_t c0 = static_cast<int64_t>(tt) * kTile;
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                 const int ci = static_cast<int>(j / ngpu);
                 cs = caps[ci] + caps[ncpu + static_cast<int>(j - static_cast<int64_t>(ci) * ngpu)];
             }
-            csum[buf * kTile + e] = cs;
+            csum[buf * kTile + e] = static_cast<float>(cs);  // small integer: exact
         }
         cp_async_commit();
     };
@@ -265,19 +273,64 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
             const double thr = valid_threshold(pbase[q], a.gamma);
             float f = static_cast<float>(thr);
             if (static_cast<double>(f) < thr) f = __uint_as_float(__float_as_uint(f) + 1u);
-            fthr[q] = f;                                  // float p valid <=> p >= fthr
-            lov[q] = 0.01 >= thr ? INFINITY : -INFINITY;  // cells clamped to 0.01: valid iff 0.01 >= thr
-            tbest[q] = INFINITY;
-            tband[q] = INFINITY;
+            fthr[q] = live[q] ? f : INFINITY;  // float p valid <=> p >= fthr (dead rows: nothing valid)
+            lov[q] = live[q] && 0.01 >= thr ? INFINITY : -INFINITY;  // cells clamped to 0.01: valid iff 0.01 >= thr
             ncand[q] = 0;
             myb[q] = BestX{0.0, 0.0, -1, 0};
         }
-        // mask owner: lane r < 16 walks row r0 + r's CSR entries tile by tile
-        int64_t mbeg = 0;
+        // ---- observed pass: the whole warp walks each row's CSR entries (coalesced),
+        // evaluates the valid ones exactly, keeps the columns for the tile masks, and
+        // seeds the row's band with the best observed cell.
+#pragma unroll 1
+        for (int rr = 0; rr < 16; ++rr) {
+            const int64_t i = r0 + rr;
+            if (i >= a.m) break;
+            const int src = (rr & 7) * 4;
+            const float fth = __shfl_sync(0xffffffffu, (rr >> 3) ? fthr[1] : fthr[0], src);
+            const int64_t rbeg = a.row_ptr[i];
+            const int rl = static_cast<int>(a.row_ptr[i + 1] - rbeg);
+            SelResult sr{-1, 0.0, 0.0, 0.0, 0, 0};
+            bool have = false;
+            int oc = 0;
+            for (int e = lane; e < rl; e += 32) {
+                const int j = a.col[rbeg + e];
+                const float v = a.val[rbeg + e];
+                if (e < kList) mylist[rr * kList + e] = static_cast<uint16_t>(j);
+                if (WRITE_COMPLETED) a.completed[i * n + j] = static_cast<double>(v);
+                if (v >= fth) {
+                    ++oc;
+                    const int ci = j / ngpu;
+                    const int cs = caps[ci] + caps[ncpu + (j - ci * ngpu)];
+                    const double pd = static_cast<double>(v);
+                    const double sv = ddiv(dsub(a.e_base, ddiv(static_cast<double>(cs), pd)), a.e_base);
+                    if (!have || sel_better(sv, pd, cs, j, sr)) {
+                        sr = SelResult{j, sv, 0.0, pd, cs, 0};
+                        have = true;
+                    }
+                }
+            }
+            const SelResult w = sel_warp_reduce(sr, have, oc);
+            if (lane == 0) {
+                myob[rr] = BestX{w.saving, w.perf, w.idx, w.sum};
+                myoc[rr] = w.ncand;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const BestX ob = myob[(g + 8 * q) & 15];
+            tbest[q] = ob.j >= 0 ? __fdividef(static_cast<float>(ob.sum), static_cast<float>(ob.p)) : INFINITY;
+            tband[q] = tbest[q] * kBand;
+        }
+        // mask owner: lane r < 16 walks row r0 + r's columns tile by tile
         int mcur = 0, mend = 0;
+        int64_t mbeg = 0;
+        bool mfull = false, mglob = false;
         if (lane < 16 && r0 + lane < a.m) {
             mbeg = a.row_ptr[r0 + lane];
             mend = static_cast<int>(a.row_ptr[r0 + lane + 1] - mbeg);
+            mfull = mend == n;        // fully observed (offline dense rows)
+            mglob = mend > kList;     // list overflow: read the columns from global memory
         }
         // ---- dense pass over the tiles (unobserved cells)
         for (int tt = 0; tt < ntiles; ++tt) {
@@ -288,21 +341,24 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
             __syncwarp();  // every lane has read the previous tile's mask words
             if (lane < 16) {
                 uint32_t* mw = mymask + lane * 8;
+                const uint32_t fill = mfull ? 0xffffffffu : 0u;
 #pragma unroll
-                for (int w = 0; w < 8; ++w) mw[w] = 0u;
-                while (mcur < mend) {
-                    const int64_t c = a.col[mbeg + mcur];
-                    if (c >= c0 + kTile) break;
-                    const int cc = static_cast<int>(c - c0);
-                    mw[2 * ((cc & 7) >> 1) + (cc >> 7)] |= 1u << ((((cc >> 3) & 15) << 1) | (cc & 1));
-                    ++mcur;
+                for (int w = 0; w < 8; ++w) mw[w] = fill;
+                if (!mfull) {
+                    while (mcur < mend) {
+                        const int c = mglob ? a.col[mbeg + mcur] : mylist[lane * kList + mcur];
+                        if (c >= c0 + kTile) break;
+                        const int cc = static_cast<int>(c - c0);
+                        mw[2 * ((cc & 7) >> 1) + (cc >> 7)] |= 1u << ((((cc >> 3) & 15) << 1) | (cc & 1));
+                        ++mcur;
+                    }
                 }
             }
             cp_async_wait_all();
             __syncthreads();  // tile tt landed, masks written
             if (tt + 1 < ntiles) load_tile(tt + 1, buf ^ 1);
             const uint4* vt = Vs + buf * kTile * 8;
-            const int32_t* cst = csum + buf * kTile;
+            const float* cst = csum + buf * kTile;
             uint32_t mk[2][2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -310,7 +366,17 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                 mk[q][0] = w.x;
                 mk[q][1] = w.y;
             }
-            const int64_t nleft = n - c0;  // columns of this tile that exist
+            if (n - c0 < kTile) {  // ragged last tile: columns >= n count as observed
+#pragma unroll
+                for (int nt = 0; nt < kNT; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (nt * 8 + 2 * t + e >= n - c0) {
+                            const uint32_t b = 1u << (((nt & 15) << 1) | e);
+                            mk[0][nt >> 4] |= b;
+                            mk[1][nt >> 4] |= b;
+                        }
+            }
 #pragma unroll 4
             for (int nt = 0; nt < kNT; ++nt) {
                 const int cc = nt * 8;
@@ -319,97 +385,88 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                 const uint4 bl = vt[(cc + g) * 8 + t + 4 * (1 - odd)];
                 float d[4];
                 mma_cell(d, bh, bl);
-                const int2 cs2 = *reinterpret_cast<const int2*>(cst + cc + 2 * t);
+                const float2 cs2 = *reinterpret_cast<const float2*>(cst + cc + 2 * t);
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int jc = cc + 2 * t + e;
-                    const bool jin = jc < nleft;
-                    const int cs = e ? cs2.y : cs2.x;
-                    const float csf = static_cast<float>(cs);
+                    const float csf = e ? cs2.y : cs2.x;
                     const int bit = ((nt & 15) << 1) | e;
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const float pf = d[2 * q + e] * inv_s;
                         const bool ob = (mk[q][nt >> 4] >> bit) & 1u;
-                        const bool use = live[q] && jin && !ob;
                         const bool lo = pf <= 0.01f;
                         const float pc = fminf(pf, 1.25f);
                         const float pv = lo ? lov[q] : pc;
-                        const bool valid = use && pv >= fthr[q];
-                        ncand[q] += valid ? 1 : 0;
+                        const bool valid = !ob && pv >= fthr[q];
+                        ncand[q] += valid;
                         const float pe = fmaxf(pc, 0.01f);
-                        if (WRITE_COMPLETED && use)
+                        if (WRITE_COMPLETED && !ob && live[q])
                             a.completed[rowg[q] * n + c0 + jc] = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
                         if (valid && csf <= tband[q] * pe) {
                             const double pd = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
-                            exact_update(myb + q, pd, cs, static_cast<int>(c0) + jc, a.e_base);
+                            exact_update(myb + q, pd, static_cast<int>(csf), static_cast<int>(c0) + jc, a.e_base);
                             tbest[q] = fminf(tbest[q], __fdividef(csf, pe));
                             tband[q] = tbest[q] * kBand;
                         }
                     }
                 }
             }
+            // share the running best within the quad (the 4 lanes holding a row)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                tbest[q] = fminf(tbest[q], __shfl_xor_sync(0xffffffffu, tbest[q], 1));
+                tbest[q] = fminf(tbest[q], __shfl_xor_sync(0xffffffffu, tbest[q], 2));
+                tband[q] = tbest[q] * kBand;
+            }
         }
-        // ---- observed pass + per-row merge.  Row r = r0 + rr: its dense state is in the
-        // quad g = rr & 7 (q = rr >> 3); the whole warp walks its CSR entries.
-#pragma unroll 1
-        for (int rr = 0; rr < 16; ++rr) {
-            const int64_t i = r0 + rr;
-            if (i >= a.m) break;
-            const int qq = rr >> 3, src = (rr & 7) * 4;
-            const float my_tb = qq ? tbest[1] : tbest[0];
-            float tb = fminf(my_tb, __shfl_xor_sync(0xffffffffu, my_tb, 1));
-            tb = fminf(tb, __shfl_xor_sync(0xffffffffu, tb, 2));
-            tb = __shfl_sync(0xffffffffu, tb, src);
-            const float fth = __shfl_sync(0xffffffffu, qq ? fthr[1] : fthr[0], src);
-            const double pb = __shfl_sync(0xffffffffu, qq ? pbase[1] : pbase[0], src);
-            float tbd = tb * kBand;
-            const int64_t rbeg = a.row_ptr[i];
-            const int rl = static_cast<int>(a.row_ptr[i + 1] - rbeg);
-            BestX ob{0.0, 0.0, -1, 0};
-            int oc = 0;
-            for (int e = lane; e < rl; e += 32) {
-                const int j = a.col[rbeg + e];
-                const float v = a.val[rbeg + e];
-                const int ci = j / ngpu;
-                const int cs = caps[ci] + caps[ncpu + (j - ci * ngpu)];
-                const bool valid = v >= fth;
-                oc += valid ? 1 : 0;
-                if (WRITE_COMPLETED) a.completed[i * n + j] = static_cast<double>(v);
-                if (valid && static_cast<float>(cs) <= tbd * v) {
-                    exact_update(&ob, static_cast<double>(v), cs, j, a.e_base);
-                    tbd = fminf(tbd, __fdividef(static_cast<float>(cs), v) * kBand);
-                }
+        // ---- merge per row: the quad's dense candidates + the observed best
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            BestX b = myb[q];
+            int cnt = ncand[q];
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                BestX o;
+                o.s = __shfl_xor_sync(0xffffffffu, b.s, off);
+                o.p = __shfl_xor_sync(0xffffffffu, b.p, off);
+                o.j = __shfl_xor_sync(0xffffffffu, b.j, off);
+                o.sum = __shfl_xor_sync(0xffffffffu, b.sum, off);
+                cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+                bool better;
+                if (o.j < 0) better = false;
+                else if (b.j < 0) better = true;
+                else if (o.s != b.s) better = o.s > b.s;
+                else if (o.p != b.p) better = o.p > b.p;
+                else if (o.sum != b.sum) better = o.sum < b.sum;
+                else better = o.j < b.j;
+                if (better) b = o;
             }
-            // merge the quad's dense candidate into its lanes' observed candidate
-            if ((lane >> 2) == (rr & 7)) {
-                const BestX db = myb[qq];
-                oc += qq ? ncand[1] : ncand[0];
-                if (db.j >= 0) {
-                    bool better;
-                    if (ob.j < 0) better = true;
-                    else if (db.s != ob.s) better = db.s > ob.s;
-                    else if (db.p != ob.p) better = db.p > ob.p;
-                    else if (db.sum != ob.sum) better = db.sum < ob.sum;
-                    else better = db.j < ob.j;
-                    if (better) ob = db;
-                }
-            }
-            SelResult sr{ob.j, ob.s, 0.0, ob.p, ob.sum, 0};
-            const SelResult w = sel_warp_reduce(sr, ob.j >= 0, oc);
-            if (lane == 0) {
-                a.idx[i] = w.idx;
-                a.saving[i] = w.saving;
-                a.loss[i] = w.idx >= 0 ? dsub(1.0, ddiv(w.perf, pb)) : 0.0;
-                a.ncand[i] = w.ncand;
+            const int rr = g + 8 * q;
+            if (t == 0 && live[q]) {
+                const BestX o = myob[rr];
+                bool better;
+                if (o.j < 0) better = false;
+                else if (b.j < 0) better = true;
+                else if (o.s != b.s) better = o.s > b.s;
+                else if (o.p != b.p) better = o.p > b.p;
+                else if (o.sum != b.sum) better = o.sum < b.sum;
+                else better = o.j < b.j;
+                if (better) b = o;
+                const int64_t i = rowg[q];
+                a.idx[i] = b.j;
+                a.saving[i] = b.j >= 0 ? b.s : 0.0;
+                a.loss[i] = b.j >= 0 ? dsub(1.0, ddiv(b.p, pbase[q])) : 0.0;
+                a.ncand[i] = cnt + myoc[rr];
             }
         }
     }
 }
 
 size_t als_select_mma_smem() {
-    return sizeof(uint4) * 2 * kTile * 8 + sizeof(int32_t) * 2 * kTile + sizeof(uint32_t) * kW * 16 * 8 +
-           sizeof(BestX) * kW * 32 * 2 + sizeof(int32_t) * 512;
+    return sizeof(uint4) * 2 * kTile * 8 + sizeof(float) * 2 * kTile + sizeof(uint32_t) * kW * 16 * 8 +
+           sizeof(BestX) * (kW * 32 * 2 + kW * 16) + sizeof(int32_t) * (kW * 16 + 512) +
+           sizeof(uint16_t) * kW * 16 * kList;
 }
 
 // V -> packed select layout; U's and V's scales come from the Gram packing
