@@ -377,39 +377,69 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                             mk[1][nt >> 4] |= b;
                         }
             }
-#pragma unroll 4
-            for (int nt = 0; nt < kNT; ++nt) {
-                const int cc = nt * 8;
-                const int odd = g & 1;
-                const uint4 bh = vt[(cc + g) * 8 + t + 4 * odd];
-                const uint4 bl = vt[(cc + g) * 8 + t + 4 * (1 - odd)];
-                float d[4];
-                mma_cell(d, bh, bl);
-                const float2 cs2 = *reinterpret_cast<const float2*>(cst + cc + 2 * t);
+            // Epilogue in the accumulator's scale S = 2^(eu+ev) (all comparisons against
+            // thresholds multiplied by S are exact); branch-free over 2 n-tiles (8 cells),
+            // then one branch into the rare exact path if any cell is inside the band.
+            const float S = ldexpf(1.0f, eu + ev);
+            const float lo_s = 0.01f * S, hi_s = 1.25f * S;
+            const float fth_s[2] = {fthr[0] * S, fthr[1] * S};
+            float tb_s[2] = {tband[0] * inv_s, tband[1] * inv_s};
+#pragma unroll 2
+            for (int nt = 0; nt < kNT; nt += 2) {
+                float d[2][4];
+                float2 cs2[2];
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int jc = cc + 2 * t + e;
-                    const float csf = e ? cs2.y : cs2.x;
-                    const int bit = ((nt & 15) << 1) | e;
+                for (int u = 0; u < 2; ++u) {
+                    const int cc = (nt + u) * 8;
+                    const int odd = g & 1;
+                    const uint4 bh = vt[(cc + g) * 8 + t + 4 * odd];
+                    const uint4 bl = vt[(cc + g) * 8 + t + 4 * (1 - odd)];
+                    mma_cell(d[u], bh, bl);
+                    cs2[u] = *reinterpret_cast<const float2*>(cst + cc + 2 * t);
+                }
+                unsigned hit = 0;
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const float pf = d[2 * q + e] * inv_s;
-                        const bool ob = (mk[q][nt >> 4] >> bit) & 1u;
-                        const bool lo = pf <= 0.01f;
-                        const float pc = fminf(pf, 1.25f);
-                        const float pv = lo ? lov[q] : pc;
-                        const bool valid = !ob && pv >= fthr[q];
-                        ncand[q] += valid;
-                        const float pe = fmaxf(pc, 0.01f);
-                        if (WRITE_COMPLETED && !ob && live[q])
-                            a.completed[rowg[q] * n + c0 + jc] = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
-                        if (valid && csf <= tband[q] * pe) {
-                            const double pd = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
-                            exact_update(myb + q, pd, static_cast<int>(csf), static_cast<int>(c0) + jc, a.e_base);
-                            tbest[q] = fminf(tbest[q], __fdividef(csf, pe));
-                            tband[q] = tbest[q] * kBand;
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const float csf = e ? cs2[u].y : cs2[u].x;
+                        const int bit = (((nt + u) & 15) << 1) | e;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const float x = d[u][2 * q + e];
+                            const bool ob = (mk[q][(nt + u) >> 4] >> bit) & 1u;
+                            const bool lo = x <= lo_s;
+                            const float pc = fminf(x, hi_s);
+                            const bool valid = !ob && (lo ? lov[q] : pc) >= fth_s[q];
+                            ncand[q] += valid;
+                            if (valid && csf <= tb_s[q] * fmaxf(pc, lo_s)) hit |= 1u << (4 * u + 2 * e + q);
+                            if (WRITE_COMPLETED && !ob && live[q]) {
+                                const float pf = x * inv_s;
+                                a.completed[rowg[q] * n + c0 + (nt + u) * 8 + 2 * t + e] =
+                                    lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
+                            }
                         }
                     }
+                if (hit) {  // rare: exact FP64 evaluation of the cells inside the band
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e)
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) {
+                                if (!((hit >> (4 * u + 2 * e + q)) & 1u)) continue;
+                                const float csf = e ? cs2[u].y : cs2[u].x;
+                                const float pf = d[u][2 * q + e] * inv_s;
+                                const bool lo = pf <= 0.01f;
+                                if (csf > tb_s[q] * fmaxf(fminf(d[u][2 * q + e], hi_s), lo_s)) continue;  // band moved
+                                const double pd = lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
+                                exact_update(myb + q, pd, static_cast<int>(csf),
+                                             static_cast<int>(c0) + (nt + u) * 8 + 2 * t + e, a.e_base);
+                                const float pe = fmaxf(fminf(pf, 1.25f), 0.01f);
+                                tbest[q] = fminf(tbest[q], __fdividef(csf, pe));
+                                tband[q] = tbest[q] * kBand;
+                                tb_s[q] = tband[q] * inv_s;
+                            }
                 }
             }
             // share the running best within the quad (the 4 lanes holding a row)
