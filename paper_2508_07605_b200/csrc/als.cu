@@ -497,6 +497,25 @@ __global__ void gather_csc_kernel(int64_t nnz, const int32_t* __restrict__ perm,
     cval[q] = val[p];
 }
 
+// (row << 32 | value bits) per CSR entry, the payload of the column sort
+__global__ void expand_pairs_kernel(int64_t m, const int64_t* __restrict__ ptr, const uint32_t* __restrict__ vbits,
+                                    uint64_t* __restrict__ pairs) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < m; i += nw)
+        for (int64_t q = ptr[i] + lane; q < ptr[i + 1]; q += 32)
+            pairs[q] = (static_cast<uint64_t>(i) << 32) | vbits[q];
+}
+
+__global__ void split_pairs_kernel(int64_t nnz, const uint64_t* __restrict__ pairs, int32_t* __restrict__ crow,
+                                   uint32_t* __restrict__ cval) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nnz) return;
+    const uint64_t p = pairs[q];
+    crow[q] = static_cast<int32_t>(p >> 32);
+    cval[q] = static_cast<uint32_t>(p);
+}
+
 // col_ptr from the sorted column keys (first occurrence per column)
 __global__ void col_ptr_kernel(int64_t nnz, int64_t n, const int32_t* __restrict__ skeys, int64_t* __restrict__ cptr) {
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -604,6 +623,18 @@ cudaError_t launch_gather_csc(int64_t nnz, const int32_t* perm, const int32_t* r
                               float* cval, cudaStream_t s) {
     if (nnz == 0) return cudaSuccess;
     gather_csc_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(nnz, perm, rowid, val, crow, cval);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand_pairs(int64_t m, const int64_t* ptr, const uint32_t* vbits, uint64_t* pairs, int sm_count,
+                                cudaStream_t s) {
+    expand_pairs_kernel<<<sm_count * 8, 256, 0, s>>>(m, ptr, vbits, pairs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_pairs(int64_t nnz, const uint64_t* pairs, int32_t* crow, uint32_t* cval, cudaStream_t s) {
+    if (nnz == 0) return cudaSuccess;
+    split_pairs_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(nnz, pairs, crow, cval);
     return cudaGetLastError();
 }
 

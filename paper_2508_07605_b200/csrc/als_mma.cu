@@ -390,7 +390,20 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
         const int32_t ns = nseg_of[item];
         const float4* src = reinterpret_cast<const float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c;
         float4 s = src[0];
-        for (int32_t q = 1; q < ns; ++q) {
+        int32_t q = 1;
+        for (; q + 4 <= ns; q += 4) {  // four loads in flight; the sum order stays q = 0, 1, 2, ...
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = src[static_cast<int64_t>(q + u) * (kRec / 4)];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s.x += v[u].x;
+                s.y += v[u].y;
+                s.z += v[u].z;
+                s.w += v[u].w;
+            }
+        }
+        for (; q < ns; ++q) {
             const float4 v = src[static_cast<int64_t>(q) * (kRec / 4)];
             s.x += v.x;
             s.y += v.y;

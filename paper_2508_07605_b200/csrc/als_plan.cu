@@ -41,10 +41,6 @@ struct Buf {
     cudaError_t alloc(size_t n) { return n ? cudaMalloc(&p, sizeof(T) * n) : cudaSuccess; }
 };
 
-__global__ void iota_kernel(int64_t n, int32_t* out) {
-    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q < n) out[q] = static_cast<int32_t>(q);
-}
 
 int bits_for(int64_t n) {
     int b = 1;
@@ -68,7 +64,8 @@ struct ocg_als_plan {
     Buf<float> val;
     // CSC mirror + scratch
     Buf<int64_t> col_ptr;
-    Buf<int32_t> crow, rowid, keys_out, perm_in, perm_out;
+    Buf<int32_t> crow, keys_out;
+    Buf<uint64_t> pairs_in, pairs_out;  // (row << 32 | value bits) sorted by column
     Buf<float> cval;
     Buf<uint8_t> sort_tmp;
     size_t sort_tmp_bytes = 0;
@@ -105,16 +102,16 @@ struct ocg_als_plan {
 static int als_build_csc(ocg_als_plan* P) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
     const int sm = ocg_internal_sm_count(P->ctx);
-    ALS_CUDA(ocg::launch_expand_rows(P->m, P->row_ptr.p, P->rowid.p, sm, s));
     if (P->nnz > 0) {
-        iota_kernel<<<static_cast<unsigned>((P->nnz + 255) / 256), 256, 0, s>>>(P->nnz, P->perm_in.p);
-        ALS_CUDA(cudaGetLastError());
+        // (row, value) travel with the column key through the radix sort (stable:
+        // rows stay ascending inside a column), so no random gathers afterwards.
+        // Rank 32: the value word is the packed (fp16 hi, lo) form.
+        const uint32_t* vb = P->k == 32 ? P->valh.p : reinterpret_cast<const uint32_t*>(P->val.p);
+        ALS_CUDA(ocg::launch_expand_pairs(P->m, P->row_ptr.p, vb, P->pairs_in.p, sm, s));
         size_t bytes = P->sort_tmp_bytes;
-        ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, P->col.p, P->keys_out.p, P->perm_in.p,
-                                                 P->perm_out.p, P->nnz, 0, bits_for(P->n), s));
-        // rank 32: the column side gathers the packed values (same 4-byte moves)
-        const float* cv = P->k == 32 ? reinterpret_cast<const float*>(P->valh.p) : P->val.p;
-        ALS_CUDA(ocg::launch_gather_csc(P->nnz, P->perm_out.p, P->rowid.p, cv, P->crow.p, P->cval.p, s));
+        ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, P->col.p, P->keys_out.p, P->pairs_in.p,
+                                                 P->pairs_out.p, P->nnz, 0, bits_for(P->n), s));
+        ALS_CUDA(ocg::launch_split_pairs(P->nnz, P->pairs_out.p, P->crow.p, reinterpret_cast<uint32_t*>(P->cval.p), s));
     }
     ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
     for (int sd = 0; sd < 2; ++sd) {
@@ -182,12 +179,11 @@ static int als_alloc(ocg_als_plan* P) {
     ALS_CUDA(P->col_ptr.alloc(static_cast<size_t>(P->n + 1)));
     ALS_CUDA(P->crow.alloc(static_cast<size_t>(P->nnz)));
     ALS_CUDA(P->cval.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->rowid.alloc(static_cast<size_t>(P->nnz)));
     ALS_CUDA(P->keys_out.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->perm_in.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->perm_out.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->pairs_in.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->pairs_out.alloc(static_cast<size_t>(P->nnz)));
     size_t bytes = 0;
-    ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P->col.p, P->keys_out.p, P->perm_in.p, P->perm_out.p,
+    ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P->col.p, P->keys_out.p, P->pairs_in.p, P->pairs_out.p,
                                              P->nnz, 0, bits_for(P->n)));
     P->sort_tmp_bytes = bytes;
     ALS_CUDA(P->sort_tmp.alloc(bytes));
