@@ -371,7 +371,7 @@ def workload_joint(args, d: Dist):
     torch.cuda.synchronize(dev)
     plan = AlsPlan(m_loc, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, hyp, args.gamma,
                    on_device=True, ctx=ctx)
-    phases = [0.0, 0.0, 0.0, 0.0]
+    phases = [0.0] * 6
     if d.world == 1:
         step = lambda: plan.run(timed=True)  # noqa: E731
     else:
@@ -384,7 +384,7 @@ def workload_joint(args, d: Dist):
             driver.run(args.sweeps)
             e1.record()
             e1.synchronize()
-            return e0.elapsed_time(e1), [0.0] * 4
+            return e0.elapsed_time(e1), [0.0] * 6
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -462,19 +462,36 @@ def workload_joint(args, d: Dist):
     if d.world == 1:
         row_ms = phases[1] / args.steps / args.sweeps
         col_ms = phases[2] / args.steps / args.sweeps
-        # one kernel (als_seg_gram_kernel) serves both half-sweeps: average bytes
-        # per launch over the average launch duration
-        achieved = (row_bytes + col_bytes) / 2 / ((row_ms + col_ms) / 2 / 1e3) / 1e9
         out["phases_ms_per_step"] = {"csc_build_and_segments": phases[0] / args.steps,
                                      "row_half_sweeps": phases[1] / args.steps,
                                      "col_half_sweeps": phases[2] / args.steps,
-                                     "impute_select": phases[3] / args.steps}
-        out["roofline"] = {"bound": "hbm", "kernel": "als_seg_gram_kernel (K3 Gram accumulation)",
+                                     "impute_select": phases[3] / args.steps,
+                                     "row_gram_kernel": phases[4] / args.steps,
+                                     "col_gram_kernel": phases[5] / args.steps}
+        # K3 Gram kernel alone (CUDA events around its launches on the library
+        # stream), row and column launches averaged: gather-counted bytes per launch
+        # over the average launch duration.
+        g_row = phases[4] / args.steps / args.sweeps
+        g_col = phases[5] / args.steps / args.sweeps
+        if g_row > 0 and g_col > 0:
+            kern, t_row, t_col = "als_mma_gram32_kernel (K3 Gram accumulation, mma.sync f16 hi/lo)", g_row, g_col
+        else:  # rank 8/16: the fused SIMT Gram + solve kernel; whole half-sweeps
+            kern, t_row, t_col = "als_seg_gram_kernel (K3 Gram + K4 solve, SIMT)", row_ms, col_ms
+        achieved = (row_bytes + col_bytes) / 2 / ((t_row + t_col) / 2 / 1e3) / 1e9
+        traffic = None
+        tf = ROOT / "profiles" / "gram_dram_traffic.json"
+        if tf.exists() and k == 32:
+            tj = json.loads(tf.read_text())
+            traffic = (tj["row_bytes"] + tj["col_bytes"]) / 2
+        out["roofline"] = {"bound": "hbm", "kernel": kern,
                            "achieved": achieved, "peak": PEAKS["hbm_gbs"], "unit": "GB/s",
-                           "frac": achieved / PEAKS["hbm_gbs"], "traffic": None,
-                           "bytes_def": "gather-counted per launch: nnz*(8+4k) + items*(4k+8) (SURVEY 8d K3); "
-                                        "DRAM traffic from ncu in profiles/ (V gathers hit L2)",
-                           "launch_ms_row": row_ms, "launch_ms_col": col_ms}
+                           "frac": achieved / PEAKS["hbm_gbs"], "traffic": traffic,
+                           "bytes_def": "gather-counted per launch: nnz*(8+4k) + items*(4k+8) (SURVEY 8d K3; the "
+                                        "factor-row gathers are served mostly by L2). traffic = measured DRAM "
+                                        "read+write per launch (ncu, profiles/gram_dram_traffic.json): the "
+                                        "compulsory CSR read + per-segment Gram records written for K4",
+                           "launch_ms_row": t_row, "launch_ms_col": t_col,
+                           "half_sweep_ms_row": row_ms, "half_sweep_ms_col": col_ms}
     return out, (args.workload, m)
 
 

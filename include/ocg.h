@@ -185,8 +185,9 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
  * OCG_E_INVALID if nnz differs or the plan was created on device pointers. */
 int ocg_als_plan_upload(ocg_als_plan* plan, const int64_t* row_ptr, const int32_t* col, const float* val);
 /* one full step on device data: CSC build, fit, fused imputation+selection.
- * total_ms / phase_ms[4] (CSC, row sweeps, column sweeps, select): CUDA-event
- * times on the context stream (either may be NULL = asynchronous). */
+ * total_ms / phase_ms[6] (CSC, row sweeps, column sweeps, select, and at rank
+ * 32 the row / column Gram kernels alone): CUDA-event times on the context
+ * stream (either may be NULL = asynchronous). */
 int ocg_als_plan_run(ocg_als_plan* plan, float* total_ms, float* phase_ms);
 /* Phase-level form of _run for the row-sharded multi-GPU driver (each rank
  * holds a row shard of the CSR with all n columns): begin = CSC +

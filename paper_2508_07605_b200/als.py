@@ -64,9 +64,9 @@ class AlsPlan:
 
     def run(self, timed: bool = True):
         """One step (CSC build + fit + fused imputation/selection).
-        Returns (total_ms, [csc_ms, row_sweeps_ms, col_sweeps_ms, select_ms])."""
+        Returns (total_ms, [csc_ms, row_sweeps_ms, col_sweeps_ms, select_ms, row_gram_ms, col_gram_ms])."""
         tot = ctypes.c_float(0)
-        ph = (ctypes.c_float * 4)()
+        ph = (ctypes.c_float * 6)()
         check(lib.ocg_als_plan_run(self._h, ctypes.byref(tot) if timed else None, ph if timed else None))
         return float(tot.value), [float(x) for x in ph]
 

@@ -42,8 +42,9 @@ namespace {
 constexpr int K = 32;
 constexpr int GSZ = K * K + K + 1;
 constexpr int kWarps = 8;
-// per warp: double stage [2][32 rows][8 x 16 B] + packed r stage [2][32] u32
-constexpr int kStageU4 = 2 * 32 * 8 + 16;
+// per warp: double stage [2][32 rows][RS x 16 B] + index/value ring [8 slots][32] x 2
+constexpr int RS = 9;  // stage row stride in 16-byte units (144 B: conflict-free fragment loads, no swizzle)
+constexpr int kStageU4 = 2 * 32 * RS + (8 * 32 * 2 * 4) / 16;
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -51,6 +52,10 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, i
 }
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -144,224 +149,293 @@ constexpr int kCnt = 608;
 __host__ __device__ constexpr int tri_off(int i) { return 4 * ((i >> 2) + 1) * (2 * (i >> 2) + (i & 3)); }
 static_assert(tri_off(32) == kRhs, "record layout");
 
-// K3.  MODE 0 and 1 are identical here (every segment writes its record to
-// slot = segment id); the difference is in the reduce step.
+// K3.  One record per segment, slot = segment id (the reduce step decides
+// what happens to it).
 //
-// Gathers: 8 lanes copy one 128-byte factor row with 16-byte cp.async (rows
-// past the chunk are zero-filled); 16-byte chunk c of stage row o sits at
-// chunk c ^ (o & 7), which makes the fragment loads conflict-free.  (One TMA
-// bulk copy per row was measured 1.4x slower: per-operation cost of the
-// bulk-copy unit at 128 B.)
-// Pipelining: a segment's first chunk is gathered while the previous
-// segment's record is written, its metadata two segments ahead, and every
-// chunk's (index, value) pair one chunk ahead of its gather.
+// Work: blocks of 32 consecutive work indices (segments; column side in
+// seg_order, i.e. sorted by first row) handed out by an atomic counter; a warp
+// walks its blocks chunk by chunk (chunk = <= 32 observations of one segment;
+// an empty segment is one empty chunk).  Two cursors walk the same chunk
+// sequence:
+//  * the refill cursor, kAhead chunks ahead, copies each chunk's (index,
+//    packed value) pairs into a kRC-slot ring in shared memory (4-byte
+//    cp.async, no register round trip), crossing segment and block
+//    boundaries freely, so no global-load latency is ever exposed at a
+//    segment start;
+//  * the consumer issues the factor-row gathers of chunk c+1 from the ring
+//    (8 lanes per 128-byte row, 16-byte cp.async, zero-filled past the chunk;
+//    stage rows padded to 144 B: conflict-free fragment loads, and the copy
+//    addresses are immediate offsets), runs the MMAs of chunk c, and writes the segment's record
+//    after its last chunk (assembled in the drained stage buffer, stored with
+//    16-byte coalesced writes).
+// (One TMA bulk copy per factor row was measured 1.4x slower than the cp.async
+// gathers: per-operation cost of the bulk-copy unit at 128 B.)
+constexpr int kRC = 8;     // ring slots (chunks)
+constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
 __global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
-    const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, int64_t nitems, const int32_t* __restrict__ idx,
+    const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
-    const unsigned* __restrict__ vmax, float* __restrict__ rec) {
+    const unsigned* __restrict__ vmax, float* __restrict__ rec, int32_t* __restrict__ blk_ctr) {
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    uint4* stage = dyn4 + warp * kStageU4;  // [2][32][8] uint4
-    uint32_t* rstage = reinterpret_cast<uint32_t*>(stage + 2 * 32 * 8);  // [2][32] packed r
+    uint4* stage = dyn4 + warp * kStageU4;                                 // [2][32][RS] uint4
+    int32_t* ring_j = reinterpret_cast<int32_t*>(stage + 2 * 32 * RS);     // [kRC][32]
+    uint32_t* ring_r = reinterpret_cast<uint32_t*>(ring_j + kRC * 32);     // [kRC][32]
     const int ey = als_scale_exp(*ymax), ev = als_scale_exp(*vmax);
     const float inv_s2 = ldexpf(1.0f, -2 * ey), inv_sv = ldexpf(1.0f, -(ey + ev));
     const int32_t nsegs = *total_segs;
-    const int64_t nnz = ptr[nitems];
-    const int32_t stride = gridDim.x * kWarps;
+    const int32_t nblk = (nsegs + 31) / 32;
     const uint32_t rsel = g == 0 ? 0x5410u : 0x7632u;  // rhs B column 0 = r_hi, column 1 = r_lo
     const uint32_t rmask = g < 2 ? 0xffffffffu : 0u;
 
-    auto ldidx = [&](int64_t base, int64_t end, int& j, uint32_t& r) {
-        j = 0;
-        r = 0u;
-        if (base + lane < end) {
-            j = __ldg(idx + base + lane);
-            r = __ldg(valh + base + lane);
+    auto grab = [&]() {
+        int32_t b = 0;
+        if (lane == 0) b = atomicAdd(blk_ctr, 1);
+        return __shfl_sync(0xffffffffu, b, 0);
+    };
+    // lane i <- segment of work index 32 b + i, or b + i * nblk when the work
+    // order is sorted by band (column side: the warps active at any moment then
+    // gather from one band of the factor matrix); sg < 0: none
+    auto load_meta = [&](int32_t b, int32_t& sg, int64_t& beg, int64_t& end) {
+        const int32_t k = seg_order ? b + lane * nblk : b * 32 + lane;
+        sg = -1;
+        beg = end = 0;
+        if (b < nblk && k < nsegs) {
+            sg = seg_order ? seg_order[k] : k;
+            const int32_t it = seg_item[sg];
+            beg = seg_beg[sg];
+            end = min(beg + kSeg, ptr[it + 1]);
         }
     };
-    // gather a chunk of cnt rows (indices j, packed values r of lane = row) into buffer buf
-    auto issue = [&](int buf, int cnt, int j, uint32_t r) {
-        rstage[buf * 32 + lane] = lane < cnt ? r : 0u;
-        uint4* st = stage + buf * 32 * 8;
-        const int c16 = lane & 7, osub = lane >> 3;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int o = q * 4 + osub;
-            const int jo = __shfl_sync(0xffffffffu, j, o);
-            cp_async16_zfill(st + o * 8 + (c16 ^ (o & 7)), Yh + static_cast<int64_t>(o < cnt ? jo : 0) * 8 + c16,
-                             o < cnt ? 16 : 0);
+    auto bcast64 = [&](int64_t v, int src) {
+        return static_cast<int64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(v), src));
+    };
+
+    // ---- refill cursor (producer of ring slots)
+    int32_t rb = grab();
+    if (rb >= nblk) return;
+    int32_t r_sg;
+    int64_t r_beg, r_end;
+    load_meta(rb, r_sg, r_beg, r_end);
+    // consumer block = the refill's first block
+    int32_t cb = rb, c_sg = r_sg;
+    int64_t c_beg = r_beg, c_end = r_end;
+    int rk = 0;
+    int64_t rpos = bcast64(r_beg, 0), r_e = bcast64(r_end, 0);  // refill segment: position, end
+    bool rex = false;   // refill block exhausted
+    bool rdone = false;
+    int prod = 0;  // chunks produced
+    auto refill = [&]() {
+        if (rdone) return;
+        if (rex) {
+            if (rb != cb) return;  // the consumer still needs the pending block's metadata: wait
+            rb = grab();
+            load_meta(rb, r_sg, r_beg, r_end);
+            rk = 0;
+            if (rb >= nblk || __shfl_sync(0xffffffffu, r_sg, 0) < 0) {
+                rdone = true;
+                return;
+            }
+            rex = false;
+            rpos = bcast64(r_beg, 0);
+            r_e = bcast64(r_end, 0);
         }
+        const int cnt = min32(r_e - rpos < 0 ? 0 : r_e - rpos);
+        const int slot = (prod % kRC) * 32 + lane;
+        if (lane < cnt) {
+            cp_async4(ring_j + slot, idx + rpos + lane);
+            cp_async4(ring_r + slot, valh + rpos + lane);
+        } else {
+            ring_j[slot] = 0;
+            ring_r[slot] = 0u;
+        }
+        ++prod;
+        rpos += 32;
+        if (rpos >= r_e) {  // next segment (shuffles only at segment transitions)
+            ++rk;
+            rex = rk == 32 || __shfl_sync(0xffffffffu, r_sg, rk & 31) < 0;
+            if (!rex) {
+                rpos = bcast64(r_beg, rk);
+                r_e = bcast64(r_end, rk);
+            }
+        }
+    };
+
+    // ---- consumer cursor: current chunk (ck, cpos, cend)
+    int ck = 0;
+    int64_t cpos = bcast64(c_beg, 0), cend = bcast64(c_end, 0);
+    // gathers of a chunk (segment lane k of the consumer block, position pos) from ring slot cons
+    // lane = 8 * rg + c16 copies 16-byte chunk c16 of rows 8 rg + q (q = 0..7): its 8 row
+    // indices are two 16-byte ring loads (0 past the chunk: a valid address, zero-filled)
+    auto gather = [&](int buf, int cons, int64_t pos, int64_t e) {
+        const int cnt = min32(e - pos < 0 ? 0 : e - pos);
+        const int c16 = lane & 7, rg = lane >> 3;
+        uint4* st = stage + buf * 32 * RS + rg * 8 * RS + c16;
+        const int4* rj = reinterpret_cast<const int4*>(ring_j + (cons % kRC) * 32 + rg * 8);
+        const int4 j0 = rj[0], j1 = rj[1];
+        const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
+        const uint4* src = Yh + c16;
+        const int nv = cnt - rg * 8;  // rows of this lane group inside the chunk
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            cp_async16_zfill(st + q * RS, src + static_cast<uint32_t>(jj[q]) * 8u, q < nv ? 16 : 0);
+    };
+
+    for (int i = 0; i < kAhead; ++i) {
+        refill();
         cp_async_commit();
-    };
-
-    // work index k -> segment id (seg_order: column side sorted by first row, so
-    // concurrently running warps gather from one band of the factor matrix)
-    auto seg_of = [&](int32_t k) { return seg_order ? seg_order[k] : k; };
-    int32_t wk = blockIdx.x * kWarps + warp;
-    if (wk >= nsegs) return;
-    int32_t sg = seg_of(wk);
-    int32_t item = seg_item[sg];
-    int64_t beg = seg_beg[sg];
-    int64_t end = min(beg + kSeg, ptr[item + 1]);
-    {
-        int j;
-        uint32_t r;
-        ldidx(beg, end, j, r);
-        issue(1, min32(end - beg), j, r);
     }
-    int ja = 0, jb = 0;  // index queue: chunks 1 and 2 of the current segment
-    uint32_t ra = 0u, rb = 0u;
-    ldidx(beg + 32, end, ja, ra);
-    ldidx(beg + 64, end, jb, rb);
-    int32_t nwk = wk + stride;
-    int32_t nsg = nwk < nsegs ? seg_of(nwk) : 0;
-    int32_t nitem = nwk < nsegs ? seg_item[nsg] : 0;
-    int64_t nbeg = nwk < nsegs ? seg_beg[nsg] : 0;
-    while (true) {
-        // the next segment's end / first indices and the one after's metadata: in flight over this segment
-        // (its first three chunks' indices: chunk 0 is gathered during this
-        // segment's record write, chunks 1-2 seed the next index queue)
-        int64_t nend = 0;
-        int j0n = 0, j1n = 0, j2n = 0;
-        uint32_t r0n = 0u, r1n = 0u, r2n = 0u;
-        if (nwk < nsegs) {
-            nend = min(nbeg + kSeg, ptr[nitem + 1]);
-            ldidx(nbeg, nnz, j0n, r0n);  // speculative: masked to the segment when issued
-            ldidx(nbeg + 32, nnz, j1n, r1n);
-            ldidx(nbeg + 64, nnz, j2n, r2n);
-        }
-        const int32_t nnwk = nwk + stride;
-        const int32_t nnsg = nnwk < nsegs ? seg_of(nnwk) : 0;
-        const int32_t nnitem = nnwk < nsegs ? seg_item[nnsg] : 0;
-        const int64_t nnbeg = nnwk < nsegs ? seg_beg[nnsg] : 0;
+    cp_async_wait<0>();
+    __syncwarp();
+    gather(0, 0, cpos, cend);
+    cp_async_commit();
 
-        float acc[6][4], racc[2][4];
+    float acc[6][4], racc[2][4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 4; ++e) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) acc[q][e] = 0.0f;
-            racc[0][e] = racc[1][e] = 0.0f;
-        }
-        if (beg >= end) cp_async_wait<0>();  // empty item: its (zero-fill) gather must land before buffer 1 is reused
-        int buf = 1;
-        for (int64_t base = beg; base < end; base += 32) {
-            const int cnt = min32(end - base);
-            if (base + 32 < end) {
-                // index queue (ja: chunk t+1, jb: chunk t+2); chunk t+3's load has two iterations to land
-                issue(buf ^ 1, min32(end - base - 32), ja, ra);
-                ja = jb;
-                ra = rb;
-                if (base + 96 < end) ldidx(base + 96, end, jb, rb);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncwarp();
-            const uint4* st = stage + buf * 32 * 8;
-            const uint32_t* rs = rstage + buf * 32;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (h == 1 && cnt <= 16) break;
-                const int o0 = h * 16 + 2 * t;  // rows o0, o0+1, o0+8, o0+9 have (row & 7) = (2t, 2t+1, 2t, 2t+1)
-                const uint4 q0 = st[o0 * 8 + (g ^ (2 * t))], q1 = st[(o0 + 1) * 8 + (g ^ (2 * t + 1))];
-                const uint4 q2 = st[(o0 + 8) * 8 + (g ^ (2 * t))], q3 = st[(o0 + 9) * 8 + (g ^ (2 * t + 1))];
-                // B fragments of n-tile j (factor dim 4g+j): {b0, b1} for hi (h) and lo (l)
-                uint32_t bh0[4], bh1[4], bl0[4], bl1[4];
-                bh0[0] = prmt(q0.x, q1.x, 0x5410);
-                bh0[1] = prmt(q0.x, q1.x, 0x7632);
-                bh0[2] = prmt(q0.y, q1.y, 0x5410);
-                bh0[3] = prmt(q0.y, q1.y, 0x7632);
-                bh1[0] = prmt(q2.x, q3.x, 0x5410);
-                bh1[1] = prmt(q2.x, q3.x, 0x7632);
-                bh1[2] = prmt(q2.y, q3.y, 0x5410);
-                bh1[3] = prmt(q2.y, q3.y, 0x7632);
-                bl0[0] = prmt(q0.z, q1.z, 0x5410);
-                bl0[1] = prmt(q0.z, q1.z, 0x7632);
-                bl0[2] = prmt(q0.w, q1.w, 0x5410);
-                bl0[3] = prmt(q0.w, q1.w, 0x7632);
-                bl1[0] = prmt(q2.z, q3.z, 0x5410);
-                bl1[1] = prmt(q2.z, q3.z, 0x7632);
-                bl1[2] = prmt(q2.w, q3.w, 0x5410);
-                bl1[3] = prmt(q2.w, q3.w, 0x7632);
-                // rhs B fragment from the packed (hi, lo) values of observations o0, o0+1 / o0+8, o0+9
-                const uint2 ra = *reinterpret_cast<const uint2*>(rs + o0);
-                const uint2 rb = *reinterpret_cast<const uint2*>(rs + o0 + 8);
-                const uint32_t rb0 = prmt(ra.x, ra.y, rsel) & rmask, rb1 = prmt(rb.x, rb.y, rsel) & rmask;
-                // G lower tiles (i,j) = (0,0) (0,1) (1,0) (1,1) (1,2) (1,3): H^T H + H^T L + L^T H
-                mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bh0[0], bh1[0]);
-                mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bl0[0], bl1[0]);
-                mma16816(acc[0], bl0[0], bl0[1], bl1[0], bl1[1], bh0[0], bh1[0]);
-                mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bh0[1], bh1[1]);
-                mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bl0[1], bl1[1]);
-                mma16816(acc[1], bl0[0], bl0[1], bl1[0], bl1[1], bh0[1], bh1[1]);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bh0[j], bh1[j]);
-                    mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bl0[j], bl1[j]);
-                    mma16816(acc[2 + j], bl0[2], bl0[3], bl1[2], bl1[3], bh0[j], bh1[j]);
+        for (int q = 0; q < 6; ++q) acc[q][e] = 0.0f;
+        racc[0][e] = racc[1][e] = 0.0f;
+    }
+    int buf = 0;
+    for (int cons = 0;; ++cons) {
+        const bool last_of_seg = cpos + 32 >= cend;
+        // locate the next chunk (shuffles only at segment transitions)
+        int nk = ck;
+        int64_t npos = cpos + 32, nend = cend;
+        bool nblock = false, finished = false;
+        if (last_of_seg) {
+            nk = ck + 1;
+            if (nk == 32 || __shfl_sync(0xffffffffu, c_sg, nk & 31) < 0) {
+                // a starved refill cursor (it paused on a short block) may not have
+                // fetched the next block yet: let it, before deciding the warp is done
+                while (rb == cb && !rdone) {
+                    refill();
+                    cp_async_commit();
+                    cp_async_wait<0>();
+                    __syncwarp();
                 }
-                // rhs: (H + L)^T [r_hi r_lo]
-                mma16816(racc[0], bh0[0], bh0[1], bh1[0], bh1[1], rb0, rb1);
-                mma16816(racc[0], bl0[0], bl0[1], bl1[0], bl1[1], rb0, rb1);
-                mma16816(racc[1], bh0[2], bh0[3], bh1[2], bh1[3], rb0, rb1);
-                mma16816(racc[1], bl0[2], bl0[3], bl1[2], bl1[3], rb0, rb1);
+                // next block: the refill cursor holds its metadata (or the warp is done)
+                if (rb == cb || rb >= nblk) finished = true;
+                else nblock = true;
+                nk = 0;
             }
-            __syncwarp();
-            buf ^= 1;
-        }
-        // both buffers drained: gather the next segment's first chunk while the record is written
-        if (nwk < nsegs) issue(1, min32(nend - nbeg), j0n, r0n);
-        // ---- record, assembled in buffer 0 then stored with 16-byte coalesced writes.
-        // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) -> natural
-        // dims (pi(M), pi(N)); every unordered pair is owned by exactly one (M >= N) element.
-        float* rs_ = reinterpret_cast<float*>(stage);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const int i = q < 2 ? 0 : 1, j = q < 2 ? q : q - 2;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
-                if (M >= N) {
-                    const int a = pi_dim(M), b = pi_dim(N);
-                    const int hi = a > b ? a : b, lo = a > b ? b : a;
-                    rs_[tri_off(hi) + lo] = acc[q][e] * inv_s2;
-                }
+            if (!finished) {
+                npos = nblock ? bcast64(r_beg, 0) : bcast64(c_beg, nk);
+                nend = nblock ? bcast64(r_end, 0) : bcast64(c_end, nk);
             }
         }
-        if (t == 0) {
-            float4 rv;
-            rv.x = (racc[0][0] + racc[0][1]) * inv_sv;  // dim 4g
-            rv.y = (racc[0][2] + racc[0][3]) * inv_sv;  // dim 4g+1
-            rv.z = (racc[1][0] + racc[1][1]) * inv_sv;  // dim 4g+2
-            rv.w = (racc[1][2] + racc[1][3]) * inv_sv;  // dim 4g+3
-            *reinterpret_cast<float4*>(rs_ + kRhs + 4 * g) = rv;
-        }
-        if (lane == 0) rs_[kCnt] = static_cast<float>(end - beg);
+        if (!finished) gather(buf ^ 1, cons + 1, npos, nend);
+        refill();
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncwarp();
-        {
+        const int cnt = min32(cend - cpos < 0 ? 0 : cend - cpos);
+        const uint4* st = stage + buf * 32 * RS;
+        const uint32_t* rs = ring_r + (cons % kRC) * 32;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h * 16 >= cnt) break;
+            const int o0 = h * 16 + 2 * t;
+            const uint4 q0 = st[o0 * RS + g], q1 = st[(o0 + 1) * RS + g];
+            const uint4 q2 = st[(o0 + 8) * RS + g], q3 = st[(o0 + 9) * RS + g];
+            // B fragments of n-tile j (factor dim 4g+j): {b0, b1} for hi (h) and lo (l)
+            uint32_t bh0[4], bh1[4], bl0[4], bl1[4];
+            bh0[0] = prmt(q0.x, q1.x, 0x5410);
+            bh0[1] = prmt(q0.x, q1.x, 0x7632);
+            bh0[2] = prmt(q0.y, q1.y, 0x5410);
+            bh0[3] = prmt(q0.y, q1.y, 0x7632);
+            bh1[0] = prmt(q2.x, q3.x, 0x5410);
+            bh1[1] = prmt(q2.x, q3.x, 0x7632);
+            bh1[2] = prmt(q2.y, q3.y, 0x5410);
+            bh1[3] = prmt(q2.y, q3.y, 0x7632);
+            bl0[0] = prmt(q0.z, q1.z, 0x5410);
+            bl0[1] = prmt(q0.z, q1.z, 0x7632);
+            bl0[2] = prmt(q0.w, q1.w, 0x5410);
+            bl0[3] = prmt(q0.w, q1.w, 0x7632);
+            bl1[0] = prmt(q2.z, q3.z, 0x5410);
+            bl1[1] = prmt(q2.z, q3.z, 0x7632);
+            bl1[2] = prmt(q2.w, q3.w, 0x5410);
+            bl1[3] = prmt(q2.w, q3.w, 0x7632);
+            // rhs B fragment from the packed (hi, lo) values of observations o0, o0+1 / o0+8, o0+9
+            // (ring entries past the chunk are 0)
+            const uint2 ra = *reinterpret_cast<const uint2*>(rs + o0);
+            const uint2 rb2 = *reinterpret_cast<const uint2*>(rs + o0 + 8);
+            const uint32_t rb0 = prmt(ra.x, ra.y, rsel) & rmask, rb1 = prmt(rb2.x, rb2.y, rsel) & rmask;
+            // G lower tiles (i,j) = (0,0) (0,1) (1,0) (1,1) (1,2) (1,3): H^T H + H^T L + L^T H
+            mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bh0[0], bh1[0]);
+            mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bl0[0], bl1[0]);
+            mma16816(acc[0], bl0[0], bl0[1], bl1[0], bl1[1], bh0[0], bh1[0]);
+            mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bh0[1], bh1[1]);
+            mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bl0[1], bl1[1]);
+            mma16816(acc[1], bl0[0], bl0[1], bl1[0], bl1[1], bh0[1], bh1[1]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bh0[j], bh1[j]);
+                mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bl0[j], bl1[j]);
+                mma16816(acc[2 + j], bl0[2], bl0[3], bl1[2], bl1[3], bh0[j], bh1[j]);
+            }
+            // rhs: (H + L)^T [r_hi r_lo]
+            mma16816(racc[0], bh0[0], bh0[1], bh1[0], bh1[1], rb0, rb1);
+            mma16816(racc[0], bl0[0], bl0[1], bl1[0], bl1[1], rb0, rb1);
+            mma16816(racc[1], bh0[2], bh0[3], bh1[2], bh1[3], rb0, rb1);
+            mma16816(racc[1], bl0[2], bl0[3], bl1[2], bl1[3], rb0, rb1);
+        }
+        __syncwarp();
+        if (last_of_seg) {
+            // ---- record, assembled in the drained buffer, stored with 16-byte coalesced writes.
+            // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) ->
+            // natural dims (pi(M), pi(N)); each unordered pair is owned by exactly one (M >= N) element.
+            float* rs_ = reinterpret_cast<float*>(stage + buf * 32 * RS);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const int i = q < 2 ? 0 : 1, j = q < 2 ? q : q - 2;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
+                    if (M >= N) {
+                        const int a = pi_dim(M), b = pi_dim(N);
+                        const int hi = a > b ? a : b, lo = a > b ? b : a;
+                        rs_[tri_off(hi) + lo] = acc[q][e] * inv_s2;
+                    }
+                    acc[q][e] = 0.0f;
+                }
+            }
+            if (t == 0) {
+                float4 rv;
+                rv.x = (racc[0][0] + racc[0][1]) * inv_sv;  // dim 4g
+                rv.y = (racc[0][2] + racc[0][3]) * inv_sv;  // dim 4g+1
+                rv.z = (racc[1][0] + racc[1][1]) * inv_sv;  // dim 4g+2
+                rv.w = (racc[1][2] + racc[1][3]) * inv_sv;  // dim 4g+3
+                *reinterpret_cast<float4*>(rs_ + kRhs + 4 * g) = rv;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) racc[0][e] = racc[1][e] = 0.0f;
+            const int32_t sg = __shfl_sync(0xffffffffu, c_sg, ck);
+            const int64_t sbeg = bcast64(c_beg, ck);  // (outside the lane-0 branch: full-warp shuffle)
+            if (lane == 0) rs_[kCnt] = static_cast<float>(cend - sbeg);
+            __syncwarp();
             float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
             const float4* src = reinterpret_cast<const float4*>(rs_);
 #pragma unroll
             for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots carry stale values, never read
+            __syncwarp();
         }
-        __syncwarp();
-        ja = j1n;
-        ra = r1n;
-        jb = j2n;
-        rb = r2n;
-        if (nwk >= nsegs) break;
-        wk = nwk;
-        sg = nsg;
-        item = nitem;
-        beg = nbeg;
-        end = nend;
-        nwk = nnwk;
-        nsg = nnsg;
-        nitem = nnitem;
-        nbeg = nnbeg;
+        if (finished) break;
+        if (nblock) {
+            cb = rb;
+            c_sg = r_sg;
+            c_beg = r_beg;
+            c_end = r_end;
+        }
+        ck = nk;
+        cpos = npos;
+        cend = nend;
+        buf ^= 1;
     }
+    cp_async_wait<0>();
 }
 
 // observed values -> packed (fp16 hi, fp16 lo) of val * 2^ev
@@ -584,15 +658,19 @@ static cudaError_t launch_solve(int64_t nitems, const int32_t* first, const floa
 cudaError_t launch_als_mma_half(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
     const size_t smem = als_mma_smem_bytes();
     int64_t blocks = (h.max_segs + kWarps - 1) / kWarps;
-    const int64_t cap = static_cast<int64_t>(sm_count) * 3;
+    const int64_t cap = static_cast<int64_t>(sm_count) * 2;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    cudaFuncSetAttribute(als_mma_gram32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    als_mma_gram32_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
-        h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.nitems, h.idx, h.valh, h.Yh, h.ymax, h.vmax,
-        h.partial);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(als_mma_gram32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (h.ev_gram0) cudaEventRecord(h.ev_gram0, s);
+    als_mma_gram32_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+        h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.idx, h.valh, h.Yh, h.ymax, h.vmax, h.partial,
+        h.blk_ctr);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (h.ev_gram1) cudaEventRecord(h.ev_gram1, s);
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
     if (mode == 1) {
         als_reduce_records_kernel<<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,

@@ -71,7 +71,7 @@ struct ocg_als_plan {
     size_t sort_tmp_bytes = 0;
     // segment tables (index 0: rows over CSR, 1: columns over CSC)
     struct Side {
-        Buf<int32_t> nseg, first, nmulti, pfirst, seg_item, total;  // total: [0] segments, [1] multi items
+        Buf<int32_t> nseg, first, nmulti, pfirst, seg_item, total;  // total: [0] segments, [1] multi items, [2] block counter
         Buf<int32_t> multi_list;
         Buf<int32_t> seg_order, seg_key, seg_key_out, seg_id;  // column side: processing order
         Buf<uint8_t> order_tmp;
@@ -92,7 +92,7 @@ struct ocg_als_plan {
     Buf<uint4> Vsel;  // V in the tensor-core selection layout  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[10] = {};
     ~ocg_als_plan() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
@@ -151,6 +151,7 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     h.multi_list = S.multi_list.p;
     h.multi_count = S.total.p + 1;
     h.seg_order = S.seg_order.p;
+    h.blk_ctr = S.total.p + 2;
     h.Y = sd == 0 ? P->V.p : P->U.p;
     h.X = sd == 0 ? P->U.p : P->V.p;
     h.partial = S.partial.p;
@@ -195,7 +196,7 @@ static int als_alloc(ocg_als_plan* P) {
         S.max_segs = static_cast<int32_t>(ms);
         ALS_CUDA(S.nseg.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.first.alloc(static_cast<size_t>(items)));
-        ALS_CUDA(S.total.alloc(2));
+        ALS_CUDA(S.total.alloc(3));
         ALS_CUDA(S.multi_list.alloc(static_cast<size_t>(items)));
         if (sd == 1 && P->k == 32) {
             ALS_CUDA(S.seg_order.alloc(static_cast<size_t>(ms)));
@@ -354,7 +355,8 @@ static int launch_select(ocg_als_plan* P) {
     return OCG_OK;
 }
 
-// phase_ms (optional, 4 floats): CSC build, row half-sweeps, column half-sweeps, select
+// phase_ms (optional, 6 floats): CSC build, row half-sweeps, column half-sweeps, select,
+// and (rank 32) the row / column Gram kernels alone
 int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
     cudaStream_t s = ocg_internal_stream(P->ctx);
@@ -365,13 +367,20 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
     if ((rc = als_pack(P, 1))) return rc;
     ALS_CUDA(cudaEventRecord(P->ev[1], s));
-    float row_ms = 0.f, col_ms = 0.f;
+    float row_ms = 0.f, col_ms = 0.f, rgram_ms = 0.f, cgram_ms = 0.f;
     for (int it = 0; it < P->sweeps; ++it) {
+        ocg::AlsHalf hr = als_half(P, 0), hc = als_half(P, 1);
+        if (phase_ms) {
+            hr.ev_gram0 = P->ev[6];
+            hr.ev_gram1 = P->ev[7];
+            hc.ev_gram0 = P->ev[8];
+            hc.ev_gram1 = P->ev[9];
+        }
         ALS_CUDA(cudaEventRecord(P->ev[2], s));
-        ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 0), 0, sm, s));
+        ALS_CUDA(ocg::launch_als_half(P->k, hr, 0, sm, s));
         if ((rc = als_pack(P, 0))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[3], s));
-        ALS_CUDA(ocg::launch_als_half(P->k, als_half(P, 1), 0, sm, s));
+        ALS_CUDA(ocg::launch_als_half(P->k, hc, 0, sm, s));
         if ((rc = als_pack(P, 1))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[4], s));
         if (phase_ms) {
@@ -381,6 +390,12 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             ALS_CUDA(cudaEventElapsedTime(&b, P->ev[3], P->ev[4]));
             row_ms += a;
             col_ms += b;
+            if (P->k == 32) {
+                ALS_CUDA(cudaEventElapsedTime(&a, P->ev[6], P->ev[7]));
+                ALS_CUDA(cudaEventElapsedTime(&b, P->ev[8], P->ev[9]));
+                rgram_ms += a;
+                cgram_ms += b;
+            }
         }
     }
     ALS_CUDA(cudaEventRecord(P->ev[2], s));
@@ -394,6 +409,8 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             phase_ms[1] = row_ms;
             phase_ms[2] = col_ms;
             ALS_CUDA(cudaEventElapsedTime(&phase_ms[3], P->ev[2], P->ev[5]));
+            phase_ms[4] = rgram_ms;  // Gram kernel alone (rank 32; 0 otherwise)
+            phase_ms[5] = cgram_ms;
         }
     }
     return OCG_OK;
