@@ -2,7 +2,7 @@
 """bench.py — B200 online CF completion + selection (OPEN online phase).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c0xn|ingest]
+                  [--workload c2|c1|c4|c0xn|ingest]
 
 One JSON line on rank 0.  For N>1 launch with
 torch.distributed.run; each rank takes an equal shard of the units (weak
@@ -336,6 +336,7 @@ JOINT = {  # SURVEY §8d joint configs
     "c1": dict(m=10_000, grid=(16, 16), density=0.05, dense_rows=10, rank=8),
     "c2": dict(m=1_000_000, grid=(64, 64), density=0.02, dense_rows=1000, rank=32),
 }
+JOINT["c4"] = dict(JOINT["c2"])  # streaming refits on the C2 matrix
 
 
 def _joint_matrix(name, rank, world):
@@ -495,7 +496,84 @@ def workload_joint(args, d: Dist):
     return out, (args.workload, m)
 
 
-WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "ingest": workload_ingest}
+def workload_c4(args, d: Dist):
+    """streaming online phase on the C2 matrix.  Each arrival batch adds one
+    new observation to 1% of the rows (paper_2508_07605_b200.stream); a refit = upload of the
+    new CSR from pinned host memory + full completion + selection from scratch (reference
+    semantics) + decisions read back.  Reported: latency per refit (wall clock, the refit
+    is synchronous), as cells/s, and the warm-start latency (2 sweeps from the previous
+    factors: a flagged deviation) at N=1.  N>1: each rank refits its row shard with the
+    sharded schedule."""
+    import torch
+
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+    from paper_2508_07605_b200.dist import GpuAlsBackend, ShardedAlsDriver
+    from paper_2508_07605_b200.stream import add_observations
+
+    cfg, grid, A = _joint_matrix("c4", d.rank, d.world)
+    m, n = cfg["m"], grid.n
+    ctx = ocg.Context(d.local)
+    dev = torch.device("cuda", d.local)
+    hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
+    batches = [add_observations(A, grid, frac=0.01, seed=1000 * d.rank + b) for b in (1, 2)]
+    pins = [[torch.from_numpy(x).pin_memory() for x in (B.row_ptr, B.col, B.val)] for B in batches]
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+
+    def refit(b):
+        plan.upload(*(int(x.data_ptr()) for x in pins[b % 2]))
+        if d.world == 1:
+            plan.run(timed=False)
+        else:
+            ShardedAlsDriver(GpuAlsBackend(plan, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
+        return plan.results()
+
+    def timed(nsteps, base):
+        ts = []
+        for b in range(nsteps):
+            ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+            torch.cuda.synchronize(dev)
+            d.barrier()
+            t0 = time.perf_counter()
+            r = refit(base + b)
+            ts.append(d.max(time.perf_counter() - t0))
+        return ts, r
+
+    for b in range(args.warmup):
+        refit(b)
+    with Clocks(d.local) as clk:
+        ts, r = timed(args.steps, args.warmup)
+    assert (r[0] >= 0).all()
+    lat = statistics.median(ts)
+    out = {"metric": "CF-completed matrix cells/sec", "value": m * n / lat, "unit": "cells/s",
+           "ms_per_step": lat * 1e3, "scaling": "strong", "dtype": "f32 factors / f64 selection",
+           "refit_latency_ms": {"from_scratch_median": lat * 1e3, "all": [t * 1e3 for t in ts]},
+           "selections_per_sec": m / lat,
+           "e2e": {"value": m * n / lat, "unit": "cells/s",
+                   "h2d_bytes_per_step": int(sum(x.nbytes for x in (batches[0].row_ptr, batches[0].col,
+                                                                   batches[0].val))) * d.world,
+                   "d2h_bytes_per_step": int(sum(x.nbytes for x in r)) * d.world},
+           "config": {"workload": "c4", "apps": m, "settings": n, "rank": cfg["rank"],
+                      "arrivals": "1 new observation in each of 1% of rows per refit",
+                      "observed_per_gpu": batches[0].nnz, "sweeps": args.sweeps,
+                      "parallelism": f"rows sharded over {d.world} GPU(s)" if d.world > 1 else "1 GPU",
+                      "timing": "wall clock per synchronous refit (upload + run + readback), max over ranks, "
+                                "L2 flushed before each"},
+           "gpu_launches": args.steps * (16 + args.sweeps * 4 + 2), "clocks": clk.summary()}
+    if d.world == 1:  # warm refits: a flagged deviation from the reference's from-scratch cf::complete
+        plan.set_warm(2)
+        refit(0)
+        tw, _ = timed(args.steps, 1)
+        plan.set_warm(0)
+        out["refit_latency_ms"]["warm_2_sweeps_median"] = statistics.median(tw) * 1e3
+        out["refit_latency_ms"]["warm_note"] = ("deviation: starts from the previous factors with 2 sweeps "
+                                                "instead of a from-scratch 10-sweep fit")
+    plan.close()
+    return out, ("c4", m)
+
+
+WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "c4": workload_c4,
+             "ingest": workload_ingest}
 
 
 # -------------------------------------------------------- reference (CPU)

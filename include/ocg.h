@@ -178,12 +178,17 @@ typedef struct ocg_als_plan ocg_als_plan;
 int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const int32_t* col, const float* val,
                         int on_device, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
                         int32_t ngpu, const ocg_als_hyper* hyper, double gamma, ocg_als_plan** out);
-/* new observations for an existing plan (streaming refits, end-to-end
- * timing): host CSR with the plan's m and nnz, copied asynchronously on the
- * context stream into the plan's own device buffers (pinned host memory makes
- * the copy overlap-capable); the next _run completes it from scratch.
- * OCG_E_INVALID if nnz differs or the plan was created on device pointers. */
+/* new observations for an existing plan (streaming refits, SURVEY §8d C4;
+ * end-to-end timing): host CSR with the plan's m (nnz may change: the
+ * nnz-dependent device state is rebuilt, the factors are kept), copied
+ * asynchronously on the context stream into the plan's own device buffers
+ * (pinned host memory makes the copy overlap-capable); the next _run
+ * completes it.  OCG_E_INVALID if the plan was created on device pointers. */
 int ocg_als_plan_upload(ocg_als_plan* plan, const int64_t* row_ptr, const int32_t* col, const float* val);
+/* warm refits (a flagged deviation from the reference's from-scratch cf::complete):
+ * warm_sweeps > 0 makes every later _run after the first start from the previous
+ * factors (no V initialisation) and run warm_sweeps sweeps; 0 restores from-scratch. */
+int ocg_als_plan_set_warm(ocg_als_plan* plan, int32_t warm_sweeps);
 /* one full step on device data: CSC build, fit, fused imputation+selection.
  * total_ms / phase_ms[6] (CSC, row sweeps, column sweeps, select, and at rank
  * 32 the row / column Gram kernels alone): CUDA-event times on the context

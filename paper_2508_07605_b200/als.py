@@ -51,7 +51,7 @@ class AlsPlan:
                                       ptr(gpu), len(gpu), ctypes.byref(h), gamma, ctypes.byref(self._h)))
 
     def upload(self, row_ptr, col, val):
-        """New observations (same m and nnz) from host memory: numpy arrays, or
+        """New observations (same m; nnz may change) from host memory: numpy arrays, or
         host addresses (ints, e.g. pinned buffers) the caller keeps alive until
         the next run completes."""
         if isinstance(row_ptr, int):
@@ -61,6 +61,11 @@ class AlsPlan:
                           np.ascontiguousarray(val, np.float32))
             args = tuple(ptr(a) for a in self._keep)
         check(lib.ocg_als_plan_upload(self._h, *args))
+
+    def set_warm(self, sweeps: int):
+        """Warm refits (deviation from from-scratch semantics): later runs start from the
+        previous factors and run ``sweeps`` sweeps; 0 = from scratch."""
+        check(lib.ocg_als_plan_set_warm(self._h, int(sweeps)))
 
     def run(self, timed: bool = True):
         """One step (CSC build + fit + fused imputation/selection).

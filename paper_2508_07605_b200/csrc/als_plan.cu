@@ -38,7 +38,13 @@ struct Buf {
     ~Buf() {
         if (p && own) cudaFree(p);
     }
-    cudaError_t alloc(size_t n) { return n ? cudaMalloc(&p, sizeof(T) * n) : cudaSuccess; }
+    // (re)allocation: an owned previous buffer is released first
+    cudaError_t alloc(size_t n) {
+        if (p && own) cudaFree(p);
+        p = nullptr;
+        own = true;
+        return n ? cudaMalloc(&p, sizeof(T) * n) : cudaSuccess;
+    }
 };
 
 
@@ -54,6 +60,8 @@ struct ocg_als_plan {
     ocg_ctx* ctx = nullptr;
     int64_t m = 0, n = 0, nnz = 0;
     int k = 32, sweeps = 10;
+    int warm_sweeps = 0;  // > 0: runs keep the previous factors (no V init) and do this many sweeps
+    bool fitted = false;  // a run has completed (factors exist)
     float lambda = 0.05f;
     uint64_t seed = 0;
     double gamma = 0.05, e_base = 0.0;
@@ -176,6 +184,7 @@ static int als_pack(ocg_als_plan* P, int sd) {
     return OCG_OK;
 }
 
+// buffers whose size depends on nnz (reallocated when an upload changes it)
 static int als_alloc(ocg_als_plan* P) {
     ALS_CUDA(P->col_ptr.alloc(static_cast<size_t>(P->n + 1)));
     ALS_CUDA(P->crow.alloc(static_cast<size_t>(P->nnz)));
@@ -223,6 +232,12 @@ static int als_alloc(ocg_als_plan* P) {
         P->scan_tmp_bytes = std::max(P->scan_tmp_bytes, b);
     }
     ALS_CUDA(P->scan_tmp.alloc(P->scan_tmp_bytes));
+    if (P->k == 32) ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
+    return OCG_OK;
+}
+
+// buffers that depend on m, n, k only (they survive an upload with a new nnz)
+static int als_alloc_fixed(ocg_als_plan* P) {
     ALS_CUDA(P->U.alloc(static_cast<size_t>(P->m * P->k)));
     ALS_CUDA(P->V.alloc(static_cast<size_t>(P->n * P->k)));
     ALS_CUDA(P->Vt.alloc(static_cast<size_t>(P->n * P->k)));
@@ -236,7 +251,8 @@ static int als_alloc(ocg_als_plan* P) {
     ALS_CUDA(P->ncand.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->saving.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->loss.alloc(static_cast<size_t>(P->m)));
-    for (auto& e : P->ev) ALS_CUDA(cudaEventCreate(&e));
+    for (auto& e : P->ev)
+        if (!e) ALS_CUDA(cudaEventCreate(&e));
     return OCG_OK;
 }
 
@@ -296,9 +312,9 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     }
     if (P->nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: nnz >= 2^31");
     if ((rc = als_alloc(P.get()))) return rc;
+    if ((rc = als_alloc_fixed(P.get()))) return rc;
     if (P->k == 32) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(ctx), s));
-        ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
     }
     ALS_CUDA(P->cpu.alloc(static_cast<size_t>(ncpu)));
@@ -313,8 +329,17 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
 int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* col, const float* val) {
     if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
-    if (row_ptr[P->m] != P->nnz) return ocg_internal_fail(OCG_E_INVALID, "als upload: nnz differs from the plan's");
+    const int64_t nnz = row_ptr[P->m];
+    if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
+    if (nnz != P->nnz) {  // new observations: nnz-dependent device state is rebuilt (factors survive)
+        ALS_CUDA(cudaStreamSynchronize(s));
+        P->nnz = nnz;
+        ALS_CUDA(P->col.alloc(static_cast<size_t>(nnz)));
+        ALS_CUDA(P->val.alloc(static_cast<size_t>(nnz)));
+        int rc = als_alloc(P);
+        if (rc) return rc;
+    }
     ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
@@ -322,6 +347,13 @@ int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* 
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
     }
+    return OCG_OK;
+}
+
+int ocg_als_plan_set_warm(ocg_als_plan* P, int32_t warm_sweeps) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    if (warm_sweeps < 0) return ocg_internal_fail(OCG_E_INVALID, "als: warm_sweeps < 0");
+    P->warm_sweeps = warm_sweeps;
     return OCG_OK;
 }
 
@@ -364,11 +396,15 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     ALS_CUDA(cudaEventRecord(P->ev[0], s));
     int rc = als_build_csc(P);
     if (rc) return rc;
-    ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
-    if ((rc = als_pack(P, 1))) return rc;
+    const bool warm = P->warm_sweeps > 0 && P->fitted;
+    if (!warm) {
+        ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
+        if ((rc = als_pack(P, 1))) return rc;
+    }
+    const int sweeps = warm ? P->warm_sweeps : P->sweeps;
     ALS_CUDA(cudaEventRecord(P->ev[1], s));
     float row_ms = 0.f, col_ms = 0.f, rgram_ms = 0.f, cgram_ms = 0.f;
-    for (int it = 0; it < P->sweeps; ++it) {
+    for (int it = 0; it < sweeps; ++it) {
         ocg::AlsHalf hr = als_half(P, 0), hc = als_half(P, 1);
         if (phase_ms) {
             hr.ev_gram0 = P->ev[6];
@@ -401,6 +437,7 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     ALS_CUDA(cudaEventRecord(P->ev[2], s));
     if ((rc = launch_select(P))) return rc;
     ALS_CUDA(cudaEventRecord(P->ev[5], s));
+    P->fitted = true;
     if (total_ms || phase_ms) {
         ALS_CUDA(cudaEventSynchronize(P->ev[5]));
         if (total_ms) ALS_CUDA(cudaEventElapsedTime(total_ms, P->ev[0], P->ev[5]));

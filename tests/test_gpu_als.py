@@ -146,7 +146,21 @@ def test_als_upload_refit_matches_fresh_plan(ctx):
     want = fresh.results()
     for g_, w_ in zip(got, want):
         np.testing.assert_array_equal(g_, w_)
-    rp2 = A.row_ptr.copy()
-    rp2[-1] -= 1  # nnz differs from the plan's
-    with pytest.raises(Exception):
-        plan.upload(rp2, A.col[:-1], val2[:-1])
+    # streaming arrival (nnz grows): one new observation in 1% of the rows
+    from paper_2508_07605_b200 import stream
+
+    B = stream.add_observations(A, grid, frac=0.01, seed=5)
+    assert B.nnz > A.nnz
+    plan.upload(B.row_ptr, B.col, B.val)
+    plan.run()
+    got = plan.results()
+    fresh = AlsPlan(B.m, B.row_ptr, B.col, B.val, grid, hyp, 0.05, ctx=ctx)
+    fresh.run()
+    for g_, w_ in zip(got, fresh.results()):
+        np.testing.assert_array_equal(g_, w_)
+    # warm refit (flagged deviation): starts from the previous factors, still a valid fit
+    plan.set_warm(2)
+    plan.upload(A.row_ptr, A.col, A.val)
+    plan.run()
+    idx, sav, loss, nc = plan.results()
+    assert (idx >= 0).all() and (nc >= 1).all()
