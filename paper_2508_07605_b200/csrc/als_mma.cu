@@ -490,24 +490,25 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
     }
 }
 
-// K4: 16 items per warp, TWO LANES PER ITEM (lane = 16*parity + item): the
-// item's record is staged in shared memory and the lane pair runs a
-// left-looking Cholesky of G + lambda*cnt*I in place, lane p computing the
-// rows i == p (mod 2) of each column (row K of the record is the rhs, so the
-// forward substitution rides along: L[K][j] = y_j).  Both lanes then run the
-// back substitution.  Record of item i at slot first[i] (first == nullptr:
-// slot i).  Two lanes per item instead of one halve the shared memory per
-// warp (39 KB), so 5 warps share an SM.
-constexpr int kSys = 16;
+// K4: LPS lanes per item (32/LPS items per warp; lane = (32/LPS) * part + item):
+// the item's record is staged in shared memory and its lanes run a
+// left-looking Cholesky of G + lambda*cnt*I in place, lane `part` computing
+// the rows i == part (mod LPS) of each column, two rows per step (row K of the
+// record is the rhs, so the forward substitution rides along: L[K][j] = y_j).
+// All lanes of an item then run the back substitution.  Record of item i at
+// slot first[i] (first == nullptr: slot i).  The 8 lanes of a 16-byte
+// shared-memory phase are 8 different items at the same record offset (record
+// stride 153 x 16 B: 8 distinct bank groups).  With LPS = 4 a warp needs 19.6
+// KB, so 11 warps share an SM (the kernel is latency-bound: occupancy pays
+// for the redundant per-column work of the 4 lanes).
+constexpr int kLPS = 4;
+constexpr int kSys = 32 / kLPS;
 constexpr int kSolveSmem = kSys * kRec * 4;
 __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
                                                                const float* __restrict__ rec, float* __restrict__ X,
                                                                float lambda) {
     extern __shared__ __align__(16) float srec[];
-    // lane = 16 * parity + item: the 8 lanes of a 16-byte shared-memory phase
-    // are 8 different items at the same record offset (stride 153 x 16 B: 8
-    // distinct bank groups)
-    const int lane = threadIdx.x, sys = lane & 15, par = lane >> 4;
+    const int lane = threadIdx.x, sys = lane % kSys, par = lane / kSys;
     float* S = srec + sys * kRec;
     const int64_t nbatch = (nitems + kSys - 1) / kSys;
     for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
         const float diag = lambda * cnt;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            // row j of L (columns < j) -> registers (both lanes: broadcast)
+            // row j of L (columns < j) -> registers (all lanes of the item: broadcast)
             float rj[K];
             const float* Rj = S + tri_off(j);
 #pragma unroll
@@ -552,14 +553,18 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
                 else d0 = fmaf(-rj[q], rj[q], d0);
             }
             const float r = rsqrt_ftz(d0 + d1);
-            // rows i > j with i == par (mod 2), two per iteration (independent chains)
-            int i = j + 1 + ((j + 1 + par) & 1);
-            int off = tri_off(i);
+            // rows i > j with i == par (mod LPS), two per iteration (independent chains)
+            static_assert(kLPS == 4, "incremental row offsets below assume 4 lanes per item");
+            int i = j + 1 + ((par - (j + 1)) % kLPS + kLPS) % kLPS;
+            // T(i) and T(i+4) incrementally: with i = 4a + p, T(i+4) - T(i) = 16a + 16 + 4p and
+            // T(i+8) - T(i) = 32a + 48 + 8p (row lengths padded to multiples of 4)
+            int offa = tri_off(i);
 #pragma unroll 1
-            for (; i + 2 <= K; i += 4) {
-                const int off2 = off + 4 * ((i >> 2) + 1) + 4 * (((i + 1) >> 2) + 1);
-                const float* Ra = S + off;
-                const float* Rb = S + off2;
+            for (; i + kLPS <= K; i += 2 * kLPS) {
+                const int a4 = (i >> 2) * 16 + 4 * par;
+                const int offb = offa + a4 + 16;
+                const float* Ra = S + offa;
+                const float* Rb = S + offb;
                 float a0 = Ra[j], a1 = 0.0f, b0 = Rb[j], b1 = 0.0f;
 #pragma unroll
                 for (int q = 0; q + 4 <= j; q += 4) {
@@ -579,12 +584,12 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
                     a0 = fmaf(-Ra[q], rj[q], a0);
                     b0 = fmaf(-Rb[q], rj[q], b0);
                 }
-                S[off + j] = (a0 + a1) * r;
-                S[off2 + j] = (b0 + b1) * r;
-                off = off2 + 4 * (((i + 2) >> 2) + 1) + 4 * (((i + 3) >> 2) + 1);
+                S[offa + j] = (a0 + a1) * r;
+                S[offb + j] = (b0 + b1) * r;
+                offa += 2 * a4 + 48;
             }
             if (i <= K) {
-                const float* Ra = S + off;
+                const float* Ra = S + offa;
                 float a0 = Ra[j], a1 = 0.0f;
 #pragma unroll
                 for (int q = 0; q + 4 <= j; q += 4) {
@@ -596,13 +601,13 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
                 }
 #pragma unroll
                 for (int q = j & ~3; q < j; ++q) a0 = fmaf(-Ra[q], rj[q], a0);
-                S[off + j] = (a0 + a1) * r;
+                S[offa + j] = (a0 + a1) * r;
             }
             __syncwarp();
             if (par == 0) S[tri_off(j) + j] = r;  // the diagonal slot keeps 1 / L[j][j]
         }
         __syncwarp();
-        // L^T x = y (y = row K of the factorised record), column-oriented, both lanes
+        // L^T x = y (y = row K of the factorised record), column-oriented, all lanes of the item
         float y[K];
 #pragma unroll
         for (int q = 0; q < K; q += 4) {
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
 #pragma unroll
             for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
         }
-        if (live && par == 0) {  // both lanes hold x; parity 0 writes the 128-byte row
+        if (live && par == 0) {  // every lane of the item holds x; part 0 writes the 128-byte row
             float4* xo = reinterpret_cast<float4*>(X + (i0 + sys) * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
@@ -646,7 +651,7 @@ static cudaError_t launch_solve(int64_t nitems, const int32_t* first, const floa
     cudaFuncSetAttribute(als_solve_records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
     const int64_t nbatch = (nitems + kSys - 1) / kSys;
     int64_t blocks = nbatch;
-    const int64_t cap = static_cast<int64_t>(sm_count) * 5;
+    const int64_t cap = static_cast<int64_t>(sm_count) * (kLPS == 4 ? 11 : 5);  // shared-memory bound
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     als_solve_records_kernel<<<static_cast<unsigned>(blocks), 32, kSolveSmem, s>>>(nitems, first, rec, X, lambda);
