@@ -397,29 +397,40 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                     mma_cell(d[u], bh, bl);
                     cs2[u] = *reinterpret_cast<const float2*>(cst + cc + 2 * t);
                 }
+                // per row q, cell c = 2u + e of the group: validity and band-candidate bits;
+                // the lane's observed bits of the group are 4 consecutive mask bits
                 unsigned hit = 0;
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
+                for (int q = 0; q < 2; ++q) {
+                    unsigned vb = 0u, hb = 0u;
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const float csf = e ? cs2[u].y : cs2[u].x;
-                        const int bit = (((nt + u) & 15) << 1) | e;
+                    for (int u = 0; u < 2; ++u)
 #pragma unroll
-                        for (int q = 0; q < 2; ++q) {
+                        for (int e = 0; e < 2; ++e) {
+                            const float csf = e ? cs2[u].y : cs2[u].x;
                             const float x = d[u][2 * q + e];
-                            const bool ob = (mk[q][(nt + u) >> 4] >> bit) & 1u;
                             const bool lo = x <= lo_s;
                             const float pc = fminf(x, hi_s);
-                            const bool valid = !ob && (lo ? lov[q] : pc) >= fth_s[q];
-                            ncand[q] += valid;
-                            if (valid && csf <= tb_s[q] * fmaxf(pc, lo_s)) hit |= 1u << (4 * u + 2 * e + q);
-                            if (WRITE_COMPLETED && !ob && live[q]) {
+                            if ((lo ? lov[q] : pc) >= fth_s[q]) vb |= 1u << (2 * u + e);
+                            if (csf <= tb_s[q] * fmaxf(pc, lo_s)) hb |= 1u << (2 * u + e);
+                        }
+                    const unsigned ob4 = (mk[q][nt >> 4] >> ((nt & 15) * 2)) & 0xFu;
+                    vb &= ~ob4;
+                    ncand[q] += __popc(vb);
+                    hit |= (hb & vb) << (4 * q);
+                    if (WRITE_COMPLETED && live[q]) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                if ((ob4 >> (2 * u + e)) & 1u) continue;
+                                const float x = d[u][2 * q + e];
                                 const float pf = x * inv_s;
                                 a.completed[rowg[q] * n + c0 + (nt + u) * 8 + 2 * t + e] =
-                                    lo ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
+                                    x <= lo_s ? 0.01 : (pf > 1.25f ? 1.25 : static_cast<double>(pf));
                             }
-                        }
                     }
+                }
                 if (hit) {  // rare: exact FP64 evaluation of the cells inside the band
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
@@ -427,7 +438,7 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                         for (int e = 0; e < 2; ++e)
 #pragma unroll
                             for (int q = 0; q < 2; ++q) {
-                                if (!((hit >> (4 * u + 2 * e + q)) & 1u)) continue;
+                                if (!((hit >> (4 * q + 2 * u + e)) & 1u)) continue;
                                 const float csf = e ? cs2[u].y : cs2[u].x;
                                 const float pf = d[u][2 * q + e] * inv_s;
                                 const bool lo = pf <= 0.01f;
