@@ -164,3 +164,39 @@ def test_als_upload_refit_matches_fresh_plan(ctx):
     plan.run()
     idx, sav, loss, nc = plan.results()
     assert (idx >= 0).all() and (nc >= 1).all()
+
+
+def test_als_rank32_multisegment_rows_and_empty_items(ctx, port):
+    """Rank 32 (tensor-core path) with rows longer than one segment (dense rows over
+    2048 settings -> 2 segments, reduced in segment order), a column nobody observed
+    (zero factor, like ocgo_als_fit) and an app row with no observations."""
+    from oracle import bind
+    from paper_2508_07605_b200 import PowerGrid
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid = PowerGrid.spanning(64, 32)
+    n = grid.n
+    rng = np.random.default_rng(7)
+    m = 300
+    mask = rng.random((m, n)) < 0.03
+    mask[:3, :] = True        # dense rows: 2048 observations = 2 segments
+    mask[:, 5] = False        # cold column
+    mask[10, :] = False       # app without observations
+    mask[3:, -1] = True       # baseline observed elsewhere
+    mask[10, :] = False
+    vals = rng.uniform(0.2, 1.2, (m, n))
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(mask.sum(1))
+    ii, jj = np.nonzero(mask)
+    col, val = jj.astype(np.int32), vals[ii, jj].astype(np.float32)
+    hyp = AlsHyper(rank=32, lam=0.003, sweeps=4, seed=5)
+    plan = AlsPlan(m, rp, col, val, grid, hyp, 0.05, ctx=ctx)
+    plan.run()
+    Ug, Vg = plan.factors()
+    Uo, Vo = bind.als_fit(port, m, n, rp, col, val, 32, 0.003, 4, 5)
+    assert np.all(Vg[5] == 0) and np.all(Ug[10] == 0)
+    assert np.all(Vo[5] == 0) and np.all(Uo[10] == 0)
+    Pg = np.clip(Ug.astype(np.float64) @ Vg.T.astype(np.float64), 0.01, 1.25)
+    Po = np.clip(Uo @ Vo.T, 0.01, 1.25)
+    rel = np.abs(Pg - Po) / Po
+    assert np.quantile(rel, 0.999) < PRED_RTOL, (rel.max(), np.quantile(rel, 0.999))
