@@ -556,8 +556,10 @@ cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* n
     return cudaGetLastError();
 }
 
-// rank 32 (tensor-core path): packed lower-triangle record of als_mma.cu
-size_t als_gram_record_floats(int k) { return k == 32 ? als_record_floats32() : static_cast<size_t>(k) * k + k + 1; }
+// ranks 32/64 (tensor-core path): packed lower-triangle record of als_mma.cu
+size_t als_gram_record_floats(int k) {
+    return (k == 32 || k == 64) ? als_record_floats_mma(k) : static_cast<size_t>(k) * k + k + 1;
+}
 
 template <int K>
 static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
@@ -589,7 +591,7 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
 }
 
 cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
-    if (k == 32 && h.Yh) return launch_als_mma_half(h, mode, sm_count, s);
+    if ((k == 32 || k == 64) && h.Yh) return launch_als_mma_half(k, h, mode, sm_count, s);
     switch (k) {
         case 8: return launch_half_k<8>(h, mode, sm_count, s);
         case 16: return launch_half_k<16>(h, mode, sm_count, s);
@@ -600,7 +602,7 @@ cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cud
 
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                        cudaStream_t s) {
-    if (k == 32) return launch_als_solve_records(nitems, G, X, lambda, sm_count, s);
+    if (k == 32 || k == 64) return launch_als_solve_records(k, nitems, G, X, lambda, sm_count, s);
     int64_t blocks = (nitems + 7) / 8;
     if (blocks > sm_count * 16) blocks = sm_count * 16;
     if (blocks < 1) blocks = 1;

@@ -50,12 +50,13 @@ cudaError_t launch_seg_fill(int64_t nitems, const int64_t* ptr, const int32_t* n
 size_t als_gram_record_floats(int k);
 // mode 0: solve in place; mode 1: write reduced Gram records to gram_out
 cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
-// rank-32 tensor-core half-sweep (Gram records -> reduce -> batched solve) + the packing of a factor matrix it gathers (als_mma.cu)
-cudaError_t launch_als_mma_half(const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
-cudaError_t launch_als_solve_records(int64_t nitems, const float* G, float* X, float lambda, int sm_count,
+// rank-32/64 tensor-core half-sweep (Gram records -> reduce -> batched solve) + the packing
+cudaError_t launch_als_mma_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s);
+cudaError_t launch_als_solve_records(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                      cudaStream_t s);
-size_t als_record_floats32();
-cudaError_t launch_als_pack(int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count, cudaStream_t s);
+size_t als_record_floats_mma(int k);
+cudaError_t launch_als_pack(int k, int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count,
+                            cudaStream_t s);
 cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vmax, uint32_t* out, cudaStream_t s);
 cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int sm_count, cudaStream_t s);
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,

@@ -39,12 +39,7 @@ namespace ocg {
 
 namespace {
 
-constexpr int K = 32;
-constexpr int GSZ = K * K + K + 1;
 constexpr int kWarps = 8;
-// per warp: double stage [2][32 rows][RS x 16 B] + index/value ring [8 slots][32] x 2
-constexpr int RS = 9;  // stage row stride in 16-byte units (144 B: conflict-free fragment loads, no swizzle)
-constexpr int kStageU4 = 2 * 32 * RS + (8 * 32 * 2 * 4) / 16;
 
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -84,10 +79,34 @@ __device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
 
 __device__ __forceinline__ int min32(int64_t v) { return v < 32 ? static_cast<int>(v) : 32; }
 
-// MMA index X in [0,32) <-> natural factor dim pi(X) = 4*(X%8) + X/8
-__device__ __forceinline__ int pi_dim(int x) { return 4 * (x & 7) + (x >> 3); }
-
 }  // namespace
+
+// ---- record layout (floats): padded lower triangle, row i at T(i) with its
+// length rounded up to 4 (16-byte aligned rows), then rhs (K), count (1).
+__host__ __device__ constexpr int tri_off(int i) { return 4 * ((i >> 2) + 1) * (2 * (i >> 2) + (i & 3)); }
+
+// Per-rank constants of the tensor-core path (K = 32 or 64).
+//  D   factor dims per lane group (= MMA n-tiles), MT m-tiles, NLT lower tiles
+//  RU4 packed factor row in 16-byte units: K=32 chunk g = {hi[4g..4g+3], lo[4g..4g+3]};
+//      K=64 chunks 0-7 = hi[8g..8g+7], chunks 8-15 = lo[8g..8g+7]
+//  RS  stage row stride (16-byte units): conflict-free fragment loads, and at K=64 a
+//      record fits one stage buffer
+template <int K>
+struct Cfg {
+    static_assert(K == 32 || K == 64, "tensor-core ALS ranks");
+    static constexpr int D = K / 8, MT = K / 16, NLT = MT * (MT + 1);
+    static constexpr int RU4 = K / 4;
+    static constexpr int RS = K == 32 ? 9 : 19;
+    static constexpr int kStageU4 = 2 * 32 * RS + (8 * 32 * 2 * 4) / 16;  // + index/value ring [8][32] x 2
+    static constexpr int kRhs = tri_off(K), kCnt = kRhs + K, kRec = (kCnt + 1 + 3) & ~3;
+    static constexpr int kMinBlocks = K == 32 ? 2 : 1;
+};
+static_assert(Cfg<32>::kRec == 612 && Cfg<32>::kRhs == 576, "rank-32 record layout");
+static_assert(Cfg<64>::kRec * 4 <= 32 * Cfg<64>::RS * 16, "rank-64 record fits a stage buffer");
+
+// MMA index X in [0,K) <-> natural factor dim pi(X) = D*(X%8) + X/8
+template <int K>
+__device__ __forceinline__ int pi_dim(int x) { return Cfg<K>::D * (x & 7) + (x >> 3); }
 
 // power-of-two scale with max|y| * s <= 2^14 (exponent clamped so s^2 and its
 // inverse stay finite in FP32)
@@ -118,21 +137,31 @@ __global__ void als_absmax_kernel(int64_t count, const float* __restrict__ x, un
     }
 }
 
-// X (rows x 32 f32) -> packed hi/lo rows (8 x uint4 per row)
+// X (rows x K f32) -> packed hi/lo rows (Cfg<K>::RU4 x uint4 per row); thread = (row, group g)
+template <int K>
 __global__ void als_pack_kernel(int64_t rows, const float* __restrict__ X, const unsigned* __restrict__ maxbits,
                                 uint4* __restrict__ Xh) {
-    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // chunk id
+    constexpr int D = Cfg<K>::D;
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= rows * 8) return;
+    const int64_t r = q >> 3;
+    const int g = static_cast<int>(q & 7);
     const float s = ldexpf(1.0f, als_scale_exp(*maxbits));
-    const float4 v = reinterpret_cast<const float4*>(X)[q];
-    const float y[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
-    __half h[4], l[4];
+    const float* x = X + r * K + D * g;
+    uint32_t hw[D / 2], lw[D / 2];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        h[c] = __float2half_rn(y[c]);
-        l[c] = __float2half_rn(y[c] - __half2float(h[c]));
+    for (int c = 0; c < D; c += 2) {
+        const float y0 = x[c] * s, y1 = x[c + 1] * s;
+        const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
+        hw[c / 2] = pack_h2(h0, h1);
+        lw[c / 2] = pack_h2(__float2half_rn(y0 - __half2float(h0)), __float2half_rn(y1 - __half2float(h1)));
     }
-    Xh[q] = make_uint4(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]), pack_h2(l[0], l[1]), pack_h2(l[2], l[3]));
+    if constexpr (K == 32) {
+        Xh[r * 8 + g] = make_uint4(hw[0], hw[1], lw[0], lw[1]);
+    } else {
+        Xh[r * 16 + g] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        Xh[r * 16 + 8 + g] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
 }
 
 __device__ __forceinline__ float rsqrt_ftz(float x) {
@@ -141,13 +170,6 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return y;
 }
 
-// ---- record layout (floats): padded lower triangle, row i at T(i) with its
-// length rounded up to 4 (16-byte aligned rows), rhs at 576, count at 608.
-constexpr int kRec = 612;
-constexpr int kRhs = 576;
-constexpr int kCnt = 608;
-__host__ __device__ constexpr int tri_off(int i) { return 4 * ((i >> 2) + 1) * (2 * (i >> 2) + (i & 3)); }
-static_assert(tri_off(32) == kRhs, "record layout");
 
 // K3.  One record per segment, slot = segment id (the reduce step decides
 // what happens to it).
@@ -172,15 +194,19 @@ static_assert(tri_off(32) == kRhs, "record layout");
 // gathers: per-operation cost of the bulk-copy unit at 128 B.)
 constexpr int kRC = 8;     // ring slots (chunks)
 constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
-__global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
     const unsigned* __restrict__ vmax, float* __restrict__ rec, int32_t* __restrict__ blk_ctr) {
+    using C = Cfg<K>;
+    constexpr int D = C::D, MT = C::MT, NLT = C::NLT, RU4 = C::RU4, RS = C::RS;
+    constexpr int kRec = C::kRec, kRhs = C::kRhs, kCnt = C::kCnt;
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    uint4* stage = dyn4 + warp * kStageU4;                                 // [2][32][RS] uint4
+    uint4* stage = dyn4 + warp * C::kStageU4;                              // [2][32][RS] uint4
     int32_t* ring_j = reinterpret_cast<int32_t*>(stage + 2 * 32 * RS);     // [kRC][32]
     uint32_t* ring_r = reinterpret_cast<uint32_t*>(ring_j + kRC * 32);     // [kRC][32]
     const int ey = als_scale_exp(*ymax), ev = als_scale_exp(*vmax);
@@ -279,8 +305,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
         const uint4* src = Yh + c16;
         const int nv = cnt - rg * 8;  // rows of this lane group inside the chunk
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            cp_async16_zfill(st + q * RS, src + static_cast<uint32_t>(jj[q]) * 8u, q < nv ? 16 : 0);
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int h = 0; h < RU4 / 8; ++h)  // K=64: the lane's second 16-byte chunk of the row
+                cp_async16_zfill(st + q * RS + 8 * h, src + static_cast<uint32_t>(jj[q]) * RU4 + 8 * h,
+                                 q < nv ? 16 : 0);
+        }
     };
 
     for (int i = 0; i < kAhead; ++i) {
@@ -292,12 +322,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
     gather(0, 0, cpos, cend);
     cp_async_commit();
 
-    float acc[6][4], racc[2][4];
+    float acc[NLT][4], racc[MT][4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
 #pragma unroll
-        for (int q = 0; q < 6; ++q) acc[q][e] = 0.0f;
-        racc[0][e] = racc[1][e] = 0.0f;
+        for (int q = 0; q < NLT; ++q) acc[q][e] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < MT; ++q) racc[q][e] = 0.0f;
     }
     int buf = 0;
     for (int cons = 0;; ++cons) {
@@ -339,49 +370,61 @@ __global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
         for (int h = 0; h < 2; ++h) {
             if (h * 16 >= cnt) break;
             const int o0 = h * 16 + 2 * t;
-            const uint4 q0 = st[o0 * RS + g], q1 = st[(o0 + 1) * RS + g];
-            const uint4 q2 = st[(o0 + 8) * RS + g], q3 = st[(o0 + 9) * RS + g];
-            // B fragments of n-tile j (factor dim 4g+j): {b0, b1} for hi (h) and lo (l)
-            uint32_t bh0[4], bh1[4], bl0[4], bl1[4];
-            bh0[0] = prmt(q0.x, q1.x, 0x5410);
-            bh0[1] = prmt(q0.x, q1.x, 0x7632);
-            bh0[2] = prmt(q0.y, q1.y, 0x5410);
-            bh0[3] = prmt(q0.y, q1.y, 0x7632);
-            bh1[0] = prmt(q2.x, q3.x, 0x5410);
-            bh1[1] = prmt(q2.x, q3.x, 0x7632);
-            bh1[2] = prmt(q2.y, q3.y, 0x5410);
-            bh1[3] = prmt(q2.y, q3.y, 0x7632);
-            bl0[0] = prmt(q0.z, q1.z, 0x5410);
-            bl0[1] = prmt(q0.z, q1.z, 0x7632);
-            bl0[2] = prmt(q0.w, q1.w, 0x5410);
-            bl0[3] = prmt(q0.w, q1.w, 0x7632);
-            bl1[0] = prmt(q2.z, q3.z, 0x5410);
-            bl1[1] = prmt(q2.z, q3.z, 0x7632);
-            bl1[2] = prmt(q2.w, q3.w, 0x5410);
-            bl1[3] = prmt(q2.w, q3.w, 0x7632);
+            // hi / lo words of dims D*g .. D*g+D-1 of rows o0, o0+1, o0+8, o0+9
+            uint32_t hw[4][D / 2], lw[4][D / 2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int o = o0 + (r & 1) + 8 * (r >> 1);
+                if constexpr (K == 32) {
+                    const uint4 q = st[o * RS + g];
+                    hw[r][0] = q.x;
+                    hw[r][1] = q.y;
+                    lw[r][0] = q.z;
+                    lw[r][1] = q.w;
+                } else {
+                    const uint4 qh = st[o * RS + g], ql = st[o * RS + 8 + g];
+                    hw[r][0] = qh.x;
+                    hw[r][1] = qh.y;
+                    hw[r][2] = qh.z;
+                    hw[r][3] = qh.w;
+                    lw[r][0] = ql.x;
+                    lw[r][1] = ql.y;
+                    lw[r][2] = ql.z;
+                    lw[r][3] = ql.w;
+                }
+            }
+            // B fragments of n-tile j (factor dim D*g + j): {b0, b1} for hi (h) and lo (l);
+            // the A fragment of m-tile i is {B0(2i), B0(2i+1), B1(2i), B1(2i+1)}
+            uint32_t bh0[D], bh1[D], bl0[D], bl1[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
+                bh0[j] = prmt(hw[0][j >> 1], hw[1][j >> 1], sel);
+                bh1[j] = prmt(hw[2][j >> 1], hw[3][j >> 1], sel);
+                bl0[j] = prmt(lw[0][j >> 1], lw[1][j >> 1], sel);
+                bl1[j] = prmt(lw[2][j >> 1], lw[3][j >> 1], sel);
+            }
             // rhs B fragment from the packed (hi, lo) values of observations o0, o0+1 / o0+8, o0+9
             // (ring entries past the chunk are 0)
             const uint2 ra = *reinterpret_cast<const uint2*>(rs + o0);
             const uint2 rb2 = *reinterpret_cast<const uint2*>(rs + o0 + 8);
             const uint32_t rb0 = prmt(ra.x, ra.y, rsel) & rmask, rb1 = prmt(rb2.x, rb2.y, rsel) & rmask;
-            // G lower tiles (i,j) = (0,0) (0,1) (1,0) (1,1) (1,2) (1,3): H^T H + H^T L + L^T H
-            mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bh0[0], bh1[0]);
-            mma16816(acc[0], bh0[0], bh0[1], bh1[0], bh1[1], bl0[0], bl1[0]);
-            mma16816(acc[0], bl0[0], bl0[1], bl1[0], bl1[1], bh0[0], bh1[0]);
-            mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bh0[1], bh1[1]);
-            mma16816(acc[1], bh0[0], bh0[1], bh1[0], bh1[1], bl0[1], bl1[1]);
-            mma16816(acc[1], bl0[0], bl0[1], bl1[0], bl1[1], bh0[1], bh1[1]);
+            // G lower tiles (i, j <= 2i+1), tile index i(i+1)+j: H^T H + H^T L + L^T H
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bh0[j], bh1[j]);
-                mma16816(acc[2 + j], bh0[2], bh0[3], bh1[2], bh1[3], bl0[j], bl1[j]);
-                mma16816(acc[2 + j], bl0[2], bl0[3], bl1[2], bl1[3], bh0[j], bh1[j]);
-            }
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j <= 2 * i + 1; ++j) {
+                    float (&a)[4] = acc[i * (i + 1) + j];
+                    mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bh0[j], bh1[j]);
+                    mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bl0[j], bl1[j]);
+                    mma16816(a, bl0[2 * i], bl0[2 * i + 1], bl1[2 * i], bl1[2 * i + 1], bh0[j], bh1[j]);
+                }
             // rhs: (H + L)^T [r_hi r_lo]
-            mma16816(racc[0], bh0[0], bh0[1], bh1[0], bh1[1], rb0, rb1);
-            mma16816(racc[0], bl0[0], bl0[1], bl1[0], bl1[1], rb0, rb1);
-            mma16816(racc[1], bh0[2], bh0[3], bh1[2], bh1[3], rb0, rb1);
-            mma16816(racc[1], bl0[2], bl0[3], bl1[2], bl1[3], rb0, rb1);
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                mma16816(racc[i], bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], rb0, rb1);
+                mma16816(racc[i], bl0[2 * i], bl0[2 * i + 1], bl1[2 * i], bl1[2 * i + 1], rb0, rb1);
+            }
         }
         __syncwarp();
         if (last_of_seg) {
@@ -390,29 +433,31 @@ __global__ void __launch_bounds__(kWarps * 32, 2) als_mma_gram32_kernel(
             // natural dims (pi(M), pi(N)); each unordered pair is owned by exactly one (M >= N) element.
             float* rs_ = reinterpret_cast<float*>(stage + buf * 32 * RS);
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                const int i = q < 2 ? 0 : 1, j = q < 2 ? q : q - 2;
+            for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
-                    if (M >= N) {
-                        const int a = pi_dim(M), b = pi_dim(N);
-                        const int hi = a > b ? a : b, lo = a > b ? b : a;
-                        rs_[tri_off(hi) + lo] = acc[q][e] * inv_s2;
+                for (int j = 0; j <= 2 * i + 1; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
+                        float& v = acc[i * (i + 1) + j][e];
+                        if (M >= N) {
+                            const int a = pi_dim<K>(M), b = pi_dim<K>(N);
+                            const int hi = a > b ? a : b, lo = a > b ? b : a;
+                            rs_[tri_off(hi) + lo] = v * inv_s2;
+                        }
+                        v = 0.0f;
                     }
-                    acc[q][e] = 0.0f;
+            if (t == 0) {  // lane (g, 0) holds the rhs of dims D*g + 2i (+1)
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    rs_[kRhs + D * g + 2 * i] = (racc[i][0] + racc[i][1]) * inv_sv;
+                    rs_[kRhs + D * g + 2 * i + 1] = (racc[i][2] + racc[i][3]) * inv_sv;
                 }
             }
-            if (t == 0) {
-                float4 rv;
-                rv.x = (racc[0][0] + racc[0][1]) * inv_sv;  // dim 4g
-                rv.y = (racc[0][2] + racc[0][3]) * inv_sv;  // dim 4g+1
-                rv.z = (racc[1][0] + racc[1][1]) * inv_sv;  // dim 4g+2
-                rv.w = (racc[1][2] + racc[1][3]) * inv_sv;  // dim 4g+3
-                *reinterpret_cast<float4*>(rs_ + kRhs + 4 * g) = rv;
-            }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) racc[0][e] = racc[1][e] = 0.0f;
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) racc[i][e] = 0.0f;
             const int32_t sg = __shfl_sync(0xffffffffu, c_sg, ck);
             const int64_t sbeg = bcast64(c_beg, ck);  // (outside the lane-0 branch: full-warp shuffle)
             if (lane == 0) rs_[kCnt] = static_cast<float>(cend - sbeg);
@@ -451,42 +496,44 @@ __global__ void als_pack_vals_kernel(int64_t n, const float* __restrict__ val, c
 // Sum each multi-segment item's segment records in segment order.  list ==
 // nullptr: every item, result to out[item] (multi-GPU Gram records); else the
 // listed items, result to rec[first[item]] in place.
+template <int K>
 __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems, const int32_t* __restrict__ list,
                                                                  const int32_t* __restrict__ list_count,
                                                                  const int32_t* __restrict__ nseg_of,
                                                                  const int32_t* __restrict__ first,
                                                                  float* __restrict__ rec, float* __restrict__ out) {
+    constexpr int kRec = Cfg<K>::kRec;
     const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
-    const int c = threadIdx.x;  // float4 chunk of the record
-    if (c >= kRec / 4) return;
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
         const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
         const int32_t ns = nseg_of[item];
-        const float4* src = reinterpret_cast<const float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c;
-        float4 s = src[0];
-        int32_t q = 1;
-        for (; q + 4 <= ns; q += 4) {  // four loads in flight; the sum order stays q = 0, 1, 2, ...
-            float4 v[4];
+        for (int c = threadIdx.x; c < kRec / 4; c += blockDim.x) {  // float4 chunk of the record
+            const float4* src = reinterpret_cast<const float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c;
+            float4 s = src[0];
+            int32_t q = 1;
+            for (; q + 4 <= ns; q += 4) {  // four loads in flight; the sum order stays q = 0, 1, 2, ...
+                float4 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = src[static_cast<int64_t>(q + u) * (kRec / 4)];
+                for (int u = 0; u < 4; ++u) v[u] = src[static_cast<int64_t>(q + u) * (kRec / 4)];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                s.x += v[u].x;
-                s.y += v[u].y;
-                s.z += v[u].z;
-                s.w += v[u].w;
+                for (int u = 0; u < 4; ++u) {
+                    s.x += v[u].x;
+                    s.y += v[u].y;
+                    s.z += v[u].z;
+                    s.w += v[u].w;
+                }
             }
+            for (; q < ns; ++q) {
+                const float4 v = src[static_cast<int64_t>(q) * (kRec / 4)];
+                s.x += v.x;
+                s.y += v.y;
+                s.z += v.z;
+                s.w += v.w;
+            }
+            float4* dst = list ? reinterpret_cast<float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c
+                               : reinterpret_cast<float4*>(out + item * kRec) + c;
+            *dst = s;
         }
-        for (; q < ns; ++q) {
-            const float4 v = src[static_cast<int64_t>(q) * (kRec / 4)];
-            s.x += v.x;
-            s.y += v.y;
-            s.z += v.z;
-            s.w += v.w;
-        }
-        float4* dst = list ? reinterpret_cast<float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c
-                           : reinterpret_cast<float4*>(out + item * kRec) + c;
-        *dst = s;
     }
 }
 
@@ -503,10 +550,13 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
 // for the redundant per-column work of the 4 lanes).
 constexpr int kLPS = 4;
 constexpr int kSys = 32 / kLPS;
-constexpr int kSolveSmem = kSys * kRec * 4;
+template <int K>
+constexpr int solve_smem() { return kSys * Cfg<K>::kRec * 4; }
+template <int K>
 __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
                                                                const float* __restrict__ rec, float* __restrict__ X,
                                                                float lambda) {
+    constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
     extern __shared__ __align__(16) float srec[];
     const int lane = threadIdx.x, sys = lane % kSys, par = lane / kSys;
     float* S = srec + sys * kRec;
@@ -644,33 +694,35 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
     }
 }
 
-size_t als_mma_smem_bytes() { return sizeof(uint4) * kWarps * kStageU4; }
-
-static cudaError_t launch_solve(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
-                                int sm_count, cudaStream_t s) {
-    cudaFuncSetAttribute(als_solve_records_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmem);
+template <int K>
+static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
+                                  int sm_count, cudaStream_t s) {
+    constexpr int smem = solve_smem<K>();
+    cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t nbatch = (nitems + kSys - 1) / kSys;
     int64_t blocks = nbatch;
-    const int64_t cap = static_cast<int64_t>(sm_count) * (kLPS == 4 ? 11 : 5);  // shared-memory bound
+    const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 11 : 3);  // shared-memory bound
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    als_solve_records_kernel<<<static_cast<unsigned>(blocks), 32, kSolveSmem, s>>>(nitems, first, rec, X, lambda);
+    als_solve_records_kernel<K><<<static_cast<unsigned>(blocks), 32, smem, s>>>(nitems, first, rec, X, lambda);
     return cudaGetLastError();
 }
 
-// one rank-32 half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
+// one tensor-core half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
 // -> per-item Gram records in h.gram_out (mode 1, multi-GPU column side)
-cudaError_t launch_als_mma_half(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
-    const size_t smem = als_mma_smem_bytes();
+template <int K>
+static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+    using C = Cfg<K>;
+    const size_t smem = sizeof(uint4) * kWarps * C::kStageU4;
     int64_t blocks = (h.max_segs + kWarps - 1) / kWarps;
-    const int64_t cap = static_cast<int64_t>(sm_count) * 2;
+    const int64_t cap = static_cast<int64_t>(sm_count) * C::kMinBlocks;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(als_mma_gram32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(als_mma_gram_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (h.ev_gram0) cudaEventRecord(h.ev_gram0, s);
-    als_mma_gram32_kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+    als_mma_gram_kernel<K><<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
         h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.idx, h.valh, h.Yh, h.ymax, h.vmax, h.partial,
         h.blk_ctr);
     e = cudaGetLastError();
@@ -678,34 +730,46 @@ cudaError_t launch_als_mma_half(const AlsHalf& h, int mode, int sm_count, cudaSt
     if (h.ev_gram1) cudaEventRecord(h.ev_gram1, s);
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
     if (mode == 1) {
-        als_reduce_records_kernel<<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
-                                                          h.gram_out);
+        als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
+                                                             h.gram_out);
         return cudaGetLastError();
     }
-    als_reduce_records_kernel<<<rblocks, 160, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.nseg, h.first,
-                                                      h.partial, nullptr);
+    als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.nseg, h.first,
+                                                         h.partial, nullptr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_solve(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s);
+    return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s);
 }
 
-cudaError_t launch_als_solve_records(int64_t nitems, const float* G, float* X, float lambda, int sm_count,
+cudaError_t launch_als_mma_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+    if (k == 32) return launch_half_k<32>(h, mode, sm_count, s);
+    if (k == 64) return launch_half_k<64>(h, mode, sm_count, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_als_solve_records(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                      cudaStream_t s) {
-    return launch_solve(nitems, nullptr, G, X, lambda, sm_count, s);
+    if (k == 32) return launch_solve_k<32>(nitems, nullptr, G, X, lambda, sm_count, s);
+    if (k == 64) return launch_solve_k<64>(nitems, nullptr, G, X, lambda, sm_count, s);
+    return cudaErrorInvalidValue;
 }
 
-size_t als_record_floats32() { return kRec; }
+size_t als_record_floats_mma(int k) { return k == 64 ? Cfg<64>::kRec : Cfg<32>::kRec; }
 
 // max |X| -> *maxbits (zeroed here), then X -> packed hi/lo rows
-cudaError_t launch_als_pack(int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count, cudaStream_t s) {
+cudaError_t launch_als_pack(int k, int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count,
+                            cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(maxbits, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
-    const int64_t cnt = rows * K;
+    const int64_t cnt = rows * k;
     int64_t blocks = (cnt + 255) / 256;
     if (blocks > sm_count * 8) blocks = sm_count * 8;
     if (blocks < 1) blocks = 1;
     als_absmax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(cnt, X, maxbits);
-    als_pack_kernel<<<static_cast<unsigned>((rows * 8 + 255) / 256), 256, 0, s>>>(rows, X, maxbits, Xh);
+    const unsigned pb = static_cast<unsigned>((rows * 8 + 255) / 256);
+    if (k == 32) als_pack_kernel<32><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);
+    else if (k == 64) als_pack_kernel<64><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 

@@ -48,6 +48,9 @@ struct Buf {
 };
 
 
+// ranks on the tensor-core path (als_mma.cu / als_select_mma.cu)
+bool mma_rank(int k) { return k == 32 || k == 64; }
+
 int bits_for(int64_t n) {
     int b = 1;
     while ((int64_t(1) << b) < n + 1) ++b;
@@ -114,7 +117,7 @@ static int als_build_csc(ocg_als_plan* P) {
         // (row, value) travel with the column key through the radix sort (stable:
         // rows stay ascending inside a column), so no random gathers afterwards.
         // Rank 32: the value word is the packed (fp16 hi, lo) form.
-        const uint32_t* vb = P->k == 32 ? P->valh.p : reinterpret_cast<const uint32_t*>(P->val.p);
+        const uint32_t* vb = mma_rank(P->k) ? P->valh.p : reinterpret_cast<const uint32_t*>(P->val.p);
         ALS_CUDA(ocg::launch_expand_pairs(P->m, P->row_ptr.p, vb, P->pairs_in.p, sm, s));
         size_t bytes = P->sort_tmp_bytes;
         ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, P->col.p, P->keys_out.p, P->pairs_in.p,
@@ -165,7 +168,7 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     h.partial = S.partial.p;
     h.gram_out = nullptr;
     h.lambda = P->lambda;
-    if (P->k == 32) {
+    if (mma_rank(P->k)) {
         h.valh = sd == 0 ? P->valh.p : reinterpret_cast<const uint32_t*>(P->cval.p);
         h.Yh = sd == 0 ? P->Vh.p : P->Uh.p;
         h.ymax = P->maxbits.p + (sd == 0 ? 1 : 0);
@@ -176,9 +179,9 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
 
 // after a half-sweep (or V init): repack the factor the next half gathers
 static int als_pack(ocg_als_plan* P, int sd) {
-    if (P->k != 32) return OCG_OK;
+    if (!mma_rank(P->k)) return OCG_OK;
     const int64_t rows = sd == 0 ? P->m : P->n;
-    ALS_CUDA(ocg::launch_als_pack(rows, sd == 0 ? P->U.p : P->V.p, P->maxbits.p + (sd == 0 ? 0 : 1),
+    ALS_CUDA(ocg::launch_als_pack(P->k, rows, sd == 0 ? P->U.p : P->V.p, P->maxbits.p + (sd == 0 ? 0 : 1),
                                   sd == 0 ? P->Uh.p : P->Vh.p, ocg_internal_sm_count(P->ctx),
                                   ocg_internal_stream(P->ctx)));
     return OCG_OK;
@@ -207,7 +210,7 @@ static int als_alloc(ocg_als_plan* P) {
         ALS_CUDA(S.first.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.total.alloc(3));
         ALS_CUDA(S.multi_list.alloc(static_cast<size_t>(items)));
-        if (sd == 1 && P->k == 32) {
+        if (sd == 1 && mma_rank(P->k)) {
             ALS_CUDA(S.seg_order.alloc(static_cast<size_t>(ms)));
             ALS_CUDA(S.seg_key.alloc(static_cast<size_t>(ms)));
             ALS_CUDA(S.seg_key_out.alloc(static_cast<size_t>(ms)));
@@ -223,7 +226,7 @@ static int als_alloc(ocg_als_plan* P) {
         // partial Grams only for items with >1 segment: sum of their nseg <= 2*nnz/kSeg
         // (the column side may also run in MODE 1 — every segment keeps a slot)
         // (rank 32: every segment writes a record, slot = segment id)
-        const int64_t mp = (sd == 1 || P->k == 32) ? ms : std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
+        const int64_t mp = (sd == 1 || mma_rank(P->k)) ? ms : std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
         ALS_CUDA(S.nmulti.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.pfirst.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.partial.alloc(static_cast<size_t>(mp) * ocg::als_gram_record_floats(P->k)));
@@ -232,7 +235,7 @@ static int als_alloc(ocg_als_plan* P) {
         P->scan_tmp_bytes = std::max(P->scan_tmp_bytes, b);
     }
     ALS_CUDA(P->scan_tmp.alloc(P->scan_tmp_bytes));
-    if (P->k == 32) ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
+    if (mma_rank(P->k)) ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
     return OCG_OK;
 }
 
@@ -241,11 +244,11 @@ static int als_alloc_fixed(ocg_als_plan* P) {
     ALS_CUDA(P->U.alloc(static_cast<size_t>(P->m * P->k)));
     ALS_CUDA(P->V.alloc(static_cast<size_t>(P->n * P->k)));
     ALS_CUDA(P->Vt.alloc(static_cast<size_t>(P->n * P->k)));
-    if (P->k == 32) {
-        ALS_CUDA(P->Uh.alloc(static_cast<size_t>(P->m * 8)));
-        ALS_CUDA(P->Vh.alloc(static_cast<size_t>(P->n * 8)));
+    if (mma_rank(P->k)) {
+        ALS_CUDA(P->Uh.alloc(static_cast<size_t>(P->m * (P->k / 4))));  // K/4 x 16 B per packed row
+        ALS_CUDA(P->Vh.alloc(static_cast<size_t>(P->n * (P->k / 4))));
         ALS_CUDA(P->maxbits.alloc(3));
-        ALS_CUDA(P->Vsel.alloc(static_cast<size_t>(P->n * 8)));
+        ALS_CUDA(P->Vsel.alloc(static_cast<size_t>(P->n * (P->k / 4))));
     }
     ALS_CUDA(P->idx.alloc(static_cast<size_t>(P->m)));
     ALS_CUDA(P->ncand.alloc(static_cast<size_t>(P->m)));
@@ -259,8 +262,8 @@ static int als_alloc_fixed(ocg_als_plan* P) {
 static int als_check(int64_t m, int64_t n, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
                      const ocg_als_hyper* h, double gamma) {
     if (!h) return ocg_internal_fail(OCG_E_INVALID, "als: null hyperparameters");
-    if (h->rank != 8 && h->rank != 16 && h->rank != 32)
-        return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: rank must be 8, 16 or 32");
+    if (h->rank != 8 && h->rank != 16 && h->rank != 32 && h->rank != 64)
+        return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: rank must be 8, 16, 32 or 64");
     if (h->lambda <= 0.0f || h->sweeps <= 0) return ocg_internal_fail(OCG_E_INVALID, "als: bad hyperparameters");
     if (m <= 0 || n <= 0) return ocg_internal_fail(OCG_E_INVALID, "als: empty matrix");
     if (gamma <= 0.0 || gamma >= 1.0) return ocg_internal_fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
@@ -313,7 +316,7 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     if (P->nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: nnz >= 2^31");
     if ((rc = als_alloc(P.get()))) return rc;
     if ((rc = als_alloc_fixed(P.get()))) return rc;
-    if (P->k == 32) {
+    if (mma_rank(P->k)) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(ctx), s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
     }
@@ -343,7 +346,7 @@ int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* 
     ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
-    if (P->k == 32) {
+    if (mma_rank(P->k)) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
     }
@@ -359,7 +362,7 @@ int ocg_als_plan_set_warm(ocg_als_plan* P, int32_t warm_sweeps) {
 
 static int launch_select(ocg_als_plan* P) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
-    if (P->k != 32) ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
+    if (!mma_rank(P->k)) ALS_CUDA(ocg::launch_transpose(P->n, P->k, P->V.p, P->Vt.p, s));
     ocg::AlsSelectArgs a{};
     a.m = P->m;
     a.n = P->n;
@@ -380,7 +383,7 @@ static int launch_select(ocg_als_plan* P) {
     a.loss = P->loss.p;
     a.ncand = P->ncand.p;
     a.completed = nullptr;
-    if (P->k == 32)
+    if (mma_rank(P->k))
         ALS_CUDA(ocg::launch_als_select_mma(a, P->Vsel.p, P->maxbits.p, P->maxbits.p + 1, ocg_internal_sm_count(P->ctx), s));
     else
         ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));
@@ -426,7 +429,7 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             ALS_CUDA(cudaEventElapsedTime(&b, P->ev[3], P->ev[4]));
             row_ms += a;
             col_ms += b;
-            if (P->k == 32) {
+            if (mma_rank(P->k)) {
                 ALS_CUDA(cudaEventElapsedTime(&a, P->ev[6], P->ev[7]));
                 ALS_CUDA(cudaEventElapsedTime(&b, P->ev[8], P->ev[9]));
                 rgram_ms += a;
@@ -550,7 +553,7 @@ int ocg_als_plan_completed_rows(ocg_als_plan* P, int64_t row0, int64_t nrows, do
     a.loss = dl.p;
     a.ncand = dn.p;
     a.completed = d.p;
-    if (P->k == 32)
+    if (mma_rank(P->k))
         ALS_CUDA(ocg::launch_als_select_mma(a, P->Vsel.p, P->maxbits.p, P->maxbits.p + 1, ocg_internal_sm_count(P->ctx), s));
     else
         ALS_CUDA(ocg::launch_als_select(a, ocg_internal_sm_count(P->ctx), s));

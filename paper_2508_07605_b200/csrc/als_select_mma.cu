@@ -42,7 +42,6 @@ namespace ocg {
 
 namespace {
 
-constexpr int K = 32;
 constexpr int kW = 8;          // warps per CTA
 constexpr int kTile = 256;     // V columns per tile
 constexpr int kNT = kTile / 8;  // n-tiles per tile
@@ -131,6 +130,8 @@ __device__ __noinline__ void exact_update(BestX* b, double pd, int cs, int j, do
 // V (n x 32 f32) -> per column 8 x 16 B: chunk t of the hi (lo) half holds dims
 // {2t, 2t+1, 2t+8, 2t+9, 2t+16, 2t+17, 2t+24, 2t+25}; hi chunks sit at
 // positions 0-3 on even columns and 4-7 on odd columns (lo the other half)
+// (rank 64: the same per block p of 32 dims, chunks 8p .. 8p+7)
+template <int K>
 __global__ void pack_vsel_kernel(int64_t n, const float* __restrict__ V, const unsigned* __restrict__ vmaxbits,
                                  uint4* __restrict__ out) {
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (column, t)
@@ -138,14 +139,17 @@ __global__ void pack_vsel_kernel(int64_t n, const float* __restrict__ V, const u
     const int64_t c = q >> 2;
     const int t = static_cast<int>(q & 3);
     const float s = ldexpf(1.0f, scale_exp(*vmaxbits));
-    const float* v = V + c * K;
-    const int d[8] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9, 2 * t + 16, 2 * t + 17, 2 * t + 24, 2 * t + 25};
-    uint32_t hi[4], lo[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) split2(v[d[2 * u]], v[d[2 * u + 1]], s, hi[u], lo[u]);
     const int odd = static_cast<int>(c & 1);
-    out[c * 8 + t + 4 * odd] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    out[c * 8 + t + 4 * (1 - odd)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+    for (int p = 0; p < K / 32; ++p) {
+        const float* v = V + c * K + 32 * p;
+        const int d[8] = {2 * t, 2 * t + 1, 2 * t + 8, 2 * t + 9, 2 * t + 16, 2 * t + 17, 2 * t + 24, 2 * t + 25};
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) split2(v[d[2 * u]], v[d[2 * u + 1]], s, hi[u], lo[u]);
+        out[c * (K / 4) + 8 * p + t + 4 * odd] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        out[c * (K / 4) + 8 * p + t + 4 * (1 - odd)] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
 }
 
 }  // namespace
@@ -157,12 +161,13 @@ struct AlsSelMmaArgs {
     const unsigned* vmax;      // max |V| bits
 };
 
-template <bool WRITE_COMPLETED>
-__global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArgs P) {
+template <int K, bool WRITE_COMPLETED>
+__global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kernel(AlsSelMmaArgs P) {
+    constexpr int KS = K / 16, CPC = K / 4;  // k-steps, 16-byte chunks per V column
     const AlsSelectArgs& a = P.a;
     extern __shared__ __align__(16) uint4 sdyn[];
     uint4* Vs = sdyn;                                                     // [2][kTile][8]
-    float* csum = reinterpret_cast<float*>(Vs + 2 * kTile * 8);           // [2][kTile] c+g per column
+    float* csum = reinterpret_cast<float*>(Vs + 2 * kTile * CPC);         // [2][kTile] c+g per column
     uint32_t* maskw = reinterpret_cast<uint32_t*>(csum + 2 * kTile);      // [kW][16][8]
     BestX* bx = reinterpret_cast<BestX*>(maskw + kW * 16 * 8);            // [kW][32 lanes][2 rows]
     BestX* obest = bx + kW * 32 * 2;                                      // [kW][16 rows] observed best
@@ -186,10 +191,10 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
 
     auto load_tile = [&](int tt, int buf) {
         const int64_t c0 = static_cast<int64_t>(tt) * kTile;
-        for (int e = tid; e < kTile * 8; e += blockDim.x) {
-            const int64_t c = c0 + e / 8;
-            uint4* dst = Vs + buf * kTile * 8 + e;
-            if (c < n) cp_async16(dst, P.Vsel + c * 8 + (e & 7));
+        for (int e = tid; e < kTile * CPC; e += blockDim.x) {
+            const int64_t c = c0 + e / CPC;
+            uint4* dst = Vs + buf * kTile * CPC + e;
+            if (c < n) cp_async16(dst, P.Vsel + c * CPC + (e % CPC));
             else *dst = make_uint4(0u, 0u, 0u, 0u);
         }
         for (int e = tid; e < kTile; e += blockDim.x) {
@@ -212,9 +217,9 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
         const int64_t rowg[2] = {r0 + g, r0 + g + 8};
         const bool live[2] = {rowg[0] < a.m, rowg[1] < a.m};
         // A fragments (rows g, g+8; k-step ks: dims 16ks + {2t,2t+1} / {2t+8,2t+9})
-        uint32_t ah[2][4], al[2][4];
+        uint32_t ah[KS][4], al[KS][4];
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int ks = 0; ks < KS; ++ks) {
             float2 v[2][2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -227,25 +232,34 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
             split2(v[0][1].x, v[0][1].y, su, ah[ks][2], al[ks][2]);  // row g,   k 2t+8..
             split2(v[1][1].x, v[1][1].y, su, ah[ks][3], al[ks][3]);  // row g+8, k 2t+8..
         }
-        auto mma_cell = [&](float (&d)[4], const uint4& bh, const uint4& bl) {
+        // bh/bl[p]: the lane's hi/lo chunk of block p (k-steps 2p, 2p+1)
+        auto mma_cell = [&](float (&d)[4], const uint4 (&bh)[K / 32], const uint4 (&bl)[K / 32]) {
             d[0] = d[1] = d[2] = d[3] = 0.0f;
-            mma16816(d, ah[0][0], ah[0][1], ah[0][2], ah[0][3], bh.x, bh.y);
-            mma16816(d, ah[0][0], ah[0][1], ah[0][2], ah[0][3], bl.x, bl.y);
-            mma16816(d, al[0][0], al[0][1], al[0][2], al[0][3], bh.x, bh.y);
-            mma16816(d, ah[1][0], ah[1][1], ah[1][2], ah[1][3], bh.z, bh.w);
-            mma16816(d, ah[1][0], ah[1][1], ah[1][2], ah[1][3], bl.z, bl.w);
-            mma16816(d, al[1][0], al[1][1], al[1][2], al[1][3], bh.z, bh.w);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const uint4& h = bh[ks >> 1];
+                const uint4& l = bl[ks >> 1];
+                const uint32_t h0 = (ks & 1) ? h.z : h.x, h1 = (ks & 1) ? h.w : h.y;
+                const uint32_t l0 = (ks & 1) ? l.z : l.x, l1 = (ks & 1) ? l.w : l.y;
+                mma16816(d, ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], h0, h1);
+                mma16816(d, ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], l0, l1);
+                mma16816(d, al[ks][0], al[ks][1], al[ks][2], al[ks][3], h0, h1);
+            }
         };
         // ---- baseline p_{i,n-1}: the n-tile holding column n-1, same MMA sequence
         double pbase[2];
         {
             const int64_t cb = (n - 1) & ~static_cast<int64_t>(7);  // n-tile base column
             const int64_t col = cb + g;                              // this lane's B column
-            uint4 bh = make_uint4(0u, 0u, 0u, 0u), bl = bh;
-            if (col < n) {
-                const int odd = static_cast<int>(col & 1);
-                bh = P.Vsel[col * 8 + t + 4 * odd];
-                bl = P.Vsel[col * 8 + t + 4 * (1 - odd)];
+            uint4 bh[K / 32], bl[K / 32];
+#pragma unroll
+            for (int p = 0; p < K / 32; ++p) {
+                bh[p] = bl[p] = make_uint4(0u, 0u, 0u, 0u);
+                if (col < n) {
+                    const int odd = static_cast<int>(col & 1);
+                    bh[p] = P.Vsel[col * CPC + 8 * p + t + 4 * odd];
+                    bl[p] = P.Vsel[col * CPC + 8 * p + t + 4 * (1 - odd)];
+                }
             }
             float d[4];
             mma_cell(d, bh, bl);
@@ -357,7 +371,7 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
             cp_async_wait_all();
             __syncthreads();  // tile tt landed, masks written
             if (tt + 1 < ntiles) load_tile(tt + 1, buf ^ 1);
-            const uint4* vt = Vs + buf * kTile * 8;
+            const uint4* vt = Vs + buf * kTile * CPC;
             const float* cst = csum + buf * kTile;
             uint32_t mk[2][2];
 #pragma unroll
@@ -392,8 +406,12 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
                 for (int u = 0; u < 2; ++u) {
                     const int cc = (nt + u) * 8;
                     const int odd = g & 1;
-                    const uint4 bh = vt[(cc + g) * 8 + t + 4 * odd];
-                    const uint4 bl = vt[(cc + g) * 8 + t + 4 * (1 - odd)];
+                    uint4 bh[K / 32], bl[K / 32];
+#pragma unroll
+                    for (int p = 0; p < K / 32; ++p) {
+                        bh[p] = vt[(cc + g) * CPC + 8 * p + t + 4 * odd];
+                        bl[p] = vt[(cc + g) * CPC + 8 * p + t + 4 * (1 - odd)];
+                    }
                     mma_cell(d[u], bh, bl);
                     cs2[u] = *reinterpret_cast<const float2*>(cst + cc + 2 * t);
                 }
@@ -504,32 +522,40 @@ __global__ void __launch_bounds__(kW * 32, 2) als_select_mma_kernel(AlsSelMmaArg
     }
 }
 
-size_t als_select_mma_smem() {
-    return sizeof(uint4) * 2 * kTile * 8 + sizeof(float) * 2 * kTile + sizeof(uint32_t) * kW * 16 * 8 +
+template <int K>
+static size_t select_smem() {
+    return sizeof(uint4) * 2 * kTile * (K / 4) + sizeof(float) * 2 * kTile + sizeof(uint32_t) * kW * 16 * 8 +
            sizeof(BestX) * (kW * 32 * 2 + kW * 16) + sizeof(int32_t) * (kW * 16 + 512) +
            sizeof(uint16_t) * kW * 16 * kList;
 }
 
-// V -> packed select layout; U's and V's scales come from the Gram packing
-// (maxbits[0] = max |U|, maxbits[1] = max |V|, refreshed after every half-sweep)
-cudaError_t launch_als_select_mma(const AlsSelectArgs& a, uint4* Vsel, const unsigned* umax, const unsigned* vmax,
-                                  int sm_count, cudaStream_t s) {
-    if (a.k != K) return cudaErrorInvalidValue;
-    if (static_cast<int64_t>(a.n / a.ngpu) + a.ngpu > 512) return cudaErrorInvalidValue;
-    pack_vsel_kernel<<<static_cast<unsigned>((a.n * 4 + 255) / 256), 256, 0, s>>>(a.n, a.V, vmax, Vsel);
+template <int K>
+static cudaError_t launch_select_k(const AlsSelectArgs& a, uint4* Vsel, const unsigned* umax, const unsigned* vmax,
+                                   int sm_count, cudaStream_t s) {
+    pack_vsel_kernel<K><<<static_cast<unsigned>((a.n * 4 + 255) / 256), 256, 0, s>>>(a.n, a.V, vmax, Vsel);
     AlsSelMmaArgs P{a, Vsel, umax, vmax};
-    const size_t smem = als_select_mma_smem();
+    const size_t smem = select_smem<K>();
     int64_t blocks = (a.m + kW * 16 - 1) / (kW * 16);
-    const int64_t cap = static_cast<int64_t>(sm_count) * 2;
+    const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 2 : 1);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<static_cast<unsigned>(blocks), kW * 32, smem, s>>>(P);
     };
-    if (a.completed) go(als_select_mma_kernel<true>);
-    else go(als_select_mma_kernel<false>);
+    if (a.completed) go(als_select_mma_kernel<K, true>);
+    else go(als_select_mma_kernel<K, false>);
     return cudaGetLastError();
+}
+
+// V -> packed select layout; U's and V's scales come from the Gram packing
+// (maxbits[0] = max |U|, maxbits[1] = max |V|, refreshed after every half-sweep)
+cudaError_t launch_als_select_mma(const AlsSelectArgs& a, uint4* Vsel, const unsigned* umax, const unsigned* vmax,
+                                  int sm_count, cudaStream_t s) {
+    if (static_cast<int64_t>(a.n / a.ngpu) + a.ngpu > 512) return cudaErrorInvalidValue;
+    if (a.k == 32) return launch_select_k<32>(a, Vsel, umax, vmax, sm_count, s);
+    if (a.k == 64) return launch_select_k<64>(a, Vsel, umax, vmax, sm_count, s);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace ocg

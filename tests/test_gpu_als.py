@@ -22,7 +22,7 @@ def _problem(m, nc, ng, density, dense_rows, seed):
     return grid, synth.joint_csr(m, grid, density, dense_rows, seed=seed)
 
 
-@pytest.mark.parametrize("k", [8, 16, 32])
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
 def test_als_factors_and_predictions_match_oracle(ctx, port, k):
     from oracle import bind
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
@@ -39,7 +39,7 @@ def test_als_factors_and_predictions_match_oracle(ctx, port, k):
     assert np.quantile(rel, 0.999) < PRED_RTOL, (rel.max(), np.quantile(rel, 0.999))
 
 
-@pytest.mark.parametrize("rank", [16, 32])  # 32: tensor-core imputation + selection
+@pytest.mark.parametrize("rank", [16, 32, 64])  # 32/64: tensor-core imputation + selection
 @pytest.mark.parametrize("n_grid", [(8, 16), (16, 16), (64, 64), (10, 30)])
 def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid, rank):
     """The fused kernel's decision == policy::select_caps on the very rows it
@@ -65,7 +65,7 @@ def test_als_fused_selection_exact_on_completed_rows(ctx, port, n_grid, rank):
     np.testing.assert_array_equal(nc, n2)
 
 
-@pytest.mark.parametrize("rank", [8, 32])
+@pytest.mark.parametrize("rank", [8, 32, 64])
 def test_als_selection_ties_and_clamps(ctx, port, rank):
     """Rows engineered to hit the clamp floor/ceiling and exact saving ties."""
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
@@ -94,7 +94,7 @@ def test_als_selection_ties_and_clamps(ctx, port, rank):
     np.testing.assert_array_equal(nc, n2)
 
 
-@pytest.mark.parametrize("rank", [16, 32])
+@pytest.mark.parametrize("rank", [16, 32, 64])
 def test_als_end_to_end_decisions_match_oracle_where_margin_allows(ctx, port, rank):
     from oracle import bind
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan

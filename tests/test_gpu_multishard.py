@@ -7,7 +7,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("k", [16, 32])  # 32: tensor-core Gram records (MODE 1)
+@pytest.mark.parametrize("k", [16, 32, 64])  # 32/64: tensor-core Gram records (MODE 1)
 def test_two_shard_schedule_matches_oracle(ctx, port, k):
     import torch
 
