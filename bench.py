@@ -2,7 +2,7 @@
 """bench.py — B200 online CF completion + selection (OPEN online phase).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c4|c0xn|ingest]
+                  [--workload c2|c1|c3|c4|c0xn|ingest]
 
 One JSON line on rank 0.  For N>1 launch with
 torch.distributed.run; each rank takes an equal shard of the units (weak
@@ -336,6 +336,7 @@ JOINT = {  # SURVEY §8d joint configs
     "c1": dict(m=10_000, grid=(16, 16), density=0.05, dense_rows=10, rank=8),
     "c2": dict(m=1_000_000, grid=(64, 64), density=0.02, dense_rows=1000, rank=32),
 }
+JOINT["c3"] = dict(m=4_000_000, grid=(128, 128), density=0.01, dense_rows=4000, rank=64)  # BASELINE configs[3]
 JOINT["c4"] = dict(JOINT["c2"])  # streaming refits on the C2 matrix
 
 
@@ -572,8 +573,8 @@ def workload_c4(args, d: Dist):
     return out, ("c4", m)
 
 
-WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "c4": workload_c4,
-             "ingest": workload_ingest}
+WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "c3": workload_joint,
+             "c4": workload_c4, "ingest": workload_ingest}
 
 
 # -------------------------------------------------------- reference (CPU)

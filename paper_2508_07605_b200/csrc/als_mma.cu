@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 
 #include "als.h"
 #include "ocg_common.cuh"
@@ -78,6 +80,17 @@ __device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
 }
 
 __device__ __forceinline__ int min32(int64_t v) { return v < 32 ? static_cast<int>(v) : 32; }
+
+// compile-time loop: f(integral_constant<int, 0>) ... f(<N-1>) -- forces full unrolling where
+// #pragma unroll gives up (rank 64), so register arrays stay register arrays
+template <class F, int... J>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, J...>) {
+    (f(std::integral_constant<int, J>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 }  // namespace
 
@@ -581,8 +594,8 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
         const bool live = sys < nb;
         const float cnt = live ? S[kCnt] : 1.0f;
         const float diag = lambda * cnt;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
+        static_for<K>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
             // row j of L (columns < j) -> registers (all lanes of the item: broadcast)
             float rj[K];
             const float* Rj = S + tri_off(j);
@@ -655,7 +668,7 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
             }
             __syncwarp();
             if (par == 0) S[tri_off(j) + j] = r;  // the diagonal slot keeps 1 / L[j][j]
-        }
+        });
         __syncwarp();
         // L^T x = y (y = row K of the factorised record), column-oriented, all lanes of the item
         float y[K];
@@ -667,8 +680,8 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
             y[q + 2] = v.z;
             y[q + 3] = v.w;
         }
-#pragma unroll
-        for (int q = K - 1; q >= 0; --q) {
+        static_for<K>([&](auto qc) {
+            constexpr int q = K - 1 - decltype(qc)::value;
             const float* Rq = S + tri_off(q);
             y[q] *= Rq[q];
 #pragma unroll
@@ -681,7 +694,7 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
             }
 #pragma unroll
             for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
-        }
+        });
         if (live && par == 0) {  // every lane of the item holds x; part 0 writes the 128-byte row
             float4* xo = reinterpret_cast<float4*>(X + (i0 + sys) * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
