@@ -396,7 +396,10 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
             // then one branch into the rare exact path if any cell is inside the band.
             const float S = ldexpf(1.0f, eu + ev);
             const float lo_s = 0.01f * S, hi_s = 1.25f * S;
-            const float fth_s[2] = {fthr[0] * S, fthr[1] * S};
+            // validity of an unobserved cell as ONE compare: if 0.01 >= p_thr every completed
+            // value (>= 0.01) is valid; otherwise cells clamped to 0.01 are invalid and
+            // min(x, 1.25 S) >= fthr S decides (fthr > 0.01f, and 1.25 is a float)
+            const float fth_s[2] = {lov[0] > 0.0f ? -INFINITY : fthr[0] * S, lov[1] > 0.0f ? -INFINITY : fthr[1] * S};
             float tb_s[2] = {tband[0] * inv_s, tband[1] * inv_s};
 #pragma unroll 2
             for (int nt = 0; nt < kNT; nt += 2) {
@@ -427,10 +430,9 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
                         for (int e = 0; e < 2; ++e) {
                             const float csf = e ? cs2[u].y : cs2[u].x;
                             const float x = d[u][2 * q + e];
-                            const bool lo = x <= lo_s;
                             const float pc = fminf(x, hi_s);
-                            if ((lo ? lov[q] : pc) >= fth_s[q]) vb |= 1u << (2 * u + e);
-                            if (csf <= tb_s[q] * fmaxf(pc, lo_s)) hb |= 1u << (2 * u + e);
+                            vb |= pc >= fth_s[q] ? 1u << (2 * u + e) : 0u;
+                            hb |= csf <= tb_s[q] * fmaxf(pc, lo_s) ? 1u << (2 * u + e) : 0u;
                         }
                     const unsigned ob4 = (mk[q][nt >> 4] >> ((nt & 15) * 2)) & 0xFu;
                     vb &= ~ob4;
