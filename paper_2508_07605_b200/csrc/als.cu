@@ -1,4 +1,6 @@
-// ALS completion kernels (K3 Gram accumulation + K4 batched Cholesky solve).
+// ALS completion kernels for ranks 8 and 16 (SIMT; ranks 32/64 run on the
+// tensor cores, als_mma.cu), the segment tables both paths share, and the
+// CSC-build helpers.
 //
 // No reference counterpart (the reference's CF is NCF only): the
 // semantics are defined by oracle/ocg_oracle.c (ocgo_als_fit) — weighted-
@@ -11,7 +13,7 @@
 //
 // als_seg_gram_kernel: one warp per segment.  The warp streams its
 // observations 32 at a time: (index, value) pairs are read coalesced, the 32
-// gathered factor rows (K floats, 128 B at K=32) are copied global->shared
+// gathered factor rows (K floats) are copied global->shared
 // with cp.async into a double-buffered stage (the next chunk's gathers are in
 // flight while the current chunk is accumulated), and every lane accumulates
 // a (K/8) x (K/4) block of the K x K Gram in registers (conflict-free 16-byte
@@ -35,17 +37,11 @@ namespace {
 
 template <int K>
 struct GramShape {
-    static constexpr int RB = K / 8;           // rows per lane block
-    static constexpr int CB = K / 4;           // cols per lane block
     static constexpr int GS = K + 4;           // Gram row stride (floats): 16-byte rows
-    static constexpr int TS = K == 32 ? K + 4 : K;  // staged-row stride (floats); +4 for Sym32's cross-row LDS
+    static constexpr int TS = K;  // staged-row stride (floats)
     static constexpr int GSZ = K * K + K + 1;  // global Gram record: K*K, rhs K, count
 };
 
-__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
@@ -208,101 +204,9 @@ struct GramGeneric {
     }
 };
 
-// Sym32: the 36 lower-triangular 4x4 blocks of the 32x32 Gram spread evenly:
-// lane l owns block l (28 strictly lower blocks, then diagonal blocks 0-3) for
-// every observation, and per group of 8 observations each lane also adds one
-// (diagonal block 4 + l/8, observation l%8) product — 9 block updates per
-// lane per 8 observations instead of 16, i.e. 18 FFMA per observation instead
-// of 32.  The extra blocks' 8 partial sums are reduced with shuffles at the end.
-struct GramSym32 {
-    float acc[4][4], ext[4][4];
-    float bacc;
-    __device__ __forceinline__ static void block_of(int b, int& I, int& J) {
-        if (b < 28) {  // strictly lower: rows I = 1..7, J < I
-            I = 1;
-            while (b >= I) {
-                b -= I;
-                ++I;
-            }
-            J = b;
-        } else {
-            I = J = b - 28;
-        }
-    }
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[a][c] = ext[a][c] = 0.0f;
-        bacc = 0.0f;
-    }
-    __device__ __forceinline__ void chunk(const float* st, const float* rs, int cnt, int lane) {
-        constexpr int TS = GramShape<32>::TS;
-        int I, J;
-        block_of(lane, I, J);
-        const int E = 4 + (lane >> 3);  // extra diagonal block
-        for (int g = 0; g < cnt; g += 8) {
-            const int gn = cnt - g < 8 ? cnt - g : 8;
-            for (int t = 0; t < gn; ++t) {
-                const float* row = st + (g + t) * TS;
-                const float4 xa = *reinterpret_cast<const float4*>(row + 4 * I);
-                const float4 xb = *reinterpret_cast<const float4*>(row + 4 * J);
-                const float a4[4] = {xa.x, xa.y, xa.z, xa.w}, b4[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(a4[a], b4[c], acc[a][c]);
-                bacc = fmaf(rs[g + t], row[lane], bacc);
-            }
-            const int o2 = g + (lane & 7);
-            if (o2 < cnt) {
-                const float4 xe = *reinterpret_cast<const float4*>(st + o2 * TS + 4 * E);
-                const float e4[4] = {xe.x, xe.y, xe.z, xe.w};
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) ext[a][c] = fmaf(e4[a], e4[c], ext[a][c]);
-            }
-        }
-    }
-    __device__ __forceinline__ void store(float* dst, int ld, float* rhs_out, int lane) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float v = ext[a][c];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                ext[a][c] = v;
-            }
-        int I, J;
-        block_of(lane, I, J);
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                dst[(4 * I + a) * ld + 4 * J + c] = acc[a][c];
-                dst[(4 * J + c) * ld + 4 * I + a] = acc[a][c];
-            }
-        if ((lane & 7) == 0) {
-            const int E = 4 + (lane >> 3);
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) dst[(4 * E + a) * ld + 4 * E + c] = ext[a][c];
-        }
-        if (rhs_out) rhs_out[lane] = bacc;
-    }
-};
-
 template <int K>
 struct GramPolicy {
     using type = GramGeneric<K>;
-};
-template <>
-struct GramPolicy<32> {
-    using type = GramSym32;
 };
 
 // MODE 0: fused solve of single-segment items, partials for the rest.
@@ -480,23 +384,6 @@ __global__ void als_init_kernel(int64_t n, int k, uint64_t seed, float* V) {
     V[e] = static_cast<float>(v);
 }
 
-// CSR row ids (expand row_ptr), used to build the CSC mirror
-__global__ void expand_rows_kernel(int64_t m, const int64_t* __restrict__ ptr, int32_t* __restrict__ rowid) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < m; i += nw)
-        for (int64_t q = ptr[i] + lane; q < ptr[i + 1]; q += 32) rowid[q] = static_cast<int32_t>(i);
-}
-
-__global__ void gather_csc_kernel(int64_t nnz, const int32_t* __restrict__ perm, const int32_t* __restrict__ rowid,
-                                  const float* __restrict__ val, int32_t* __restrict__ crow, float* __restrict__ cval) {
-    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= nnz) return;
-    const int32_t p = perm[q];
-    crow[q] = rowid[p];
-    cval[q] = val[p];
-}
-
 // (row << 32 | value bits) per CSR entry, the payload of the column sort
 __global__ void expand_pairs_kernel(int64_t m, const int64_t* __restrict__ ptr, const uint32_t* __restrict__ vbits,
                                     uint64_t* __restrict__ pairs) {
@@ -595,7 +482,6 @@ cudaError_t launch_als_half(int k, const AlsHalf& h, int mode, int sm_count, cud
     switch (k) {
         case 8: return launch_half_k<8>(h, mode, sm_count, s);
         case 16: return launch_half_k<16>(h, mode, sm_count, s);
-        case 32: return launch_half_k<32>(h, mode, sm_count, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -610,21 +496,8 @@ cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, fl
     switch (k) {
         case 8: als_solve_from_gram_kernel<8><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
         case 16: als_solve_from_gram_kernel<16><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
-        case 32: als_solve_from_gram_kernel<32><<<b, 256, 0, s>>>(nitems, G, X, lambda); break;
         default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_expand_rows(int64_t m, const int64_t* ptr, int32_t* rowid, int sm_count, cudaStream_t s) {
-    expand_rows_kernel<<<sm_count * 8, 256, 0, s>>>(m, ptr, rowid);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_gather_csc(int64_t nnz, const int32_t* perm, const int32_t* rowid, const float* val, int32_t* crow,
-                              float* cval, cudaStream_t s) {
-    if (nnz == 0) return cudaSuccess;
-    gather_csc_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(nnz, perm, rowid, val, crow, cval);
     return cudaGetLastError();
 }
 

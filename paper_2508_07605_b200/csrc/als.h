@@ -61,9 +61,6 @@ cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vm
 cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int sm_count, cudaStream_t s);
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,
                                        cudaStream_t s);
-cudaError_t launch_expand_rows(int64_t m, const int64_t* ptr, int32_t* rowid, int sm_count, cudaStream_t s);
-cudaError_t launch_gather_csc(int64_t nnz, const int32_t* perm, const int32_t* rowid, const float* val, int32_t* crow,
-                              float* cval, cudaStream_t s);
 cudaError_t launch_expand_pairs(int64_t m, const int64_t* ptr, const uint32_t* vbits, uint64_t* pairs, int sm_count,
                                 cudaStream_t s);
 cudaError_t launch_split_pairs(int64_t nnz, const uint64_t* pairs, int32_t* crow, uint32_t* cval, cudaStream_t s);

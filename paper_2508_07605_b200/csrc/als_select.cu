@@ -305,7 +305,6 @@ cudaError_t launch_als_select(const AlsSelectArgs& a, int sm_count, cudaStream_t
     switch (a.k) {
         case 8: wc ? go(als_select_kernel<8, true>) : go(als_select_kernel<8, false>); break;
         case 16: wc ? go(als_select_kernel<16, true>) : go(als_select_kernel<16, false>); break;
-        case 32: wc ? go(als_select_kernel<32, true>) : go(als_select_kernel<32, false>); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -98,12 +98,6 @@ __device__ __forceinline__ double dot_regs(const double* w, const double (&x)[N]
     }
 }
 
-__device__ __forceinline__ double selu(double z) {
-    double a, gf;
-    selu_fwd(z, a, gf);
-    return a;
-}
-
 // SELU split around the exp table loads: exp_pre(selu_exp_arg(z)) early,
 // selu_finish later.  Positive z takes the lambda*z branch (its exp argument is
 // a harmless -1); the result equals selu_fwd's bit for bit.
@@ -112,7 +106,6 @@ __device__ __forceinline__ double selu_exp_arg(double z) { return z > 0 ? -1.0 :
 // per-lane copy of the interleaved exp table (entry i of copy r at (i/2*8 + r)*2 + i%2)
 struct ExpTabLanes {
     const uint64_t* p;  // already offset by this lane's copy
-    __device__ __forceinline__ uint64_t operator()(int i) const { return p[(i >> 1) * 16 + (i & 1)]; }
     __device__ __forceinline__ void pair(int entry, uint64_t& tail, uint64_t& hi) const {
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p + entry * 16);
         tail = v.x;
@@ -268,7 +261,7 @@ __global__ void __launch_bounds__(kPairThreads, 2) predict_pair_kernel(PredGeom 
     double* stage = sm + kPairT + threadIdx.x;
     uint64_t* tab_s = reinterpret_cast<uint64_t*>(sm + kPairT + kPairStage * kPairThreads);
     for (int e = threadIdx.x; e < kPairTab; e += blockDim.x) {
-        const int entry = e >> 4, copy = (e >> 1) & 7, half = e & 1;  // (entry*8 + copy)*2 + half
+        const int entry = e >> 4, half = e & 1;  // e = (entry*8 + copy)*2 + half
         tab_s[e] = exp_tab(2 * entry + half);
     }
     const ExpTabLanes tab{tab_s + 2 * (threadIdx.x & 7)};
