@@ -38,6 +38,7 @@ struct AlsHalf {
     const int32_t* seg_order = nullptr;
     int32_t* blk_ctr = nullptr;  // rank 32: work-block counter (zeroed per launch)
     cudaEvent_t ev_gram0 = nullptr, ev_gram1 = nullptr;  // optional: recorded around the Gram kernel
+    bool fuse_solve = false;  // rank 32, mode 0: single-segment items solved inside the Gram kernel
 };
 
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);

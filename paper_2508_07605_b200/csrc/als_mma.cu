@@ -117,6 +117,10 @@ struct Cfg {
 static_assert(Cfg<32>::kRec == 612 && Cfg<32>::kRhs == 576, "rank-32 record layout");
 static_assert(Cfg<64>::kRec * 4 <= 32 * Cfg<64>::RS * 16, "rank-64 record fits a stage buffer");
 
+// K4 solver geometry: kLPS lanes per system, kSys systems per warp
+constexpr int kLPS = 4;
+constexpr int kSys = 32 / kLPS;
+
 // MMA index X in [0,K) <-> natural factor dim pi(X) = D*(X%8) + X/8
 template <int K>
 __device__ __forceinline__ int pi_dim(int x) { return Cfg<K>::D * (x & 7) + (x >> 3); }
@@ -205,27 +209,45 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 //    16-byte coalesced writes).
 // (One TMA bulk copy per factor row was measured 1.4x slower than the cp.async
 // gathers: per-operation cost of the bulk-copy unit at 128 B.)
+template <int K>
+__device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, float* __restrict__ X, float lambda);
+
 constexpr int kRC = 8;     // ring slots (chunks)
 constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
-template <int K>
-__global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_kernel(
+// FUSED (rank 32, row side): single-segment items are not written to global
+// memory; their records go to a per-warp batch in shared memory and every
+// kSys of them are solved in place by the warp (solve_staged), so the K4 work
+// overlaps the gathers in flight (multi-segment items keep the record path).
+template <int K, bool FUSED>
+__host__ __device__ constexpr int gram_warps() { return FUSED ? 7 : kWarps; }
+template <int K, bool FUSED>
+__host__ __device__ constexpr int gram_warp_u4() { return Cfg<K>::kStageU4 + (FUSED ? (kSys * Cfg<K>::kRec) / 4 + 4 : 0); }
+
+template <int K, bool FUSED>
+__global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K>::kMinBlocks) als_mma_gram_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
-    const unsigned* __restrict__ vmax, float* __restrict__ rec, int32_t* __restrict__ blk_ctr) {
+    const unsigned* __restrict__ vmax, float* __restrict__ rec, int32_t* __restrict__ blk_ctr,
+    const int32_t* __restrict__ nseg_of, float* __restrict__ X, float lambda) {
     using C = Cfg<K>;
     constexpr int D = C::D, MT = C::MT, NLT = C::NLT, RU4 = C::RU4, RS = C::RS;
     constexpr int kRec = C::kRec, kRhs = C::kRhs, kCnt = C::kCnt;
+    constexpr int W = gram_warps<K, FUSED>();
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    uint4* stage = dyn4 + warp * C::kStageU4;                              // [2][32][RS] uint4
+    uint4* stage = dyn4 + warp * gram_warp_u4<K, FUSED>();                 // [2][32][RS] uint4
+    float* batch = reinterpret_cast<float*>(stage + C::kStageU4);           // FUSED: [kSys][kRec]
+    int64_t* bitems = reinterpret_cast<int64_t*>(batch + kSys * kRec);      // FUSED: [kSys]
+    int bcount = 0;
     int32_t* ring_j = reinterpret_cast<int32_t*>(stage + 2 * 32 * RS);     // [kRC][32]
     uint32_t* ring_r = reinterpret_cast<uint32_t*>(ring_j + kRC * 32);     // [kRC][32]
     const int ey = als_scale_exp(*ymax), ev = als_scale_exp(*vmax);
     const float inv_s2 = ldexpf(1.0f, -2 * ey), inv_sv = ldexpf(1.0f, -(ey + ev));
     const int32_t nsegs = *total_segs;
     const int32_t nblk = (nsegs + 31) / 32;
+    (void)W;
     const uint32_t rsel = g == 0 ? 0x5410u : 0x7632u;  // rhs B column 0 = r_hi, column 1 = r_lo
     const uint32_t rmask = g < 2 ? 0xffffffffu : 0u;
 
@@ -237,15 +259,17 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
     // lane i <- segment of work index 32 b + i, or b + i * nblk when the work
     // order is sorted by band (column side: the warps active at any moment then
     // gather from one band of the factor matrix); sg < 0: none
-    auto load_meta = [&](int32_t b, int32_t& sg, int64_t& beg, int64_t& end) {
+    auto load_meta = [&](int32_t b, int32_t& sg, int64_t& beg, int64_t& end, int32_t& item) {
         const int32_t k = seg_order ? b + lane * nblk : b * 32 + lane;
         sg = -1;
         beg = end = 0;
+        item = -1;  // FUSED: the segment's item when it is the item's only segment
         if (b < nblk && k < nsegs) {
             sg = seg_order ? seg_order[k] : k;
             const int32_t it = seg_item[sg];
             beg = seg_beg[sg];
             end = min(beg + kSeg, ptr[it + 1]);
+            if (FUSED && nseg_of[it] == 1) item = it;
         }
     };
     auto bcast64 = [&](int64_t v, int src) {
@@ -255,11 +279,11 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
     // ---- refill cursor (producer of ring slots)
     int32_t rb = grab();
     if (rb >= nblk) return;
-    int32_t r_sg;
+    int32_t r_sg, r_item;
     int64_t r_beg, r_end;
-    load_meta(rb, r_sg, r_beg, r_end);
+    load_meta(rb, r_sg, r_beg, r_end, r_item);
     // consumer block = the refill's first block
-    int32_t cb = rb, c_sg = r_sg;
+    int32_t cb = rb, c_sg = r_sg, c_item = r_item;
     int64_t c_beg = r_beg, c_end = r_end;
     int rk = 0;
     int64_t rpos = bcast64(r_beg, 0), r_e = bcast64(r_end, 0);  // refill segment: position, end
@@ -271,7 +295,7 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
         if (rex) {
             if (rb != cb) return;  // the consumer still needs the pending block's metadata: wait
             rb = grab();
-            load_meta(rb, r_sg, r_beg, r_end);
+            load_meta(rb, r_sg, r_beg, r_end, r_item);
             rk = 0;
             if (rb >= nblk || __shfl_sync(0xffffffffu, r_sg, 0) < 0) {
                 rdone = true;
@@ -440,11 +464,13 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
             }
         }
         __syncwarp();
+        const int32_t fitem = FUSED && last_of_seg ? __shfl_sync(0xffffffffu, c_item, ck) : -1;
         if (last_of_seg) {
-            // ---- record, assembled in the drained buffer, stored with 16-byte coalesced writes.
+            // ---- record, assembled in the drained buffer (FUSED single-segment items: in the
+            // warp's batch slot), stored with 16-byte coalesced writes.
             // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) ->
             // natural dims (pi(M), pi(N)); each unordered pair is owned by exactly one (M >= N) element.
-            float* rs_ = reinterpret_cast<float*>(stage + buf * 32 * RS);
+            float* rs_ = fitem >= 0 ? batch + bcount * kRec : reinterpret_cast<float*>(stage + buf * 32 * RS);
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -474,17 +500,28 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
             const int32_t sg = __shfl_sync(0xffffffffu, c_sg, ck);
             const int64_t sbeg = bcast64(c_beg, ck);  // (outside the lane-0 branch: full-warp shuffle)
             if (lane == 0) rs_[kCnt] = static_cast<float>(cend - sbeg);
-            __syncwarp();
-            float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
-            const float4* src = reinterpret_cast<const float4*>(rs_);
+            if (FUSED && fitem >= 0) {
+                if (lane == 0) bitems[bcount] = fitem;
+                if (++bcount == kSys) {  // a full batch: solve it (the next chunk's gathers are in flight)
+                    __syncwarp();
+                    solve_staged<K>(batch, kSys, bitems[lane % kSys], X, lambda);
+                    bcount = 0;
+                }
+                __syncwarp();
+            } else {
+                __syncwarp();
+                float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
+                const float4* src = reinterpret_cast<const float4*>(rs_);
 #pragma unroll
-            for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots carry stale values, never read
-            __syncwarp();
+                for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots: stale, never read
+                __syncwarp();
+            }
         }
         if (finished) break;
         if (nblock) {
             cb = rb;
             c_sg = r_sg;
+            c_item = r_item;
             c_beg = r_beg;
             c_end = r_end;
         }
@@ -494,6 +531,10 @@ __global__ void __launch_bounds__(kWarps * 32, Cfg<K>::kMinBlocks) als_mma_gram_
         buf ^= 1;
     }
     cp_async_wait<0>();
+    if (FUSED && bcount > 0) {  // the last partial batch
+        __syncwarp();
+        solve_staged<K>(batch, bcount, bitems[(lane % kSys) < bcount ? lane % kSys : 0], X, lambda);
+    }
 }
 
 // observed values -> packed (fp16 hi, fp16 lo) of val * 2^ev
@@ -561,36 +602,18 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
 // stride 153 x 16 B: 8 distinct bank groups).  With LPS = 4 a warp needs 19.6
 // KB, so 11 warps share an SM (the kernel is latency-bound: occupancy pays
 // for the redundant per-column work of the 4 lanes).
-constexpr int kLPS = 4;
-constexpr int kSys = 32 / kLPS;
 template <int K>
-constexpr int solve_smem() { return kSys * Cfg<K>::kRec * 4; }
+__host__ __device__ constexpr int solve_smem() { return kSys * Cfg<K>::kRec * 4; }
+// Factorise and solve the nb <= kSys systems staged at srec (record layout,
+// record s at srec + s * kRec); lane = kSys * part + sys; `item` = the item of
+// the lane's system (valid for sys < nb): x -> X[item * K].
 template <int K>
-__global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
-                                                               const float* __restrict__ rec, float* __restrict__ X,
-                                                               float lambda) {
+__device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, float* __restrict__ X,
+                                             float lambda) {
     constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
-    extern __shared__ __align__(16) float srec[];
-    const int lane = threadIdx.x, sys = lane % kSys, par = lane / kSys;
+    const int lane = threadIdx.x & 31, sys = lane % kSys, par = lane / kSys;
     float* S = srec + sys * kRec;
-    const int64_t nbatch = (nitems + kSys - 1) / kSys;
-    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
-        const int64_t i0 = bt * kSys;
-        const int nb = static_cast<int>(nitems - i0 < kSys ? nitems - i0 : kSys);
-        // stage: the warp copies record r with coalesced 16-byte cp.async
-        const int64_t myslot = lane < nb ? (first ? static_cast<int64_t>(first[i0 + lane]) : i0 + lane) : 0;
-        for (int r = 0; r < nb; ++r) {
-            const int64_t slot = __shfl_sync(0xffffffffu, myslot, r);
-            const float4* src = reinterpret_cast<const float4*>(rec + slot * kRec);
-            float4* dst = reinterpret_cast<float4*>(srec + r * kRec);
-            for (int c = lane; c < kRec / 4; c += 32) {
-                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + c) : "memory");
-            }
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
+    {
         const bool live = sys < nb;
         const float cnt = live ? S[kCnt] : 1.0f;
         const float diag = lambda * cnt;
@@ -695,8 +718,8 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
 #pragma unroll
             for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
         });
-        if (live && par == 0) {  // every lane of the item holds x; part 0 writes the 128-byte row
-            float4* xo = reinterpret_cast<float4*>(X + (i0 + sys) * K);
+        if (live && par == 0) {  // every lane of the item holds x; part 0 writes the K-float row
+            float4* xo = reinterpret_cast<float4*>(X + item * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
             for (int q = 0; q < K / 4; ++q)
@@ -707,9 +730,48 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
     }
 }
 
+// K4 over records in global memory: items 0..nitems-1, or the listed items
+// (list != nullptr); item i's record at slot first[i] (first == nullptr: slot i).
+template <int K>
+__global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
+                                                               const float* __restrict__ rec, float* __restrict__ X,
+                                                               float lambda, const int32_t* __restrict__ list,
+                                                               const int32_t* __restrict__ list_count) {
+    constexpr int kRec = Cfg<K>::kRec;
+    extern __shared__ __align__(16) float srec[];
+    const int lane = threadIdx.x;
+    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
+    const int64_t nbatch = (nwork + kSys - 1) / kSys;
+    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+        const int64_t i0 = bt * kSys;
+        const int nb = static_cast<int>(nwork - i0 < kSys ? nwork - i0 : kSys);
+        // stage: the warp copies record r with coalesced 16-byte cp.async
+        int64_t myitem = 0, myslot = 0;
+        if (lane < nb) {
+            myitem = list ? static_cast<int64_t>(list[i0 + lane]) : i0 + lane;
+            myslot = first ? static_cast<int64_t>(first[myitem]) : myitem;
+        }
+        for (int r = 0; r < nb; ++r) {
+            const int64_t slot = __shfl_sync(0xffffffffu, myslot, r);
+            const float4* src = reinterpret_cast<const float4*>(rec + slot * kRec);
+            float4* dst = reinterpret_cast<float4*>(srec + r * kRec);
+            for (int c = lane; c < kRec / 4; c += 32) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + c) : "memory");
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        const int64_t item = __shfl_sync(0xffffffffu, myitem, lane % kSys);
+        solve_staged<K>(srec, nb, item, X, lambda);
+    }
+}
+
 template <int K>
 static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
-                                  int sm_count, cudaStream_t s) {
+                                  int sm_count, cudaStream_t s, const int32_t* list = nullptr,
+                                  const int32_t* list_count = nullptr) {
     constexpr int smem = solve_smem<K>();
     cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t nbatch = (nitems + kSys - 1) / kSys;
@@ -717,30 +779,40 @@ static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const fl
     const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 11 : 3);  // shared-memory bound
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    als_solve_records_kernel<K><<<static_cast<unsigned>(blocks), 32, smem, s>>>(nitems, first, rec, X, lambda);
+    als_solve_records_kernel<K><<<static_cast<unsigned>(blocks), 32, smem, s>>>(nitems, first, rec, X, lambda, list,
+                                                                             list_count);
     return cudaGetLastError();
 }
 
 // one tensor-core half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
 // -> per-item Gram records in h.gram_out (mode 1, multi-GPU column side)
-template <int K>
-static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
-    using C = Cfg<K>;
-    const size_t smem = sizeof(uint4) * kWarps * C::kStageU4;
-    int64_t blocks = (h.max_segs + kWarps - 1) / kWarps;
-    const int64_t cap = static_cast<int64_t>(sm_count) * C::kMinBlocks;
+template <int K, bool FUSED>
+static cudaError_t launch_gram_k(const AlsHalf& h, int sm_count, cudaStream_t s) {
+    constexpr int W = gram_warps<K, FUSED>();
+    const size_t smem = sizeof(uint4) * W * gram_warp_u4<K, FUSED>();
+    int64_t blocks = (h.max_segs + W - 1) / W;
+    const int64_t cap = static_cast<int64_t>(sm_count) * (FUSED ? 1 : Cfg<K>::kMinBlocks);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
-    if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(als_mma_gram_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(als_mma_gram_kernel<K, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
     if (h.ev_gram0) cudaEventRecord(h.ev_gram0, s);
-    als_mma_gram_kernel<K><<<static_cast<unsigned>(blocks), kWarps * 32, smem, s>>>(
+    als_mma_gram_kernel<K, FUSED><<<static_cast<unsigned>(blocks), W * 32, smem, s>>>(
         h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.idx, h.valh, h.Yh, h.ymax, h.vmax, h.partial,
-        h.blk_ctr);
-    e = cudaGetLastError();
+        h.blk_ctr, h.nseg, h.X, h.lambda);
+    const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (h.ev_gram1) cudaEventRecord(h.ev_gram1, s);
+    return cudaSuccess;
+}
+
+template <int K>
+static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    const bool fused = K == 32 && mode == 0 && h.fuse_solve;
+    e = fused ? launch_gram_k<32, true>(h, sm_count, s) : launch_gram_k<K, false>(h, sm_count, s);
+    if (e != cudaSuccess) return e;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
     if (mode == 1) {
         als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
@@ -751,6 +823,9 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
                                                          h.partial, nullptr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (fused)  // the single-segment items were solved inside the Gram kernel
+        return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s, h.multi_list,
+                                 h.multi_count);
     return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s);
 }
 

@@ -163,6 +163,10 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     h.multi_count = S.total.p + 1;
     h.seg_order = S.seg_order.p;
     h.blk_ctr = S.total.p + 2;
+    // K4 fused into the row-side Gram kernel (solve batches of single-segment rows
+    // in shared memory): measured 5.1 ms/launch vs 2.0 + 1.7 ms split (7 warps/SM
+    // for Gram + batches starve both); kept as an ablation switch, off
+    h.fuse_solve = false;
     h.Y = sd == 0 ? P->V.p : P->U.p;
     h.X = sd == 0 ? P->U.p : P->V.p;
     h.partial = S.partial.p;
