@@ -410,7 +410,12 @@ def workload_joint(args, d: Dist):
     # uploaded from pinned host memory (ocg_als_plan_upload), the plan runs
     # from scratch and the decisions are read back to the host.
     # N>1: each rank uploads its shard and runs the sharded schedule.
-    pin = [torch.from_numpy(x).pin_memory() for x in (A.row_ptr, A.col, A.val)]
+    compact = n <= 65536  # 16-bit column indices over PCIe (ocg_als_plan_upload_compact)
+    pin = [torch.from_numpy(x).pin_memory()
+           for x in (A.row_ptr, A.col.astype(np.uint16) if compact else A.col, A.val)]
+    h2d_bytes = sum(int(x.numel() * x.element_size()) for x in pin)
+    res_pin = [torch.empty(m_loc, dtype=dt).pin_memory() for dt in (torch.int32, torch.float64, torch.float64,
+                                                                      torch.int32)]
     p2 = AlsPlan(m_loc, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
     if d.world == 1:
         p2.run(timed=False)  # warm (module load, first-touch)
@@ -421,13 +426,14 @@ def workload_joint(args, d: Dist):
         ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        p2.upload(*(int(x.data_ptr()) for x in pin))
+        (p2.upload_compact if compact else p2.upload)(*(int(x.data_ptr()) for x in pin))
         if d.world == 1:
             p2.run(timed=False)
         else:
             ShardedAlsDriver(GpuAlsBackend(p2, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
-        r2 = p2.results()
+        p2.results(out=[int(x.data_ptr()) for x in res_pin])  # decisions into pinned host memory
         e2e_t += time.perf_counter() - t0
+    r2 = [x.numpy() for x in res_pin]
     p2.close()
     e2e_t = d.max(e2e_t / e2e_steps)
     if d.world == 1:
@@ -446,7 +452,7 @@ def workload_joint(args, d: Dist):
         "selections_per_sec": m * args.steps / t_dev,
         "ms_per_step": t_dev * 1e3 / args.steps,
         "e2e": {"value": cells / e2e_t, "unit": "cells/s",
-                "h2d_bytes_per_step": int(A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) * d.world,
+                "h2d_bytes_per_step": h2d_bytes * d.world,
                 "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes) * d.world,
                 "selections_per_sec": m / e2e_t},
         "dtype": "f32 factors / f64 selection",

@@ -62,6 +62,16 @@ class AlsPlan:
             args = tuple(ptr(a) for a in self._keep)
         check(lib.ocg_als_plan_upload(self._h, *args))
 
+    def upload_compact(self, row_ptr, col16, val):
+        """upload() with uint16 column indices (n <= 65536); addresses or numpy arrays."""
+        if isinstance(row_ptr, int):
+            args = (ctypes.c_void_p(row_ptr), ctypes.c_void_p(col16), ctypes.c_void_p(val))
+        else:
+            self._keep = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col16, np.uint16),
+                          np.ascontiguousarray(val, np.float32))
+            args = tuple(ptr(a) for a in self._keep)
+        check(lib.ocg_als_plan_upload_compact(self._h, *args))
+
     def set_warm(self, sweeps: int):
         """Warm refits (deviation from from-scratch semantics): later runs start from the
         previous factors and run ``sweeps`` sweeps; 0 = from scratch."""
@@ -75,7 +85,12 @@ class AlsPlan:
         check(lib.ocg_als_plan_run(self._h, ctypes.byref(tot) if timed else None, ph if timed else None))
         return float(tot.value), [float(x) for x in ph]
 
-    def results(self):
+    def results(self, out=None):
+        """(idx, saving, loss, ncand) per row.  out: optional 4 host addresses (e.g.
+        pinned buffers: int32[m], f64[m], f64[m], int32[m]) filled in place."""
+        if out is not None:
+            check(lib.ocg_als_plan_results(self._h, *(ctypes.c_void_p(a) for a in out), None, None))
+            return None
         m = self.m
         idx, nc = np.zeros(m, np.int32), np.zeros(m, np.int32)
         sv, lo = np.zeros(m), np.zeros(m)

@@ -100,7 +100,9 @@ struct ocg_als_plan {
     Buf<uint4> Uh, Vh;
     Buf<unsigned> maxbits;
     Buf<uint32_t> valh;
-    Buf<uint4> Vsel;  // V in the tensor-core selection layout  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
+    Buf<uint4> Vsel;  // V in the tensor-core selection layout
+    Buf<uint16_t> col16;  // staging of ocg_als_plan_upload_compact
+    int64_t col16_cap = 0;  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
     cudaEvent_t ev[10] = {};
@@ -350,6 +352,46 @@ int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* 
     ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
+    if (mma_rank(P->k)) {
+        ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
+        ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
+    }
+    return OCG_OK;
+}
+
+namespace {
+__global__ void widen_u16_kernel(int64_t n, const uint16_t* __restrict__ in, int32_t* __restrict__ out) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = in[q];
+}
+}  // namespace
+
+int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const uint16_t* col16, const float* val) {
+    if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als upload_compact: more than 65536 settings");
+    if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    const int64_t nnz = row_ptr[P->m];
+    if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    if (nnz != P->nnz) {
+        ALS_CUDA(cudaStreamSynchronize(s));
+        P->nnz = nnz;
+        ALS_CUDA(P->col.alloc(static_cast<size_t>(nnz)));
+        ALS_CUDA(P->val.alloc(static_cast<size_t>(nnz)));
+        int rc = als_alloc(P);
+        if (rc) return rc;
+    }
+    if (P->col16_cap < nnz) {
+        ALS_CUDA(P->col16.alloc(static_cast<size_t>(nnz)));
+        P->col16_cap = nnz;
+    }
+    ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(P->col16.p, col16, sizeof(uint16_t) * P->nnz, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
+    if (P->nnz > 0) {
+        widen_u16_kernel<<<static_cast<unsigned>((P->nnz + 255) / 256), 256, 0, s>>>(P->nnz, P->col16.p, P->col.p);
+        ALS_CUDA(cudaGetLastError());
+    }
     if (mma_rank(P->k)) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));

@@ -141,6 +141,10 @@ def test_als_upload_refit_matches_fresh_plan(ctx):
     plan.upload(A.row_ptr, A.col, val2)
     plan.run()
     got = plan.results()
+    plan.upload_compact(A.row_ptr, A.col.astype(np.uint16), val2)  # 16-bit column indices
+    plan.run()
+    for g_, c_ in zip(got, plan.results()):
+        np.testing.assert_array_equal(g_, c_)
     fresh = AlsPlan(A.m, A.row_ptr, A.col, val2, grid, hyp, 0.05, ctx=ctx)
     fresh.run()
     want = fresh.results()
