@@ -117,9 +117,17 @@ struct Cfg {
 static_assert(Cfg<32>::kRec == 612 && Cfg<32>::kRhs == 576, "rank-32 record layout");
 static_assert(Cfg<64>::kRec * 4 <= 32 * Cfg<64>::RS * 16, "rank-64 record fits a stage buffer");
 
-// K4 solver geometry: kLPS lanes per system, kSys systems per warp
-constexpr int kLPS = 4;
-constexpr int kSys = 32 / kLPS;
+// K4 solver geometry: LPS lanes per system, SYS systems per warp (rank 64: 8 lanes,
+// so 4 systems = 36 KB per warp and 6 warps share an SM)
+template <int K>
+__host__ __device__ constexpr int lps() { return K == 32 ? 4 : 8; }
+template <int K>
+__host__ __device__ constexpr int nsys() { return 32 / lps<K>(); }
+// T(i + LPS) - T(i) for i = 4a + p (padded row lengths 4((r >> 2) + 1))
+template <int LPS>
+__device__ __forceinline__ int row_step(int a, int p) {
+    return LPS == 4 ? 16 * a + 16 + 4 * p : 32 * a + 48 + 8 * p;
+}
 
 // MMA index X in [0,K) <-> natural factor dim pi(X) = D*(X%8) + X/8
 template <int K>
@@ -221,7 +229,9 @@ constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
 template <int K, bool FUSED>
 __host__ __device__ constexpr int gram_warps() { return FUSED ? 7 : kWarps; }
 template <int K, bool FUSED>
-__host__ __device__ constexpr int gram_warp_u4() { return Cfg<K>::kStageU4 + (FUSED ? (kSys * Cfg<K>::kRec) / 4 + 4 : 0); }
+__host__ __device__ constexpr int gram_warp_u4() {
+    return Cfg<K>::kStageU4 + (FUSED ? (nsys<K>() * Cfg<K>::kRec) / 4 + 4 : 0);
+}
 
 template <int K, bool FUSED>
 __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K>::kMinBlocks) als_mma_gram_kernel(
@@ -234,6 +244,7 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
     constexpr int D = C::D, MT = C::MT, NLT = C::NLT, RU4 = C::RU4, RS = C::RS;
     constexpr int kRec = C::kRec, kRhs = C::kRhs, kCnt = C::kCnt;
     constexpr int W = gram_warps<K, FUSED>();
+    constexpr int kSys = nsys<K>();
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
@@ -603,7 +614,7 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
 // KB, so 11 warps share an SM (the kernel is latency-bound: occupancy pays
 // for the redundant per-column work of the 4 lanes).
 template <int K>
-__host__ __device__ constexpr int solve_smem() { return kSys * Cfg<K>::kRec * 4; }
+__host__ __device__ constexpr int solve_smem() { return nsys<K>() * Cfg<K>::kRec * 4; }
 // Factorise and solve the nb <= kSys systems staged at srec (record layout,
 // record s at srec + s * kRec); lane = kSys * part + sys; `item` = the item of
 // the lane's system (valid for sys < nb): x -> X[item * K].
@@ -611,6 +622,7 @@ template <int K>
 __device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, float* __restrict__ X,
                                              float lambda) {
     constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
+    constexpr int kLPS = lps<K>(), kSys = nsys<K>();
     const int lane = threadIdx.x & 31, sys = lane % kSys, par = lane / kSys;
     float* S = srec + sys * kRec;
     {
@@ -640,15 +652,12 @@ __device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, 
             }
             const float r = rsqrt_ftz(d0 + d1);
             // rows i > j with i == par (mod LPS), two per iteration (independent chains)
-            static_assert(kLPS == 4, "incremental row offsets below assume 4 lanes per item");
             int i = j + 1 + ((par - (j + 1)) % kLPS + kLPS) % kLPS;
-            // T(i) and T(i+4) incrementally: with i = 4a + p, T(i+4) - T(i) = 16a + 16 + 4p and
-            // T(i+8) - T(i) = 32a + 48 + 8p (row lengths padded to multiples of 4)
+            // T(i) and T(i + LPS) incrementally (row_step; row lengths padded to multiples of 4)
             int offa = tri_off(i);
 #pragma unroll 1
             for (; i + kLPS <= K; i += 2 * kLPS) {
-                const int a4 = (i >> 2) * 16 + 4 * par;
-                const int offb = offa + a4 + 16;
+                const int offb = offa + row_step<kLPS>(i >> 2, i & 3);
                 const float* Ra = S + offa;
                 const float* Rb = S + offb;
                 float a0 = Ra[j], a1 = 0.0f, b0 = Rb[j], b1 = 0.0f;
@@ -672,7 +681,7 @@ __device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, 
                 }
                 S[offa + j] = (a0 + a1) * r;
                 S[offb + j] = (b0 + b1) * r;
-                offa += 2 * a4 + 48;
+                offa = offb + row_step<kLPS>((i >> 2) + kLPS / 4, i & 3);
             }
             if (i <= K) {
                 const float* Ra = S + offa;
@@ -737,7 +746,7 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
                                                                const float* __restrict__ rec, float* __restrict__ X,
                                                                float lambda, const int32_t* __restrict__ list,
                                                                const int32_t* __restrict__ list_count) {
-    constexpr int kRec = Cfg<K>::kRec;
+    constexpr int kRec = Cfg<K>::kRec, kSys = nsys<K>();
     extern __shared__ __align__(16) float srec[];
     const int lane = threadIdx.x;
     const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
@@ -774,9 +783,9 @@ static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const fl
                                   const int32_t* list_count = nullptr) {
     constexpr int smem = solve_smem<K>();
     cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int64_t nbatch = (nitems + kSys - 1) / kSys;
+    const int64_t nbatch = (nitems + nsys<K>() - 1) / nsys<K>();
     int64_t blocks = nbatch;
-    const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 11 : 3);  // shared-memory bound
+    const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 11 : 6);  // shared-memory bound
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     als_solve_records_kernel<K><<<static_cast<unsigned>(blocks), 32, smem, s>>>(nitems, first, rec, X, lambda, list,
