@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 2) ncf_app_batch_kernel(BatchGeom g,
 
 // reference-default architecture: app/setting dim 8, hidden {32, 16}
 template <int LANE>
-__global__ void __launch_bounds__(kThreads, 2) ncf_app_batch_kernel_k8(BatchGeom g, BatchIO io) {
+__global__ void __launch_bounds__(kThreads, 3) ncf_app_batch_kernel_k8(BatchGeom g, BatchIO io) {
     app_batch_body<LANE, FixArch<8, 8, 32, 16>>(g, io);
 }
 
