@@ -154,6 +154,19 @@ int ocg_ncf_predict(ocg_ctx* ctx, int64_t m, int64_t n, const ocg_ncf_hyper* hyp
                     const int64_t* rows, const int64_t* cols, int64_t count, int lane,
                     double* out);
 
+/* NCF model file (SURVEY §8b ocg_model_to_json / from_json): cf::NcfModel::to_json
+ * / from_json (cfcomplete.cpp:215-265, nn::model_to_json nnkit.cpp:306-365) over
+ * the flat parameter layout above, byte-identical text (nlohmann::json dump(2),
+ * the reference's own serializer).  Host-only.
+ * to_json: out == NULL queries *len (bytes including the terminating NUL).
+ * from_json: params == NULL queries the shapes (hyper dims, m, n, *nparams);
+ * then params[*nparams], app_seen[m], setting_seen[n], meta (each may be NULL). */
+int ocg_ncf_model_to_json(const ocg_ncf_hyper* hyper, int64_t m, int64_t n, const double* params,
+                          const uint8_t* app_seen, const uint8_t* setting_seen, const ocg_ncf_meta* meta,
+                          char* out, size_t cap, size_t* len);
+int ocg_ncf_model_from_json(const char* text, ocg_ncf_hyper* hyper, int64_t* m, int64_t* n, int64_t* nparams,
+                            double* params, uint8_t* app_seen, uint8_t* setting_seen, ocg_ncf_meta* meta);
+
 /* ---- ALS completion + selection (joint mode) -------
  * No reference counterpart: the reference's CF is NCF only.  Semantics are
  * defined by the CPU oracle (oracle/ocg_oracle.c, ocgo_als_fit): weighted-

@@ -78,6 +78,9 @@ _sig("ocg_online_complete_batch", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, 
      c_vp, c_i32, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_online_fit_batch_params", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp,
      ctypes.c_int, c_vp, c_i64, c_vp, c_vp)
+_sig("ocg_ncf_model_to_json", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_char_p,
+     ctypes.c_size_t, c_vp)
+_sig("ocg_ncf_model_from_json", ctypes.c_int, ctypes.c_char_p, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_ncf_predict", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
      ctypes.c_int, c_vp)
 _sig("ocg_debug_exp", ctypes.c_int, c_vp, c_vp, c_i64, c_vp)

@@ -19,7 +19,7 @@ from ._lib import lib, check, ptr
 __all__ = [
     "PowerGrid", "NcfHyper", "NcfMeta", "CapDecision", "ProbePlan", "Context", "derive_seed",
     "select_caps", "select_caps_batch", "online_complete_batch", "online_fit_batch_params", "ncf_predict",
-    "ncf_param_count", "LANE_SCALAR", "LANE_AVX2", "OnlinePlan",
+    "ncf_param_count", "LANE_SCALAR", "LANE_AVX2", "OnlinePlan", "NcfModel",
 ]
 
 LANE_SCALAR, LANE_AVX2 = _lib.LANE_SCALAR, _lib.LANE_AVX2
@@ -295,6 +295,59 @@ def ncf_predict(m: int, n: int, hyper: NcfHyper, params, app_seen, setting_seen,
     check(lib.ocg_ncf_predict(ctx.handle, m, n, ctypes.byref(h), ptr(p), ptr(a), ptr(s), ptr(r), ptr(c), len(r),
                               lane, ptr(out)))
     return out
+
+
+@dataclass
+class NcfModel:
+    """cf::NcfModel as data (cfcomplete.hpp:25-52): m apps, n settings, the flat
+    parameter vector (Adam block order), seen masks and the training meta.
+    ``to_json`` / ``from_json`` are the reference's model file (byte-identical
+    text); ``predict`` runs NcfModel::predict on the device (FP64, lane-exact)."""
+
+    hyper: NcfHyper
+    m: int
+    n: int
+    params: np.ndarray
+    app_seen: np.ndarray
+    setting_seen: np.ndarray
+    meta: NcfMeta
+
+    def to_json(self) -> str:
+        h = self.hyper.to_c()
+        p = np.ascontiguousarray(self.params, np.float64)
+        a = np.ascontiguousarray(self.app_seen, np.uint8)
+        s = np.ascontiguousarray(self.setting_seen, np.uint8)
+        mt = _lib.NcfMetaC()
+        mt.seed, mt.epochs_run = self.meta.seed, self.meta.epochs_run
+        mt.initial_train_mse, mt.final_train_mse, mt.best_val_mse = (self.meta.initial_train_mse,
+                                                                    self.meta.final_train_mse,
+                                                                    self.meta.best_val_mse)
+        ln = ctypes.c_size_t()
+        args = (ctypes.byref(h), self.m, self.n, ptr(p), ptr(a), ptr(s), ctypes.byref(mt))
+        check(lib.ocg_ncf_model_to_json(*args, None, 0, ctypes.byref(ln)))
+        buf = ctypes.create_string_buffer(ln.value)
+        check(lib.ocg_ncf_model_to_json(*args, buf, ln.value, ctypes.byref(ln)))
+        return buf.value.decode()
+
+    @staticmethod
+    def from_json(text: str) -> "NcfModel":
+        raw = text.encode()
+        h = _lib.NcfHyperC()
+        m, n, npar = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib.ocg_ncf_model_from_json(raw, ctypes.byref(h), ctypes.byref(m), ctypes.byref(n), ctypes.byref(npar),
+                                          None, None, None, None))
+        p = np.zeros(npar.value)
+        a, s = np.zeros(m.value, np.uint8), np.zeros(n.value, np.uint8)
+        mt = _lib.NcfMetaC()
+        check(lib.ocg_ncf_model_from_json(raw, ctypes.byref(h), ctypes.byref(m), ctypes.byref(n), ctypes.byref(npar),
+                                          ptr(p), ptr(a), ptr(s), ctypes.byref(mt)))
+        hyper = NcfHyper(app_dim=h.app_dim, setting_dim=h.setting_dim, hidden=[h.hidden[i] for i in range(h.n_hidden)])
+        meta = NcfMeta(mt.seed, mt.epochs_run, mt.initial_train_mse, mt.final_train_mse, mt.best_val_mse)
+        return NcfModel(hyper, m.value, n.value, p, a, s, meta)
+
+    def predict(self, rows, cols, lane: int = LANE_AVX2, ctx: Context | None = None) -> np.ndarray:
+        return ncf_predict(self.m, self.n, self.hyper, self.params, self.app_seen, self.setting_seen, rows, cols,
+                           lane, ctx)
 
 
 class OnlinePlan:

@@ -211,3 +211,25 @@ def test_online_fully_observed_row_not_refit(ctx, golden, gold_npz):
                               PowerGrid.default_grid(), ctx=ctx)
     assert r.status[0] == 0 and r.meta[0]["epochs_run"] == 0
     np.testing.assert_array_equal(r.completed[0], row[0])
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_device_fit_model_file_identical_to_reference(ctx, ref, golden, gold_npz, k):
+    """cf::fit on the device -> NcfModel::to_json text == the reference's own
+    cf::fit + to_json on the same inputs (parameters, masks, meta, formatting)."""
+    from paper_2508_07605_b200 import NcfHyper, NcfMeta, NcfModel, online_fit_batch_params
+
+    name, values, mask, seed, hyper = fit_case(golden, gold_npz, k)
+    hyper = dict(hyper, max_epochs=min(hyper.get("max_epochs", 2000), 40))
+    h = NcfHyper(**hyper)
+    params, meta, status = online_fit_batch_params(values[:-1], mask[:-1], values[-1:], mask[-1:], [seed], h, 1, ctx)
+    assert status[0] == 0
+    m, n = mask.shape
+    mt = NcfMeta(int(meta[0]["seed"]), int(meta[0]["epochs_run"]), float(meta[0]["initial_train_mse"]),
+                 float(meta[0]["final_train_mse"]), float(meta[0]["best_val_mse"]))
+    model = NcfModel(h, m, n, params[0], (mask.sum(1) > 0).astype(np.uint8), (mask.sum(0) > 0).astype(np.uint8), mt)
+    cpu, gpu = (list(DEFAULT_CPU), list(DEFAULT_GPU)) if n == 20 else ([1], list(range(1, n + 1)))
+    ref.force_lane(1)
+    rc, js, _ = ref.ncf_fit(values, mask, cpu, gpu, seed, **hyper)
+    assert rc == 0
+    assert model.to_json() == js
