@@ -100,8 +100,7 @@ __host__ __device__ constexpr int tri_off(int i) { return 4 * ((i >> 2) + 1) * (
 
 // Per-rank constants of the tensor-core path (K = 32 or 64).
 //  D   factor dims per lane group (= MMA n-tiles), MT m-tiles, NLT lower tiles
-//  RU4 packed factor row in 16-byte units: K=32 chunk g = {hi[4g..4g+3], lo[4g..4g+3]};
-//      K=64 chunks 0-7 = hi[8g..8g+7], chunks 8-15 = lo[8g..8g+7]
+//  RU4 packed factor row in 16-byte units: [hi dims 0..K-1 | lo dims 0..K-1]
 //  RS  stage row stride (16-byte units): conflict-free fragment loads, and at K=64 a
 //      record fits one stage buffer
 template <int K>
@@ -129,9 +128,6 @@ __device__ __forceinline__ int row_step(int a, int p) {
     return LPS == 4 ? 16 * a + 16 + 4 * p : 32 * a + 48 + 8 * p;
 }
 
-// MMA index X in [0,K) <-> natural factor dim pi(X) = D*(X%8) + X/8
-template <int K>
-__device__ __forceinline__ int pi_dim(int x) { return Cfg<K>::D * (x & 7) + (x >> 3); }
 
 // power-of-two scale with max|y| * s <= 2^14 (exponent clamped so s^2 and its
 // inverse stay finite in FP32)
@@ -162,31 +158,36 @@ __global__ void als_absmax_kernel(int64_t count, const float* __restrict__ x, un
     }
 }
 
-// X (rows x K f32) -> packed hi/lo rows (Cfg<K>::RU4 x uint4 per row); thread = (row, group g)
+// X (rows x K f32) -> packed hi/lo rows: [hi dims 0..K-1 | lo dims 0..K-1] (Cfg<K>::RU4 x
+// uint4 per row); thread = (row, group of 8 dims)
 template <int K>
 __global__ void als_pack_kernel(int64_t rows, const float* __restrict__ X, const unsigned* __restrict__ maxbits,
                                 uint4* __restrict__ Xh) {
-    constexpr int D = Cfg<K>::D;
+    constexpr int G = K / 8, RU4 = Cfg<K>::RU4;
     const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q >= rows * 8) return;
-    const int64_t r = q >> 3;
-    const int g = static_cast<int>(q & 7);
+    if (q >= rows * G) return;
+    const int64_t r = q / G;
+    const int c = static_cast<int>(q % G);
     const float s = ldexpf(1.0f, als_scale_exp(*maxbits));
-    const float* x = X + r * K + D * g;
-    uint32_t hw[D / 2], lw[D / 2];
+    const float* x = X + r * K + 8 * c;
+    uint32_t hw[4], lw[4];
 #pragma unroll
-    for (int c = 0; c < D; c += 2) {
-        const float y0 = x[c] * s, y1 = x[c + 1] * s;
+    for (int e = 0; e < 8; e += 2) {
+        const float y0 = x[e] * s, y1 = x[e + 1] * s;
         const __half h0 = __float2half_rn(y0), h1 = __float2half_rn(y1);
-        hw[c / 2] = pack_h2(h0, h1);
-        lw[c / 2] = pack_h2(__float2half_rn(y0 - __half2float(h0)), __float2half_rn(y1 - __half2float(h1)));
+        hw[e / 2] = pack_h2(h0, h1);
+        lw[e / 2] = pack_h2(__float2half_rn(y0 - __half2float(h0)), __float2half_rn(y1 - __half2float(h1)));
     }
-    if constexpr (K == 32) {
-        Xh[r * 8 + g] = make_uint4(hw[0], hw[1], lw[0], lw[1]);
-    } else {
-        Xh[r * 16 + g] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        Xh[r * 16 + 8 + g] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    }
+    Xh[r * RU4 + c] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    Xh[r * RU4 + RU4 / 2 + c] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                              const void* smem_row) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem_row));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(a));
 }
 
 __device__ __forceinline__ float rsqrt_ftz(float x) {
@@ -418,39 +419,19 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
         for (int h = 0; h < 2; ++h) {
             if (h * 16 >= cnt) break;
             const int o0 = h * 16 + 2 * t;
-            // hi / lo words of dims D*g .. D*g+D-1 of rows o0, o0+1, o0+8, o0+9
-            uint32_t hw[4][D / 2], lw[4][D / 2];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int o = o0 + (r & 1) + 8 * (r >> 1);
-                if constexpr (K == 32) {
-                    const uint4 q = st[o * RS + g];
-                    hw[r][0] = q.x;
-                    hw[r][1] = q.y;
-                    lw[r][0] = q.z;
-                    lw[r][1] = q.w;
-                } else {
-                    const uint4 qh = st[o * RS + g], ql = st[o * RS + 8 + g];
-                    hw[r][0] = qh.x;
-                    hw[r][1] = qh.y;
-                    hw[r][2] = qh.z;
-                    hw[r][3] = qh.w;
-                    lw[r][0] = ql.x;
-                    lw[r][1] = ql.y;
-                    lw[r][2] = ql.z;
-                    lw[r][3] = ql.w;
-                }
-            }
-            // B fragments of n-tile j (factor dim D*g + j): {b0, b1} for hi (h) and lo (l);
-            // the A fragment of m-tile i is {B0(2i), B0(2i+1), B1(2i), B1(2i+1)}
+            // B fragments of n-tile j (factor dims 8j..8j+7): b0 = observations 2t, 2t+1, b1 =
+            // 2t+8, 2t+9 (hi / lo) -- the transposing ldmatrix of the 8x8 blocks (8 observation rows
+            // x 16 bytes) hands every lane exactly its pair; the A fragment of m-tile i is
+            // {B0(2i), B0(2i+1), B1(2i), B1(2i+1)}.  Lane l addresses row (l & 7) of block l >> 3 =
+            // (k-half (l>>3) & 1, n-tile j + (l >> 4)).
             uint32_t bh0[D], bh1[D], bl0[D], bl1[D];
+            {
+                const uint4* rowp = st + (h * 16 + 8 * ((lane >> 3) & 1) + (lane & 7)) * RS + (lane >> 4);
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                const uint32_t sel = (j & 1) ? 0x7632u : 0x5410u;
-                bh0[j] = prmt(hw[0][j >> 1], hw[1][j >> 1], sel);
-                bh1[j] = prmt(hw[2][j >> 1], hw[3][j >> 1], sel);
-                bl0[j] = prmt(lw[0][j >> 1], lw[1][j >> 1], sel);
-                bl1[j] = prmt(lw[2][j >> 1], lw[3][j >> 1], sel);
+                for (int j = 0; j < D; j += 2) {
+                    ldsm_x4_trans(bh0[j], bh1[j], bh0[j + 1], bh1[j + 1], rowp + j);
+                    ldsm_x4_trans(bl0[j], bl1[j], bl0[j + 1], bl1[j + 1], rowp + RU4 / 2 + j);
+                }
             }
             // rhs B fragment from the packed (hi, lo) values of observations o0, o0+1 / o0+8, o0+9
             // (ring entries past the chunk are 0)
@@ -479,8 +460,8 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
         if (last_of_seg) {
             // ---- record, assembled in the drained buffer (FUSED single-segment items: in the
             // warp's batch slot), stored with 16-byte coalesced writes.
-            // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) ->
-            // natural dims (pi(M), pi(N)); each unordered pair is owned by exactly one (M >= N) element.
+            // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) = factor
+            // dims (M, N); each unordered pair is owned by exactly one (M >= N) element.
             float* rs_ = fitem >= 0 ? batch + bcount * kRec : reinterpret_cast<float*>(stage + buf * 32 * RS);
 #pragma unroll
             for (int i = 0; i < MT; ++i)
@@ -491,17 +472,15 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
                         const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
                         float& v = acc[i * (i + 1) + j][e];
                         if (M >= N) {
-                            const int a = pi_dim<K>(M), b = pi_dim<K>(N);
-                            const int hi = a > b ? a : b, lo = a > b ? b : a;
-                            rs_[tri_off(hi) + lo] = v * inv_s2;
+                            rs_[tri_off(M) + N] = v * inv_s2;
                         }
                         v = 0.0f;
                     }
-            if (t == 0) {  // lane (g, 0) holds the rhs of dims D*g + 2i (+1)
+            if (t == 0) {  // lane (g, 0) holds the rhs of dims 16i + g and 16i + g + 8
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {
-                    rs_[kRhs + D * g + 2 * i] = (racc[i][0] + racc[i][1]) * inv_sv;
-                    rs_[kRhs + D * g + 2 * i + 1] = (racc[i][2] + racc[i][3]) * inv_sv;
+                    rs_[kRhs + 16 * i + g] = (racc[i][0] + racc[i][1]) * inv_sv;
+                    rs_[kRhs + 16 * i + g + 8] = (racc[i][2] + racc[i][3]) * inv_sv;
                 }
             }
 #pragma unroll
@@ -863,7 +842,7 @@ cudaError_t launch_als_pack(int k, int64_t rows, const float* X, unsigned* maxbi
     if (blocks > sm_count * 8) blocks = sm_count * 8;
     if (blocks < 1) blocks = 1;
     als_absmax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(cnt, X, maxbits);
-    const unsigned pb = static_cast<unsigned>((rows * 8 + 255) / 256);
+    const unsigned pb = static_cast<unsigned>((rows * (k / 8) + 255) / 256);
     if (k == 32) als_pack_kernel<32><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);
     else if (k == 64) als_pack_kernel<64><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);
     else return cudaErrorInvalidValue;
