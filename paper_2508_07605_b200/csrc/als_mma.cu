@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <utility>
 
@@ -46,9 +47,6 @@ constexpr int kWarps = 8;
 __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -756,10 +754,170 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
     }
 }
 
+// OCG_SOLVE_STAGED=1 selects the shared-memory solver at rank 32 too (A/B measurement)
+static bool solve_rows32_off() {
+    static const bool off = [] {
+        const char* e = std::getenv("OCG_SOLVE_STAGED");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
+
+// K4 at rank 32 with register-resident rows: lane (sys = lane & 7, par = lane >> 3)
+// holds rows i = 4m + par (m = 0..7, row m = columns 0..4m+3) of system sys in
+// registers, loaded straight from the record.  Left-looking: at column j the
+// owner of row j (par == j & 3) publishes it through shared memory; every lane
+// reads it once (float4, broadcast over the item's 4 lanes) and updates its rows
+// m >= j/4 with register operands only -- 8 independent chains, no shared-memory
+// operand per FMA.  The rhs is carried as row K by all four lanes (forward
+// substitution folded in, as in solve_staged); the published rows plus 1/L[j][j]
+// then serve the column-oriented back substitution L^T x = y.  Same arithmetic as
+// solve_staged up to the order of the row-dot partial sums.
+__global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, const int32_t* __restrict__ first,
+                                                              const float* __restrict__ rec, float* __restrict__ X,
+                                                              float lambda, const int32_t* __restrict__ list,
+                                                              const int32_t* __restrict__ list_count) {
+    constexpr int K = 32, kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt, kSys = 8;
+    // per-system strides = 4 (mod 32) words: the 8 systems' 16-byte reads at one offset hit
+    // 8 distinct bank groups
+    constexpr int kTri = tri_off(K) + 4, kDiag = K + 1;
+    __shared__ __align__(16) float srow[kSys * kTri];
+    __shared__ float sdiag[kSys * kDiag];
+    const int lane = threadIdx.x, sys = lane & 7, par = lane >> 3;
+    float* S = srow + sys * kTri;
+    float* Rd = sdiag + sys * kDiag;
+    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
+    const int64_t nbatch = (nwork + kSys - 1) / kSys;
+    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+        const int64_t i0 = bt * kSys;
+        const int nb = static_cast<int>(nwork - i0 < kSys ? nwork - i0 : kSys);
+        const bool live = sys < nb;
+        const int64_t w = i0 + (live ? sys : nb - 1);  // dead lanes redo the last system, unstored
+        const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
+        const int64_t slot = first ? static_cast<int64_t>(first[item]) : item;
+        const float* R = rec + slot * kRec;
+        float L[8][K];
+        float y[K];
+        static_for<8>([&](auto mc) {
+            constexpr int m = decltype(mc)::value;
+            const float4* src = reinterpret_cast<const float4*>(R + 4 * (m + 1) * (2 * m + par));
+#pragma unroll
+            for (int c = 0; c <= m; ++c) {
+                const float4 v = __ldg(src + c);
+                L[m][4 * c] = v.x;
+                L[m][4 * c + 1] = v.y;
+                L[m][4 * c + 2] = v.z;
+                L[m][4 * c + 3] = v.w;
+            }
+        });
+#pragma unroll
+        for (int c = 0; c < K / 4; ++c) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(R + kRhs) + c);
+            y[4 * c] = v.x;
+            y[4 * c + 1] = v.y;
+            y[4 * c + 2] = v.z;
+            y[4 * c + 3] = v.w;
+        }
+        const float cnt = R[kCnt];
+        const float diag = lambda * cnt;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+                if (par == p) L[m][4 * m + p] += diag;
+        static_for<K>([&](auto jc) {
+            constexpr int j = decltype(jc)::value, mo = j >> 2;
+            constexpr int tj = tri_off(j);
+            if (par == (j & 3)) {  // publish row j: columns < j final, column j = A_jj
+#pragma unroll
+                for (int c = 0; c <= mo; ++c)
+                    *reinterpret_cast<float4*>(S + tj + 4 * c) =
+                        make_float4(L[mo][4 * c], L[mo][4 * c + 1], L[mo][4 * c + 2], L[mo][4 * c + 3]);
+            }
+            __syncwarp();
+            // rows m >= mo (rows <= j of block mo compute unused entries above the diagonal)
+            float a0[8], a1[8];
+#pragma unroll
+            for (int m = mo; m < 8; ++m) {
+                a0[m] = L[m][j];
+                a1[m] = 0.0f;
+            }
+            float d0 = S[tj + j], d1 = 0.0f, y0 = y[j], y1 = 0.0f;
+#pragma unroll
+            for (int c = 0; 4 * c < j; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(S + tj + 4 * c);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int q = 4 * c + e;
+                    if (q < j) {
+                        if (e & 1) {
+                            d1 = fmaf(-vv[e], vv[e], d1);
+                            y1 = fmaf(-vv[e], y[q], y1);
+                        } else {
+                            d0 = fmaf(-vv[e], vv[e], d0);
+                            y0 = fmaf(-vv[e], y[q], y0);
+                        }
+#pragma unroll
+                        for (int m = mo; m < 8; ++m) {
+                            if (e & 1) a1[m] = fmaf(-L[m][q], vv[e], a1[m]);
+                            else a0[m] = fmaf(-L[m][q], vv[e], a0[m]);
+                        }
+                    }
+                }
+            }
+            const float r = rsqrt_ftz(d0 + d1);
+#pragma unroll
+            for (int m = mo; m < 8; ++m) L[m][j] = (a0[m] + a1[m]) * r;
+            y[j] = (y0 + y1) * r;
+            if (par == 0) Rd[j] = r;
+        });
+        __syncwarp();
+        // L^T x = y, column-oriented over the published rows, all lanes of the item
+        static_for<K>([&](auto qc) {
+            constexpr int q = K - 1 - decltype(qc)::value;
+            const float* Rq = S + tri_off(q);
+            y[q] *= Rd[q];
+#pragma unroll
+            for (int i = 0; i + 4 <= q; i += 4) {
+                const float4 v = *reinterpret_cast<const float4*>(Rq + i);
+                y[i] = fmaf(-v.x, y[q], y[i]);
+                y[i + 1] = fmaf(-v.y, y[q], y[i + 1]);
+                y[i + 2] = fmaf(-v.z, y[q], y[i + 2]);
+                y[i + 3] = fmaf(-v.w, y[q], y[i + 3]);
+            }
+#pragma unroll
+            for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
+        });
+        if (live && par == 0) {
+            float4* xo = reinterpret_cast<float4*>(X + item * K);
+            const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
+#pragma unroll
+            for (int q = 0; q < K / 4; ++q)
+                xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
+                              : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        }
+        __syncwarp();
+    }
+}
+
 template <int K>
 static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
                                   int sm_count, cudaStream_t s, const int32_t* list = nullptr,
                                   const int32_t* list_count = nullptr) {
+    if constexpr (K == 32) {
+        if (!solve_rows32_off()) {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows32_kernel, 32, 0);
+            int64_t blocks = (nitems + 7) / 8;
+            const int64_t cap = static_cast<int64_t>(sm_count) * std::max(per_sm, 1);
+            if (blocks > cap) blocks = cap;
+            if (blocks < 1) blocks = 1;
+            als_solve_rows32_kernel<<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda,
+                                                                                list, list_count);
+            return cudaGetLastError();
+        }
+    }
     constexpr int smem = solve_smem<K>();
     cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int64_t nbatch = (nitems + nsys<K>() - 1) / nsys<K>();
