@@ -225,15 +225,19 @@ constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
 // memory; their records go to a per-warp batch in shared memory and every
 // kSys of them are solved in place by the warp (solve_staged), so the K4 work
 // overlaps the gathers in flight (multi-segment items keep the record path).
-template <int K, bool FUSED>
-__host__ __device__ constexpr int gram_warps() { return FUSED ? 7 : kWarps; }
+// SPLIT (rank 32, column side: long segments, MMA-bound): H^T L accumulated apart
+// on all tiles, 18 instead of 22 MMAs per 16 observations, at 56 more accumulator
+// registers (12 warps per SM instead of 16; the row side's short segments want
+// the occupancy and the cheaper epilogue)
+template <int K, bool FUSED, bool SPLIT = false>
+__host__ __device__ constexpr int gram_warps() { return FUSED ? 7 : (SPLIT ? 6 : kWarps); }
 template <int K, bool FUSED>
 __host__ __device__ constexpr int gram_warp_u4() {
     return Cfg<K>::kStageU4 + (FUSED ? (nsys<K>() * Cfg<K>::kRec) / 4 + 4 : 0);
 }
 
-template <int K, bool FUSED>
-__global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K>::kMinBlocks) als_mma_gram_kernel(
+template <int K, bool FUSED, bool SPLIT>
+__global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 : Cfg<K>::kMinBlocks) als_mma_gram_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
     using C = Cfg<K>;
     constexpr int D = C::D, MT = C::MT, NLT = C::NLT, RU4 = C::RU4, RS = C::RS;
     constexpr int kRec = C::kRec, kRhs = C::kRhs, kCnt = C::kCnt;
-    constexpr int W = gram_warps<K, FUSED>();
+    constexpr int W = gram_warps<K, FUSED, SPLIT>();
     constexpr int kSys = nsys<K>();
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -369,11 +373,18 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
     gather(0, 0, cpos, cend);
     cp_async_commit();
 
-    float acc[NLT][4], racc[MT][4];
+    // SPLIT: H^T L kept apart on all MT x D tiles (14 + 4 MMAs per 16 observations instead of
+    // 18 + 4); rank 64 has no registers for it
+    static_assert(!SPLIT || (K == 32 && !FUSED), "split H^T L: rank 32, record path");
+    constexpr bool kSplitHL = SPLIT;
+    constexpr int NHL = kSplitHL ? MT * D : 1;
+    float acc[NLT][4], racc[MT][4], hl[NHL][4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
 #pragma unroll
         for (int q = 0; q < NLT; ++q) acc[q][e] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < NHL; ++q) hl[q][e] = 0.0f;
 #pragma unroll
         for (int q = 0; q < MT; ++q) racc[q][e] = 0.0f;
     }
@@ -436,16 +447,30 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
             const uint2 ra = *reinterpret_cast<const uint2*>(rs + o0);
             const uint2 rb2 = *reinterpret_cast<const uint2*>(rs + o0 + 8);
             const uint32_t rb0 = prmt(ra.x, ra.y, rsel) & rmask, rb1 = prmt(rb2.x, rb2.y, rsel) & rmask;
-            // G lower tiles (i, j <= 2i+1), tile index i(i+1)+j: H^T H + H^T L + L^T H
+            if constexpr (kSplitHL) {
+                // H^T H on the lower tiles, H^T L on all tiles (L^T H = (H^T L)^T, folded in the epilogue)
 #pragma unroll
-            for (int i = 0; i < MT; ++i)
+                for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int j = 0; j <= 2 * i + 1; ++j) {
-                    float (&a)[4] = acc[i * (i + 1) + j];
-                    mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bh0[j], bh1[j]);
-                    mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bl0[j], bl1[j]);
-                    mma16816(a, bl0[2 * i], bl0[2 * i + 1], bl1[2 * i], bl1[2 * i + 1], bh0[j], bh1[j]);
-                }
+                    for (int j = 0; j < D; ++j) {
+                        if (j <= 2 * i + 1)
+                            mma16816(acc[i * (i + 1) + j], bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1],
+                                     bh0[j], bh1[j]);
+                        mma16816(hl[i * D + j], bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bl0[j],
+                                 bl1[j]);
+                    }
+            } else {
+                // G lower tiles (i, j <= 2i+1), tile index i(i+1)+j: H^T H + H^T L + L^T H
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j <= 2 * i + 1; ++j) {
+                        float (&a)[4] = acc[i * (i + 1) + j];
+                        mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bh0[j], bh1[j]);
+                        mma16816(a, bh0[2 * i], bh0[2 * i + 1], bh1[2 * i], bh1[2 * i + 1], bl0[j], bl1[j]);
+                        mma16816(a, bl0[2 * i], bl0[2 * i + 1], bl1[2 * i], bl1[2 * i + 1], bh0[j], bh1[j]);
+                    }
+            }
             // rhs: (H + L)^T [r_hi r_lo]
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
@@ -470,10 +495,24 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED>() * 32, FUSED ? 1 : Cfg<K
                         const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
                         float& v = acc[i * (i + 1) + j][e];
                         if (M >= N) {
-                            rs_[tri_off(M) + N] = v * inv_s2;
+                            rs_[tri_off(M) + N] = (kSplitHL ? v + hl[i * D + j][e] : v) * inv_s2;
                         }
                         v = 0.0f;
                     }
+            if constexpr (kSplitHL) {  // + (H^T L)(N, M) at (M, N): element (M <= N) of H^T L -> (N, M)
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int M = 16 * i + g + 8 * (e >> 1), N = 8 * j + 2 * t + (e & 1);
+                            float& v = hl[i * D + j][e];
+                            if (M <= N) rs_[tri_off(N) + M] += v * inv_s2;
+                            v = 0.0f;
+                        }
+            }
             if (t == 0) {  // lane (g, 0) holds the rhs of dims 16i + g and 16i + g + 8
 #pragma unroll
                 for (int i = 0; i < MT; ++i) {
@@ -932,18 +971,18 @@ static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const fl
 
 // one tensor-core half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
 // -> per-item Gram records in h.gram_out (mode 1, multi-GPU column side)
-template <int K, bool FUSED>
+template <int K, bool FUSED, bool SPLIT = false>
 static cudaError_t launch_gram_k(const AlsHalf& h, int sm_count, cudaStream_t s) {
-    constexpr int W = gram_warps<K, FUSED>();
+    constexpr int W = gram_warps<K, FUSED, SPLIT>();
     const size_t smem = sizeof(uint4) * W * gram_warp_u4<K, FUSED>();
     int64_t blocks = (h.max_segs + W - 1) / W;
     const int64_t cap = static_cast<int64_t>(sm_count) * (FUSED ? 1 : Cfg<K>::kMinBlocks);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    cudaFuncSetAttribute(als_mma_gram_kernel<K, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(als_mma_gram_kernel<K, FUSED, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     if (h.ev_gram0) cudaEventRecord(h.ev_gram0, s);
-    als_mma_gram_kernel<K, FUSED><<<static_cast<unsigned>(blocks), W * 32, smem, s>>>(
+    als_mma_gram_kernel<K, FUSED, SPLIT><<<static_cast<unsigned>(blocks), W * 32, smem, s>>>(
         h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.idx, h.valh, h.Yh, h.ymax, h.vmax, h.partial,
         h.blk_ctr, h.nseg, h.X, h.lambda);
     const cudaError_t e = cudaGetLastError();
@@ -957,7 +996,9 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     const bool fused = K == 32 && mode == 0 && h.fuse_solve;
-    e = fused ? launch_gram_k<32, true>(h, sm_count, s) : launch_gram_k<K, false>(h, sm_count, s);
+    if (fused) e = launch_gram_k<32, true>(h, sm_count, s);
+    else if (K == 32 && h.seg_order) e = launch_gram_k<32, false, true>(h, sm_count, s);  // column side
+    else e = launch_gram_k<K, false>(h, sm_count, s);
     if (e != cudaSuccess) return e;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
     if (mode == 1) {
