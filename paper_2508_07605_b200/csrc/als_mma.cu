@@ -793,6 +793,12 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
     }
 }
 
+// element i of a row stored as column pairs (i compile-time after unrolling)
+template <int N>
+__device__ __forceinline__ float& el(float2 (&r)[N], int i) {
+    return (i & 1) ? r[i >> 1].y : r[i >> 1].x;
+}
+
 // OCG_SOLVE_STAGED=1 selects the shared-memory solver at rank 32 too (A/B measurement)
 static bool solve_rows32_off() {
     static const bool off = [] {
@@ -819,51 +825,68 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
     constexpr int K = 32, kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt, kSys = 8;
     // per-system strides = 4 (mod 32) words: the 8 systems' 16-byte reads at one offset hit
     // 8 distinct bank groups
-    constexpr int kTri = tri_off(K) + 4, kDiag = K + 1;
+    constexpr int kTri = tri_off(K) + 4, kDiag = K + 1, kTail = 36;  // tail = rhs (32), count, pad
+    static_assert(kRec == kRhs + kTail, "rank-32 record tail");
     __shared__ __align__(16) float srow[kSys * kTri];
     __shared__ float sdiag[kSys * kDiag];
+    __shared__ __align__(16) float stail[kSys * kTail];
     const int lane = threadIdx.x, sys = lane & 7, par = lane >> 3;
     float* S = srow + sys * kTri;
     float* Rd = sdiag + sys * kDiag;
+    float* T = stail + sys * kTail;
     const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
     const int64_t nbatch = (nwork + kSys - 1) / kSys;
-    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
-        const int64_t i0 = bt * kSys;
+    int64_t bt = blockIdx.x;
+    if (bt >= nbatch) return;
+    // Software pipeline over the warp's batches: the next batch's rows are loaded into the L
+    // registers (dead after the factorisation) and its rhs/count tail is copied into shared
+    // memory while the current batch runs its back substitution.
+    constexpr bool kPipe = false;
+    float2 L[8][K / 2];  // column pairs
+    bool live;
+    int64_t item;
+    auto fetch = [&](int64_t b) {  // batch b -> L registers, tail -> T (cp.async)
+        const int64_t i0 = b * kSys;
         const int nb = static_cast<int>(nwork - i0 < kSys ? nwork - i0 : kSys);
-        const bool live = sys < nb;
+        live = sys < nb;
         const int64_t w = i0 + (live ? sys : nb - 1);  // dead lanes redo the last system, unstored
-        const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
+        item = list ? static_cast<int64_t>(list[w]) : w;
         const int64_t slot = first ? static_cast<int64_t>(first[item]) : item;
         const float* R = rec + slot * kRec;
-        float L[8][K];
-        float y[K];
         static_for<8>([&](auto mc) {
             constexpr int m = decltype(mc)::value;
             const float4* src = reinterpret_cast<const float4*>(R + 4 * (m + 1) * (2 * m + par));
 #pragma unroll
             for (int c = 0; c <= m; ++c) {
                 const float4 v = __ldg(src + c);
-                L[m][4 * c] = v.x;
-                L[m][4 * c + 1] = v.y;
-                L[m][4 * c + 2] = v.z;
-                L[m][4 * c + 3] = v.w;
+                L[m][2 * c] = make_float2(v.x, v.y);
+                L[m][2 * c + 1] = make_float2(v.z, v.w);
             }
         });
+        for (int c = par; c < kTail / 4; c += 4) {
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(T + 4 * c));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(R + kRhs + 4 * c) : "memory");
+        }
+        cp_async_commit();
+    };
+    fetch(bt);
+    for (;;) {
+        cp_async_wait<0>();
+        __syncwarp();
+        float2 y[K / 2];
 #pragma unroll
         for (int c = 0; c < K / 4; ++c) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(R + kRhs) + c);
-            y[4 * c] = v.x;
-            y[4 * c + 1] = v.y;
-            y[4 * c + 2] = v.z;
-            y[4 * c + 3] = v.w;
+            const float4 v = *reinterpret_cast<const float4*>(T + 4 * c);
+            y[2 * c] = make_float2(v.x, v.y);
+            y[2 * c + 1] = make_float2(v.z, v.w);
         }
-        const float cnt = R[kCnt];
+        const float cnt = T[kCnt - kRhs];
         const float diag = lambda * cnt;
 #pragma unroll
         for (int m = 0; m < 8; ++m)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                if (par == p) L[m][4 * m + p] += diag;
+                if (par == p) el(L[m], 4 * m + p) += diag;
         static_for<K>([&](auto jc) {
             constexpr int j = decltype(jc)::value, mo = j >> 2;
             constexpr int tj = tri_off(j);
@@ -871,72 +894,77 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
 #pragma unroll
                 for (int c = 0; c <= mo; ++c)
                     *reinterpret_cast<float4*>(S + tj + 4 * c) =
-                        make_float4(L[mo][4 * c], L[mo][4 * c + 1], L[mo][4 * c + 2], L[mo][4 * c + 3]);
+                        make_float4(L[mo][2 * c].x, L[mo][2 * c].y, L[mo][2 * c + 1].x, L[mo][2 * c + 1].y);
             }
             __syncwarp();
-            // rows m >= mo (rows <= j of block mo compute unused entries above the diagonal)
-            float a0[8], a1[8];
+            // rows m >= mo (rows <= j of block mo compute unused entries above the diagonal);
+            // paired FP32 FMAs over column pairs (q, q+1), .x / .y the two partial sums.  Finished
+            // entries are kept NEGATED (N = -L), so every update is a plain FMA:
+            //   -L[i][j] / r = -A[i][j] + sum_q N[i][q] N[j][q],   A_jj - L_jj^2 = A_jj - sum N[j][q]^2,
+            //   y_j / r = b_j + sum_q N[j][q] y_q
+            float2 acc[8];
 #pragma unroll
-            for (int m = mo; m < 8; ++m) {
-                a0[m] = L[m][j];
-                a1[m] = 0.0f;
-            }
-            float d0 = S[tj + j], d1 = 0.0f, y0 = y[j], y1 = 0.0f;
+            for (int m = mo; m < 8; ++m) acc[m] = make_float2(-el(L[m], j), 0.0f);
+            float2 ss = make_float2(0.0f, 0.0f), yy = make_float2(el(y, j), 0.0f);
 #pragma unroll
             for (int c = 0; 4 * c < j; ++c) {
                 const float4 v = *reinterpret_cast<const float4*>(S + tj + 4 * c);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int q = 4 * c + e;
-                    if (q < j) {
-                        if (e & 1) {
-                            d1 = fmaf(-vv[e], vv[e], d1);
-                            y1 = fmaf(-vv[e], y[q], y1);
-                        } else {
-                            d0 = fmaf(-vv[e], vv[e], d0);
-                            y0 = fmaf(-vv[e], y[q], y0);
-                        }
+                for (int h = 0; h < 2; ++h) {
+                    const int p = 2 * c + h;  // column pair (2p, 2p+1)
+                    const float2 nv = h ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
+                    if (2 * p + 1 < j) {
+                        ss = __ffma2_rn(nv, nv, ss);
+                        yy = __ffma2_rn(nv, y[p], yy);
 #pragma unroll
-                        for (int m = mo; m < 8; ++m) {
-                            if (e & 1) a1[m] = fmaf(-L[m][q], vv[e], a1[m]);
-                            else a0[m] = fmaf(-L[m][q], vv[e], a0[m]);
-                        }
+                        for (int m = mo; m < 8; ++m) acc[m] = __ffma2_rn(L[m][p], nv, acc[m]);
+                    } else if (2 * p < j) {  // odd j: the single column j-1
+                        ss.x = fmaf(nv.x, nv.x, ss.x);
+                        yy.x = fmaf(nv.x, y[p].x, yy.x);
+#pragma unroll
+                        for (int m = mo; m < 8; ++m) acc[m].x = fmaf(L[m][p].x, nv.x, acc[m].x);
                     }
                 }
             }
-            const float r = rsqrt_ftz(d0 + d1);
+            const float r = rsqrt_ftz(S[tj + j] - (ss.x + ss.y));
 #pragma unroll
-            for (int m = mo; m < 8; ++m) L[m][j] = (a0[m] + a1[m]) * r;
-            y[j] = (y0 + y1) * r;
+            for (int m = mo; m < 8; ++m) el(L[m], j) = (acc[m].x + acc[m].y) * r;
+            el(y, j) = (yy.x + yy.y) * r;
             if (par == 0) Rd[j] = r;
         });
         __syncwarp();
+        const bool cur_live = live;
+        const int64_t cur_item = item;
+        const int64_t nbt = bt + gridDim.x;
+        if (kPipe && nbt < nbatch) fetch(nbt);  // in flight during the back substitution
         // L^T x = y, column-oriented over the published rows, all lanes of the item
         static_for<K>([&](auto qc) {
             constexpr int q = K - 1 - decltype(qc)::value;
             const float* Rq = S + tri_off(q);
-            y[q] *= Rd[q];
+            el(y, q) *= Rd[q];
+            const float yq = el(y, q);
+            const float2 yq2 = make_float2(yq, yq);
 #pragma unroll
-            for (int i = 0; i + 4 <= q; i += 4) {
+            for (int i = 0; i + 4 <= q; i += 4) {  // y_i -= L[q][i] x_q = y_i + N[q][i] x_q
                 const float4 v = *reinterpret_cast<const float4*>(Rq + i);
-                y[i] = fmaf(-v.x, y[q], y[i]);
-                y[i + 1] = fmaf(-v.y, y[q], y[i + 1]);
-                y[i + 2] = fmaf(-v.z, y[q], y[i + 2]);
-                y[i + 3] = fmaf(-v.w, y[q], y[i + 3]);
+                y[i / 2] = __ffma2_rn(make_float2(v.x, v.y), yq2, y[i / 2]);
+                y[i / 2 + 1] = __ffma2_rn(make_float2(v.z, v.w), yq2, y[i / 2 + 1]);
             }
 #pragma unroll
-            for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
+            for (int i = q & ~3; i < q; ++i) el(y, i) = fmaf(Rq[i], yq, el(y, i));
         });
-        if (live && par == 0) {
-            float4* xo = reinterpret_cast<float4*>(X + item * K);
+        if (cur_live && par == 0) {
+            float4* xo = reinterpret_cast<float4*>(X + cur_item * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
             for (int q = 0; q < K / 4; ++q)
                 xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
-                              : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+                              : make_float4(y[2 * q].x, y[2 * q].y, y[2 * q + 1].x, y[2 * q + 1].y);
         }
         __syncwarp();
+        if (nbt >= nbatch) break;
+        if (!kPipe) fetch(nbt);
+        bt = nbt;
     }
 }
 
