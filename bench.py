@@ -482,7 +482,7 @@ def workload_joint(args, d: Dist):
         g_row = phases[4] / args.steps / args.sweeps
         g_col = phases[5] / args.steps / args.sweeps
         if g_row > 0 and g_col > 0:
-            kern, t_row, t_col = "als_mma_gram32_kernel (K3 Gram accumulation, mma.sync f16 hi/lo)", g_row, g_col
+            kern, t_row, t_col = "als_mma_gram_kernel<32> (K3 Gram accumulation, mma.sync f16 hi/lo)", g_row, g_col
         else:  # rank 8/16: the fused SIMT Gram + solve kernel; whole half-sweeps
             kern, t_row, t_col = "als_seg_gram_kernel (K3 Gram + K4 solve, SIMT)", row_ms, col_ms
         achieved = (row_bytes + col_bytes) / 2 / ((t_row + t_col) / 2 / 1e3) / 1e9

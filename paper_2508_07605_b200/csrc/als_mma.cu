@@ -1,32 +1,30 @@
-// ALS rank-32 half-sweep on B200: K3 Gram accumulation on the tensor cores,
-// K4 batched Cholesky with one system per lane.
+// ALS half-sweep on B200 at ranks 32 and 64: K3 Gram accumulation on the
+// tensor cores, K4 batched Cholesky.
 //
 // Semantics: oracle/ocg_oracle.c ocgo_als_fit (weighted-lambda ALS; no
 // reference counterpart): x_i = (G_i + lambda n_i I)^-1 b_i,
 // G_i = sum_j y_j y_j^T and b_i = sum_j r_ij y_j over item i's observations.
 //
-// K3 als_mma_gram32_kernel: warp per <= kSeg-observation segment.
+// K3 als_mma_gram_kernel<K>: warp per <= kSeg-observation segment.
 // * Factor rows are gathered as FP16 hi/lo pairs written once per half-sweep
 //   by als_pack_kernel: y*s = hi + lo (hi = fp16(y*s), lo = fp16(y*s - hi)),
 //   s = 2^e from the factor matrix's max |y| (y*s <= 2^14, lo stays normal for
-//   every entry that matters).  Packed row = 8 x 16 B, chunk g = {hi[4g..4g+3],
-//   lo[4g..4g+3]}.  Observed values are packed the same way once per plan.
+//   every entry that matters).  Packed row = [hi dims 0..K-1 | lo dims 0..K-1].
+//   Observed values are packed the same way once per plan.
 // * G = H^T H + H^T L + L^T H (L^T L is below 2^-22 relative) with mma.sync
-//   m16n8k16 f16 -> f32 on the 6 lower tiles (in MMA index space) of the
-//   32x32 Gram: a lane loads ONE 16-byte chunk g of four observation rows and
-//   byte-permutes it into the B fragments of all four n-tiles (MMA column
-//   8j+g <-> factor dim 4g+j); the A fragments of the two m-tiles are the same
-//   registers.  rhs: (H + L)^T [r_hi r_lo].  22 MMAs per 16 observations.
-// * Output: one RECORD per segment (als_rec layout below), unscaled FP32,
-//   written straight from the accumulator fragments.
+//   m16n8k16 f16 -> f32 on the lower tiles of the KxK Gram.  The B fragments
+//   come straight from the staged rows by ldmatrix.x4.trans; the A fragments of
+//   the m-tiles are the same registers.  rhs: (H + L)^T [r_hi r_lo].  Rank 32:
+//   22 MMAs per 16 observations, or 18 on the column side (SPLIT: H^T L on all
+//   tiles, its transpose folded in the epilogue).
+// * Output: one RECORD per segment (layout below), unscaled FP32, written from
+//   the accumulator fragments through shared memory with 16-byte stores.
 // Reduce (multi-segment items): records summed in segment order into the
 // item's first slot (deterministic).
-// K4 als_solve_records_kernel: 32 items per warp, ONE ITEM PER LANE: the
-// records are staged in shared memory (row stride 612 floats = 4 mod 32
-// banks, so 16-byte loads of 8 lanes at the same offset are conflict-free)
-// and each lane runs a left-looking Cholesky + two substitutions on its own
-// system -- no idle lanes, no shuffles (a lane-per-row Cholesky wastes 2/3 of
-// its FMAs on the upper triangle and serialises 64 shuffles per system).
+// K4: rank 32 als_solve_rows32_kernel (register-resident rows, 4 lanes per
+// system, paired FP32 FMAs); rank 64 als_solve_records_kernel (records staged
+// in shared memory, 8 lanes per system).  Left-looking Cholesky with the rhs
+// carried as an extra row (forward substitution folded in), then L^T x = y.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 

@@ -11,7 +11,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"als_mma_gram" -c 2 -f \
     -o gpurun_out/c2_gram python bench.py --steps 1 --warmup 0 --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"als_solve_records" -c 1 -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"als_solve" -c 1 -f \
     -o gpurun_out/c2_solve python bench.py --steps 1 --warmup 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"als_select" -c 1 -f \
     -o gpurun_out/c2_select python bench.py --steps 1 --warmup 0 --no-cpu-baseline > /dev/null 2>&1
