@@ -572,9 +572,60 @@ __global__ void als_pack_vals_kernel(int64_t n, const float* __restrict__ val, c
     out[q] = pack_h2(h, __float2half_rn(y - __half2float(h)));
 }
 
-// Sum each multi-segment item's segment records in segment order.  list ==
-// nullptr: every item, result to out[item] (multi-GPU Gram records); else the
-// listed items, result to rec[first[item]] in place.
+// Sum each multi-segment item's segment records, in two levels so that a very
+// long item (e.g. the always-profiled baseline column: ~1000 segments at C2) is
+// not one block's serial chain: level 1 sums each group of kRG consecutive
+// records in order into the group's first slot (blocks (x, y) take items x mod
+// gridDim.x and groups y mod gridDim.y); level 2 sums an item's group partials
+// in order.  list == nullptr: every item, result to out[item] (multi-GPU Gram
+// records); else the listed items, result to rec[first[item]] in place.  The
+// order is fixed, so the result is deterministic.
+constexpr int kRG = 16;
+template <int K>
+__device__ __forceinline__ float4 sum_records(const float4* src, int32_t n, int64_t stride4) {
+    float4 s = src[0];
+    int32_t q = 1;
+    for (; q + 4 <= n; q += 4) {  // four loads in flight; the sum order stays q = 0, 1, 2, ...
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = src[static_cast<int64_t>(q + u) * stride4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            s.x += v[u].x;
+            s.y += v[u].y;
+            s.z += v[u].z;
+            s.w += v[u].w;
+        }
+    }
+    for (; q < n; ++q) {
+        const float4 v = src[static_cast<int64_t>(q) * stride4];
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+    }
+    return s;
+}
+template <int K>
+__global__ void __launch_bounds__(160) als_reduce_groups_kernel(int64_t nitems, const int32_t* __restrict__ list,
+                                                                const int32_t* __restrict__ list_count,
+                                                                const int32_t* __restrict__ nseg_of,
+                                                                const int32_t* __restrict__ first,
+                                                                float* __restrict__ rec) {
+    constexpr int kRec = Cfg<K>::kRec;
+    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
+        const int32_t ns = nseg_of[item];
+        if (ns < 2) continue;
+        for (int32_t gq = blockIdx.y; gq * kRG < ns; gq += gridDim.y) {
+            const int32_t n = min(kRG, ns - gq * kRG);
+            if (n < 2) continue;
+            float4* base = reinterpret_cast<float4*>(rec + (static_cast<int64_t>(first[item]) + gq * kRG) * kRec);
+            for (int c = threadIdx.x; c < kRec / 4; c += blockDim.x) base[c] = sum_records<K>(base + c, n, kRec / 4);
+        }
+    }
+}
 template <int K>
 __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems, const int32_t* __restrict__ list,
                                                                  const int32_t* __restrict__ list_count,
@@ -585,30 +636,11 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
     const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
     for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
         const int64_t item = list ? static_cast<int64_t>(list[w]) : w;
-        const int32_t ns = nseg_of[item];
+        const int32_t ng = (nseg_of[item] + kRG - 1) / kRG;
+        if (list && ng < 2) continue;  // in place: level 1 already left the sum in the first slot
         for (int c = threadIdx.x; c < kRec / 4; c += blockDim.x) {  // float4 chunk of the record
             const float4* src = reinterpret_cast<const float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c;
-            float4 s = src[0];
-            int32_t q = 1;
-            for (; q + 4 <= ns; q += 4) {  // four loads in flight; the sum order stays q = 0, 1, 2, ...
-                float4 v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = src[static_cast<int64_t>(q + u) * (kRec / 4)];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    s.x += v[u].x;
-                    s.y += v[u].y;
-                    s.z += v[u].z;
-                    s.w += v[u].w;
-                }
-            }
-            for (; q < ns; ++q) {
-                const float4 v = src[static_cast<int64_t>(q) * (kRec / 4)];
-                s.x += v.x;
-                s.y += v.y;
-                s.z += v.z;
-                s.w += v.w;
-            }
+            const float4 s = sum_records<K>(src, ng, static_cast<int64_t>(kRG) * (kRec / 4));
             float4* dst = list ? reinterpret_cast<float4*>(rec + static_cast<int64_t>(first[item]) * kRec) + c
                                : reinterpret_cast<float4*>(out + item * kRec) + c;
             *dst = s;
@@ -1027,11 +1059,15 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     else e = launch_gram_k<K, false>(h, sm_count, s);
     if (e != cudaSuccess) return e;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
+    const dim3 gblocks(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 2))), 32);
     if (mode == 1) {
+        als_reduce_groups_kernel<K><<<gblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial);
         als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
                                                              h.gram_out);
         return cudaGetLastError();
     }
+    als_reduce_groups_kernel<K><<<gblocks, 160, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.nseg, h.first,
+                                                        h.partial);
     als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, h.multi_list, h.multi_count, h.nseg, h.first,
                                                          h.partial, nullptr);
     e = cudaGetLastError();
