@@ -21,7 +21,7 @@
 //   the accumulator fragments through shared memory with 16-byte stores.
 // Reduce (multi-segment items): records summed in segment order into the
 // item's first slot (deterministic).
-// K4: rank 32 als_solve_rows32_kernel (register-resident rows, 4 lanes per
+// K4: als_solve_rows_kernel<K> (register-resident rows, 4 / 16 lanes per
 // system, paired FP32 FMAs); rank 64 als_solve_records_kernel (records staged
 // in shared memory, 8 lanes per system).  Left-looking Cholesky with the rhs
 // carried as an extra row (forward substitution folded in), then L^T x = y.
@@ -823,14 +823,18 @@ __global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, c
     }
 }
 
+// register-row K4: lanes per system (rank 32: 4 lanes x 8 rows, rank 64: 16 lanes x 4 rows)
+template <int K>
+__host__ __device__ constexpr int rows_lps() { return K == 32 ? 4 : 16; }
+
 // element i of a row stored as column pairs (i compile-time after unrolling)
 template <int N>
 __device__ __forceinline__ float& el(float2 (&r)[N], int i) {
     return (i & 1) ? r[i >> 1].y : r[i >> 1].x;
 }
 
-// OCG_SOLVE_STAGED=1 selects the shared-memory solver at rank 32 too (A/B measurement)
-static bool solve_rows32_off() {
+// OCG_SOLVE_STAGED=1 selects the shared-memory solver (A/B measurement)
+static bool solve_rows_off() {
     static const bool off = [] {
         const char* e = std::getenv("OCG_SOLVE_STAGED");
         return e && e[0] == '1';
@@ -848,19 +852,21 @@ static bool solve_rows32_off() {
 // substitution folded in, as in solve_staged); the published rows plus 1/L[j][j]
 // then serve the column-oriented back substitution L^T x = y.  Same arithmetic as
 // solve_staged up to the order of the row-dot partial sums.
-__global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, const int32_t* __restrict__ first,
-                                                              const float* __restrict__ rec, float* __restrict__ X,
-                                                              float lambda, const int32_t* __restrict__ list,
-                                                              const int32_t* __restrict__ list_count) {
-    constexpr int K = 32, kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt, kSys = 8;
+template <int K>
+__global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, const int32_t* __restrict__ first,
+                                                            const float* __restrict__ rec, float* __restrict__ X,
+                                                            float lambda, const int32_t* __restrict__ list,
+                                                            const int32_t* __restrict__ list_count) {
+    constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
+    constexpr int LPS = rows_lps<K>(), kSys = 32 / LPS, R = K / LPS;  // lanes per system, systems, rows per lane
     // per-system strides = 4 (mod 32) words: the 8 systems' 16-byte reads at one offset hit
     // 8 distinct bank groups
-    constexpr int kTri = tri_off(K) + 4, kDiag = K + 1, kTail = 36;  // tail = rhs (32), count, pad
-    static_assert(kRec == kRhs + kTail, "rank-32 record tail");
+    constexpr int kTri = tri_off(K) + 4, kDiag = K + 1, kTail = kRec - kRhs;  // tail = rhs, count, pad
+    static_assert(kTail % 4 == 0 && kTri % 32 == 4, "record tail / bank stride");
     __shared__ __align__(16) float srow[kSys * kTri];
     __shared__ float sdiag[kSys * kDiag];
     __shared__ __align__(16) float stail[kSys * kTail];
-    const int lane = threadIdx.x, sys = lane & 7, par = lane >> 3;
+    const int lane = threadIdx.x, sys = lane % kSys, par = lane / kSys;
     float* S = srow + sys * kTri;
     float* Rd = sdiag + sys * kDiag;
     float* T = stail + sys * kTail;
@@ -872,7 +878,7 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
     // registers (dead after the factorisation) and its rhs/count tail is copied into shared
     // memory while the current batch runs its back substitution.
     constexpr bool kPipe = false;
-    float2 L[8][K / 2];  // column pairs
+    float2 L[R][K / 2];  // column pairs; row m = LPS m + par uses (m + 1) LPS columns
     bool live;
     int64_t item;
     auto fetch = [&](int64_t b) {  // batch b -> L registers, tail -> T (cp.async)
@@ -882,20 +888,22 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
         const int64_t w = i0 + (live ? sys : nb - 1);  // dead lanes redo the last system, unstored
         item = list ? static_cast<int64_t>(list[w]) : w;
         const int64_t slot = first ? static_cast<int64_t>(first[item]) : item;
-        const float* R = rec + slot * kRec;
-        static_for<8>([&](auto mc) {
+        const float* Rp = rec + slot * kRec;
+        static_for<R>([&](auto mc) {
             constexpr int m = decltype(mc)::value;
-            const float4* src = reinterpret_cast<const float4*>(R + 4 * (m + 1) * (2 * m + par));
+            // (rank 64: past a row's padded length the loads read the next rows -- entries
+            // above the diagonal, never used; the last row ends at the rhs)
+            const float4* src = reinterpret_cast<const float4*>(Rp + tri_off(LPS * m + par));
 #pragma unroll
-            for (int c = 0; c <= m; ++c) {
+            for (int c = 0; c < (m + 1) * LPS / 4; ++c) {
                 const float4 v = __ldg(src + c);
                 L[m][2 * c] = make_float2(v.x, v.y);
                 L[m][2 * c + 1] = make_float2(v.z, v.w);
             }
         });
-        for (int c = par; c < kTail / 4; c += 4) {
+        for (int c = par; c < kTail / 4; c += LPS) {
             const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(T + 4 * c));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(R + kRhs + 4 * c) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Rp + kRhs + 4 * c) : "memory");
         }
         cp_async_commit();
     };
@@ -913,16 +921,16 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
         const float cnt = T[kCnt - kRhs];
         const float diag = lambda * cnt;
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+        for (int m = 0; m < R; ++m)
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
-                if (par == p) el(L[m], 4 * m + p) += diag;
+            for (int p = 0; p < LPS; ++p)
+                if (par == p) el(L[m], LPS * m + p) += diag;
         static_for<K>([&](auto jc) {
-            constexpr int j = decltype(jc)::value, mo = j >> 2;
+            constexpr int j = decltype(jc)::value, mo = j / LPS;
             constexpr int tj = tri_off(j);
-            if (par == (j & 3)) {  // publish row j: columns < j final, column j = A_jj
+            if (par == j % LPS) {  // publish row j: columns < j final, column j = A_jj
 #pragma unroll
-                for (int c = 0; c <= mo; ++c)
+                for (int c = 0; c <= j / 4; ++c)
                     *reinterpret_cast<float4*>(S + tj + 4 * c) =
                         make_float4(L[mo][2 * c].x, L[mo][2 * c].y, L[mo][2 * c + 1].x, L[mo][2 * c + 1].y);
             }
@@ -932,9 +940,9 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
             // entries are kept NEGATED (N = -L), so every update is a plain FMA:
             //   -L[i][j] / r = -A[i][j] + sum_q N[i][q] N[j][q],   A_jj - L_jj^2 = A_jj - sum N[j][q]^2,
             //   y_j / r = b_j + sum_q N[j][q] y_q
-            float2 acc[8];
+            float2 acc[R];
 #pragma unroll
-            for (int m = mo; m < 8; ++m) acc[m] = make_float2(-el(L[m], j), 0.0f);
+            for (int m = mo; m < R; ++m) acc[m] = make_float2(-el(L[m], j), 0.0f);
             float2 ss = make_float2(0.0f, 0.0f), yy = make_float2(el(y, j), 0.0f);
 #pragma unroll
             for (int c = 0; 4 * c < j; ++c) {
@@ -947,18 +955,18 @@ __global__ void __launch_bounds__(32) als_solve_rows32_kernel(int64_t nitems, co
                         ss = __ffma2_rn(nv, nv, ss);
                         yy = __ffma2_rn(nv, y[p], yy);
 #pragma unroll
-                        for (int m = mo; m < 8; ++m) acc[m] = __ffma2_rn(L[m][p], nv, acc[m]);
+                        for (int m = mo; m < R; ++m) acc[m] = __ffma2_rn(L[m][p], nv, acc[m]);
                     } else if (2 * p < j) {  // odd j: the single column j-1
                         ss.x = fmaf(nv.x, nv.x, ss.x);
                         yy.x = fmaf(nv.x, y[p].x, yy.x);
 #pragma unroll
-                        for (int m = mo; m < 8; ++m) acc[m].x = fmaf(L[m][p].x, nv.x, acc[m].x);
+                        for (int m = mo; m < R; ++m) acc[m].x = fmaf(L[m][p].x, nv.x, acc[m].x);
                     }
                 }
             }
             const float r = rsqrt_ftz(S[tj + j] - (ss.x + ss.y));
 #pragma unroll
-            for (int m = mo; m < 8; ++m) el(L[m], j) = (acc[m].x + acc[m].y) * r;
+            for (int m = mo; m < R; ++m) el(L[m], j) = (acc[m].x + acc[m].y) * r;
             el(y, j) = (yy.x + yy.y) * r;
             if (par == 0) Rd[j] = r;
         });
@@ -1002,18 +1010,17 @@ template <int K>
 static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
                                   int sm_count, cudaStream_t s, const int32_t* list = nullptr,
                                   const int32_t* list_count = nullptr) {
-    if constexpr (K == 32) {
-        if (!solve_rows32_off()) {
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows32_kernel, 32, 0);
-            int64_t blocks = (nitems + 7) / 8;
-            const int64_t cap = static_cast<int64_t>(sm_count) * std::max(per_sm, 1);
-            if (blocks > cap) blocks = cap;
-            if (blocks < 1) blocks = 1;
-            als_solve_rows32_kernel<<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda,
-                                                                                list, list_count);
-            return cudaGetLastError();
-        }
+    if (!solve_rows_off()) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows_kernel<K>, 32, 0);
+        constexpr int kSys = 32 / rows_lps<K>();
+        int64_t blocks = (nitems + kSys - 1) / kSys;
+        const int64_t cap = static_cast<int64_t>(sm_count) * std::max(per_sm, 1);
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        als_solve_rows_kernel<K><<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda, list,
+                                                                              list_count);
+        return cudaGetLastError();
     }
     constexpr int smem = solve_smem<K>();
     cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
