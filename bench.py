@@ -505,12 +505,13 @@ def workload_joint(args, d: Dist):
 
 def workload_c4(args, d: Dist):
     """streaming online phase on the C2 matrix.  Each arrival batch adds one
-    new observation to 1% of the rows (paper_2508_07605_b200.stream); a refit = upload of the
-    new CSR from pinned host memory + full completion + selection from scratch (reference
-    semantics) + decisions read back.  Reported: latency per refit (wall clock, the refit
-    is synchronous), as cells/s, and the warm-start latency (2 sweeps from the previous
-    factors: a flagged deviation) at N=1.  N>1: each rank refits its row shard with the
-    sharded schedule."""
+    new observation to 1% of the rows (paper_2508_07605_b200.stream), on top of the previous
+    batches; a refit = the new cells merged into the device CSR (ocg_als_plan_add_observations:
+    only the new cells cross PCIe, from pinned host memory) + full completion + selection from
+    scratch (reference semantics) + decisions read back.  Reported: latency per refit (wall
+    clock, the refit is synchronous), as cells/s, and the warm-start latency (2 sweeps from the
+    previous factors: a flagged deviation) at N=1.  N>1: each rank refits its row shard with
+    the sharded schedule (arrivals in its own rows)."""
     import torch
 
     import paper_2508_07605_b200 as ocg
@@ -523,17 +524,26 @@ def workload_c4(args, d: Dist):
     ctx = ocg.Context(d.local)
     dev = torch.device("cuda", d.local)
     hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
-    batches = [add_observations(A, grid, frac=0.01, seed=1000 * d.rank + b) for b in (1, 2)]
-    pins = [[torch.from_numpy(x).pin_memory() for x in (B.row_ptr, B.col, B.val)] for B in batches]
+    nref = args.warmup + args.steps + (1 + args.steps if d.world == 1 else 0)
+    deltas, B = [], A
+    for b in range(nref):  # the arrival stream, prepared on the host before timing
+        B, dl = add_observations(B, grid, frac=0.01, seed=1000 * d.rank + b + 1, return_delta=True)
+        deltas.append([torch.from_numpy(x).pin_memory() for x in dl])
     plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, args.gamma, ctx=ctx)
+    lib = ocg._lib.lib
+    res_pin = [torch.empty(A.m, dtype=dt).pin_memory() for dt in (torch.int32, torch.float64, torch.float64,
+                                                                   torch.int32)]
 
     def refit(b):
-        plan.upload(*(int(x.data_ptr()) for x in pins[b % 2]))
+        r_, c_, v_ = deltas[b]
+        ocg._lib.check(lib.ocg_als_plan_add_observations(plan._h, r_.numel(), r_.data_ptr(), c_.data_ptr(),
+                                                         v_.data_ptr()))
         if d.world == 1:
             plan.run(timed=False)
         else:
             ShardedAlsDriver(GpuAlsBackend(plan, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
-        return plan.results()
+        plan.results(out=[int(x.data_ptr()) for x in res_pin])  # decisions into pinned host memory
+        return res_pin
 
     def timed(nsteps, base):
         ts = []
@@ -550,27 +560,27 @@ def workload_c4(args, d: Dist):
         refit(b)
     with Clocks(d.local) as clk:
         ts, r = timed(args.steps, args.warmup)
-    assert (r[0] >= 0).all()
+    base = args.warmup + args.steps
+    assert bool((r[0] >= 0).all())
     lat = statistics.median(ts)
     out = {"metric": "CF-completed matrix cells/sec", "value": m * n / lat, "unit": "cells/s",
            "ms_per_step": lat * 1e3, "scaling": "strong", "dtype": "f32 factors / f64 selection",
            "refit_latency_ms": {"from_scratch_median": lat * 1e3, "all": [t * 1e3 for t in ts]},
            "selections_per_sec": m / lat,
            "e2e": {"value": m * n / lat, "unit": "cells/s",
-                   "h2d_bytes_per_step": int(sum(x.nbytes for x in (batches[0].row_ptr, batches[0].col,
-                                                                   batches[0].val))) * d.world,
-                   "d2h_bytes_per_step": int(sum(x.nbytes for x in r)) * d.world},
+                   "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in deltas[0])) * d.world,
+                   "d2h_bytes_per_step": int(sum(x.numel() * x.element_size() for x in r)) * d.world},
            "config": {"workload": "c4", "apps": m, "settings": n, "rank": cfg["rank"],
-                      "arrivals": "1 new observation in each of 1% of rows per refit",
-                      "observed_per_gpu": batches[0].nnz, "sweeps": args.sweeps,
+                      "arrivals": "1 new observation in each of 1% of rows per refit, cumulative",
+                      "observed_per_gpu": A.nnz, "sweeps": args.sweeps,
                       "parallelism": f"rows sharded over {d.world} GPU(s)" if d.world > 1 else "1 GPU",
-                      "timing": "wall clock per synchronous refit (upload + run + readback), max over ranks, "
-                                "L2 flushed before each"},
+                      "timing": "wall clock per synchronous refit (new cells H2D + device CSR merge + run + "
+                                "readback), max over ranks, L2 flushed before each"},
            "gpu_launches": args.steps * (16 + args.sweeps * 4 + 2), "clocks": clk.summary()}
     if d.world == 1:  # warm refits: a flagged deviation from the reference's from-scratch cf::complete
         plan.set_warm(2)
-        refit(0)
-        tw, _ = timed(args.steps, 1)
+        refit(base)
+        tw, _ = timed(args.steps, base + 1)
         plan.set_warm(0)
         out["refit_latency_ms"]["warm_2_sweeps_median"] = statistics.median(tw) * 1e3
         out["refit_latency_ms"]["warm_note"] = ("deviation: starts from the previous factors with 2 sweeps "

@@ -201,6 +201,13 @@ int ocg_als_plan_upload(ocg_als_plan* plan, const int64_t* row_ptr, const int32_
 /* the same with 16-bit column indices (n <= 65536: every grid of the paper and
  * of C1-C4), widened on the device: 25% fewer bytes over PCIe per refit */
 int ocg_als_plan_upload_compact(ocg_als_plan* plan, const int64_t* row_ptr, const uint16_t* col16, const float* val);
+/* streaming arrivals: merge `count` new observed cells (host
+ * arrays sorted by (row, col); cells not observed yet) into the plan's device CSR
+ * -- the same matrix as uploading the merged CSR, with only the new cells crossing
+ * PCIe.  OCG_E_INVALID for unsorted / out-of-range / already observed cells (the
+ * plan is left unchanged).  Synchronises the context stream. */
+int ocg_als_plan_add_observations(ocg_als_plan* plan, int64_t count, const int32_t* rows, const int32_t* cols,
+                                  const float* vals);
 /* warm refits (a flagged deviation from the reference's from-scratch cf::complete):
  * warm_sweeps > 0 makes every later _run after the first start from the previous
  * factors (no V initialisation) and run warm_sweeps sweeps; 0 restores from-scratch. */

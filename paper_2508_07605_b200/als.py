@@ -72,6 +72,16 @@ class AlsPlan:
             args = tuple(ptr(a) for a in self._keep)
         check(lib.ocg_als_plan_upload_compact(self._h, *args))
 
+    def add_observations(self, rows, cols, vals):
+        """Merge new observed cells (sorted by (row, col), not observed yet) into the device
+        CSR; only these cells cross PCIe.  Same matrix as upload() of the merged CSR."""
+        r = np.ascontiguousarray(rows, np.int32)
+        c = np.ascontiguousarray(cols, np.int32)
+        v = np.ascontiguousarray(vals, np.float32)
+        if not (len(r) == len(c) == len(v)):
+            raise ValueError("rows/cols/vals lengths differ")
+        check(lib.ocg_als_plan_add_observations(self._h, len(r), ptr(r), ptr(c), ptr(v)))
+
     def set_warm(self, sweeps: int):
         """Warm refits (deviation from from-scratch semantics): later runs start from the
         previous factors and run ``sweeps`` sweeps; 0 = from scratch."""

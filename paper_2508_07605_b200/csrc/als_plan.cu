@@ -101,6 +101,19 @@ struct ocg_als_plan {
     Buf<unsigned> maxbits;
     Buf<uint32_t> valh;
     Buf<uint4> Vsel;  // V in the tensor-core selection layout
+    // capacities: nnz_cap sizes every nnz-dependent buffer (als_alloc), col_cap the CSR arrays;
+    // both grow with headroom, so streaming arrivals rarely reallocate.  col_alt/val_alt/rp_alt:
+    // the merge target of ocg_als_plan_add_observations (swapped with col/val/row_ptr)
+    int64_t nnz_cap = 0, col_cap = 0, alt_cap = 0;
+    Buf<int32_t> col_alt;
+    Buf<float> val_alt;
+    Buf<int64_t> rp_alt;
+    // add_observations scratch (kept: no allocation per arrival batch)
+    Buf<int32_t> add_rc, add_inc, add_ex, add_err;
+    Buf<float> add_v;
+    Buf<uint8_t> add_tmp;
+    int64_t add_cap = 0;
+    size_t add_tmp_bytes = 0;
     Buf<uint16_t> col16;  // staging of ocg_als_plan_upload_compact
     int64_t col16_cap = 0;  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
@@ -195,21 +208,23 @@ static int als_pack(ocg_als_plan* P, int sd) {
 
 // buffers whose size depends on nnz (reallocated when an upload changes it)
 static int als_alloc(ocg_als_plan* P) {
+    P->nnz_cap = std::max(P->nnz, P->nnz_cap);
+    const int64_t cap = P->nnz_cap;
     ALS_CUDA(P->col_ptr.alloc(static_cast<size_t>(P->n + 1)));
-    ALS_CUDA(P->crow.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->cval.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->keys_out.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->pairs_in.alloc(static_cast<size_t>(P->nnz)));
-    ALS_CUDA(P->pairs_out.alloc(static_cast<size_t>(P->nnz)));
+    ALS_CUDA(P->crow.alloc(static_cast<size_t>(cap)));
+    ALS_CUDA(P->cval.alloc(static_cast<size_t>(cap)));
+    ALS_CUDA(P->keys_out.alloc(static_cast<size_t>(cap)));
+    ALS_CUDA(P->pairs_in.alloc(static_cast<size_t>(cap)));
+    ALS_CUDA(P->pairs_out.alloc(static_cast<size_t>(cap)));
     size_t bytes = 0;
     ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P->col.p, P->keys_out.p, P->pairs_in.p, P->pairs_out.p,
-                                             P->nnz, 0, bits_for(P->n)));
+                                             cap, 0, bits_for(P->n)));
     P->sort_tmp_bytes = bytes;
     ALS_CUDA(P->sort_tmp.alloc(bytes));
     for (int sd = 0; sd < 2; ++sd) {
         auto& S = P->side[sd];
         const int64_t items = sd == 0 ? P->m : P->n;
-        const int64_t ms = items + P->nnz / ocg::kSeg + 1;
+        const int64_t ms = items + cap / ocg::kSeg + 1;
         if (ms >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_UNSUPPORTED, "als: too many segments");
         S.max_segs = static_cast<int32_t>(ms);
         ALS_CUDA(S.nseg.alloc(static_cast<size_t>(items)));
@@ -232,7 +247,7 @@ static int als_alloc(ocg_als_plan* P) {
         // partial Grams only for items with >1 segment: sum of their nseg <= 2*nnz/kSeg
         // (the column side may also run in MODE 1 — every segment keeps a slot)
         // (rank 32: every segment writes a record, slot = segment id)
-        const int64_t mp = (sd == 1 || mma_rank(P->k)) ? ms : std::min<int64_t>(ms, 2 * (P->nnz / ocg::kSeg) + 2);
+        const int64_t mp = (sd == 1 || mma_rank(P->k)) ? ms : std::min<int64_t>(ms, 2 * (cap / ocg::kSeg) + 2);
         ALS_CUDA(S.nmulti.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.pfirst.alloc(static_cast<size_t>(items)));
         ALS_CUDA(S.partial.alloc(static_cast<size_t>(mp) * ocg::als_gram_record_floats(P->k)));
@@ -241,7 +256,7 @@ static int als_alloc(ocg_als_plan* P) {
         P->scan_tmp_bytes = std::max(P->scan_tmp_bytes, b);
     }
     ALS_CUDA(P->scan_tmp.alloc(P->scan_tmp_bytes));
-    if (mma_rank(P->k)) ALS_CUDA(P->valh.alloc(static_cast<size_t>(P->nnz)));
+    if (mma_rank(P->k)) ALS_CUDA(P->valh.alloc(static_cast<size_t>(cap)));
     return OCG_OK;
 }
 
@@ -312,6 +327,7 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
         P->val.own = false;
     } else {
         P->nnz = row_ptr[m];
+        P->col_cap = P->nnz;
         ALS_CUDA(P->row_ptr.alloc(static_cast<size_t>(m + 1)));
         ALS_CUDA(P->col.alloc(static_cast<size_t>(P->nnz)));
         ALS_CUDA(P->val.alloc(static_cast<size_t>(P->nnz)));
@@ -335,18 +351,34 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     return OCG_OK;
 }
 
+static int64_t grow_cap(int64_t n) { return n + n / 16 + 4096; }
+
+// P->nnz = nnz; CSR arrays and nnz-dependent state grow (with headroom) only past their capacity
+static int als_set_nnz(ocg_als_plan* P, int64_t nnz) {
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    if (nnz > P->col_cap) {
+        ALS_CUDA(cudaStreamSynchronize(s));
+        P->col_cap = grow_cap(nnz);
+        ALS_CUDA(P->col.alloc(static_cast<size_t>(P->col_cap)));
+        ALS_CUDA(P->val.alloc(static_cast<size_t>(P->col_cap)));
+    }
+    P->nnz = nnz;
+    if (nnz > P->nnz_cap) {
+        ALS_CUDA(cudaStreamSynchronize(s));
+        P->nnz_cap = grow_cap(nnz);
+        return als_alloc(P);
+    }
+    return OCG_OK;
+}
+
 int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* col, const float* val) {
     if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
-    if (nnz != P->nnz) {  // new observations: nnz-dependent device state is rebuilt (factors survive)
-        ALS_CUDA(cudaStreamSynchronize(s));
-        P->nnz = nnz;
-        ALS_CUDA(P->col.alloc(static_cast<size_t>(nnz)));
-        ALS_CUDA(P->val.alloc(static_cast<size_t>(nnz)));
-        int rc = als_alloc(P);
+    {  // new observations: nnz-dependent device state grows when needed (factors survive)
+        int rc = als_set_nnz(P, nnz);
         if (rc) return rc;
     }
     ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
@@ -366,6 +398,56 @@ __global__ void widen_u16_kernel(int64_t n, const uint16_t* __restrict__ in, int
 }
 }  // namespace
 
+namespace {
+
+// ---- streaming arrivals: merge new observations into the device CSR
+// per-row insertion counts (additions sorted by (row, col))
+__global__ void add_count_kernel(int64_t count, const int32_t* __restrict__ arow, int32_t* __restrict__ inc) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < count) atomicAdd(inc + arow[t], 1);
+}
+// warp per row: the row's old entries shift by the additions before them (earlier rows:
+// ex[r]; this row: those with a smaller column), each addition lands after the old
+// entries with a smaller column; an addition on an observed cell sets *err
+__global__ void add_merge_kernel(int64_t m, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const float* __restrict__ val, const int32_t* __restrict__ inc,
+                                 const int32_t* __restrict__ ex, const int32_t* __restrict__ acol,
+                                 const float* __restrict__ aval, int64_t* __restrict__ rp2, int32_t* __restrict__ col2,
+                                 float* __restrict__ val2, int32_t* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < m; r += nw) {
+        const int64_t b = rp[r], e = rp[r + 1];
+        const int32_t na = inc[r], a0 = ex[r];
+        const int64_t b2 = b + a0;
+        if (lane == 0) {
+            rp2[r] = b2;
+            if (r == m - 1) rp2[m] = e + a0 + na;
+        }
+        for (int64_t q = b + lane; q < e; q += 32) {
+            const int32_t c = col[q];
+            int32_t sh = 0;
+            for (int32_t t = 0; t < na; ++t) sh += acol[a0 + t] < c;
+            col2[b2 + (q - b) + sh] = c;
+            val2[b2 + (q - b) + sh] = val[q];
+        }
+        for (int32_t t = lane; t < na; t += 32) {
+            const int32_t c = acol[a0 + t];
+            int64_t lo = b, hi = e;  // first old entry with col >= c
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (col[mid] < c) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo < e && col[lo] == c) atomicExch(err, 1);
+            col2[b2 + (lo - b) + t] = c;
+            val2[b2 + (lo - b) + t] = aval[a0 + t];
+        }
+    }
+}
+
+}  // namespace
+
 int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const uint16_t* col16, const float* val) {
     if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als upload_compact: more than 65536 settings");
@@ -373,12 +455,8 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
-    if (nnz != P->nnz) {
-        ALS_CUDA(cudaStreamSynchronize(s));
-        P->nnz = nnz;
-        ALS_CUDA(P->col.alloc(static_cast<size_t>(nnz)));
-        ALS_CUDA(P->val.alloc(static_cast<size_t>(nnz)));
-        int rc = als_alloc(P);
+    {  // new observations: nnz-dependent device state grows when needed (factors survive)
+        int rc = als_set_nnz(P, nnz);
         if (rc) return rc;
     }
     if (P->col16_cap < nnz) {
@@ -394,6 +472,79 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
     }
     if (mma_rank(P->k)) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
+        ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
+    }
+    return OCG_OK;
+}
+
+int ocg_als_plan_add_observations(ocg_als_plan* P, int64_t count, const int32_t* rows, const int32_t* cols,
+                                  const float* vals) {
+    if (!P || count < 0 || (count > 0 && (!rows || !cols || !vals)))
+        return ocg_internal_fail(OCG_E_INVALID, "als add_observations: bad arguments");
+    if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (count == 0) return OCG_OK;
+    for (int64_t t = 0; t < count; ++t) {  // sorted by (row, col), in range
+        if (rows[t] < 0 || rows[t] >= P->m || cols[t] < 0 || cols[t] >= P->n)
+            return ocg_internal_fail(OCG_E_INVALID, "als add_observations: cell out of range");
+        if (t > 0 && (rows[t] < rows[t - 1] || (rows[t] == rows[t - 1] && cols[t] <= cols[t - 1])))
+            return ocg_internal_fail(OCG_E_INVALID, "als add_observations: cells not sorted by (row, col) / repeated");
+    }
+    const int64_t nnz2 = P->nnz + count;
+    if (nnz2 >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als add_observations: bad nnz");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const int sm = ocg_internal_sm_count(P->ctx);
+    if (!P->add_inc.p) {
+        ALS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, P->add_tmp_bytes, P->add_inc.p, P->add_ex.p, P->m));
+        ALS_CUDA(P->add_tmp.alloc(P->add_tmp_bytes));
+        ALS_CUDA(P->add_inc.alloc(static_cast<size_t>(P->m)));
+        ALS_CUDA(P->add_ex.alloc(static_cast<size_t>(P->m)));
+        ALS_CUDA(P->add_err.alloc(1));
+    }
+    if (P->add_cap < count) {
+        P->add_cap = grow_cap(count);
+        ALS_CUDA(P->add_rc.alloc(static_cast<size_t>(2 * P->add_cap)));
+        ALS_CUDA(P->add_v.alloc(static_cast<size_t>(P->add_cap)));
+    }
+    int32_t* arow = P->add_rc.p;
+    int32_t* acol = P->add_rc.p + P->add_cap;
+    float* aval = P->add_v.p;
+    int32_t* inc = P->add_inc.p;
+    int32_t* ex = P->add_ex.p;
+    int32_t* err = P->add_err.p;
+    size_t tb = P->add_tmp_bytes;
+    if (!P->rp_alt.p) ALS_CUDA(P->rp_alt.alloc(static_cast<size_t>(P->m + 1)));
+    if (P->alt_cap < nnz2) {
+        P->alt_cap = grow_cap(nnz2);
+        ALS_CUDA(P->col_alt.alloc(static_cast<size_t>(P->alt_cap)));
+        ALS_CUDA(P->val_alt.alloc(static_cast<size_t>(P->alt_cap)));
+    }
+    ALS_CUDA(cudaMemcpyAsync(arow, rows, sizeof(int32_t) * count, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(acol, cols, sizeof(int32_t) * count, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemcpyAsync(aval, vals, sizeof(float) * count, cudaMemcpyHostToDevice, s));
+    ALS_CUDA(cudaMemsetAsync(inc, 0, sizeof(int32_t) * P->m, s));
+    ALS_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
+    add_count_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(count, arow, inc);
+    ALS_CUDA(cudaGetLastError());
+    ALS_CUDA(cub::DeviceScan::ExclusiveSum(P->add_tmp.p, tb, inc, ex, P->m, s));
+    add_merge_kernel<<<sm * 8, 256, 0, s>>>(P->m, P->row_ptr.p, P->col.p, P->val.p, inc, ex, acol, aval,
+                                            P->rp_alt.p, P->col_alt.p, P->val_alt.p, err);
+    ALS_CUDA(cudaGetLastError());
+    int32_t herr = 0;
+    ALS_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaStreamSynchronize(s));
+    if (herr) return ocg_internal_fail(OCG_E_INVALID, "als add_observations: a cell is already observed");
+    std::swap(P->row_ptr.p, P->rp_alt.p);
+    std::swap(P->col.p, P->col_alt.p);
+    std::swap(P->val.p, P->val_alt.p);
+    std::swap(P->col_cap, P->alt_cap);
+    P->nnz = nnz2;
+    if (nnz2 > P->nnz_cap) {
+        P->nnz_cap = grow_cap(nnz2);
+        int rc = als_alloc(P);
+        if (rc) return rc;
+    }
+    if (mma_rank(P->k)) {
+        ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, sm, s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
     }
     return OCG_OK;

@@ -17,7 +17,9 @@ from .api import PowerGrid
 from .synth import CsrMatrix
 
 
-def add_observations(A: CsrMatrix, grid: PowerGrid, frac: float = 0.01, seed: int = 0) -> CsrMatrix:
+def add_observations(A: CsrMatrix, grid: PowerGrid, frac: float = 0.01, seed: int = 0, return_delta: bool = False):
+    """The merged CSR; with return_delta also the new cells (rows, cols, vals), sorted by
+    (row, col) -- the arguments of ``AlsPlan.add_observations``."""
     m, n = A.m, grid.n
     rng = np.random.default_rng(seed)
     rp = A.row_ptr
@@ -61,4 +63,7 @@ def add_observations(A: CsrMatrix, grid: PowerGrid, frac: float = 0.01, seed: in
     add[rows] = 1
     rp2 = rp.copy()
     rp2[1:] += np.cumsum(add)
-    return CsrMatrix(m, n, rp2, col2, val2)
+    B = CsrMatrix(m, n, rp2, col2, val2)
+    if return_delta:
+        return B, (rows.astype(np.int32), cols.astype(np.int32), vals.astype(A.val.dtype))
+    return B

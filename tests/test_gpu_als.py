@@ -204,3 +204,44 @@ def test_als_rank32_multisegment_rows_and_empty_items(ctx, port):
     Po = np.clip(Uo @ Vo.T, 0.01, 1.25)
     rel = np.abs(Pg - Po) / Po
     assert np.quantile(rel, 0.999) < PRED_RTOL, (rel.max(), np.quantile(rel, 0.999))
+
+
+@pytest.mark.parametrize("rank", [16, 32])
+def test_als_add_observations_matches_merged_upload(ctx, rank):
+    """ocg_als_plan_add_observations (device-side merge of new cells) == a plan on the
+    merged CSR: same factors and decisions, bit for bit; bad arrivals are rejected
+    and leave the plan usable."""
+    from paper_2508_07605_b200 import stream
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(1200, 8, 16, 0.1, 3, seed=17)
+    hyp = AlsHyper(rank=rank, sweeps=3)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+    plan.run()
+    B, (r, c, v) = stream.add_observations(A, grid, frac=0.05, seed=9, return_delta=True)
+    plan.add_observations(r, c, v)
+    plan.run()
+    fresh = AlsPlan(B.m, B.row_ptr, B.col, B.val, grid, hyp, 0.05, ctx=ctx)
+    fresh.run()
+    for g_, w_ in zip(plan.factors(), fresh.factors()):
+        np.testing.assert_array_equal(g_, w_)
+    for g_, w_ in zip(plan.results(), fresh.results()):
+        np.testing.assert_array_equal(g_, w_)
+    # a second arrival on top of the first
+    C, (r2, c2, v2) = stream.add_observations(B, grid, frac=0.02, seed=10, return_delta=True)
+    plan.add_observations(r2, c2, v2)
+    plan.run()
+    fresh = AlsPlan(C.m, C.row_ptr, C.col, C.val, grid, hyp, 0.05, ctx=ctx)
+    fresh.run()
+    for g_, w_ in zip(plan.results(), fresh.results()):
+        np.testing.assert_array_equal(g_, w_)
+    # rejected: an observed cell, unsorted cells, out-of-range column
+    row0 = int(np.nonzero(np.diff(C.row_ptr) > 0)[0][0])
+    for bad in ((np.array([row0]), np.array([C.col[C.row_ptr[row0]]]), np.array([0.5])),
+                (np.array([5, 4]), np.array([0, 0]), np.array([0.5, 0.5])),
+                (np.array([0]), np.array([grid.n]), np.array([0.5]))):
+        with pytest.raises(Exception):
+            plan.add_observations(*bad)
+    plan.run()
+    for g_, w_ in zip(plan.results(), fresh.results()):
+        np.testing.assert_array_equal(g_, w_)
