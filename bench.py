@@ -433,9 +433,32 @@ def workload_joint(args, d: Dist):
             ShardedAlsDriver(GpuAlsBackend(p2, dev), d.world, lambda g: d.pg.all_reduce(g)).run(args.sweeps)
         p2.results(out=[int(x.data_ptr()) for x in res_pin])  # decisions into pinned host memory
         e2e_t += time.perf_counter() - t0
+    e2e_t = d.max(e2e_t / e2e_steps)
+    e2e_serial_t = e2e_t
+    e2e_mode = "serial: per step upload, run, readback (L2 flushed before each)"
+    if d.world == 1 and compact:
+        # pipelined refits (double-buffered input, ocg_als_plan_stage_compact): step i+1's CSR
+        # crosses PCIe on a side stream while step i runs; every step still copies its whole
+        # CSR in and its decisions out inside the timed region.  No L2 flush between steps
+        # (the 663 MB CSR is larger than L2).
+        ptrs = [int(x.data_ptr()) for x in pin]
+        e2e_p = max(args.steps, 3)
+        p2.stage_compact(*ptrs)  # warm: staging buffers, side stream
+        p2.run(timed=False)
+        p2.results(out=[int(x.data_ptr()) for x in res_pin])
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        p2.stage_compact(*ptrs)
+        for i in range(e2e_p):
+            p2.run(timed=False)
+            if i + 1 < e2e_p:
+                p2.stage_compact(*ptrs)
+            p2.results(out=[int(x.data_ptr()) for x in res_pin])
+        e2e_t = (time.perf_counter() - t0) / e2e_p
+        e2e_mode = (f"pipelined over {e2e_p} steps: step i+1's CSR staged (side-stream H2D) while step i runs, "
+                    "decisions read back every step; no L2 flush (inputs larger than L2)")
     r2 = [x.numpy() for x in res_pin]
     p2.close()
-    e2e_t = d.max(e2e_t / e2e_steps)
     if d.world == 1:
         assert np.array_equal(r2[0], idx)
     cells = m * n
@@ -454,7 +477,8 @@ def workload_joint(args, d: Dist):
         "e2e": {"value": cells / e2e_t, "unit": "cells/s",
                 "h2d_bytes_per_step": h2d_bytes * d.world,
                 "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes) * d.world,
-                "selections_per_sec": m / e2e_t},
+                "selections_per_sec": m / e2e_t, "mode": e2e_mode,
+                "serial_value": cells / e2e_serial_t},
         "dtype": "f32 factors / f64 selection",
         "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "observed_per_gpu": nnz,
                    "density": cfg["density"], "offline_dense_rows": cfg["dense_rows"], "solver": "als",

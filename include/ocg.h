@@ -201,6 +201,13 @@ int ocg_als_plan_upload(ocg_als_plan* plan, const int64_t* row_ptr, const int32_
 /* the same with 16-bit column indices (n <= 65536: every grid of the paper and
  * of C1-C4), widened on the device: 25% fewer bytes over PCIe per refit */
 int ocg_als_plan_upload_compact(ocg_als_plan* plan, const int64_t* row_ptr, const uint16_t* col16, const float* val);
+/* double-buffered input (pipelined refits): copies the next step's CSR (16-bit
+ * columns, pinned host memory) on a side stream into staging buffers while the
+ * current step may still run; the next ocg_als_plan_run swaps it in (waits for the
+ * copy on the device, not the host).  The host buffers must stay unchanged until
+ * that run has completed.  One staged CSR at a time; _upload / _add_observations
+ * are refused while one is pending (OCG_E_INVALID). */
+int ocg_als_plan_stage_compact(ocg_als_plan* plan, const int64_t* row_ptr, const uint16_t* col16, const float* val);
 /* streaming arrivals: merge `count` new observed cells (host
  * arrays sorted by (row, col); cells not observed yet) into the plan's device CSR
  * -- the same matrix as uploading the merged CSR, with only the new cells crossing

@@ -72,6 +72,22 @@ class AlsPlan:
             args = tuple(ptr(a) for a in self._keep)
         check(lib.ocg_als_plan_upload_compact(self._h, *args))
 
+    def stage_compact(self, row_ptr, col16, val):
+        """Double-buffered upload: the next step's CSR (16-bit columns) is copied on a side
+        stream while the current step may still run; the next run() swaps it in.  Host
+        addresses (pinned, unchanged until that run completes) or numpy arrays (kept alive
+        by the plan)."""
+        keep = None
+        if isinstance(row_ptr, int):
+            args = (ctypes.c_void_p(row_ptr), ctypes.c_void_p(col16), ctypes.c_void_p(val))
+        else:
+            keep = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col16, np.uint16),
+                    np.ascontiguousarray(val, np.float32))
+            args = tuple(ptr(x) for x in keep)
+        check(lib.ocg_als_plan_stage_compact(self._h, *args))
+        if keep is not None:
+            self._keep_staged = keep
+
     def add_observations(self, rows, cols, vals):
         """Merge new observed cells (sorted by (row, col), not observed yet) into the device
         CSR; only these cells cross PCIe.  Same matrix as upload() of the merged CSR."""

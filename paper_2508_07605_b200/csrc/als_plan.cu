@@ -114,7 +114,15 @@ struct ocg_als_plan {
     Buf<uint8_t> add_tmp;
     int64_t add_cap = 0;
     size_t add_tmp_bytes = 0;
-    Buf<uint16_t> col16;  // staging of ocg_als_plan_upload_compact
+    Buf<uint16_t> col16;  // staging of ocg_als_plan_upload_compact / _stage_compact
+    // ocg_als_plan_stage_compact: the next step's CSR copied on a side stream into
+    // rp_next / col16 / val_next while the current step runs; the next _run swaps it in
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_free = nullptr;
+    bool staged = false, free_recorded = false;
+    int64_t staged_nnz = 0;
+    Buf<int64_t> rp_next;
+    Buf<float> val_next;
     int64_t col16_cap = 0;  // CSR values packed for the tensor-core Gram (the CSC copy is gathered into cval)
     Buf<int32_t> cpu, gpu, idx, ncand;
     Buf<double> saving, loss;
@@ -122,6 +130,10 @@ struct ocg_als_plan {
     ~ocg_als_plan() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamSynchronize(copy_stream);
+        if (ev_staged) cudaEventDestroy(ev_staged);
+        if (ev_free) cudaEventDestroy(ev_free);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 };
 
@@ -361,6 +373,7 @@ static int als_set_nnz(ocg_als_plan* P, int64_t nnz) {
         P->col_cap = grow_cap(nnz);
         ALS_CUDA(P->col.alloc(static_cast<size_t>(P->col_cap)));
         ALS_CUDA(P->val.alloc(static_cast<size_t>(P->col_cap)));
+        if (P->val_next.p) ALS_CUDA(P->val_next.alloc(static_cast<size_t>(P->col_cap)));
     }
     P->nnz = nnz;
     if (nnz > P->nnz_cap) {
@@ -372,6 +385,7 @@ static int als_set_nnz(ocg_als_plan* P, int64_t nnz) {
 }
 
 int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* col, const float* val) {
+    if (P && P->staged) return ocg_internal_fail(OCG_E_INVALID, "als upload: a staged CSR is pending (run first)");
     if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
     const int64_t nnz = row_ptr[P->m];
@@ -448,7 +462,16 @@ __global__ void add_merge_kernel(int64_t m, const int64_t* __restrict__ rp, cons
 
 }  // namespace
 
+namespace ocg {
+cudaError_t launch_widen_u16(int64_t n, const uint16_t* in, int32_t* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    widen_u16_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(n, in, out);
+    return cudaGetLastError();
+}
+}  // namespace ocg
+
 int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const uint16_t* col16, const float* val) {
+    if (P && P->staged) return ocg_internal_fail(OCG_E_INVALID, "als upload: a staged CSR is pending (run first)");
     if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als upload_compact: more than 65536 settings");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
@@ -477,11 +500,53 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
     return OCG_OK;
 }
 
+int ocg_als_plan_stage_compact(ocg_als_plan* P, const int64_t* row_ptr, const uint16_t* col16, const float* val) {
+    if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als stage_compact: more than 65536 settings");
+    if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (P->staged) return ocg_internal_fail(OCG_E_INVALID, "als stage_compact: a staged CSR is pending (run first)");
+    const int64_t nnz = row_ptr[P->m];
+    if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    if (!P->copy_stream) {
+        ALS_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_staged, cudaEventDisableTiming));
+        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_free, cudaEventDisableTiming));
+    }
+    if (nnz > P->col_cap || nnz > P->nnz_cap || P->col16_cap < nnz || !P->rp_next.p || !P->val_next.p) {
+        // growth (rare): drain both streams, then size every buffer for nnz
+        ALS_CUDA(cudaStreamSynchronize(s));
+        ALS_CUDA(cudaStreamSynchronize(P->copy_stream));
+        const int64_t keep = P->nnz;
+        int rc = als_set_nnz(P, std::max(nnz, keep));
+        if (rc) return rc;
+        P->nnz = keep;
+        if (P->col16_cap < nnz) {
+            P->col16_cap = grow_cap(nnz);
+            ALS_CUDA(P->col16.alloc(static_cast<size_t>(P->col16_cap)));
+        }
+        if (!P->rp_next.p) ALS_CUDA(P->rp_next.alloc(static_cast<size_t>(P->m + 1)));
+        if (!P->val_next.p) ALS_CUDA(P->val_next.alloc(static_cast<size_t>(P->col_cap)));
+    }
+    // rp_next / val_next / col16 are free once the step that last used them has passed its
+    // swap point (ev_free, recorded on the compute stream)
+    if (P->free_recorded) ALS_CUDA(cudaStreamWaitEvent(P->copy_stream, P->ev_free, 0));
+    cudaStream_t c = P->copy_stream;
+    ALS_CUDA(cudaMemcpyAsync(P->rp_next.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, c));
+    ALS_CUDA(cudaMemcpyAsync(P->col16.p, col16, sizeof(uint16_t) * nnz, cudaMemcpyHostToDevice, c));
+    ALS_CUDA(cudaMemcpyAsync(P->val_next.p, val, sizeof(float) * nnz, cudaMemcpyHostToDevice, c));
+    ALS_CUDA(cudaEventRecord(P->ev_staged, c));
+    P->staged = true;
+    P->staged_nnz = nnz;
+    return OCG_OK;
+}
+
 int ocg_als_plan_add_observations(ocg_als_plan* P, int64_t count, const int32_t* rows, const int32_t* cols,
                                   const float* vals) {
     if (!P || count < 0 || (count > 0 && (!rows || !cols || !vals)))
         return ocg_internal_fail(OCG_E_INVALID, "als add_observations: bad arguments");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (P->staged) return ocg_internal_fail(OCG_E_INVALID, "als add_observations: a staged CSR is pending (run first)");
     if (count == 0) return OCG_OK;
     for (int64_t t = 0; t < count; ++t) {  // sorted by (row, col), in range
         if (rows[t] < 0 || rows[t] >= P->m || cols[t] < 0 || cols[t] >= P->n)
@@ -594,6 +659,20 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
     const int sm = ocg_internal_sm_count(P->ctx);
     ALS_CUDA(cudaEventRecord(P->ev[0], s));
+    if (P->staged) {  // swap in the CSR staged by ocg_als_plan_stage_compact
+        ALS_CUDA(cudaStreamWaitEvent(s, P->ev_staged, 0));
+        std::swap(P->row_ptr.p, P->rp_next.p);
+        std::swap(P->val.p, P->val_next.p);
+        P->nnz = P->staged_nnz;
+        P->staged = false;
+        ALS_CUDA(ocg::launch_widen_u16(P->nnz, P->col16.p, P->col.p, s));
+        if (mma_rank(P->k)) {
+            ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, sm, s));
+            ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
+        }
+        ALS_CUDA(cudaEventRecord(P->ev_free, s));
+        P->free_recorded = true;
+    }
     int rc = als_build_csc(P);
     if (rc) return rc;
     const bool warm = P->warm_sweeps > 0 && P->fitted;

@@ -245,3 +245,37 @@ def test_als_add_observations_matches_merged_upload(ctx, rank):
     plan.run()
     for g_, w_ in zip(plan.results(), fresh.results()):
         np.testing.assert_array_equal(g_, w_)
+
+
+def test_als_stage_compact_pipelined_matches_upload(ctx):
+    """ocg_als_plan_stage_compact (side-stream copy, swapped in by the next run) gives the
+    same decisions as a synchronous upload, also when the next CSR is staged while the
+    current run is still in flight, and when its nnz differs."""
+    from paper_2508_07605_b200 import stream
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(1500, 8, 16, 0.1, 3, seed=23)
+    B = stream.add_observations(A, grid, frac=0.2, seed=4)
+    hyp = AlsHyper(rank=32, sweeps=3)
+    want = {}
+    for name, M in (("A", A), ("B", B)):
+        p = AlsPlan(M.m, M.row_ptr, M.col, M.val, grid, hyp, 0.05, ctx=ctx)
+        p.run()
+        want[name] = p.results()
+        p.close()
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+    seq = ["B", "A", "B", "B", "A"]
+    mats = {"A": A, "B": B}
+    plan.stage_compact(B.row_ptr, B.col.astype(np.uint16), B.val)
+    with pytest.raises(Exception):  # one staged CSR at a time
+        plan.stage_compact(A.row_ptr, A.col.astype(np.uint16), A.val)
+    keep = []
+    for i, name in enumerate(seq):
+        plan.run(timed=False)
+        if i + 1 < len(seq):  # stage the next input while this run is in flight
+            M = mats[seq[i + 1]]
+            arrs = (M.row_ptr.copy(), M.col.astype(np.uint16), M.val.copy())
+            keep.append(arrs)
+            plan.stage_compact(*(int(x.ctypes.data) for x in arrs))
+        for g_, w_ in zip(plan.results(), want[name]):
+            np.testing.assert_array_equal(g_, w_)
