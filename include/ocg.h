@@ -241,6 +241,12 @@ int ocg_als_plan_col_solve(ocg_als_plan* plan, const float* d_gram);
 int ocg_als_plan_select(ocg_als_plan* plan);
 int ocg_als_plan_results(ocg_als_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand,
                          float* U, float* V);
+/* the decisions (not the factors) copied into host buffers asynchronously on the context
+ * stream, behind the run that produced them: a following _run may be enqueued at once
+ * (pipelined refits); _results_wait blocks until the copies have landed.  Pinned host
+ * buffers make the copies truly asynchronous. */
+int ocg_als_plan_results_async(ocg_als_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand);
+int ocg_als_plan_results_wait(ocg_als_plan* plan);
 int ocg_als_plan_completed_rows(ocg_als_plan* plan, int64_t row0, int64_t nrows, double* out);
 void ocg_als_plan_destroy(ocg_als_plan* plan);
 

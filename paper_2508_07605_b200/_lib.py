@@ -154,6 +154,8 @@ _sig("ocg_als_plan_upload_compact", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_set_warm", ctypes.c_int, c_vp, ctypes.c_int32)
 _sig("ocg_als_plan_add_observations", ctypes.c_int, c_vp, ctypes.c_int64, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_stage_compact", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_als_plan_results_async", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_als_plan_results_wait", ctypes.c_int, c_vp)
 _sig("ocg_als_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_als_plan_completed_rows", ctypes.c_int, c_vp, c_i64, c_i64, c_vp)
 _sig("ocg_als_plan_destroy", None, c_vp)

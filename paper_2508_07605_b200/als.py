@@ -88,6 +88,14 @@ class AlsPlan:
         if keep is not None:
             self._keep_staged = keep
 
+    def results_async(self, out):
+        """Enqueue the decisions' copy into 4 host addresses (pinned: int32[m], f64[m], f64[m],
+        int32[m]) behind the current run; returns at once.  results_wait() blocks until done."""
+        check(lib.ocg_als_plan_results_async(self._h, *(ctypes.c_void_p(a) for a in out)))
+
+    def results_wait(self):
+        check(lib.ocg_als_plan_results_wait(self._h))
+
     def add_observations(self, rows, cols, vals):
         """Merge new observed cells (sorted by (row, col), not observed yet) into the device
         CSR; only these cells cross PCIe.  Same matrix as upload() of the merged CSR."""

@@ -118,7 +118,7 @@ struct ocg_als_plan {
     // ocg_als_plan_stage_compact: the next step's CSR copied on a side stream into
     // rp_next / col16 / val_next while the current step runs; the next _run swaps it in
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev_staged = nullptr, ev_free = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_free = nullptr, ev_results = nullptr;
     bool staged = false, free_recorded = false;
     int64_t staged_nnz = 0;
     Buf<int64_t> rp_next;
@@ -133,6 +133,7 @@ struct ocg_als_plan {
         if (copy_stream) cudaStreamSynchronize(copy_stream);
         if (ev_staged) cudaEventDestroy(ev_staged);
         if (ev_free) cudaEventDestroy(ev_free);
+        if (ev_results) cudaEventDestroy(ev_results);
         if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 };
@@ -792,6 +793,25 @@ int ocg_als_plan_results(ocg_als_plan* P, int32_t* idx, double* saving, double* 
     if (U) ALS_CUDA(cudaMemcpyAsync(U, P->U.p, sizeof(float) * m * P->k, cudaMemcpyDeviceToHost, s));
     if (V) ALS_CUDA(cudaMemcpyAsync(V, P->V.p, sizeof(float) * P->n * P->k, cudaMemcpyDeviceToHost, s));
     ALS_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+int ocg_als_plan_results_async(ocg_als_plan* P, int32_t* idx, double* saving, double* loss, int32_t* ncand) {
+    if (!P || !idx || !saving || !loss || !ncand) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const size_t m = static_cast<size_t>(P->m);
+    if (!P->ev_results) ALS_CUDA(cudaEventCreateWithFlags(&P->ev_results, cudaEventDisableTiming));
+    ALS_CUDA(cudaMemcpyAsync(idx, P->idx.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaMemcpyAsync(saving, P->saving.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaMemcpyAsync(loss, P->loss.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaMemcpyAsync(ncand, P->ncand.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    ALS_CUDA(cudaEventRecord(P->ev_results, s));
+    return OCG_OK;
+}
+
+int ocg_als_plan_results_wait(ocg_als_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    if (P->ev_results) ALS_CUDA(cudaEventSynchronize(P->ev_results));
     return OCG_OK;
 }
 
