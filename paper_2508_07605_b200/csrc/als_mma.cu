@@ -859,6 +859,10 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
                                                             const int32_t* __restrict__ list_count) {
     constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
     constexpr int LPS = rows_lps<K>(), kSys = 32 / LPS, R = K / LPS;  // lanes per system, systems, rows per lane
+    // rank 64: the rhs / solution is distributed (lane p keeps the column pairs p, p + LPS, ...;
+    // row-K dot products reduced over the system's lanes by shuffles) -- 64 fewer registers
+    constexpr bool DY = K == 64;
+    constexpr int NP = DY ? K / 2 / LPS : K / 2;
     // per-system strides = 4 (mod 32) words: the 8 systems' 16-byte reads at one offset hit
     // 8 distinct bank groups
     constexpr int kTri = tri_off(K) + 4, kDiag = K + 1, kTail = kRec - kRhs;  // tail = rhs, count, pad
@@ -911,12 +915,17 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
     for (;;) {
         cp_async_wait<0>();
         __syncwarp();
-        float2 y[K / 2];
+        float2 y[NP];
+        if constexpr (DY) {
 #pragma unroll
-        for (int c = 0; c < K / 4; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(T + 4 * c);
-            y[2 * c] = make_float2(v.x, v.y);
-            y[2 * c + 1] = make_float2(v.z, v.w);
+            for (int q = 0; q < NP; ++q) y[q] = *reinterpret_cast<const float2*>(T + 2 * (par + LPS * q));
+        } else {
+#pragma unroll
+            for (int c = 0; c < K / 4; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(T + 4 * c);
+                y[2 * c] = make_float2(v.x, v.y);
+                y[2 * c + 1] = make_float2(v.z, v.w);
+            }
         }
         const float cnt = T[kCnt - kRhs];
         const float diag = lambda * cnt;
@@ -943,7 +952,7 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
             float2 acc[R];
 #pragma unroll
             for (int m = mo; m < R; ++m) acc[m] = make_float2(-el(L[m], j), 0.0f);
-            float2 ss = make_float2(0.0f, 0.0f), yy = make_float2(el(y, j), 0.0f);
+            float2 ss = make_float2(0.0f, 0.0f), yy = make_float2(DY ? 0.0f : el(y, j), 0.0f);
 #pragma unroll
             for (int c = 0; 4 * c < j; ++c) {
                 const float4 v = *reinterpret_cast<const float4*>(S + tj + 4 * c);
@@ -953,12 +962,12 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
                     const float2 nv = h ? make_float2(v.z, v.w) : make_float2(v.x, v.y);
                     if (2 * p + 1 < j) {
                         ss = __ffma2_rn(nv, nv, ss);
-                        yy = __ffma2_rn(nv, y[p], yy);
+                        if constexpr (!DY) yy = __ffma2_rn(nv, y[p], yy);
 #pragma unroll
                         for (int m = mo; m < R; ++m) acc[m] = __ffma2_rn(L[m][p], nv, acc[m]);
                     } else if (2 * p < j) {  // odd j: the single column j-1
                         ss.x = fmaf(nv.x, nv.x, ss.x);
-                        yy.x = fmaf(nv.x, y[p].x, yy.x);
+                        if constexpr (!DY) yy.x = fmaf(nv.x, y[p].x, yy.x);
 #pragma unroll
                         for (int m = mo; m < R; ++m) acc[m].x = fmaf(L[m][p].x, nv.x, acc[m].x);
                     }
@@ -967,7 +976,25 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
             const float r = rsqrt_ftz(S[tj + j] - (ss.x + ss.y));
 #pragma unroll
             for (int m = mo; m < R; ++m) el(L[m], j) = (acc[m].x + acc[m].y) * r;
-            el(y, j) = (yy.x + yy.y) * r;
+            if constexpr (DY) {  // the lane's pairs' share of sum_q N[j][q] y_q, reduced over the system
+                float tot = 0.0f;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    const int pp = par + LPS * q;  // (entries past the row are masked, never multiplied)
+                    const float2 w = *reinterpret_cast<const float2*>(S + tj + 2 * pp);
+                    tot = fmaf(2 * pp < j ? w.x : 0.0f, y[q].x, tot);
+                    tot = fmaf(2 * pp + 1 < j ? w.y : 0.0f, y[q].y, tot);
+                }
+#pragma unroll
+                for (int o = kSys; o < 32; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                constexpr int pj = j / 2;
+                if (par == pj % LPS) {
+                    float& yj = (j & 1) ? y[pj / LPS].y : y[pj / LPS].x;
+                    yj = (yj + tot) * r;
+                }
+            } else {
+                el(y, j) = (yy.x + yy.y) * r;
+            }
             if (par == 0) Rd[j] = r;
         });
         __syncwarp();
@@ -976,7 +1003,21 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
         const int64_t nbt = bt + gridDim.x;
         if (kPipe && nbt < nbatch) fetch(nbt);  // in flight during the back substitution
         // L^T x = y, column-oriented over the published rows, all lanes of the item
-        static_for<K>([&](auto qc) {
+        if constexpr (DY) static_for<K>([&](auto qc) {  // x_q from its owner, then every lane's pairs
+            constexpr int q = K - 1 - decltype(qc)::value, pq = q / 2;
+            const float* Rq = S + tri_off(q);
+            float& yo = (q & 1) ? y[pq / LPS].y : y[pq / LPS].x;
+            const float xq = __shfl_sync(0xffffffffu, yo * Rd[q], (pq % LPS) * kSys + sys);
+            if (par == pq % LPS) yo = xq;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const int pp = par + LPS * i;
+                const float2 w = *reinterpret_cast<const float2*>(Rq + 2 * pp);
+                y[i] = __ffma2_rn(make_float2(2 * pp < q ? w.x : 0.0f, 2 * pp + 1 < q ? w.y : 0.0f),
+                                  make_float2(xq, xq), y[i]);
+            }
+        });
+        else static_for<K>([&](auto qc) {
             constexpr int q = K - 1 - decltype(qc)::value;
             const float* Rq = S + tri_off(q);
             el(y, q) *= Rd[q];
@@ -991,7 +1032,13 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
 #pragma unroll
             for (int i = q & ~3; i < q; ++i) el(y, i) = fmaf(Rq[i], yq, el(y, i));
         });
-        if (cur_live && par == 0) {
+        if (DY && cur_live) {
+            const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+                *reinterpret_cast<float2*>(X + cur_item * K + 2 * (par + LPS * i)) =
+                    empty ? make_float2(0.0f, 0.0f) : y[i];
+        } else if (!DY && cur_live && par == 0) {
             float4* xo = reinterpret_cast<float4*>(X + cur_item * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
