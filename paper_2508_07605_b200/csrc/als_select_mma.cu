@@ -34,6 +34,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "als.h"
 #include "ocg_common.cuh"
 #include "select_dev.cuh"
@@ -346,6 +348,8 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
             mfull = mend == n;        // fully observed (offline dense rows)
             mglob = mend > kList;     // list overflow: read the columns from global memory
         }
+        // every row of the warp has p_thr > 0.01 (the common case): the cheaper epilogue
+        const bool fast = !__any_sync(0xffffffffu, lov[0] > 0.0f || lov[1] > 0.0f);
         // ---- dense pass over the tiles (unobserved cells)
         for (int tt = 0; tt < ntiles; ++tt) {
             const int buf = tt & 1;
@@ -401,6 +405,8 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
             // min(x, 1.25 S) >= fthr S decides (fthr > 0.01f, and 1.25 is a float)
             const float fth_s[2] = {lov[0] > 0.0f ? -INFINITY : fthr[0] * S, lov[1] > 0.0f ? -INFINITY : fthr[1] * S};
             float tb_s[2] = {tband[0] * inv_s, tband[1] * inv_s};
+            const float fthp[2] = {fth_s[0] <= hi_s ? fth_s[0] : INFINITY, fth_s[1] <= hi_s ? fth_s[1] : INFINITY};
+            auto tiles = [&](auto FAST) {
 #pragma unroll 2
             for (int nt = 0; nt < kNT; nt += 2) {
                 float d[2][4];
@@ -430,9 +436,17 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
                         for (int e = 0; e < 2; ++e) {
                             const float csf = e ? cs2[u].y : cs2[u].x;
                             const float x = d[u][2 * q + e];
-                            const float pc = fminf(x, hi_s);
-                            vb |= pc >= fth_s[q] ? 1u << (2 * u + e) : 0u;
-                            hb |= csf <= tb_s[q] * fmaxf(pc, lo_s) ? 1u << (2 * u + e) : 0u;
+                            if constexpr (decltype(FAST)::value) {
+                                // no row of the warp has p_thr <= 0.01: valid cells have x > 0.01 S,
+                                // min(x, 1.25 S) >= fth <=> x >= fthp, and the band test on the raw
+                                // x is a superset of the clamped one (the exact path re-checks)
+                                vb |= x >= fthp[q] ? 1u << (2 * u + e) : 0u;
+                                hb |= csf <= tb_s[q] * x ? 1u << (2 * u + e) : 0u;
+                            } else {
+                                const float pc = fminf(x, hi_s);
+                                vb |= pc >= fth_s[q] ? 1u << (2 * u + e) : 0u;
+                                hb |= csf <= tb_s[q] * fmaxf(pc, lo_s) ? 1u << (2 * u + e) : 0u;
+                            }
                         }
                     const unsigned ob4 = (mk[q][nt >> 4] >> ((nt & 15) * 2)) & 0xFu;
                     vb &= ~ob4;
@@ -473,6 +487,9 @@ __global__ void __launch_bounds__(kW * 32, K == 32 ? 2 : 1) als_select_mma_kerne
                             }
                 }
             }
+            };
+            if (fast) tiles(std::true_type{});
+            else tiles(std::false_type{});
             // share the running best within the quad (the 4 lanes holding a row)
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
