@@ -412,6 +412,40 @@ __global__ void col_ptr_kernel(int64_t nnz, int64_t n, const int32_t* __restrict
     for (int32_t c = prev + 1; c <= cur; ++c) cptr[c] = q;
 }
 
+// packed 32-bit CSC keys (m <= 2^rb, n <= 2^(32-rb)): key = col << rb | row, built from
+// the CSR (warp per row); sorted on the column bits only (stable: rows stay ascending),
+// the value words ride along as the 32-bit payload
+__global__ void expand_keys_kernel(int64_t m, int rb, const int64_t* __restrict__ ptr,
+                                   const int32_t* __restrict__ col, uint32_t* __restrict__ keys) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < m; i += nw)
+        for (int64_t q = ptr[i] + lane; q < ptr[i + 1]; q += 32)
+            keys[q] = (static_cast<uint32_t>(col[q]) << rb) | static_cast<uint32_t>(i);
+}
+// sorted keys -> crow (row bits) and col_ptr (first occurrence of each column)
+__global__ void split_keys_kernel(int64_t nnz, int64_t n, int rb, const uint32_t* __restrict__ skeys,
+                                  int32_t* __restrict__ crow, int64_t* __restrict__ cptr) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q > nnz) return;
+    const uint32_t rmask = (rb >= 32) ? 0xffffffffu : ((1u << rb) - 1u);
+    const int64_t cur = q < nnz ? static_cast<int64_t>(skeys[q] >> rb) : n;
+    const int64_t prev = q > 0 ? static_cast<int64_t>(skeys[q - 1] >> rb) : -1;
+    if (q < nnz) crow[q] = static_cast<int32_t>(skeys[q] & rmask);
+    for (int64_t c = prev + 1; c <= cur; ++c) cptr[c] = q;
+}
+
+cudaError_t launch_expand_keys(int64_t m, int rb, const int64_t* ptr, const int32_t* col, uint32_t* keys,
+                               int sm_count, cudaStream_t s) {
+    expand_keys_kernel<<<sm_count * 8, 256, 0, s>>>(m, rb, ptr, col, keys);
+    return cudaGetLastError();
+}
+cudaError_t launch_split_keys(int64_t nnz, int64_t n, int rb, const uint32_t* skeys, int32_t* crow, int64_t* cptr,
+                              cudaStream_t s) {
+    split_keys_kernel<<<static_cast<unsigned>((nnz + 1 + 255) / 256), 256, 0, s>>>(nnz, n, rb, skeys, crow, cptr);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s) {
     const int64_t tot = n * k;
     als_init_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(n, k, seed, V);

@@ -66,6 +66,11 @@ cudaError_t launch_expand_pairs(int64_t m, const int64_t* ptr, const uint32_t* v
                                 cudaStream_t s);
 cudaError_t launch_split_pairs(int64_t nnz, const uint64_t* pairs, int32_t* crow, uint32_t* cval, cudaStream_t s);
 cudaError_t launch_col_ptr(int64_t nnz, int64_t n, const int32_t* skeys, int64_t* cptr, cudaStream_t s);
+// packed-key CSC (key = col << rb | row, 32 bits): keys from the CSR, then crow + col_ptr
+cudaError_t launch_expand_keys(int64_t m, int rb, const int64_t* ptr, const int32_t* col, uint32_t* keys,
+                               int sm_count, cudaStream_t s);
+cudaError_t launch_split_keys(int64_t nnz, int64_t n, int rb, const uint32_t* skeys, int32_t* crow, int64_t* cptr,
+                              cudaStream_t s);
 
 // fused completion + Algorithm-2 selection over all rows (als_select.cu)
 struct AlsSelectArgs {

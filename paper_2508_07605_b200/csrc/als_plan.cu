@@ -51,6 +51,12 @@ struct Buf {
 // ranks on the tensor-core path (als_mma.cu / als_select_mma.cu)
 bool mma_rank(int k) { return k == 32 || k == 64; }
 
+// OCG_CSC_PAIRS=1: the 64-bit-payload radix sort even when packed 32-bit keys fit (A/B runs)
+bool csc_pairs_forced() {
+    const char* e = std::getenv("OCG_CSC_PAIRS");  // read per build (cheap; tests toggle it)
+    return e && e[0] == '1';
+}
+
 int bits_for(int64_t n) {
     int b = 1;
     while ((int64_t(1) << b) < n + 1) ++b;
@@ -141,7 +147,23 @@ struct ocg_als_plan {
 static int als_build_csc(ocg_als_plan* P) {
     cudaStream_t s = ocg_internal_stream(P->ctx);
     const int sm = ocg_internal_sm_count(P->ctx);
-    if (P->nnz > 0) {
+    const int rb = bits_for(P->m - 1), cb = bits_for(P->n - 1);
+    const bool key32 = rb + cb <= 32 && !csc_pairs_forced();
+    if (key32) {
+        // one 32-bit key (col << rb | row) per observation, sorted on its column bits only
+        // (stable: rows stay ascending inside a column); the value word is the payload and
+        // lands in cval directly
+        const uint32_t* vb = mma_rank(P->k) ? P->valh.p : reinterpret_cast<const uint32_t*>(P->val.p);
+        uint32_t* kin = reinterpret_cast<uint32_t*>(P->pairs_in.p);
+        uint32_t* kout = reinterpret_cast<uint32_t*>(P->pairs_out.p);
+        if (P->nnz > 0) {
+            ALS_CUDA(ocg::launch_expand_keys(P->m, rb, P->row_ptr.p, P->col.p, kin, sm, s));
+            size_t bytes = P->sort_tmp_bytes;
+            ALS_CUDA(cub::DeviceRadixSort::SortPairs(P->sort_tmp.p, bytes, kin, kout, vb,
+                                                     reinterpret_cast<uint32_t*>(P->cval.p), P->nnz, rb, rb + cb, s));
+        }
+        ALS_CUDA(ocg::launch_split_keys(P->nnz, P->n, rb, kout, P->crow.p, P->col_ptr.p, s));
+    } else if (P->nnz > 0) {
         // (row, value) travel with the column key through the radix sort (stable:
         // rows stay ascending inside a column), so no random gathers afterwards.
         // Rank 32: the value word is the packed (fp16 hi, lo) form.
@@ -152,7 +174,7 @@ static int als_build_csc(ocg_als_plan* P) {
                                                  P->pairs_out.p, P->nnz, 0, bits_for(P->n), s));
         ALS_CUDA(ocg::launch_split_pairs(P->nnz, P->pairs_out.p, P->crow.p, reinterpret_cast<uint32_t*>(P->cval.p), s));
     }
-    ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
+    if (!key32) ALS_CUDA(ocg::launch_col_ptr(P->nnz, P->n, P->keys_out.p, P->col_ptr.p, s));
     for (int sd = 0; sd < 2; ++sd) {
         auto& S = P->side[sd];
         const int64_t items = sd == 0 ? P->m : P->n;
@@ -229,9 +251,14 @@ static int als_alloc(ocg_als_plan* P) {
     ALS_CUDA(P->keys_out.alloc(static_cast<size_t>(cap)));
     ALS_CUDA(P->pairs_in.alloc(static_cast<size_t>(cap)));
     ALS_CUDA(P->pairs_out.alloc(static_cast<size_t>(cap)));
-    size_t bytes = 0;
+    size_t bytes = 0, b32 = 0;
     ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, P->col.p, P->keys_out.p, P->pairs_in.p, P->pairs_out.p,
                                              cap, 0, bits_for(P->n)));
+    ALS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b32, reinterpret_cast<uint32_t*>(P->pairs_in.p),
+                                             reinterpret_cast<uint32_t*>(P->pairs_out.p),
+                                             static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                             cap, 0, 32));
+    bytes = std::max(bytes, b32);
     P->sort_tmp_bytes = bytes;
     ALS_CUDA(P->sort_tmp.alloc(bytes));
     for (int sd = 0; sd < 2; ++sd) {

@@ -279,3 +279,29 @@ def test_als_stage_compact_pipelined_matches_upload(ctx):
             plan.stage_compact(*(int(x.ctypes.data) for x in arrs))
         for g_, w_ in zip(plan.results(), want[name]):
             np.testing.assert_array_equal(g_, w_)
+
+
+@pytest.mark.parametrize("k", [16, 32])
+def test_als_csc_packed_keys_identical_to_pair_sort(ctx, k, monkeypatch):
+    """The packed 32-bit-key CSC build (col << rb | row, default when m and n fit) and the
+    64-bit-payload radix sort (OCG_CSC_PAIRS=1) give the same CSC, so the fits are
+    bit-identical; includes fully observed rows and an empty row."""
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+    from paper_2508_07605_b200.synth import CsrMatrix
+
+    grid, A = _problem(2500, 8, 16, 0.2, 5, seed=29)
+    keep = np.ones(A.nnz, bool)
+    keep[A.row_ptr[11]:A.row_ptr[12]] = False
+    cnt = np.diff(A.row_ptr).copy()
+    cnt[11] = 0
+    A = CsrMatrix(A.m, A.n, np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64), A.col[keep], A.val[keep])
+    hyp = AlsHyper(rank=k, lam=0.003, sweeps=3, seed=5)
+    out = []
+    for forced in ("0", "1"):
+        monkeypatch.setenv("OCG_CSC_PAIRS", forced)
+        plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
+        plan.run()
+        out.append(plan.factors() + plan.results())
+        plan.close()
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)
