@@ -1113,7 +1113,9 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     else e = launch_gram_k<K, false>(h, sm_count, s);
     if (e != cudaSuccess) return e;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
-    const dim3 gblocks(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 2))), 32);
+    // column side: a few items with many segments (y spreads their groups); row side: many short items
+    const dim3 gblocks(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 2))),
+                       h.seg_order ? 32 : 2);
     if (mode == 1) {
         als_reduce_groups_kernel<K><<<gblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial);
         als_reduce_records_kernel<K><<<rblocks, 160, 0, s>>>(h.nitems, nullptr, nullptr, h.nseg, h.first, h.partial,
