@@ -842,6 +842,10 @@ static bool solve_rows_off() {
     return off;
 }
 
+// the register-row K4 also leaves max |x| in AlsHalf::xmax (launch_als_pack can skip its pass)
+bool als_solve_tracks_max() { return !solve_rows_off(); }
+
+
 // K4 at rank 32 with register-resident rows: lane (sys = lane & 7, par = lane >> 3)
 // holds rows i = 4m + par (m = 0..7, row m = columns 0..4m+3) of system sys in
 // registers, loaded straight from the record.  Left-looking: at column j the
@@ -856,7 +860,8 @@ template <int K>
 __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, const int32_t* __restrict__ first,
                                                             const float* __restrict__ rec, float* __restrict__ X,
                                                             float lambda, const int32_t* __restrict__ list,
-                                                            const int32_t* __restrict__ list_count) {
+                                                            const int32_t* __restrict__ list_count,
+                                                            unsigned* __restrict__ xmax) {
     constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
     constexpr int LPS = rows_lps<K>(), kSys = 32 / LPS, R = K / LPS;  // lanes per system, systems, rows per lane
     // rank 64: the rhs / solution is distributed (lane p keeps the column pairs p, p + LPS, ...;
@@ -911,6 +916,7 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
         }
         cp_async_commit();
     };
+    float lmax = 0.0f;  // max |x| of the rows this lane stored (xmax: the next packing's scale)
     fetch(bt);
     for (;;) {
         cp_async_wait<0>();
@@ -1035,9 +1041,11 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
         if (DY && cur_live) {
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
 #pragma unroll
-            for (int i = 0; i < NP; ++i)
+            for (int i = 0; i < NP; ++i) {
                 *reinterpret_cast<float2*>(X + cur_item * K + 2 * (par + LPS * i)) =
                     empty ? make_float2(0.0f, 0.0f) : y[i];
+                if (!empty) lmax = fmaxf(lmax, fmaxf(fabsf(y[i].x), fabsf(y[i].y)));
+            }
         } else if (!DY && cur_live && par == 0) {
             float4* xo = reinterpret_cast<float4*>(X + cur_item * K);
             const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
@@ -1045,18 +1053,26 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
             for (int q = 0; q < K / 4; ++q)
                 xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
                               : make_float4(y[2 * q].x, y[2 * q].y, y[2 * q + 1].x, y[2 * q + 1].y);
+            if (!empty)
+#pragma unroll
+                for (int q = 0; q < K / 2; ++q) lmax = fmaxf(lmax, fmaxf(fabsf(y[q].x), fabsf(y[q].y)));
         }
         __syncwarp();
         if (nbt >= nbatch) break;
         if (!kPipe) fetch(nbt);
         bt = nbt;
     }
+    if (xmax) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+        if (lane == 0) atomicMax(xmax, __float_as_uint(lmax));  // non-negative floats order as unsigned
+    }
 }
 
 template <int K>
 static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
                                   int sm_count, cudaStream_t s, const int32_t* list = nullptr,
-                                  const int32_t* list_count = nullptr) {
+                                  const int32_t* list_count = nullptr, unsigned* xmax = nullptr) {
     if (!solve_rows_off()) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows_kernel<K>, 32, 0);
@@ -1066,7 +1082,7 @@ static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const fl
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
         als_solve_rows_kernel<K><<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda, list,
-                                                                              list_count);
+                                                                              list_count, xmax);
         return cudaGetLastError();
     }
     constexpr int smem = solve_smem<K>();
@@ -1108,6 +1124,8 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
     const bool fused = K == 32 && mode == 0 && h.fuse_solve;
+    unsigned* xmax = (mode == 0 && !fused && h.xmax && als_solve_tracks_max()) ? h.xmax : nullptr;
+    if (xmax && (e = cudaMemsetAsync(xmax, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
     if (fused) e = launch_gram_k<32, true>(h, sm_count, s);
     else if (K == 32 && h.seg_order) e = launch_gram_k<32, false, true>(h, sm_count, s);  // column side
     else e = launch_gram_k<K, false>(h, sm_count, s);
@@ -1131,7 +1149,7 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
     if (fused)  // the single-segment items were solved inside the Gram kernel
         return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s, h.multi_list,
                                  h.multi_count);
-    return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s);
+    return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s, nullptr, nullptr, xmax);
 }
 
 cudaError_t launch_als_mma_half(int k, const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
@@ -1151,14 +1169,16 @@ size_t als_record_floats_mma(int k) { return k == 64 ? Cfg<64>::kRec : Cfg<32>::
 
 // max |X| -> *maxbits (zeroed here), then X -> packed hi/lo rows
 cudaError_t launch_als_pack(int k, int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count,
-                            cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(maxbits, 0, sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
-    const int64_t cnt = rows * k;
-    int64_t blocks = (cnt + 255) / 256;
-    if (blocks > sm_count * 8) blocks = sm_count * 8;
-    if (blocks < 1) blocks = 1;
-    als_absmax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(cnt, X, maxbits);
+                            cudaStream_t s, bool have_max) {
+    if (!have_max) {  // (else the K4 that wrote X left max |X| in *maxbits)
+        cudaError_t e = cudaMemsetAsync(maxbits, 0, sizeof(unsigned), s);
+        if (e != cudaSuccess) return e;
+        const int64_t cnt = rows * k;
+        int64_t blocks = (cnt + 255) / 256;
+        if (blocks > sm_count * 8) blocks = sm_count * 8;
+        if (blocks < 1) blocks = 1;
+        als_absmax_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(cnt, X, maxbits);
+    }
     const unsigned pb = static_cast<unsigned>((rows * (k / 8) + 255) / 256);
     if (k == 32) als_pack_kernel<32><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);
     else if (k == 64) als_pack_kernel<64><<<pb, 256, 0, s>>>(rows, X, maxbits, Xh);

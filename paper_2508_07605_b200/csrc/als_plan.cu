@@ -232,12 +232,12 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
 }
 
 // after a half-sweep (or V init): repack the factor the next half gathers
-static int als_pack(ocg_als_plan* P, int sd) {
+static int als_pack(ocg_als_plan* P, int sd, bool have_max = false) {
     if (!mma_rank(P->k)) return OCG_OK;
     const int64_t rows = sd == 0 ? P->m : P->n;
     ALS_CUDA(ocg::launch_als_pack(P->k, rows, sd == 0 ? P->U.p : P->V.p, P->maxbits.p + (sd == 0 ? 0 : 1),
                                   sd == 0 ? P->Uh.p : P->Vh.p, ocg_internal_sm_count(P->ctx),
-                                  ocg_internal_stream(P->ctx)));
+                                  ocg_internal_stream(P->ctx), have_max));
     return OCG_OK;
 }
 
@@ -719,12 +719,17 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             hc.ev_gram0 = P->ev[8];
             hc.ev_gram1 = P->ev[9];
         }
+        const bool track = mma_rank(P->k) && !hr.fuse_solve && ocg::als_solve_tracks_max();
+        if (mma_rank(P->k)) {
+            hr.xmax = P->maxbits.p + 0;  // U's packing scale, produced by the row-side K4
+            hc.xmax = P->maxbits.p + 1;  // V's
+        }
         ALS_CUDA(cudaEventRecord(P->ev[2], s));
         ALS_CUDA(ocg::launch_als_half(P->k, hr, 0, sm, s));
-        if ((rc = als_pack(P, 0))) return rc;
+        if ((rc = als_pack(P, 0, track))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[3], s));
         ALS_CUDA(ocg::launch_als_half(P->k, hc, 0, sm, s));
-        if ((rc = als_pack(P, 1))) return rc;
+        if ((rc = als_pack(P, 1, track))) return rc;
         ALS_CUDA(cudaEventRecord(P->ev[4], s));
         if (phase_ms) {
             float a = 0, b = 0;
