@@ -305,3 +305,26 @@ def test_als_csc_packed_keys_identical_to_pair_sort(ctx, k, monkeypatch):
         plan.close()
     for a, b in zip(out[0], out[1]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_als_results_async_matches_results(ctx):
+    """ocg_als_plan_results_async + _results_wait (copies queued behind the run, the next run
+    queued right after) return what the synchronous ocg_als_plan_results returns."""
+    import torch
+
+    from paper_2508_07605_b200.als import AlsHyper, AlsPlan
+
+    grid, A = _problem(1000, 8, 16, 0.1, 2, seed=31)
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, AlsHyper(rank=32, sweeps=3), 0.05, ctx=ctx)
+    plan.run(timed=False)
+    want = plan.results()
+    outs = [torch.empty(A.m, dtype=dt).pin_memory() for dt in (torch.int32, torch.float64, torch.float64,
+                                                                torch.int32)]
+    plan.results_async([int(x.data_ptr()) for x in outs])
+    plan.run(timed=False)  # queued behind the copy: must not disturb it
+    plan.results_wait()
+    for g_, w_ in zip(outs, want):
+        np.testing.assert_array_equal(g_.numpy(), w_)
+    plan.results_wait()  # the second run (same inputs) gives the same decisions
+    for g_, w_ in zip(plan.results(), want):
+        np.testing.assert_array_equal(g_, w_)
