@@ -167,6 +167,47 @@ int ocg_ncf_model_to_json(const ocg_ncf_hyper* hyper, int64_t m, int64_t n, cons
 int ocg_ncf_model_from_json(const char* text, ocg_ncf_hyper* hyper, int64_t* m, int64_t* n, int64_t* nparams,
                             double* params, uint8_t* app_seen, uint8_t* setting_seen, ocg_ncf_meta* meta);
 
+/* ---- NCF completion + selection over a whole matrix (SURVEY §8a a9 + a10) -
+ * A fitted cf::NcfModel (cfcomplete.hpp:25-55) resident in HBM, and a plan
+ * binding it to a sparse matrix: cf::complete's imputation of every unobserved
+ * cell (cfcomplete.cpp:208-211, NcfModel::predict :47-58; observed cells kept
+ * verbatim) fused with policy::select_caps (policy.cpp:17-64) on every row.
+ * The completed m x n matrix is never materialised.
+ *   OCG_NCF_EXACT: FP64 in the operation order of `lane`, glibc exp —
+ *                  predictions and decisions bit-identical to the reference.
+ *   OCG_NCF_FAST:  FP32 + tcgen05 tensor cores (hidden {32, 16} only), |dp|/p
+ *                  ~1e-6; decisions identical wherever the margin exceeds it
+ *                  (the baseline p_{i,n-1} is always computed exactly).
+ * Model: params in the flat layout [app m x ka | setting n x ks | W0 b0 W1 b1 ...]
+ * (as ocg_ncf_model_from_json returns), app_seen[m], setting_seen[n].
+ * Matrix: CSR row_ptr[m+1] (int64), col[nnz] (int32, ascending per row), val[nnz]
+ * (FP64, (0, 1.25]); on_device = 1: device pointers used in place.
+ * Errors (from _results / _completed_rows, as the reference would throw for the
+ * whole call): OCG_E_RANGE column index out of range; OCG_E_INVALID row without
+ * observed entries (cfcomplete.cpp:199-205) or value outside (0, 1.25]
+ * (core.cpp:145-147); OCG_E_COLD cold app row / setting column (:50-55);
+ * OCG_E_UNSUPPORTED fast path with |W0 . x| >= 80 (use EXACT). */
+typedef struct ocg_ncf_model ocg_ncf_model;
+typedef struct ocg_ncf_plan ocg_ncf_plan;
+enum { OCG_NCF_EXACT = 0, OCG_NCF_FAST = 1 };
+int ocg_ncf_model_create(ocg_ctx* ctx, const ocg_ncf_hyper* hyper, int64_t m, int64_t n, const double* params,
+                         const uint8_t* app_seen, const uint8_t* setting_seen, ocg_ncf_model** out);
+/* NcfModel::from_json (cfcomplete.cpp:235-265) straight into HBM */
+int ocg_ncf_model_from_json_text(ocg_ctx* ctx, const char* text, ocg_ncf_model** out);
+void ocg_ncf_model_destroy(ocg_ncf_model* model);
+int ocg_ncf_plan_create(ocg_ncf_model* model, const int64_t* row_ptr, const int32_t* col, const double* val,
+                        int on_device, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                        double gamma, int precision, int lane, ocg_ncf_plan** out);
+/* a new matrix (same m) for the plan, host CSR copied on the context stream */
+int ocg_ncf_plan_upload(ocg_ncf_plan* plan, const int64_t* row_ptr, const int32_t* col, const double* val);
+/* one completion + selection of every row; total_ms / phase_ms[2] (prep: validation,
+ * A/B precompute, baselines, observed cells; dense pass) as CUDA-event times (NULL = async) */
+int ocg_ncf_plan_run(ocg_ncf_plan* plan, float* total_ms, float* phase_ms);
+int ocg_ncf_plan_results(ocg_ncf_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand);
+/* completed values (nrows x n, FP64) of the listed rows (test / inspection hook) */
+int ocg_ncf_plan_completed_rows(ocg_ncf_plan* plan, const int64_t* rows, int64_t nrows, double* out);
+void ocg_ncf_plan_destroy(ocg_ncf_plan* plan);
+
 /* ---- ALS completion + selection (joint mode) -------
  * No reference counterpart: the reference's CF is NCF only.  Semantics are
  * defined by the CPU oracle (oracle/ocg_oracle.c, ocgo_als_fit): weighted-

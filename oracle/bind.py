@@ -222,6 +222,9 @@ class Ref:
         L.ref_online_batch.argtypes = [c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_sz, c_dbl, c_vp,
                                        ctypes.c_int, c_vp, c_vp]
         L.ref_force_lane.argtypes = [ctypes.c_int]
+        L.ref_ncf_complete_select_rows.argtypes = [c_sz, c_sz, c_vp, c_sz, c_sz, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
+                                                   c_sz, c_vp, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp,
+                                                   c_vp, c_vp]
         L.ref_complete_select_batch.restype = c_dbl
         L.ref_complete_select_batch.argtypes = [c_sz, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_dbl,
                                                 ctypes.c_int, c_vp]
@@ -288,6 +291,28 @@ class Ref:
         rc = self.L.ref_ncf_predict(model_json.encode(), P(rows), P(cols), len(rows), P(out))
         return rc, out
 
+    def ncf_complete_select_rows(self, ka, ks, hidden, params_sub, app_seen, setting_seen, cpu, gpu, values, mask,
+                                 gamma=0.05, threads=1, want_completed=True):
+        """NcfModel::predict of every unobserved cell of the given rows (a model whose app
+        table holds exactly these rows) + policy::select_caps per row.  Returns
+        (rc, completed | None, idx, saving, loss, ncand, seconds)."""
+        values = np.ascontiguousarray(values, np.float64)
+        mask = np.ascontiguousarray(mask, np.uint8)
+        r = values.shape[0]
+        cpu, gpu = np.asarray(cpu, np.int32), np.asarray(gpu, np.int32)
+        hid = np.asarray(hidden, np.uint64)
+        p = np.ascontiguousarray(params_sub, np.float64)
+        aseen = np.ascontiguousarray(app_seen, np.uint8)
+        sseen = np.ascontiguousarray(setting_seen, np.uint8)
+        comp = np.zeros_like(values) if want_completed else None
+        idx, nc = np.zeros(r, np.int32), np.zeros(r, np.int32)
+        sv, lo = np.zeros(r), np.zeros(r)
+        secs = c_dbl()
+        rc = self.L.ref_ncf_complete_select_rows(ka, ks, P(hid), len(hid), r, P(p), P(aseen), P(sseen), P(cpu),
+                                                 len(cpu), P(gpu), len(gpu), P(values), P(mask), gamma, threads,
+                                                 P(comp), P(idx), P(sv), P(lo), P(nc), ctypes.byref(secs))
+        return rc, comp, idx, sv, lo, nc, secs.value
+
     def offline_default(self, seed=42):
         dense = np.zeros(10 * 20)
         rows = c_sz()
@@ -305,6 +330,14 @@ class Ref:
                                        ctypes.byref(out))
         assert rc == 0, self.err()
         return out
+
+
+def sub_model_params(params, m, n, ka, ks, rows):
+    """Flat parameters of the model restricted to app rows `rows` (same setting table
+    and MLP): NcfModel::predict(i, j) depends only on row i's embedding."""
+    params = np.asarray(params, np.float64)
+    app = params[: m * ka].reshape(m, ka)[np.asarray(rows, np.int64)].ravel()
+    return np.concatenate([app, params[m * ka:]])
 
 
 def model_params_from_json(text: str) -> np.ndarray:

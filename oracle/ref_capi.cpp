@@ -18,6 +18,7 @@
 #include <thread>
 #include <vector>
 
+#include "json.hpp"
 #include "opencap/cfcomplete.hpp"
 #include "opencap/core.hpp"
 #include "opencap/kernels.hpp"
@@ -502,6 +503,101 @@ double ref_complete_select_batch(size_t nprob, size_t m, const int* cpu, size_t 
     }
     for (auto& th : pool) th.join();
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- NCF completion + selection of given rows (fused-kernel parity / reference arm)
+//
+// Builds the reference's NCF model file (the layout of NcfModel::to_json,
+// cfcomplete.cpp:215-233 + nn::model_to_json nnkit.cpp:306-330) for a model
+// whose app table holds `nrows` rows (the rows to complete, in order), loads it
+// with NcfModel::from_json (:235-265), then per row: every unobserved cell via
+// NcfModel::predict (:47-58), observed cells verbatim (:208-211), and
+// policy::select_caps (policy.cpp:17-64) on the completed row.  Rows are spread
+// over `threads` std::threads.  *seconds = wall time of the predict + select
+// loop (model parse excluded).
+static std::string ncf_model_json(size_t ka, size_t ks, const size_t* hidden, size_t nh, size_t m, size_t n,
+                                  const double* params, const uint8_t* app_seen, const uint8_t* setting_seen) {
+    std::vector<size_t> dims{ka + ks};
+    std::vector<std::string> acts;
+    for (size_t l = 0; l < nh; ++l) {
+        dims.push_back(hidden[l]);
+        acts.emplace_back("selu");
+    }
+    dims.push_back(1);
+    acts.emplace_back("identity");
+    nlohmann::json doc;
+    doc["format_version"] = 1;
+    doc["architecture"] = {{"dims", dims}, {"activations", acts}};
+    const double* p = params + m * ka + n * ks;
+    nlohmann::json jl = nlohmann::json::array();
+    for (size_t l = 0; l + 1 < dims.size(); ++l) {
+        nlohmann::json w = nlohmann::json::array();
+        for (size_t o = 0; o < dims[l + 1]; ++o) {
+            nlohmann::json row = nlohmann::json::array();
+            for (size_t i = 0; i < dims[l]; ++i) row.push_back(p[o * dims[l] + i]);
+            w.push_back(std::move(row));
+        }
+        p += dims[l] * dims[l + 1];
+        std::vector<double> b(p, p + dims[l + 1]);
+        p += dims[l + 1];
+        jl.push_back({{"weights", std::move(w)}, {"biases", b}});
+    }
+    doc["layers"] = std::move(jl);
+    const auto table = [](const double* v, size_t rows, size_t dim) {
+        nlohmann::json vals = nlohmann::json::array();
+        for (size_t i = 0; i < rows; ++i) vals.push_back(std::vector<double>(v + i * dim, v + (i + 1) * dim));
+        return nlohmann::json{{"rows", rows}, {"dim", dim}, {"values", std::move(vals)}};
+    };
+    doc["embeddings"] = {{"app", table(params, m, ka)}, {"setting", table(params + m * ka, n, ks)}};
+    doc["observed"] = {{"app_seen", std::vector<uint8_t>(app_seen, app_seen + m)},
+                       {"setting_seen", std::vector<uint8_t>(setting_seen, setting_seen + n)}};
+    doc["training"] = {{"seed", 0}, {"epochs_run", 0}, {"initial_train_mse", 0.0}, {"final_train_mse", 0.0},
+                       {"best_val_mse", 0.0}};
+    return doc.dump(2);
+}
+
+int ref_ncf_complete_select_rows(size_t ka, size_t ks, const size_t* hidden, size_t nh, size_t nrows,
+                                 const double* params, const uint8_t* app_seen, const uint8_t* setting_seen,
+                                 const int* cpu, size_t ncpu, const int* gpu, size_t ngpu, const double* values,
+                                 const uint8_t* mask, double gamma, int threads, double* completed, int32_t* idx,
+                                 double* saving, double* loss, int32_t* ncand, double* seconds) {
+    try {
+        const auto grid = make_grid(cpu, ncpu, gpu, ngpu);
+        const size_t n = grid.settings().size();
+        const auto model = cf::NcfModel::from_json(
+            ncf_model_json(ka, ks, hidden, nh, nrows, n, params, app_seen, setting_seen));
+        const policy::SelectionConfig cfg{grid, gamma};
+        const auto settings = grid.settings();
+        std::atomic<int> rc{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        const int nt = std::max(1, threads);
+        for (int t = 0; t < nt; ++t) {
+            pool.emplace_back([&, t] {
+                std::vector<double> row(n);
+                for (size_t i = static_cast<size_t>(t); i < nrows; i += static_cast<size_t>(nt)) {
+                    try {
+                        for (size_t j = 0; j < n; ++j)
+                            row[j] = mask[i * n + j] ? values[i * n + j] : model.predict(i, j);
+                        if (completed) std::copy(row.begin(), row.end(), completed + i * n);
+                        const auto d = policy::select_caps(row, cfg);
+                        idx[i] = static_cast<int32_t>(std::find(settings.begin(), settings.end(), d.setting) -
+                                                      settings.begin());
+                        saving[i] = d.pred_saving;
+                        loss[i] = d.pred_loss;
+                        ncand[i] = static_cast<int32_t>(d.candidates_considered);
+                    } catch (...) {
+                        rc = map_exception();
+                    }
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return rc.load();
+    } catch (...) {
+        return map_exception();
+    }
 }
 
 }  // extern "C"

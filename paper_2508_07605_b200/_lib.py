@@ -176,3 +176,16 @@ _sig("ocg_predictor_destroy", ctypes.c_int, c_vp)
 OCG_PRED_DEVICE_PTRS, OCG_PRED_GENERIC = 1, 2
 _sig("ocg_predict_perf_batch", ctypes.c_int, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i64,
      ctypes.c_int, c_vp)
+
+# fused NCF completion + selection over a whole matrix (ocg_ncf_model_* / ocg_ncf_plan_*)
+OCG_NCF_EXACT, OCG_NCF_FAST = 0, 1
+_sig("ocg_ncf_model_create", ctypes.c_int, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp))
+_sig("ocg_ncf_model_from_json_text", ctypes.c_int, c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp))
+_sig("ocg_ncf_model_destroy", None, c_vp)
+_sig("ocg_ncf_plan_create", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_i32, c_vp, c_i32, c_dbl,
+     ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_vp))
+_sig("ocg_ncf_plan_upload", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_run", ctypes.c_int, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_completed_rows", ctypes.c_int, c_vp, c_vp, c_i64, c_vp)
+_sig("ocg_ncf_plan_destroy", None, c_vp)

@@ -110,7 +110,9 @@ struct ocg_als_plan {
     // capacities: nnz_cap sizes every nnz-dependent buffer (als_alloc), col_cap the CSR arrays;
     // both grow with headroom, so streaming arrivals rarely reallocate.  col_alt/val_alt/rp_alt:
     // the merge target of ocg_als_plan_add_observations (swapped with col/val/row_ptr)
-    int64_t nnz_cap = 0, col_cap = 0, alt_cap = 0;
+    // val_cap / val_next_cap: each value buffer's own size (val swaps with val_alt in
+    // add_observations and with val_next at a staged run, so it cannot share col_cap)
+    int64_t nnz_cap = 0, col_cap = 0, alt_cap = 0, val_cap = 0, val_next_cap = 0;
     Buf<int32_t> col_alt;
     Buf<float> val_alt;
     Buf<int64_t> rp_alt;
@@ -368,6 +370,7 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
     } else {
         P->nnz = row_ptr[m];
         P->col_cap = P->nnz;
+        P->val_cap = P->nnz;
         ALS_CUDA(P->row_ptr.alloc(static_cast<size_t>(m + 1)));
         ALS_CUDA(P->col.alloc(static_cast<size_t>(P->nnz)));
         ALS_CUDA(P->val.alloc(static_cast<size_t>(P->nnz)));
@@ -400,8 +403,11 @@ static int als_set_nnz(ocg_als_plan* P, int64_t nnz) {
         ALS_CUDA(cudaStreamSynchronize(s));
         P->col_cap = grow_cap(nnz);
         ALS_CUDA(P->col.alloc(static_cast<size_t>(P->col_cap)));
-        ALS_CUDA(P->val.alloc(static_cast<size_t>(P->col_cap)));
-        if (P->val_next.p) ALS_CUDA(P->val_next.alloc(static_cast<size_t>(P->col_cap)));
+    }
+    if (nnz > P->val_cap) {
+        ALS_CUDA(cudaStreamSynchronize(s));
+        P->val_cap = grow_cap(nnz);
+        ALS_CUDA(P->val.alloc(static_cast<size_t>(P->val_cap)));
     }
     P->nnz = nnz;
     if (nnz > P->nnz_cap) {
@@ -498,6 +504,16 @@ cudaError_t launch_widen_u16(int64_t n, const uint16_t* in, int32_t* out, cudaSt
 }
 }  // namespace ocg
 
+// side stream + events of the staged (pipelined) upload path, created on first use
+static int als_copy_objs(ocg_als_plan* P) {
+    if (!P->copy_stream) {
+        ALS_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_staged, cudaEventDisableTiming));
+        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_free, cudaEventDisableTiming));
+    }
+    return OCG_OK;
+}
+
 int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const uint16_t* col16, const float* val) {
     if (P && P->staged) return ocg_internal_fail(OCG_E_INVALID, "als upload: a staged CSR is pending (run first)");
     if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
@@ -521,6 +537,14 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
         widen_u16_kernel<<<static_cast<unsigned>((P->nnz + 255) / 256), 256, 0, s>>>(P->nnz, P->col16.p, P->col.p);
         ALS_CUDA(cudaGetLastError());
     }
+    // col16 is read by the widen above: a later _stage_compact must not overwrite it before
+    // the widen has run (its side-stream copy waits on ev_free)
+    {
+        int rc = als_copy_objs(P);
+        if (rc) return rc;
+    }
+    ALS_CUDA(cudaEventRecord(P->ev_free, s));
+    P->free_recorded = true;
     if (mma_rank(P->k)) {
         ALS_CUDA(ocg::launch_absmax(P->nnz, P->val.p, P->maxbits.p + 2, ocg_internal_sm_count(P->ctx), s));
         ALS_CUDA(ocg::launch_als_pack_vals(P->nnz, P->val.p, P->maxbits.p + 2, P->valh.p, s));
@@ -536,12 +560,11 @@ int ocg_als_plan_stage_compact(ocg_als_plan* P, const int64_t* row_ptr, const ui
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
-    if (!P->copy_stream) {
-        ALS_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
-        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_staged, cudaEventDisableTiming));
-        ALS_CUDA(cudaEventCreateWithFlags(&P->ev_free, cudaEventDisableTiming));
+    {
+        int rc = als_copy_objs(P);
+        if (rc) return rc;
     }
-    if (nnz > P->col_cap || nnz > P->nnz_cap || P->col16_cap < nnz || !P->rp_next.p || !P->val_next.p) {
+    if (nnz > P->col_cap || nnz > P->nnz_cap || P->col16_cap < nnz || !P->rp_next.p || nnz > P->val_next_cap) {
         // growth (rare): drain both streams, then size every buffer for nnz
         ALS_CUDA(cudaStreamSynchronize(s));
         ALS_CUDA(cudaStreamSynchronize(P->copy_stream));
@@ -554,7 +577,10 @@ int ocg_als_plan_stage_compact(ocg_als_plan* P, const int64_t* row_ptr, const ui
             ALS_CUDA(P->col16.alloc(static_cast<size_t>(P->col16_cap)));
         }
         if (!P->rp_next.p) ALS_CUDA(P->rp_next.alloc(static_cast<size_t>(P->m + 1)));
-        if (!P->val_next.p) ALS_CUDA(P->val_next.alloc(static_cast<size_t>(P->col_cap)));
+        if (nnz > P->val_next_cap) {
+            P->val_next_cap = grow_cap(nnz);
+            ALS_CUDA(P->val_next.alloc(static_cast<size_t>(P->val_next_cap)));
+        }
     }
     // rp_next / val_next / col16 are free once the step that last used them has passed its
     // swap point (ev_free, recorded on the compute stream)
@@ -629,7 +655,10 @@ int ocg_als_plan_add_observations(ocg_als_plan* P, int64_t count, const int32_t*
     std::swap(P->row_ptr.p, P->rp_alt.p);
     std::swap(P->col.p, P->col_alt.p);
     std::swap(P->val.p, P->val_alt.p);
-    std::swap(P->col_cap, P->alt_cap);
+    // col/val move to the alt pair (both sized alt_cap); the old pair becomes the next merge target
+    const int64_t old_col_cap = P->col_cap, old_val_cap = P->val_cap;
+    P->col_cap = P->val_cap = P->alt_cap;
+    P->alt_cap = std::min(old_col_cap, old_val_cap);
     P->nnz = nnz2;
     if (nnz2 > P->nnz_cap) {
         P->nnz_cap = grow_cap(nnz2);
@@ -691,6 +720,7 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
         ALS_CUDA(cudaStreamWaitEvent(s, P->ev_staged, 0));
         std::swap(P->row_ptr.p, P->rp_next.p);
         std::swap(P->val.p, P->val_next.p);
+        std::swap(P->val_cap, P->val_next_cap);
         P->nnz = P->staged_nnz;
         P->staged = false;
         ALS_CUDA(ocg::launch_widen_u16(P->nnz, P->col16.p, P->col.p, s));

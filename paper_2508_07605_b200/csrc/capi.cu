@@ -561,6 +561,9 @@ int ocg_ctx_flush_l2(ocg_ctx* ctx) {
 
 int ocg_ctx_set_stream(ocg_ctx* ctx, void* stream) {
     if (!ctx) return fail(OCG_E_INVALID, "null context");
+    // work already queued on the current stream must finish before later kernels run on
+    // the new one (they may read what it writes): drain it before switching
+    if (ctx->stream) OCG_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     ctx->own_stream = false;
     ctx->stream = static_cast<cudaStream_t>(stream);
