@@ -2,7 +2,7 @@
 """bench.py — B200 online CF completion + selection (OPEN online phase).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c3|c4|c0xn|ingest]
+                  [--workload c2-ncf|c2|c1-ncf|c1|c3|c4|c0xn|ingest]
 
 One JSON line on rank 0.  For N>1 launch with
 torch.distributed.run; each rank takes an equal shard of the units (weak
@@ -10,8 +10,13 @@ scaling for the sharded workloads), timing is the max over ranks of CUDA-event
 device time.  A "step" is one pass of the hot path over one batch of
 synthetic input:
 
-  c2    SURVEY §8d C2 (BASELINE configs[2]): 1M apps x 4096 settings, rank 32,
-        2% observed — ALS completion + fused imputation + Algorithm-2 selection
+  c2-ncf  (default) SURVEY §8d C2 (BASELINE configs[2]): 1M apps x 4096 settings,
+        rank 32, 2% observed — the reference's CF model (NCF) given fitted weights:
+        cf::complete's imputation of every unobserved cell fused with Algorithm-2
+        selection on every row (FP32 + tcgen05; reference parity: exact mode
+        bit-identical, fast mode within 1e-5); the reference arm runs the same
+        weights through NcfModel::predict + select_caps
+  c2    the same matrix completed by ALS (fit included; no reference counterpart)
   c1    C1 (configs[1]): 10K x 256, rank 8, 5% observed, same path
   c0xn  the reference's own online semantics at scale: N independent apps,
         each cf::complete'd against the paper-scale offline block + selected
@@ -618,8 +623,175 @@ def workload_c4(args, d: Dist):
     return out, ("c4", m)
 
 
+NCF = {  # fused NCF completion + selection (SURVEY §8a a9 + a10): the joint matrices with a fitted model
+    "c2-ncf": dict(JOINT["c2"]),
+    "c1-ncf": dict(JOINT["c1"]),
+}
+NCF_MODEL_SEED, NCF_EMB_SCALE = 5, 0.6
+
+
+def _ncf_flops_per_cell(k):
+    """Algorithmic FP32 work per imputed cell of the fast kernel: layer 0 (A_i + B_j, SELU on 32),
+    layer 1 (32 x 16 MACs, tensor cores), SELU on 16, layer 2 (16 MACs), clamp."""
+    return 32 + 4 * 32 + 2 * 32 * 16 + 16 + 4 * 16 + 2 * 16 + 2
+
+
+def workload_ncf(args, d: Dist):
+    """cf::complete's imputation (cfcomplete.cpp:208-211, NcfModel::predict :47-58) of every
+    unobserved cell of the C2 matrix, fused with policy::select_caps (policy.cpp:17-64) on every
+    row, given a fitted model (reference model-file layout; synthetic weights: the reference cannot
+    fit C2).  Rows shard over ranks with no collective (weak... strong: total rows fixed)."""
+    import torch
+
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+    from paper_2508_07605_b200.dist import shard_rows
+    from paper_2508_07605_b200.ncf import EXACT, FAST, DeviceNcfModel, NcfPlan, model_rows, random_model
+
+    cfg = NCF[args.workload]
+    grid = ocg.PowerGrid.spanning(*cfg["grid"])
+    m, n, k = cfg["m"], grid.n, cfg["rank"]
+    r0, r1 = shard_rows(m, d.world, d.rank)
+    A = synth.joint_csr(m, grid, cfg["density"], cfg["dense_rows"], seed=42, dtype=np.float64, rows=(r0, r1))
+    full = random_model(m, n, k, seed=NCF_MODEL_SEED, emb_scale=NCF_EMB_SCALE)
+    model = model_rows(full, r0, r1)
+    del full
+    m_loc, nnz = A.m, A.nnz
+    ctx = ocg.Context(d.local)
+    dev = torch.device("cuda", d.local)
+    torch.cuda.set_device(dev)
+    dm = DeviceNcfModel(model, ctx=ctx)
+    t_rp, t_col, t_val = (torch.from_numpy(x).to(dev) for x in (A.row_ptr, A.col, A.val))
+    torch.cuda.synchronize(dev)
+    plan = NcfPlan(dm, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, args.gamma, FAST, args.lane,
+                   on_device=True)
+    for _ in range(args.warmup):
+        plan.run(timed=False)
+    idx0 = plan.results(m_loc)[0]
+    assert (idx0 >= 0).all()
+    d.barrier()
+    tot, ph = 0.0, [0.0, 0.0]
+    with Clocks(d.local) as clk:
+        for _ in range(args.steps):
+            ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+            ms, p = plan.run(timed=True)
+            tot += ms
+            ph = [a + b for a, b in zip(ph, p)]
+    d.barrier()
+    t_dev = d.max(tot / 1e3)
+    idx, sav, loss, ncand = plan.results(m_loc)
+    assert np.array_equal(idx, idx0) and (ncand >= 1).all()
+    # the exact (FP64, reference lane order) precision on the same data: one timed step
+    eplan = NcfPlan(dm, t_rp.data_ptr(), t_col.data_ptr(), t_val.data_ptr(), grid, args.gamma, EXACT, args.lane,
+                    on_device=True)
+    ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
+    exact_ms, _ = eplan.run(timed=True)
+    ex_idx = eplan.results(m_loc)[0]
+    agree = float((ex_idx == idx).mean())
+    eplan.close()
+    plan.close()
+    del t_rp, t_col, t_val
+    # end to end through the public API with host buffers: the model is resident (created once);
+    # per step the matrix's CSR crosses PCIe from pinned host memory (ocg_ncf_plan_upload), the
+    # completion + selection runs, and the decisions come back into pinned host memory.
+    pin = [torch.from_numpy(x).pin_memory() for x in (A.row_ptr, A.col, A.val)]
+    h2d_bytes = sum(int(x.numel() * x.element_size()) for x in pin)
+    res = [np.zeros(m_loc, np.int32), np.zeros(m_loc), np.zeros(m_loc), np.zeros(m_loc, np.int32)]
+    p2 = NcfPlan(dm, A.row_ptr, A.col, A.val, grid, args.gamma, FAST, args.lane)
+    p2.run(timed=False)
+    p2.results(m_loc)
+    e2e_steps = max(args.steps, 3)
+    d.barrier()
+    e2e_t = 0.0
+    lib = ocg._lib.lib
+    for _ in range(e2e_steps):
+        ocg._lib.check(lib.ocg_ctx_flush_l2(ctx.handle))
+        t0 = time.perf_counter()
+        p2.upload(*(int(x.data_ptr()) for x in pin))
+        p2.run(timed=False)
+        ocg._lib.check(lib.ocg_ncf_plan_results(p2._h, *(ocg._lib.ptr(r) for r in res)))
+        e2e_t += time.perf_counter() - t0
+    e2e_t = d.max(e2e_t / e2e_steps)
+    assert np.array_equal(res[0], idx)
+    p2.close()
+    dm.close()
+    cells = m * n
+    imputed = m_loc * n - nnz
+    peaks, src = _simt_peaks()
+    dense_ms = ph[1] / args.steps
+    achieved = _ncf_flops_per_cell(k) * imputed / (dense_ms / 1e3) / 1e12
+    out = {
+        "metric": "CF-completed matrix cells/sec",
+        "value": cells * args.steps / t_dev,
+        "unit": "cells/s",
+        "selections_per_sec": m * args.steps / t_dev,
+        "ms_per_step": t_dev * 1e3 / args.steps,
+        "e2e": {"value": cells / e2e_t, "unit": "cells/s", "h2d_bytes_per_step": h2d_bytes * d.world,
+                "d2h_bytes_per_step": int(sum(r.nbytes for r in res)) * d.world, "selections_per_sec": m / e2e_t,
+                "mode": "serial: per step CSR upload (pinned, FP64 values), run, decisions read back; L2 flushed"},
+        "dtype": "f32 (tcgen05 f16 hi/lo layer 1) / f64 selection",
+        "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "hidden": [32, 16],
+                   "observed_per_gpu": nnz, "density": cfg["density"], "offline_dense_rows": cfg["dense_rows"],
+                   "solver": "ncf inference (given a fitted model)", "precision": "fast",
+                   "model": f"reference NCF model layout, synthetic weights (ncf.random_model seed "
+                            f"{NCF_MODEL_SEED}, embeddings +-{NCF_EMB_SCALE})", "gamma": args.gamma,
+                   "parallelism": f"rows sharded over {d.world} GPU(s), no collective" if d.world > 1 else "1 GPU",
+                   "l2": "L2 flushed (256 MB write) before every timed step; CSR %.0f MB/GPU" %
+                         ((A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) / 1e6)},
+        "phases_ms_per_step": {"prep (validate, A/B precompute, baselines, observed cells)": ph[0] / args.steps,
+                               "dense ncf_fast_kernel": dense_ms},
+        "exact_precision": {"ms_per_step": exact_ms, "value": cells / (exact_ms / 1e3) if d.world == 1 else None,
+                            "decisions_equal_to_fast": agree,
+                            "note": "OCG_NCF_EXACT: FP64 in the reference lane's operation order, glibc exp"},
+        "scaling": "strong",
+        "gpu_launches": args.steps * 9,
+        "roofline": {"bound": "fp32", "kernel": "ncf_fast_kernel (tcgen05.mma kind::f16 M128 N16 K16 x6 per "
+                                                "128 cells, TMA-staged B_j tiles)",
+                     "achieved": achieved, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["fp32_tflops"], "traffic": None,
+                     "bytes_per_cell": 0.0,
+                     "note": f"algorithmic {_ncf_flops_per_cell(k)} flop per imputed cell (SURVEY 8d K2) over the "
+                             f"dense kernel's event time; peak = FP32 SIMT {src}. HBM is irrelevant (~1.2 GB/step)."},
+        "clocks": clk.summary(),
+    }
+    return out, (args.workload, m)
+
+
+def reference_ncf(workload: str, threads: int, rows_per_thread: int, lane: int = 1):
+    """The reference's NcfModel::predict of every unobserved cell + policy::select_caps on sampled
+    rows of the same matrix with the same weights (oracle/_ref; inputs generated by the reference's
+    own sim code, no product library).  The per-cell cost is size-independent: linear extrapolation."""
+    import importlib.util
+
+    from oracle import bind
+
+    # the pure-numpy input module, loaded standalone: the reference arm never maps libocg.so
+    spec = importlib.util.spec_from_file_location("ocg_weights", ROOT / "paper_2508_07605_b200" / "weights.py")
+    wmod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(wmod)
+    cfg = NCF[workload]
+    cpu, gpu = wmod.spanning_caps(*cfg["grid"])
+    m, n, k = cfg["m"], len(cpu) * len(gpu), cfg["rank"]
+    nrows = max(1, threads * rows_per_thread)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(m, nrows, replace=False)).astype(np.int64)
+    ref = bind.Ref()
+    ref.force_lane(lane)
+    vals, mask = ref.joint_rows_dense(m, cpu, gpu, cfg["density"], cfg["dense_rows"], rows, seed=42)
+    params = wmod.random_ncf_params(m, n, k, NCF_MODEL_SEED, NCF_EMB_SCALE)
+    sub = bind.sub_model_params(params, m, n, k, k, rows)
+    rc, _, idx, sv, lo, nc, secs = ref.ncf_complete_select_rows(k, k, [32, 16], sub, np.ones(nrows, np.uint8),
+                                                                np.ones(n, np.uint8), cpu, gpu, vals, mask, 0.05,
+                                                                threads, want_completed=False)
+    assert rc == 0, ref.err()
+    desc = (f"{nrows} rows sampled from {workload} ({m} x {n}, rank {k}): reference NcfModel::predict of every "
+            f"unobserved cell + select_caps per row, same weights, AVX2 lane, {threads} threads; per-cell cost is "
+            f"size-independent, so rows/s extrapolate linearly to all {m} rows")
+    return nrows * n / secs, desc, secs
+
+
 WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "c3": workload_joint,
-             "c4": workload_c4, "ingest": workload_ingest}
+             "c4": workload_c4, "ingest": workload_ingest, "c2-ncf": workload_ncf, "c1-ncf": workload_ncf}
 
 
 # -------------------------------------------------------- reference (CPU)
@@ -688,6 +860,11 @@ def reference_joint(workload: str, threads: int, nprob: int, max_epochs: int = 1
 
 
 def cpu_baseline(workload: str, threads: int):
+    if workload in NCF:
+        v1, d1, s1 = reference_ncf(workload, 1, 24)
+        v, desc, secs = reference_ncf(workload, threads, 48)
+        return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
+                "seconds": secs, "one_core": {"value": v1, "sample": d1, "seconds": s1}}
     if workload in JOINT:
         v, desc, secs = reference_joint(workload, threads, nprob=2 * threads)
         return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
@@ -747,6 +924,26 @@ def run_reference(args, d: Dist):
                 "cpu_baseline": {"value": v, "unit": "estimates/s", "cores": threads, "kind": "reference",
                                  "sample": f"{cnt // args.steps} samples per step, pred::predict_perf, AVX2 lane"},
                 "e2e": {"value": v, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    if args.workload in NCF:
+        for _ in range(args.warmup):
+            reference_ncf(args.workload, threads, 4)
+        tot, cells = 0.0, 0
+        for _ in range(args.steps):
+            v, desc, secs = reference_ncf(args.workload, threads, 32)
+            tot += secs
+            cells += v * secs
+        v = cells / tot
+        line = {"impl": "reference", "metric": "CF-completed matrix cells/sec", "value": v, "unit": "cells/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8d generator run by the reference)",
+                "config": {"workload": args.workload, "apps": NCF[args.workload]["m"],
+                           "rank": NCF[args.workload]["rank"], "solver": "ncf inference (given a fitted model)"},
+                "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
+                                 "sample": desc},
+                "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
     if args.workload in JOINT:

@@ -225,6 +225,8 @@ class Ref:
         L.ref_ncf_complete_select_rows.argtypes = [c_sz, c_sz, c_vp, c_sz, c_sz, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
                                                    c_sz, c_vp, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp,
                                                    c_vp, c_vp]
+        L.ref_joint_rows_dense.argtypes = [c_i64, c_vp, c_sz, c_vp, c_sz, c_dbl, c_i64, c_u64, c_vp, c_i64,
+                                           ctypes.c_int, c_vp, c_vp]
         L.ref_complete_select_batch.restype = c_dbl
         L.ref_complete_select_batch.argtypes = [c_sz, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_dbl,
                                                 ctypes.c_int, c_vp]
@@ -312,6 +314,18 @@ class Ref:
                                                  len(cpu), P(gpu), len(gpu), P(values), P(mask), gamma, threads,
                                                  P(comp), P(idx), P(sv), P(lo), P(nc), ctypes.byref(secs))
         return rc, comp, idx, sv, lo, nc, secs.value
+
+    def joint_rows_dense(self, m, cpu, gpu, density, dense_rows, rows, seed=42, as_float=False):
+        """SURVEY 8d joint-matrix rows generated by the reference's own sim/policy code."""
+        cpu, gpu = np.asarray(cpu, np.int32), np.asarray(gpu, np.int32)
+        rows = np.ascontiguousarray(rows, np.int64)
+        n = len(cpu) * len(gpu)
+        vals = np.zeros((len(rows), n))
+        mask = np.zeros((len(rows), n), np.uint8)
+        rc = self.L.ref_joint_rows_dense(m, P(cpu), len(cpu), P(gpu), len(gpu), density, dense_rows, seed, P(rows),
+                                         len(rows), 1 if as_float else 0, P(vals), P(mask))
+        assert rc == 0, self.err()
+        return vals, mask
 
     def offline_default(self, seed=42):
         dense = np.zeros(10 * 20)

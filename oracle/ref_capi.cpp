@@ -600,4 +600,62 @@ int ref_ncf_complete_select_rows(size_t ka, size_t ks, const size_t* hidden, siz
     }
 }
 
+// Rows of the SURVEY §8d joint matrix generated with the reference's own code:
+// specs from sim::make_suite (evaluation role, noise 0.01, m/4 per archetype),
+// the sampled-setting set of ProbePlan::default_plan, a Bernoulli(p) draw over
+// the other columns from Rng(derive_seed(seed, "synth.row", i)), values
+// clamp(sim::true_perf * exp(0.01 N(0,1)), 0.01, 1.25) — the generator the
+// product's synth.cpp restates (tests/test_synth.py pins the two together), so
+// the bench's reference arm needs no product code.  as_float: values rounded
+// through FP32 (as the FP32 CSR carries them).
+int ref_joint_rows_dense(int64_t m, const int* cpu, size_t ncpu, const int* gpu, size_t ngpu, double density,
+                         int64_t dense_rows, uint64_t seed, const int64_t* rows, int64_t nrows, int as_float,
+                         double* values, uint8_t* mask) {
+    try {
+        const auto grid = make_grid(cpu, ncpu, gpu, ngpu);
+        const auto settings = grid.settings();
+        const int64_t n = static_cast<int64_t>(settings.size());
+        sim::SuiteParams sp;
+        const auto q = static_cast<int32_t>(m / 4);
+        sp.counts = {q, q, q, static_cast<int32_t>(m - 3 * static_cast<int64_t>(q))};
+        sp.seed = seed;
+        sp.noise_sigma = 0.01;
+        sp.role = sim::SuiteRole::evaluation;
+        sp.cpu_phase_fraction = 0.0;
+        const auto specs = sim::make_suite(sp, grid);
+        const auto plan = policy::ProbePlan::default_plan(grid);
+        std::vector<uint8_t> in_plan(static_cast<size_t>(n), 0);
+        for (const auto& st : plan.settings)
+            in_plan[static_cast<size_t>(std::find(settings.begin(), settings.end(), st) - settings.begin())] = 1;
+        double p = 0.0;
+        if (m > dense_rows) {
+            const double want = density * static_cast<double>(m) * static_cast<double>(n);
+            const double fixed = static_cast<double>(dense_rows) * n + static_cast<double>(m - dense_rows) *
+                                 static_cast<double>(plan.settings.size());
+            p = (want - fixed) / (static_cast<double>(m - dense_rows) * static_cast<double>(n - plan.settings.size()));
+            p = std::min(1.0, std::max(0.0, p));
+        }
+        std::memset(mask, 0, static_cast<size_t>(nrows * n));
+        std::memset(values, 0, sizeof(double) * static_cast<size_t>(nrows * n));
+        for (int64_t r = 0; r < nrows; ++r) {
+            const int64_t i = rows[r];
+            if (i < 0 || i >= m) throw std::out_of_range("row out of range");
+            Rng rng(derive_seed(seed, "synth.row", static_cast<uint64_t>(i)));
+            for (int64_t j = 0; j < n; ++j) {
+                bool obs = i < dense_rows || in_plan[static_cast<size_t>(j)];
+                if (!obs) obs = rng.uniform() < p;
+                if (!obs) continue;
+                const double v = std::clamp(sim::true_perf(specs[static_cast<size_t>(i)], settings[static_cast<size_t>(j)]) *
+                                                std::exp(0.01 * rng.normal()),
+                                            0.01, 1.25);
+                values[r * n + j] = as_float ? static_cast<double>(static_cast<float>(v)) : v;
+                mask[r * n + j] = 1;
+            }
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 }  // extern "C"

@@ -111,24 +111,20 @@ class NcfPlan:
 
 
 def random_model(m: int, n: int, k: int = 32, seed: int = 0, emb_scale: float = 1.0) -> NcfModel:
-    """Reference-format NCF weights for benches/tests at sizes the reference cannot fit
-    (C2: 1M x 4096, k = 32): embedding rows uniform in +-emb_scale, the MLP with the
-    reference's Glorot-uniform bound (nnkit.cpp:58-61), hidden {32, 16}; the output
-    layer is scaled (x0.25, bias 0.7) so predictions spread over (0.01, 1.25] the way a
-    fitted model's do (random Glorot output weights put ~55 % of cells on a clamp)."""
-    from .api import NcfMeta, ncf_param_count
+    """Reference-format NCF model with synthetic weights (weights.random_ncf_params) for benches and
+    tests at sizes the reference cannot fit (C2: 1M x 4096, k = 32)."""
+    from .api import NcfMeta
+    from .weights import random_ncf_params
+
     h = NcfHyper(app_dim=k, setting_dim=k)
-    rng = np.random.default_rng(seed)
-    parts = [rng.uniform(-emb_scale, emb_scale, m * k), rng.uniform(-emb_scale, emb_scale, n * k)]
-    dims = [2 * k, 32, 16, 1]
-    for l in range(3):
-        b = np.sqrt(6.0 / (dims[l] + dims[l + 1]))
-        w = rng.uniform(-b, b, dims[l] * dims[l + 1])
-        bias = rng.uniform(-0.1, 0.1, dims[l + 1])
-        if l == 2:  # output layer: predictions centred in the normalized-performance range
-            w *= 0.25
-            bias[:] = 0.7
-        parts += [w, bias]
-    p = np.concatenate(parts)
-    assert len(p) == ncf_param_count(m, n, h)
+    p = random_ncf_params(m, n, k, seed, emb_scale)
     return NcfModel(h, m, n, p, np.ones(m, np.uint8), np.ones(n, np.uint8), NcfMeta(seed, 0, 0.0, 0.0, 0.0))
+
+
+def model_rows(model: NcfModel, r0: int, r1: int) -> NcfModel:
+    """The model restricted to app rows [r0, r1) (a rank's shard): NcfModel::predict(i, j)
+    reads only row i of the app table, so a row shard completes its rows identically."""
+    k = model.hyper.app_dim
+    p = np.concatenate([model.params[r0 * k: r1 * k], model.params[model.m * k:]])
+    return NcfModel(model.hyper, r1 - r0, model.n, p, model.app_seen[r0:r1].copy(), model.setting_seen.copy(),
+                    model.meta)
