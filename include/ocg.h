@@ -208,6 +208,59 @@ int ocg_ncf_plan_results(ocg_ncf_plan* plan, int32_t* idx, double* saving, doubl
 int ocg_ncf_plan_completed_rows(ocg_ncf_plan* plan, const int64_t* rows, int64_t nrows, double* out);
 void ocg_ncf_plan_destroy(ocg_ncf_plan* plan);
 
+/* ---- cf:: over one whole matrix, every solver ---------------
+ * Matrix: host CSR row_ptr[m+1] (int64), col[nnz] (int32, strictly ascending per
+ * row), val[nnz] (FP64 in (0, 1.25]), columns in PowerGrid::settings() order.
+ * Rejections mirror PerformanceMatrix::set (core.cpp:142-148: OCG_E_RANGE for a
+ * column index, OCG_E_INVALID for a value) plus the CSR invariants.
+ * Solvers:
+ *   OCG_SOLVER_NCF_REF  the reference's NCF and schedule in FP64, operation order
+ *                       of `lane`: parameters, meta and predictions bit-identical
+ *                       to cf::fit / cf::complete
+ *   OCG_SOLVER_NCF_FAST the same NCF and schedule in FP32 (FP32 tensor-core
+ *                       inference for hidden {32, 16})
+ *   OCG_SOLVER_ALS      rank-k ALS (ocg_als_hyper; no reference counterpart) */
+enum { OCG_SOLVER_NCF_REF = 0, OCG_SOLVER_NCF_FAST = 1, OCG_SOLVER_ALS = 2 };
+
+/* cf::fit (cfcomplete.hpp:59; cfcomplete.cpp:63-196), joint mode: one model over
+ * the whole matrix on the context's GPU.  Outputs (host, each may be NULL):
+ * params in the flat layout [app m x ka | setting n x ks | W0 b0 W1 b1 ...],
+ * app_seen[m], setting_seen[n], meta.  Errors: OCG_E_INVALID bad hyperparameters
+ * / no observed entries (:64-72), OCG_E_DIVERGE non-finite validation loss
+ * (:180), OCG_E_LOGIC non-finite final weight (nnkit.cpp:106-113),
+ * OCG_E_UNSUPPORTED dims beyond the kernel (embedding > 64, hidden > 64,
+ * > 3 hidden layers, batch_size > 32). */
+int ocg_cf_fit(ocg_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+               const ocg_ncf_hyper* hyper, uint64_t seed, int solver, int lane, double* params, uint8_t* app_seen,
+               uint8_t* setting_seen, ocg_ncf_meta* meta);
+/* same, also returning the minibatch steps run and the fit's CUDA-event time */
+int ocg_cf_fit_stats(ocg_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                     const ocg_ncf_hyper* hyper, uint64_t seed, int solver, int lane, double* params, uint8_t* app_seen,
+                     uint8_t* setting_seen, ocg_ncf_meta* meta, int64_t* steps, double* device_ms);
+
+/* ALS hyperparameters (OCG_SOLVER_ALS, ocg_als_plan_*) */
+typedef struct {
+    int32_t rank;   /* 8, 16, 32 or 64 */
+    float lambda;   /* weighted-lambda regularisation */
+    int32_t sweeps; /* row + column half-sweeps per fit */
+    uint64_t seed;  /* V initialisation (ocgo_als_init_value) */
+} ocg_als_hyper;
+
+/* cf::complete (cfcomplete.hpp:63; cfcomplete.cpp:198-213): completed m x n
+ * matrix (observed cells verbatim, every other cell the model's clamped
+ * prediction; fully observed input returned unchanged without a fit), written
+ * row-major into `completed` (host, may be NULL).  With cpu_caps != NULL, also
+ * policy::select_caps (policy.cpp:17-64) of every completed row into
+ * idx/saving/loss/ncand (host, m each) — fused with the imputation, the
+ * completed matrix need not be materialised.  `hyper` is used by the NCF
+ * solvers, `als` by OCG_SOLVER_ALS.  Errors as ocg_cf_fit, plus OCG_E_INVALID
+ * for a row without observed entries (:199-205) and OCG_E_COLD for a cell in a
+ * column that had no observation at fit time (:50-55). */
+int ocg_cf_complete(ocg_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col, const double* val,
+                    const ocg_ncf_hyper* hyper, const ocg_als_hyper* als, uint64_t seed, int solver, int lane,
+                    const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu, double gamma,
+                    double* completed, int32_t* idx, double* saving, double* loss, int32_t* ncand);
+
 /* ---- ALS completion + selection (joint mode) -------
  * No reference counterpart: the reference's CF is NCF only.  Semantics are
  * defined by the CPU oracle (oracle/ocg_oracle.c, ocgo_als_fit): weighted-
@@ -217,12 +270,6 @@ void ocg_ncf_plan_destroy(ocg_ncf_plan* plan);
  * FP32 factors, FP64 selection arithmetic.  Parity vs the reference:
  * unpinned (vs the oracle: within tolerance; selections exact given the
  * completed rows). */
-typedef struct {
-    int32_t rank;   /* 8, 16 or 32 */
-    float lambda;   /* weighted-lambda regularisation */
-    int32_t sweeps; /* row + column half-sweeps per fit */
-    uint64_t seed;  /* V initialisation (ocgo_als_init_value) */
-} ocg_als_hyper;
 
 typedef struct ocg_als_plan ocg_als_plan;
 /* CSR input: row_ptr[m+1] (int64), col[nnz] (int32, ascending per row),

@@ -189,3 +189,12 @@ _sig("ocg_ncf_plan_run", ctypes.c_int, c_vp, c_vp, c_vp)
 _sig("ocg_ncf_plan_results", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_ncf_plan_completed_rows", ctypes.c_int, c_vp, c_vp, c_i64, c_vp)
 _sig("ocg_ncf_plan_destroy", None, c_vp)
+
+# cf:: over one whole matrix, every solver (ocg_cf_fit / ocg_cf_complete)
+OCG_SOLVER_NCF_REF, OCG_SOLVER_NCF_FAST, OCG_SOLVER_ALS = 0, 1, 2
+_sig("ocg_cf_fit", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_u64, ctypes.c_int, ctypes.c_int, c_vp,
+     c_vp, c_vp, c_vp)
+_sig("ocg_cf_fit_stats", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_u64, ctypes.c_int, ctypes.c_int,
+     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_cf_complete", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_u64, ctypes.c_int,
+     ctypes.c_int, c_vp, c_i32, c_vp, c_i32, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp)
