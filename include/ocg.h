@@ -338,6 +338,32 @@ int ocg_als_plan_results_wait(ocg_als_plan* plan);
 int ocg_als_plan_completed_rows(ocg_als_plan* plan, int64_t row0, int64_t nrows, double* out);
 void ocg_als_plan_destroy(ocg_als_plan* plan);
 
+/* ---- file formats (host only, no GPU needed; SURVEY §8b loaders, §8f-2) ----
+ * A host matrix: app ids, one (cpu, gpu) setting per column, observed cells as
+ * CSR (row_ptr int64 [m+1], col int32 ascending, val FP64 in (0, 1.25]).
+ * read_csv   <- read_matrix_csv_file (core.cpp:213-254): OCG_E_MISSING if the file
+ *               is absent, OCG_E_INVALID for config_error (header, labels, ragged
+ *               or non-numeric cells) and invalid_argument (empty / duplicate /
+ *               delimiter-bearing app ids, duplicate settings, a value outside
+ *               (0, 1.25]) — in the reference's check order.
+ * write_csv  <- write_matrix_csv (core.cpp:191-205), round-trip-exact values
+ *               (format_double, core.cpp:171-175): byte-identical to the reference's.
+ * save_bin / load_bin: the same matrix as a binary CSR ("OCGCSR1"; no reference
+ *               counterpart — CSV at C2 is tens of GB of text); load_bin validates
+ *               like ocg_matrix_create. */
+typedef struct ocg_matrix ocg_matrix;
+int ocg_matrix_read_csv(const char* path, ocg_matrix** out);
+int ocg_matrix_write_csv(const ocg_matrix* mat, const char* path);
+int ocg_matrix_create(int64_t m, int64_t n, const char* const* app_ids, const int32_t* cpu, const int32_t* gpu,
+                      const int64_t* row_ptr, const int32_t* col, const double* val, ocg_matrix** out);
+int ocg_matrix_shape(const ocg_matrix* mat, int64_t* m, int64_t* n, int64_t* nnz);
+int ocg_matrix_get(const ocg_matrix* mat, int32_t* cpu, int32_t* gpu, int64_t* row_ptr, int32_t* col, double* val);
+const char* ocg_matrix_app_id(const ocg_matrix* mat, int64_t i);
+int ocg_matrix_save_bin(const ocg_matrix* mat, const char* path);
+int ocg_matrix_load_bin(const char* path, ocg_matrix** out);
+void ocg_matrix_destroy(ocg_matrix* mat);
+
+
 /* ---- synthetic inputs (benches/tests; host only, no GPU needed) --------
  * Restatements of the reference's input generators so benches never need
  * the reference: sim::make_suite (simnode.cpp:192-244), sim::true_perf
@@ -412,6 +438,19 @@ int ocg_predictor_create(ocg_ctx* ctx, int32_t n_layers, const int64_t* dims, co
 int ocg_predictor_run(ocg_predictor* pred, const double* counters, int64_t count, int lane, double* out,
                       uint32_t flags);
 int ocg_predictor_destroy(ocg_predictor* pred);
+
+/* Predictor model file <- pred::load_predictor / predictor_from_json
+ * (predictor.cpp:301-331) over nn::model_from_json (nnkit.cpp:332-365), with
+ * the same checks: OCG_E_MISSING absent file; OCG_E_LOGIC bad json, format_version,
+ * inconsistent architecture, weight / bias / feature_stats shapes, non-finite
+ * weight; OCG_E_INVALID unknown activation.
+ * parse: two-phase (NULL arrays query n_layers / nparams); acts 0 selu, 1 relu,
+ * 2 identity; params per layer W (out x in, row-major) then b.
+ * load / from_json: parse, then ocg_predictor_create on the context's device. */
+int ocg_predictor_parse(const char* text, int32_t* n_layers, int64_t* dims, int32_t* acts, double* params,
+                        int64_t* nparams, double* mean7, double* std7, int* has_stats);
+int ocg_predictor_from_json(ocg_ctx* ctx, const char* text, ocg_predictor** out);
+int ocg_predictor_load(ocg_ctx* ctx, const char* path, ocg_predictor** out);
 
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */

@@ -227,6 +227,8 @@ class Ref:
                                                    c_vp, c_vp]
         L.ref_joint_rows_dense.argtypes = [c_i64, c_vp, c_sz, c_vp, c_sz, c_dbl, c_i64, c_u64, c_vp, c_i64,
                                            ctypes.c_int, c_vp, c_vp]
+        L.ref_matrix_csv_roundtrip.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_vp, c_vp, c_vp]
+        L.ref_load_predictor.argtypes = [ctypes.c_char_p, c_vp]
         L.ref_complete_select_batch.restype = c_dbl
         L.ref_complete_select_batch.argtypes = [c_sz, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_dbl,
                                                 ctypes.c_int, c_vp]
@@ -326,6 +328,18 @@ class Ref:
                                          len(rows), 1 if as_float else 0, P(vals), P(mask))
         assert rc == 0, self.err()
         return vals, mask
+
+    def matrix_csv_roundtrip(self, in_path, out_path=None):
+        """read_matrix_csv_file (+ write_matrix_csv): (rc, (m, n, nnz))."""
+        m, n, nnz = c_sz(), c_sz(), c_sz()
+        rc = self.L.ref_matrix_csv_roundtrip(str(in_path).encode(), None if out_path is None else str(out_path).encode(),
+                                             ctypes.byref(m), ctypes.byref(n), ctypes.byref(nnz))
+        return rc, (m.value, n.value, nnz.value)
+
+    def load_predictor(self, path):
+        hs = ctypes.c_int()
+        rc = self.L.ref_load_predictor(str(path).encode(), ctypes.byref(hs))
+        return rc, bool(hs.value)
 
     def offline_default(self, seed=42):
         dense = np.zeros(10 * 20)

@@ -658,4 +658,31 @@ int ref_joint_rows_dense(int64_t m, const int* cpu, size_t ncpu, const int* gpu,
     }
 }
 
+// read_matrix_csv_file (core.cpp:250-254) then, if out_path, write_matrix_csv
+// (core.cpp:208-211): the reference's own loader / writer for format tests
+int ref_matrix_csv_roundtrip(const char* in_path, const char* out_path, size_t* m, size_t* n, size_t* nnz) {
+    try {
+        const auto pm = read_matrix_csv_file(in_path);
+        if (m) *m = pm.rows();
+        if (n) *n = pm.cols();
+        if (nnz) *nnz = pm.observed_count();
+        if (out_path) write_matrix_csv(pm, std::string(out_path));
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// pred::load_predictor (predictor.cpp:325-331): 0 or the mapped exception
+int ref_load_predictor(const char* path, int* has_stats) {
+    try {
+        const auto model = pred::load_predictor(path);
+        if (has_stats) *has_stats = model.has_stats ? 1 : 0;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 }  // extern "C"
+

@@ -5,4 +5,4 @@ runs in sm_100a kernels behind the C-ABI in include/ocg.h (libocg.so).
 """
 from .api import *  # noqa: F401,F403
 from .api import OnlineBatchResult, META_DTYPE, default_context  # noqa: F401
-from ._lib import OcgError, InvalidArgument, OutOfRange, ColdError, DivergenceError, CudaError  # noqa: F401
+from ._lib import OcgError, InvalidArgument, MissingArtifact, OutOfRange, ColdError, DivergenceError, CudaError  # noqa: F401

@@ -117,7 +117,11 @@ class CudaError(OcgError):
     pass
 
 
-_EXC = {OCG_E_INVALID: InvalidArgument, OCG_E_RANGE: OutOfRange, OCG_E_COLD: ColdError,
+class MissingArtifact(OcgError, FileNotFoundError):
+    pass
+
+
+_EXC = {OCG_E_INVALID: InvalidArgument, OCG_E_MISSING: MissingArtifact, OCG_E_RANGE: OutOfRange, OCG_E_COLD: ColdError,
         OCG_E_DIVERGE: DivergenceError, OCG_E_CUDA: CudaError}
 
 
@@ -198,3 +202,17 @@ _sig("ocg_cf_fit_stats", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_v
      c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_cf_complete", ctypes.c_int, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_u64, ctypes.c_int,
      ctypes.c_int, c_vp, c_i32, c_vp, c_i32, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp)
+
+# file formats (host only): matrix CSV / binary CSR, predictor model file
+_sig("ocg_matrix_read_csv", ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(c_vp))
+_sig("ocg_matrix_write_csv", ctypes.c_int, c_vp, ctypes.c_char_p)
+_sig("ocg_matrix_create", ctypes.c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_vp))
+_sig("ocg_matrix_shape", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_matrix_get", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_matrix_app_id", ctypes.c_char_p, c_vp, c_i64)
+_sig("ocg_matrix_save_bin", ctypes.c_int, c_vp, ctypes.c_char_p)
+_sig("ocg_matrix_load_bin", ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(c_vp))
+_sig("ocg_matrix_destroy", None, c_vp)
+_sig("ocg_predictor_parse", ctypes.c_int, ctypes.c_char_p, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_predictor_from_json", ctypes.c_int, c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp))
+_sig("ocg_predictor_load", ctypes.c_int, c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp))

@@ -67,6 +67,11 @@ int bits_for(int64_t n) {
 
 struct ocg_als_plan {
     ocg_ctx* ctx = nullptr;
+    // input validation (run on the device before every fit on a new CSR): error bits
+    // (1 << OCG_E_*) and a column-seen bitmap; dirty = the CSR changed since the last check
+    Buf<int> err;
+    Buf<unsigned> seen;
+    bool dirty = true;
     int64_t m = 0, n = 0, nnz = 0;
     int k = 32, sweeps = 10;
     int warm_sweeps = 0;  // > 0: runs keep the previous factors (no V init) and do this many sweeps
@@ -322,6 +327,111 @@ static int als_alloc_fixed(ocg_als_plan* P) {
     return OCG_OK;
 }
 
+// The checks the reference applies to the same matrix (PerformanceMatrix::set,
+// core.cpp:142-148: out_of_range for a column index, invalid_argument for a value
+// outside (0, 1.25]; cf::complete, cfcomplete.cpp:199-205: invalid_argument for a
+// row without observations; NcfModel::predict :53-55: a cold setting column),
+// plus sorted unique columns per row.  Bad entries are neutralised in place
+// (column 0, value 1) so the fit that follows stays in bounds; the run's results
+// then report the error instead of decisions.  One warp per row.
+__global__ void als_validate_kernel(int64_t m, int64_t n, const int64_t* __restrict__ rp, int32_t* col, float* val,
+                                    unsigned* seen, int* err) {
+    extern __shared__ unsigned sseen[];
+    const int nw = static_cast<int>((n + 31) / 32);
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) sseen[w] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    int bits = 0;
+    for (int64_t i = gw; i < m; i += nwarps) {
+        const int64_t b = rp[i], e = rp[i + 1];
+        if (e <= b) bits |= 1 << OCG_E_INVALID;
+        int32_t carry = -1;  // last column of the previous chunk
+        for (int64_t q0 = b; q0 < e; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const bool on = q < e;
+            const int32_t c = on ? col[q] : 0;
+            const float v = on ? val[q] : 1.0f;
+            int32_t prev = __shfl_up_sync(0xffffffffu, c, 1);
+            if (lane == 0) prev = carry;
+            carry = __shfl_sync(0xffffffffu, c, 31);
+            if (on) {
+                const bool in = c >= 0 && c < n;
+                if (!in) {
+                    bits |= 1 << OCG_E_RANGE;
+                    col[q] = 0;
+                } else {
+                    atomicOr(sseen + (c >> 5), 1u << (c & 31));
+                }
+                if (q > b && prev >= c) bits |= 1 << OCG_E_INVALID;
+                if (!(v > 0.0f && v <= 1.25f)) {  // NaN fails too
+                    bits |= 1 << OCG_E_INVALID;
+                    val[q] = 1.0f;
+                }
+            }
+        }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits) atomicOr(err, bits);
+    __syncthreads();
+    for (int w = threadIdx.x; w < nw; w += blockDim.x)
+        if (sseen[w]) atomicOr(seen + w, sseen[w]);
+}
+
+__global__ void als_cold_kernel(int64_t n, const unsigned* seen, int* err) {
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
+        if (!((seen[j >> 5] >> (j & 31)) & 1u)) {
+            atomicOr(err, 1 << OCG_E_COLD);
+            return;
+        }
+}
+
+static int als_validate(ocg_als_plan* P) {
+    if (!P->dirty) return OCG_OK;
+    cudaStream_t s = ocg_internal_stream(P->ctx);
+    const int nw = static_cast<int>((P->n + 31) / 32);
+    if (!P->err.p) {
+        ALS_CUDA(P->err.alloc(1));
+        ALS_CUDA(P->seen.alloc(static_cast<size_t>(nw)));
+    }
+    ALS_CUDA(cudaMemsetAsync(P->err.p, 0, sizeof(int), s));
+    ALS_CUDA(cudaMemsetAsync(P->seen.p, 0, sizeof(unsigned) * nw, s));
+    if (P->m > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>((P->m + 7) / 8, 4 * ocg_internal_sm_count(P->ctx)));
+        als_validate_kernel<<<grid, 256, sizeof(unsigned) * nw, s>>>(P->m, P->n, P->row_ptr.p, P->col.p, P->val.p,
+                                                                      P->seen.p, P->err.p);
+        ALS_CUDA(cudaGetLastError());
+        als_cold_kernel<<<1, 256, 0, s>>>(P->n, P->seen.p, P->err.p);
+        ALS_CUDA(cudaGetLastError());
+    }
+    P->dirty = false;
+    return OCG_OK;
+}
+
+// error of the last validated CSR (synchronises the stream), reported like the reference would throw
+static int als_error(ocg_als_plan* P) {
+    if (!P->err.p) return OCG_OK;
+    int bits = 0;
+    ALS_CUDA(cudaMemcpyAsync(&bits, P->err.p, sizeof(int), cudaMemcpyDeviceToHost, ocg_internal_stream(P->ctx)));
+    ALS_CUDA(cudaStreamSynchronize(ocg_internal_stream(P->ctx)));
+    if (bits & (1 << OCG_E_RANGE)) return ocg_internal_fail(OCG_E_RANGE, "matrix index out of range");
+    if (bits & (1 << OCG_E_INVALID))
+        return ocg_internal_fail(OCG_E_INVALID, "als: a row without observed entries, a value outside (0, 1.25] "
+                                                "or unsorted / repeated columns");
+    if (bits & (1 << OCG_E_COLD))
+        return ocg_internal_fail(OCG_E_COLD, "als: cold setting column (no observed entries at fit time)");
+    return OCG_OK;
+}
+
+// row_ptr invariants, host side (the device check covers columns and values)
+static int check_row_ptr(const int64_t* rp, int64_t m) {
+    if (rp[0] != 0) return ocg_internal_fail(OCG_E_INVALID, "csr: row_ptr[0] must be 0");
+    for (int64_t i = 0; i < m; ++i)
+        if (rp[i + 1] < rp[i]) return ocg_internal_fail(OCG_E_INVALID, "csr: row_ptr must be non-decreasing");
+    return OCG_OK;
+}
+
 static int als_check(int64_t m, int64_t n, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu,
                      const ocg_als_hyper* h, double gamma) {
     if (!h) return ocg_internal_fail(OCG_E_INVALID, "als: null hyperparameters");
@@ -332,8 +442,13 @@ static int als_check(int64_t m, int64_t n, const int32_t* cpu, int32_t ncpu, con
     if (gamma <= 0.0 || gamma >= 1.0) return ocg_internal_fail(OCG_E_INVALID, "select_caps: gamma must lie in (0, 1)");
     if (static_cast<int64_t>(ncpu) * ngpu != n) return ocg_internal_fail(OCG_E_INVALID, "row length does not cover the grid");
     if (ncpu + ngpu > 512) return ocg_internal_fail(OCG_E_UNSUPPORTED, "grid too large");
-    (void)cpu;
-    (void)gpu;
+    if (!cpu || !gpu) return ocg_internal_fail(OCG_E_INVALID, "cap list is empty");
+    for (int32_t k = 0; k < ncpu; ++k)  // PowerGrid (core.cpp:38-45)
+        if (cpu[k] <= 0 || (k > 0 && cpu[k] <= cpu[k - 1]))
+            return ocg_internal_fail(OCG_E_INVALID, "cpu caps must be positive and strictly increasing");
+    for (int32_t k = 0; k < ngpu; ++k)
+        if (gpu[k] <= 0 || (k > 0 && gpu[k] <= gpu[k - 1]))
+            return ocg_internal_fail(OCG_E_INVALID, "gpu caps must be positive and strictly increasing");
     return OCG_OK;
 }
 
@@ -368,6 +483,7 @@ int ocg_als_plan_create(ocg_ctx* ctx, int64_t m, const int64_t* row_ptr, const i
         P->val.p = const_cast<float*>(val);
         P->val.own = false;
     } else {
+        if ((rc = check_row_ptr(row_ptr, m))) return rc;
         P->nnz = row_ptr[m];
         P->col_cap = P->nnz;
         P->val_cap = P->nnz;
@@ -422,6 +538,7 @@ int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* 
     if (P && P->staged) return ocg_internal_fail(OCG_E_INVALID, "als upload: a staged CSR is pending (run first)");
     if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (int rc = check_row_ptr(row_ptr, P->m)) return rc;
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
@@ -429,6 +546,7 @@ int ocg_als_plan_upload(ocg_als_plan* P, const int64_t* row_ptr, const int32_t* 
         int rc = als_set_nnz(P, nnz);
         if (rc) return rc;
     }
+    P->dirty = true;
     ALS_CUDA(cudaMemcpyAsync(P->row_ptr.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->col.p, col, sizeof(int32_t) * P->nnz, cudaMemcpyHostToDevice, s));
     ALS_CUDA(cudaMemcpyAsync(P->val.p, val, sizeof(float) * P->nnz, cudaMemcpyHostToDevice, s));
@@ -519,6 +637,7 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
     if (!P || !row_ptr || !col16 || !val) return ocg_internal_fail(OCG_E_INVALID, "null plan/buffer");
     if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als upload_compact: more than 65536 settings");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
+    if (int rc = check_row_ptr(row_ptr, P->m)) return rc;
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
@@ -526,6 +645,7 @@ int ocg_als_plan_upload_compact(ocg_als_plan* P, const int64_t* row_ptr, const u
         int rc = als_set_nnz(P, nnz);
         if (rc) return rc;
     }
+    P->dirty = true;
     if (P->col16_cap < nnz) {
         ALS_CUDA(P->col16.alloc(static_cast<size_t>(nnz)));
         P->col16_cap = nnz;
@@ -557,6 +677,7 @@ int ocg_als_plan_stage_compact(ocg_als_plan* P, const int64_t* row_ptr, const ui
     if (P->n > 65536) return ocg_internal_fail(OCG_E_INVALID, "als stage_compact: more than 65536 settings");
     if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "als upload: plan uses caller device buffers");
     if (P->staged) return ocg_internal_fail(OCG_E_INVALID, "als stage_compact: a staged CSR is pending (run first)");
+    if (int rc = check_row_ptr(row_ptr, P->m)) return rc;
     const int64_t nnz = row_ptr[P->m];
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als upload: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
@@ -607,7 +728,10 @@ int ocg_als_plan_add_observations(ocg_als_plan* P, int64_t count, const int32_t*
             return ocg_internal_fail(OCG_E_INVALID, "als add_observations: cell out of range");
         if (t > 0 && (rows[t] < rows[t - 1] || (rows[t] == rows[t - 1] && cols[t] <= cols[t - 1])))
             return ocg_internal_fail(OCG_E_INVALID, "als add_observations: cells not sorted by (row, col) / repeated");
+        if (!(vals[t] > 0.0f && vals[t] <= 1.25f))  // PerformanceMatrix::set (core.cpp:144-146)
+            return ocg_internal_fail(OCG_E_INVALID, "normalized performance outside (0, 1.25]");
     }
+    P->dirty = true;
     const int64_t nnz2 = P->nnz + count;
     if (nnz2 >= (int64_t(1) << 31)) return ocg_internal_fail(OCG_E_INVALID, "als add_observations: bad nnz");
     cudaStream_t s = ocg_internal_stream(P->ctx);
@@ -730,9 +854,11 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
         }
         ALS_CUDA(cudaEventRecord(P->ev_free, s));
         P->free_recorded = true;
+        P->dirty = true;
     }
-    int rc = als_build_csc(P);
+    int rc = als_validate(P);
     if (rc) return rc;
+    if ((rc = als_build_csc(P))) return rc;
     const bool warm = P->warm_sweeps > 0 && P->fitted;
     if (!warm) {
         ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, s));
@@ -799,7 +925,9 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
 // (all asynchronous on the context stream; see ocg_ctx_set_stream)
 int ocg_als_plan_begin(ocg_als_plan* P) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
-    int rc = als_build_csc(P);
+    int rc = als_validate(P);
+    if (rc) return rc;
+    rc = als_build_csc(P);
     if (rc) return rc;
     ALS_CUDA(ocg::launch_als_init(P->n, P->k, P->seed, P->V.p, ocg_internal_stream(P->ctx)));
     return als_pack(P, 1);
@@ -846,6 +974,8 @@ int ocg_als_plan_select(ocg_als_plan* P) {
 int ocg_als_plan_results(ocg_als_plan* P, int32_t* idx, double* saving, double* loss, int32_t* ncand, float* U,
                          float* V) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    if (idx || saving || loss || ncand)  // decisions of a rejected matrix are not returned (factors stay inspectable)
+        if (int rc = als_error(P)) return rc;
     cudaStream_t s = ocg_internal_stream(P->ctx);
     const size_t m = static_cast<size_t>(P->m);
     if (idx) ALS_CUDA(cudaMemcpyAsync(idx, P->idx.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
@@ -874,13 +1004,14 @@ int ocg_als_plan_results_async(ocg_als_plan* P, int32_t* idx, double* saving, do
 int ocg_als_plan_results_wait(ocg_als_plan* P) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
     if (P->ev_results) ALS_CUDA(cudaEventSynchronize(P->ev_results));
-    return OCG_OK;
+    return als_error(P);
 }
 
 // completed rows [row0, row0+nrows) as the selection saw them (FP64), for tests
 int ocg_als_plan_completed_rows(ocg_als_plan* P, int64_t row0, int64_t nrows, double* out) {
     if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
     if (row0 < 0 || nrows < 0 || row0 + nrows > P->m) return ocg_internal_fail(OCG_E_RANGE, "row range");
+    if (int rc = als_error(P)) return rc;
     cudaStream_t s = ocg_internal_stream(P->ctx);
     Buf<double> d;
     Buf<int32_t> di, dn;

@@ -5,7 +5,6 @@ JSON + feature_stats, predictor.cpp:292-316)."""
 from __future__ import annotations
 
 import ctypes
-import json
 from dataclasses import dataclass
 
 import numpy as np
@@ -27,20 +26,24 @@ class PredictorModel:
 
     @staticmethod
     def from_json(text: str) -> "PredictorModel":
-        """pred::predictor_from_json (predictor.cpp:302-316) / nn::model_from_json (nnkit.cpp:332-365)."""
-        doc = json.loads(text)
-        if doc.get("format_version") != 1:
-            raise ValueError("model file: unsupported format_version")
-        dims = [int(d) for d in doc["architecture"]["dims"]]
-        acts = [_ACT[a] for a in doc["architecture"]["activations"]]
-        parts = []
-        for layer in doc["layers"]:
-            parts.append(np.asarray(layer["weights"], np.float64).ravel())
-            parts.append(np.asarray(layer["biases"], np.float64).ravel())
-        fs = doc.get("feature_stats")
-        mean = np.asarray(fs["mean"] if fs else [0.0] * 7, np.float64)
-        std = np.asarray(fs["std"] if fs else [1.0] * 7, np.float64)
-        return PredictorModel(dims, acts, np.concatenate(parts), mean, std, fs is not None)
+        """pred::predictor_from_json (predictor.cpp:302-316) / nn::model_from_json (nnkit.cpp:332-365),
+        with the reference's shape / finiteness / activation checks (parsed in C++, formats.cpp)."""
+        from .formats import parse_predictor
+
+        dims, acts, params, mean, std, has_stats = parse_predictor(text)
+        return PredictorModel([int(d) for d in dims], [int(a) for a in acts], params, mean, std, has_stats)
+
+    @staticmethod
+    def load(path) -> "PredictorModel":
+        """pred::load_predictor (predictor.cpp:325-331): OCG_E_MISSING if the file is absent."""
+        from pathlib import Path
+
+        from ._lib import MissingArtifact, OCG_E_MISSING
+
+        p = Path(path)
+        if not p.is_file():
+            raise MissingArtifact(OCG_E_MISSING, f"missing predictor model: {path}")
+        return PredictorModel.from_json(p.read_text())
 
 
 def predict_perf_batch(model: PredictorModel, counters, lane: int = LANE_AVX2,

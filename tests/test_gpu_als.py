@@ -173,7 +173,9 @@ def test_als_upload_refit_matches_fresh_plan(ctx):
 def test_als_rank32_multisegment_rows_and_empty_items(ctx, port):
     """Rank 32 (tensor-core path) with rows longer than one segment (dense rows over
     2048 settings -> 2 segments, reduced in segment order), a column nobody observed
-    (zero factor, like ocgo_als_fit) and an app row with no observations."""
+    (zero factor, like ocgo_als_fit) and an app row with no observations.  Such a
+    matrix is rejected for decisions (test_gpu_als_validation.py); the factors stay
+    inspectable and match the oracle."""
     from oracle import bind
     from paper_2508_07605_b200 import PowerGrid
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
@@ -285,7 +287,9 @@ def test_als_stage_compact_pipelined_matches_upload(ctx):
 def test_als_csc_packed_keys_identical_to_pair_sort(ctx, k, monkeypatch):
     """The packed 32-bit-key CSC build (col << rb | row, default when m and n fit) and the
     64-bit-payload radix sort (OCG_CSC_PAIRS=1) give the same CSC, so the fits are
-    bit-identical; includes fully observed rows and an empty row."""
+    bit-identical; includes fully observed rows and an empty row (which makes the
+    matrix invalid for decisions, as cf::complete refuses it; the factors compare)."""
+    import paper_2508_07605_b200 as ocg
     from paper_2508_07605_b200.als import AlsHyper, AlsPlan
     from paper_2508_07605_b200.synth import CsrMatrix
 
@@ -301,7 +305,9 @@ def test_als_csc_packed_keys_identical_to_pair_sort(ctx, k, monkeypatch):
         monkeypatch.setenv("OCG_CSC_PAIRS", forced)
         plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, 0.05, ctx=ctx)
         plan.run()
-        out.append(plan.factors() + plan.results())
+        out.append(plan.factors())
+        with pytest.raises(ocg.InvalidArgument):
+            plan.results()
         plan.close()
     for a, b in zip(out[0], out[1]):
         np.testing.assert_array_equal(a, b)
