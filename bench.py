@@ -17,6 +17,8 @@ synthetic input:
         bit-identical, fast mode within 1e-5); the reference arm runs the same
         weights through NcfModel::predict + select_caps
   c2    the same matrix completed by ALS (fit included; no reference counterpart)
+  c1-fit  C1 (configs[1]) through the reference's whole CF path, bit for bit: cf::fit
+        (NCF, reference schedule, early stopping) + imputation + selection
   c1    C1 (configs[1]): 10K x 256, rank 8, 5% observed, same path
   c0xn  the reference's own online semantics at scale: N independent apps,
         each cf::complete'd against the paper-scale offline block + selected
@@ -101,57 +103,108 @@ class Dist:
 
 
 class Clocks:
-    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md)."""
+    """SM clock and clock-event (throttle) reasons during the timed region, read through
+    NVML (the library nvidia-smi uses): a sampler thread every 10 ms plus one sample per
+    step (tick()), so even a sub-second timed region carries >= steps samples
+    (B200_PROFILING.md clocks line; falls back to nvidia-smi -lms 200 without NVML)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.sm, self.reasons, self.smax = [], set(), None
+        self.nvml = None
+        self.stop = threading.Event()
+        self.thread = None
+        self.smi = None
+
+    def _sample(self):
+        try:
+            self.sm.append(float(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM)))
+            bits = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS:
+                if bits & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def tick(self):
+        if self.nvml:
+            self._sample()
 
     def __enter__(self):
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while not self.stop.is_set():
+                    self._sample()
+                    time.sleep(0.01)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
+            try:
+                fd, self.path = tempfile.mkstemp(suffix=".csv")
+                os.close(fd)
+                self.smi = subprocess.Popen(["nvidia-smi", f"--id={self.device}",
+                                             "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                                             "clocks_event_reasons.sw_thermal_slowdown,"
+                                             "clocks_event_reasons.hw_thermal_slowdown,"
+                                             "clocks_event_reasons.sw_power_cap",
+                                             "--format=csv,noheader,nounits", "-lms", "200"],
+                                            stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except Exception:
+                self.smi = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if self.smi:
+            self.smi.terminate()
             try:
-                self.proc.wait(timeout=5)
+                self.smi.wait(timeout=5)
             except Exception:
-                self.proc.kill()
+                self.smi.kill()
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    self.sm.append(float(f[0]))
+                    self.smax = float(f[1])
+                except (ValueError, IndexError):
+                    continue
+                for (name, _), v in zip(self.REASONS, f[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(name)
+            os.unlink(self.path)
 
     def summary(self):
-        if not self.path or not os.path.exists(self.path):
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
-            except ValueError:
-                continue
-            for name, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        os.unlink(self.path)
-        load = [s for s in sm if smax and s > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": ["no clock samples"], "samples": 0}
+        load = [x for x in self.sm if self.smax and x > 0.5 * self.smax] or self.sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": self.smax, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self.nvml else "nvidia-smi"}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 # --------------------------------------------------------------- workloads
@@ -182,6 +235,7 @@ def workload_c0xn(args, d: Dist):
         for _ in range(args.steps):
             ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
             ms += plan.run(timed=True)
+            clk.tick()
     d.barrier()
     t_dev = d.max(ms / 1e3)
     res = plan.results()
@@ -283,6 +337,7 @@ def workload_ingest(args, d: Dist):
             e0.record(stream)
             pred.run_device(c_dev.data_ptr(), count, out.data_ptr(), args.lane)
             e1.record(stream)
+            clk.tick()
         torch.cuda.synchronize()
     ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
     d.barrier()
@@ -401,6 +456,7 @@ def workload_joint(args, d: Dist):
         for _ in range(args.steps):
             ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
             ms, ph = step()
+            clk.tick()
             tot_ms += ms
             phases = [a + b for a, b in zip(phases, ph)]
     torch.cuda.synchronize(dev)
@@ -516,7 +572,7 @@ def workload_joint(args, d: Dist):
         g_row = phases[4] / args.steps / args.sweeps
         g_col = phases[5] / args.steps / args.sweeps
         if g_row > 0 and g_col > 0:
-            kern, t_row, t_col = "als_mma_gram_kernel<32> (K3 Gram accumulation, mma.sync f16 hi/lo)", g_row, g_col
+            kern, t_row, t_col = f"als_mma_gram_kernel<{k}> (K3 Gram accumulation, mma.sync f16 hi/lo)", g_row, g_col
         else:  # rank 8/16: the fused SIMT Gram + solve kernel; whole half-sweeps
             kern, t_row, t_col = "als_seg_gram_kernel (K3 Gram + K4 solve, SIMT)", row_ms, col_ms
         achieved = (row_bytes + col_bytes) / 2 / ((t_row + t_col) / 2 / 1e3) / 1e9
@@ -675,6 +731,7 @@ def workload_ncf(args, d: Dist):
         for _ in range(args.steps):
             ocg._lib.check(ocg._lib.lib.ocg_ctx_flush_l2(ctx.handle))
             ms, p = plan.run(timed=True)
+            clk.tick()
             tot += ms
             ph = [a + b for a, b in zip(ph, p)]
     d.barrier()
@@ -757,6 +814,35 @@ def workload_ncf(args, d: Dist):
     return out, (args.workload, m)
 
 
+def _weights_module():
+    """The pure-numpy input module loaded standalone: the reference arm never maps libocg.so."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("ocg_weights", ROOT / "paper_2508_07605_b200" / "weights.py")
+    wmod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(wmod)
+    return wmod
+
+
+def composed_fit(k, m, n, density):
+    """The reference's cf::fit at a size it cannot run, composed from its own components timed
+    here: one minibatch step = dense embedding-gradient zeroing + 32 x
+    nn::backprop_sample + nn::AdamState::step over every parameter; x steps per epoch."""
+    from oracle import bind
+
+    ref = bind.Ref()
+    ref.force_lane(1)
+    secs, parts = ref.time_fit_step(m, n, k, (32, 16), iters=3)
+    nnz = density * m * n
+    steps = int(np.ceil(0.9 * nnz / 32))
+    return {"kind": "composed", "seconds_per_step": secs,
+            "parts_s": {"grad_zeroing": parts[0], "backprop_32_samples": parts[1], "adam_all_params": parts[2]},
+            "steps_per_epoch": steps, "hours_per_epoch": secs * steps / 3600, "cores": 1,
+            "note": "reference cf::fit minibatch step composed from its own components at this model size "
+                    "(oracle/_ref ref_time_fit_step, AVX2 lane, 1 core: the reference is single-threaded); "
+                    "an early-stopped fit runs hundreds of epochs"}
+
+
 def reference_ncf(workload: str, threads: int, rows_per_thread: int, lane: int = 1):
     """The reference's NcfModel::predict of every unobserved cell + policy::select_caps on sampled
     rows of the same matrix with the same weights (oracle/_ref; inputs generated by the reference's
@@ -765,10 +851,7 @@ def reference_ncf(workload: str, threads: int, rows_per_thread: int, lane: int =
 
     from oracle import bind
 
-    # the pure-numpy input module, loaded standalone: the reference arm never maps libocg.so
-    spec = importlib.util.spec_from_file_location("ocg_weights", ROOT / "paper_2508_07605_b200" / "weights.py")
-    wmod = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(wmod)
+    wmod = _weights_module()
     cfg = NCF[workload]
     cpu, gpu = wmod.spanning_caps(*cfg["grid"])
     m, n, k = cfg["m"], len(cpu) * len(gpu), cfg["rank"]
@@ -790,8 +873,137 @@ def reference_ncf(workload: str, threads: int, rows_per_thread: int, lane: int =
     return nrows * n / secs, desc, secs
 
 
+C1_FIT = dict(JOINT["c1"])
+C1_GOLDEN_EPOCHS = {1: 388, 0: 374}  # the reference's own full C1 fit (tests/golden/joint_c1_lane*.npz)
+
+
+def workload_c1_fit(args, d: Dist):
+    """The reference's complete online CF path at C1 (BASELINE configs[1]), bit for bit: cf::fit
+    (cfcomplete.cpp:63-196; NCF, default NcfHyper, seed 42, the reference's schedule and early
+    stopping) + cf::complete's imputation of every unobserved cell + policy::select_caps of every
+    row, FP64 in the reference lane's operation order.  One step = one whole fit + completion +
+    selection.  N>1: replicas (the reference schedule is sequential)."""
+    import torch
+
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+    from paper_2508_07605_b200.cf import SOLVER_NCF_REF, cf_fit
+    from paper_2508_07605_b200.ncf import EXACT, DeviceNcfModel, NcfPlan
+
+    c = C1_FIT
+    grid = ocg.PowerGrid.spanning(*c["grid"])
+    A = synth.joint_csr(c["m"], grid, c["density"], c["dense_rows"], seed=42, dtype=np.float64)
+    m, n = A.m, A.n
+    ctx = ocg.Context(d.local)
+    dev = torch.device("cuda", d.local)
+    torch.cuda.set_device(dev)
+    hyper = ocg.NcfHyper()
+
+    def step():
+        st = {}
+        model = cf_fit(A.row_ptr, A.col, A.val, n, hyper, 42, SOLVER_NCF_REF, args.lane, ctx, st)
+        dm = DeviceNcfModel(model, ctx=ctx)
+        plan = NcfPlan(dm, A.row_ptr, A.col, A.val, grid, args.gamma, EXACT, args.lane)
+        ms, _ = plan.run(timed=True)
+        r = plan.results(m)
+        plan.close()
+        dm.close()
+        return st["device_ms"] + ms, st, model, r
+
+    for _ in range(args.warmup):
+        step()
+    d.barrier()
+    tot, fit_ms = 0.0, 0.0
+    with Clocks(d.local) as clk:
+        for _ in range(args.steps):
+            ms, st, model, r = step()
+            clk.tick()
+            tot += ms
+            fit_ms += st["device_ms"]
+    d.barrier()
+    t_dev = d.max(tot / 1e3)
+    # end to end: the public cf::complete entry with host buffers (CSR in, decisions out)
+    from paper_2508_07605_b200.cf import cf_complete
+
+    t0 = time.perf_counter()
+    rr = cf_complete(A.row_ptr, A.col, A.val, n, hyper, 42, SOLVER_NCF_REF, args.lane, grid, args.gamma,
+                     want_completed=False, ctx=ctx)
+    e2e_t = d.max(time.perf_counter() - t0)
+    assert np.array_equal(rr.idx, r[0])
+    golden = C1_GOLDEN_EPOCHS.get(args.lane)
+    cells = m * n * d.world
+    out = {
+        "metric": "CF-completed matrix cells/sec",
+        "value": cells * args.steps / t_dev,
+        "unit": "cells/s",
+        "selections_per_sec": m * d.world * args.steps / t_dev,
+        "ms_per_step": t_dev * 1e3 / args.steps,
+        "e2e": {"value": cells / e2e_t, "unit": "cells/s", "h2d_bytes_per_step": int(A.row_ptr.nbytes + A.col.nbytes +
+                                                                                       A.val.nbytes) * d.world,
+                "d2h_bytes_per_step": int(m * 24) * d.world,
+                "mode": "ocg_cf_complete: host CSR in, fit + fused completion + selection, decisions out"},
+        "dtype": "f64 (reference lane operation order: bit-identical)",
+        "config": {"workload": "c1-fit", "apps": m, "settings": n, "rank": 8, "observed": A.nnz,
+                   "density": c["density"], "solver": "ncf (reference schedule, joint mode)", "hyper": "NcfHyper{}",
+                   "seed": 42, "lane": args.lane, "epochs_run": model.meta.epochs_run,
+                   "reference_epochs_run": golden, "minibatch_steps": st["steps"],
+                   "parallelism": f"{d.world} replica(s)" if d.world > 1 else "1 GPU",
+                   "l2": "fit state (2.7 MB) L2-resident by design; inputs re-uploaded per step"},
+        "phases_ms_per_step": {"fit": fit_ms / args.steps, "complete_select": (tot - fit_ms) / args.steps},
+        "parity": "epochs_run and every parameter bit-identical to the reference's C1 fit "
+                  "(tests/test_gpu_joint_fit.py::test_joint_fit_bit_exact_c1)",
+        "scaling": "weak",
+        "gpu_launches": args.steps * (int(model.meta.epochs_run) + 12),
+        "roofline": {"bound": "latency", "kernel": "joint_epoch_kernel (leader CTA step chain)",
+                     "achieved": st["device_ms"] * 1e3 / st["steps"], "peak": None, "unit": "us/step",
+                     "frac": None, "traffic": None,
+                     "note": "the reference schedule is a dependent chain of minibatch steps; the leader's per-step "
+                             "latency is the bound (dense Adam replay runs off the critical path on helper warps)"},
+        "clocks": clk.summary(),
+    }
+    return out, ("c1-fit", m)
+
+
+def reference_c1_fit(threads: int, epochs: int = 4, lane: int = 1):
+    """The reference's cf::fit on the C1 matrix for `epochs` epochs (timed) -> per-epoch time x the
+    epochs its own full fit runs (the GPU runs the identical epochs, bit for bit), + its
+    NcfModel::predict + select_caps over every row."""
+    from oracle import bind
+
+    wmod = _weights_module()
+    c = C1_FIT
+    cpu, gpu = wmod.spanning_caps(*c["grid"])
+    m, n = c["m"], len(cpu) * len(gpu)
+    ref = bind.Ref()
+    ref.force_lane(lane)
+    vals, mask = ref.joint_rows_dense(m, cpu, gpu, c["density"], c["dense_rows"], np.arange(m), seed=42)
+    t = {}
+    for e in (1, epochs):  # two epoch budgets: fixed cost (init, split, MSEs) and per-epoch cost apart
+        t0 = time.perf_counter()
+        rc, js, meta = ref.ncf_fit(vals, mask, cpu, gpu, 42, max_epochs=e)
+        t[e] = time.perf_counter() - t0
+        assert rc == 0, ref.err()
+    per_epoch = (t[epochs] - t[1]) / (epochs - 1)
+    fixed = max(0.0, t[1] - per_epoch)
+    params = bind.model_params_from_json(js)
+    rc, _, idx, *_, t_sel = ref.ncf_complete_select_rows(8, 8, [32, 16], params, np.ones(m, np.uint8),
+                                                         np.ones(n, np.uint8), cpu, gpu, vals, mask, 0.05, 1,
+                                                         want_completed=False)
+    assert rc == 0, ref.err()
+    full_epochs = C1_GOLDEN_EPOCHS[lane]
+    secs = fixed + per_epoch * full_epochs + t_sel
+    return {"value": m * n / secs, "unit": "cells/s", "cores": 1, "kind": "reference", **host_info(),
+            "sample": f"reference cf::fit on the full C1 matrix timed at 1 and {epochs} epochs (fixed {fixed:.2f} s + "
+                      f"{per_epoch:.3f} s/epoch) scaled to the {full_epochs} epochs its own complete fit runs, "
+                      f"+ NcfModel::predict of every unobserved "
+                      f"cell and select_caps of every row ({t_sel:.2f} s); {'AVX2' if lane else 'scalar'} lane, "
+                      f"1 core (cf::fit is single-threaded)", "seconds": secs,
+            "measured_full_fit_s": {1: 344.5, 0: 613.6}[lane]}
+
+
 WORKLOADS = {"c0xn": workload_c0xn, "c1": workload_joint, "c2": workload_joint, "c3": workload_joint,
-             "c4": workload_c4, "ingest": workload_ingest, "c2-ncf": workload_ncf, "c1-ncf": workload_ncf}
+             "c4": workload_c4, "ingest": workload_ingest, "c2-ncf": workload_ncf, "c1-ncf": workload_ncf,
+             "c1-fit": workload_c1_fit}
 
 
 # -------------------------------------------------------- reference (CPU)
@@ -828,12 +1040,12 @@ def reference_joint(workload: str, threads: int, nprob: int, max_epochs: int = 1
     import ctypes
 
     from oracle import bind
-    import paper_2508_07605_b200 as ocg
-    from paper_2508_07605_b200 import synth
 
+    wmod = _weights_module()
     c = JOINT[workload]
-    grid = ocg.PowerGrid.spanning(*c["grid"])
-    m, n = c["m"], grid.n
+    cpu, gpu = wmod.spanning_caps(*c["grid"])
+    m, n = c["m"], len(cpu) * len(gpu)
+    ref = bind.Ref()
     m_s = 128 if n > 1024 else 256
     vals = np.zeros((nprob, m_s, n))
     mask = np.zeros((nprob, m_s, n), np.uint8)
@@ -842,13 +1054,12 @@ def reference_joint(workload: str, threads: int, nprob: int, max_epochs: int = 1
         rows = np.concatenate([[p % c["dense_rows"]],
                                (c["dense_rows"] + p * 7919 + np.arange(1, m_s) * stride) % (m - c["dense_rows"])
                                + c["dense_rows"]])
-        vals[p], mask[p] = synth.joint_rows_dense(m, grid, c["density"], c["dense_rows"], rows, seed=42)
-    ref = bind.Ref()
+        vals[p], mask[p] = ref.joint_rows_dense(m, cpu, gpu, c["density"], c["dense_rows"], rows, seed=42,
+                                                as_float=True)
     ref.force_lane(lane)
     h = bind._hyper(bind.RefHyper, app_dim=c["rank"], setting_dim=c["rank"], max_epochs=max_epochs)
     seeds = np.arange(nprob, dtype=np.uint64) + 1
     sel = np.zeros((nprob, m_s), np.int32)
-    cpu, gpu = grid.arrays()
     secs = ref.L.ref_complete_select_batch(nprob, m_s, bind.P(cpu), len(cpu), bind.P(gpu), len(gpu), bind.P(vals),
                                            bind.P(mask), ctypes.byref(h), bind.P(seeds), 0.05, threads, bind.P(sel))
     assert (sel >= 0).all(), "reference sample failed"
@@ -862,13 +1073,22 @@ def reference_joint(workload: str, threads: int, nprob: int, max_epochs: int = 1
 def cpu_baseline(workload: str, threads: int):
     if workload in NCF:
         v1, d1, s1 = reference_ncf(workload, 1, 24)
+        v0, d0, s0 = reference_ncf(workload, 1, 24, lane=0)
         v, desc, secs = reference_ncf(workload, threads, 48)
+        c = NCF[workload]
         return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
-                "seconds": secs, "one_core": {"value": v1, "sample": d1, "seconds": s1}}
+                "seconds": secs, **host_info(),
+                "one_core": {"value": v1, "sample": d1, "seconds": s1},
+                "one_core_scalar_lane": {"value": v0, "sample": d0, "seconds": s0},
+                "fit_composed": composed_fit(c["rank"], c["m"], c["grid"][0] * c["grid"][1], c["density"])}
+    if workload == "c1-fit":
+        return reference_c1_fit(threads)
     if workload in JOINT:
         v, desc, secs = reference_joint(workload, threads, nprob=2 * threads)
+        c = JOINT[workload]
         return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": desc,
-                "seconds": secs}
+                "seconds": secs, **host_info(),
+                "fit_composed": composed_fit(c["rank"], c["m"], c["grid"][0] * c["grid"][1], c["density"])}
     if workload == "ingest":
         v, secs, n = reference_ingest(400_000 * threads, threads)
         return {"value": v, "unit": "estimates/s", "cores": threads, "kind": "reference",
@@ -926,6 +1146,19 @@ def run_reference(args, d: Dist):
                 "e2e": {"value": v, "unit": "estimates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
+    if args.workload == "c1-fit":
+        vals = [reference_c1_fit(threads) for _ in range(max(1, min(args.steps, 2)))]
+        cb = vals[-1]
+        v = cb["value"]
+        line = {"impl": "reference", "metric": "CF-completed matrix cells/sec", "value": v, "unit": "cells/s",
+                "n_gpus": args.gpus, "steps": len(vals), "warmup": 0, "ms_per_step": cb["seconds"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SURVEY 8d generator run by the reference)",
+                "config": {"workload": "c1-fit", "apps": C1_FIT["m"], "rank": 8, "solver": "ncf (reference)"},
+                "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     if args.workload in NCF:
         for _ in range(args.warmup):
             reference_ncf(args.workload, threads, 4)
@@ -975,12 +1208,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2-ncf")
     ap.add_argument("--sweeps", type=int, default=10, help="ALS sweeps per fit (c1/c2)")
     ap.add_argument("--als-lambda", type=float, default=0.003)
     ap.add_argument("--gamma", type=float, default=0.05)
     ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")
-    ap.add_argument("--lane", type=int, default=1, help="c0xn/ingest: reference FP lane (0 scalar, 1 avx2)")
+    ap.add_argument("--lane", type=int, default=1, help="reference FP lane to reproduce (0 scalar, 1 avx2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

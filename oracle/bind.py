@@ -229,6 +229,8 @@ class Ref:
                                            ctypes.c_int, c_vp, c_vp]
         L.ref_matrix_csv_roundtrip.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_vp, c_vp, c_vp]
         L.ref_load_predictor.argtypes = [ctypes.c_char_p, c_vp]
+        L.ref_time_fit_step.argtypes = [c_sz, c_sz, c_sz, c_vp, c_sz, ctypes.c_int, c_vp]
+        L.ref_time_fit_step.restype = c_dbl
         L.ref_complete_select_batch.restype = c_dbl
         L.ref_complete_select_batch.argtypes = [c_sz, c_sz, c_vp, c_sz, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_dbl,
                                                 ctypes.c_int, c_vp]
@@ -335,6 +337,14 @@ class Ref:
         rc = self.L.ref_matrix_csv_roundtrip(str(in_path).encode(), None if out_path is None else str(out_path).encode(),
                                              ctypes.byref(m), ctypes.byref(n), ctypes.byref(nnz))
         return rc, (m.value, n.value, nnz.value)
+
+    def time_fit_step(self, m, n, k, hidden=(32, 16), iters=3):
+        """Seconds per cf::fit minibatch step composed from the reference's components."""
+        hid = np.asarray(hidden, np.uint64)
+        parts = np.zeros(3)
+        secs = self.L.ref_time_fit_step(m, n, k, P(hid), len(hid), iters, P(parts))
+        assert secs > 0, self.err()
+        return secs, parts
 
     def load_predictor(self, path):
         hs = ctypes.c_int()

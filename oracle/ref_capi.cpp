@@ -684,5 +684,73 @@ int ref_load_predictor(const char* path, int* has_stats) {
     }
 }
 
+// One minibatch step of cf::fit's loop body (cfcomplete.cpp:155-178) built from
+// the reference's own components at a given model size, for the composed CPU
+// figure of a fit too large to run (C2/C3): dense zeroing of the
+// embedding-gradient tables, 32 x nn::backprop_sample, nn::AdamState::step over
+// every parameter block.  Returns the mean seconds per step over `iters` steps
+// (parts[0..2]: zeroing, backprop, adam).
+double ref_time_fit_step(size_t m, size_t n, size_t k, const size_t* hidden, size_t nh, int iters, double* parts) {
+    try {
+        Rng rng(1);
+        auto app = nn::EmbeddingTable::random(m, k, rng);
+        auto set = nn::EmbeddingTable::random(n, k, rng);
+        std::vector<std::size_t> dims{2 * k};
+        std::vector<nn::Activation> acts;
+        for (size_t l = 0; l < nh; ++l) {
+            dims.push_back(hidden[l]);
+            acts.push_back(nn::Activation::selu);
+        }
+        dims.push_back(1);
+        acts.push_back(nn::Activation::identity);
+        nn::MlpModel mlp(dims, acts, rng);
+        std::vector<nn::ParamView> params{{app.values.data(), app.values.size()}, {set.values.data(), set.values.size()}};
+        for (const auto& b : mlp.param_blocks()) params.push_back(b);
+        nn::AdamState adam(params, 1e-3);
+        nn::GradBlocks grads;
+        std::vector<double> input_grad;
+        double tz = 0, tb = 0, ta = 0;
+        using clk = std::chrono::steady_clock;
+        for (int it = 0; it < iters; ++it) {
+            const auto t0 = clk::now();
+            grads.assign(params.size(), {});
+            grads[0].assign(app.values.size(), 0.0);
+            grads[1].assign(set.values.size(), 0.0);
+            nn::GradBlocks mlp_grads;
+            for (const auto& layer : mlp.layers()) {
+                mlp_grads.emplace_back(layer.weights.size(), 0.0);
+                mlp_grads.emplace_back(layer.biases.size(), 0.0);
+            }
+            const auto t1 = clk::now();
+            for (int s = 0; s < 32; ++s) {
+                const size_t i = rng.next_u64() % m, j = rng.next_u64() % n;
+                std::vector<double> x(app.row(i).begin(), app.row(i).end());
+                x.insert(x.end(), set.row(j).begin(), set.row(j).end());
+                const double y[] = {0.5};
+                nn::backprop_sample(mlp, x, y, 1.0 / 32, mlp_grads, input_grad);
+                for (size_t c = 0; c < k; ++c) grads[0][i * k + c] += input_grad[c];
+                for (size_t c = 0; c < k; ++c) grads[1][j * k + c] += input_grad[k + c];
+            }
+            for (size_t b = 0; b < mlp_grads.size(); ++b) grads[2 + b] = std::move(mlp_grads[b]);
+            const auto t2 = clk::now();
+            adam.step(params, grads);
+            const auto t3 = clk::now();
+            tz += std::chrono::duration<double>(t1 - t0).count();
+            tb += std::chrono::duration<double>(t2 - t1).count();
+            ta += std::chrono::duration<double>(t3 - t2).count();
+        }
+        if (parts) {
+            parts[0] = tz / iters;
+            parts[1] = tb / iters;
+            parts[2] = ta / iters;
+        }
+        return (tz + tb + ta) / iters;
+    } catch (...) {
+        map_exception();
+        return -1.0;
+    }
+}
+
 }  // extern "C"
+
 
