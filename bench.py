@@ -868,7 +868,7 @@ def reference_ncf(workload: str, threads: int, rows_per_thread: int, lane: int =
                                                                 threads, want_completed=False)
     assert rc == 0, ref.err()
     desc = (f"{nrows} rows sampled from {workload} ({m} x {n}, rank {k}): reference NcfModel::predict of every "
-            f"unobserved cell + select_caps per row, same weights, AVX2 lane, {threads} threads; per-cell cost is "
+            f"unobserved cell + select_caps per row, same weights, {'AVX2' if lane else 'scalar'} lane, {threads} threads; per-cell cost is "
             f"size-independent, so rows/s extrapolate linearly to all {m} rows")
     return nrows * n / secs, desc, secs
 
