@@ -411,6 +411,81 @@ def _joint_matrix(name, rank, world):
     return c, grid, A
 
 
+def quality_rows(m_loc, dense_rows, nblocks=20, block=100):
+    """Row sample for the quality block: nblocks blocks of `block` rows spread over the
+    local rows past the dense ones (every archetype of make_suite's suite is covered)."""
+    lo = min(dense_rows, max(0, m_loc - block))
+    starts = np.linspace(lo, m_loc - block, nblocks).astype(np.int64)
+    return [(int(s), block) for s in np.unique(starts)]
+
+
+def completion_quality(m, grid, A, blocks, completed, idx_completed, gamma, ctx, goff=0):
+    """Held-out quality of a completion on the sampled local rows (blocks of (r0, count),
+    completed rows stacked in that order):
+      * RMSE of the imputed cells against the simulator's ground truth sim::true_perf
+        (simnode.cpp:43-45), absolute and relative;
+      * truth_optimal_frac: rows whose selection equals policy::select_caps on the TRUE row
+        (SURVEY 6: the reference's C1 run reported RMSE 0.018, 61 % truth-optimal);
+      * true_saving_regret: mean true energy saving lost vs the true optimum, and the share
+        of rows whose chosen setting violates the true performance-loss bound gamma."""
+    import paper_2508_07605_b200 as ocg
+    from paper_2508_07605_b200 import synth
+
+    rows = np.concatenate([np.arange(r0, r0 + c) for r0, c in blocks])
+    truth = synth.true_rows(m, grid, rows + goff)
+    mask = np.zeros_like(completed, bool)
+    for k, i in enumerate(rows):
+        mask[k, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = True
+    held = ~mask
+    err = completed[held] - truth[held]
+    idx_t, *_ = ocg.select_caps_batch(truth, grid, gamma, ctx)
+    idx_c = np.asarray(idx_completed)
+    cpu, gpu = grid.arrays()
+    csum = (np.repeat(cpu, len(gpu)) + np.tile(gpu, len(cpu))).astype(np.float64)
+    e_base = float(csum[-1])
+    sav = (e_base - csum[None, :] / truth) / e_base
+    loss = 1.0 - truth / truth[:, -1:]
+    r = np.arange(len(rows))
+    return {"rows": int(len(rows)), "heldout_cells": int(held.sum()),
+            "heldout_rmse": float(np.sqrt(np.mean(err ** 2))),
+            "heldout_rel_rmse": float(np.sqrt(np.mean((err / truth[held]) ** 2))),
+            "truth_optimal_frac": float(np.mean(idx_c == idx_t)),
+            "true_saving_regret": float(np.mean(sav[r, idx_t] - sav[r, idx_c])),
+            "true_loss_violation_frac": float(np.mean(loss[r, idx_c] > gamma))}
+
+
+def als_sweeps_rule(A, grid, hyp, gamma, ctx, m, goff=0, tol=1e-3, cap=40):
+    """Sweep count by a stated convergence rule: the smallest number of ALS sweeps after which
+    the held-out predictions of the quality row sample change by less than `tol` (relative
+    RMS) from one sweep to the next (calibration run outside the timed region); also returns
+    the held-out RMSE after every sweep."""
+    from paper_2508_07605_b200 import synth
+    from paper_2508_07605_b200.als import AlsPlan
+    import paper_2508_07605_b200._lib as L
+
+    plan = AlsPlan(A.m, A.row_ptr, A.col, A.val, grid, hyp, gamma, ctx=ctx)
+    blocks = quality_rows(A.m, 0, nblocks=10, block=100)
+    rows = np.concatenate([np.arange(r0, r0 + c) for r0, c in blocks])
+    truth = synth.true_rows(m, grid, rows + goff)
+    L.check(L.lib.ocg_als_plan_begin(plan._h))
+    prev, sweeps, delta, curve = None, cap, None, []
+    for s_ in range(1, cap + 1):
+        L.check(L.lib.ocg_als_plan_row_half(plan._h))
+        L.check(L.lib.ocg_als_plan_col_half(plan._h))
+        cur = np.concatenate([plan.completed_rows(r0, c) for r0, c in blocks])
+        curve.append(float(np.sqrt(np.mean((cur - truth) ** 2))))
+        if prev is not None:
+            delta = float(np.sqrt(np.mean(((cur - prev) / prev) ** 2)))
+            if delta < tol:
+                sweeps = s_
+                break
+        prev = cur
+    plan.close()
+    return sweeps, {"rule": f"smallest sweep count whose predictions on {len(rows)} sampled rows change < {tol:g} "
+                            f"(relative RMS) from the previous sweep (cap {cap})", "sweeps": sweeps,
+                    "last_change": delta, "rmse_vs_truth_by_sweep": curve}
+
+
 def workload_joint(args, d: Dist):
     """ALS completion + fused imputation + Algorithm-2 selection of a joint matrix.
     N=1: the fused single-GPU plan; N>1: rows sharded over ranks, column Gram
@@ -425,6 +500,14 @@ def workload_joint(args, d: Dist):
     m_loc, n, nnz = A.m, grid.n, A.nnz
     m = cfg["m"]
     ctx = ocg.Context(d.local)
+    sweeps_rule = {"rule": "fixed by --sweeps", "sweeps": args.sweeps}
+    if args.sweeps <= 0:  # the stated convergence rule picks the sweep count (rank 0 decides, all ranks use it)
+        from paper_2508_07605_b200.dist import shard_rows as _sr
+
+        sw, sweeps_rule = als_sweeps_rule(A, grid, AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=1, seed=42),
+                                          args.gamma, ctx, m, goff=_sr(m, d.world, d.rank)[0])
+        args.sweeps = int(d.max(float(sw)))
+        sweeps_rule["sweeps"] = args.sweeps
     hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
     dev = torch.device("cuda", d.local)
     t_rp = torch.from_numpy(A.row_ptr).to(dev)
@@ -464,6 +547,13 @@ def workload_joint(args, d: Dist):
     t_dev = d.max(tot_ms / 1e3)
     idx, sav, loss, ncand = plan.results()
     assert (idx >= 0).all() and (ncand >= 1).all()
+    from paper_2508_07605_b200.dist import shard_rows
+
+    qb = quality_rows(m_loc, cfg["dense_rows"] if d.rank == 0 else 0)
+    qrows = np.concatenate([np.arange(r0, r0 + c) for r0, c in qb])
+    quality = completion_quality(m, grid, A, qb, np.concatenate([plan.completed_rows(r0, c) for r0, c in qb]),
+                                 idx[qrows], args.gamma, ctx, goff=shard_rows(m, d.world, d.rank)[0])
+    quality["sweeps_rule"] = sweeps_rule
     plan.close()
     del t_rp, t_col, t_val
     # end to end through the public API with host buffers: a plan created once
@@ -553,6 +643,7 @@ def workload_joint(args, d: Dist):
                    if d.world > 1 else "1 GPU",
                    "l2": "inputs (CSR %.0f MB/GPU) larger than L2, and L2 flushed before every timed step" %
                          ((A.row_ptr.nbytes + A.col.nbytes + A.val.nbytes) / 1e6)},
+        "quality": quality,
         "scaling": "strong",
         "gpu_launches": args.steps * (16 + args.sweeps * (4 if d.world == 1 else 5) + 2),
         "clocks": clk.summary(),
@@ -899,6 +990,9 @@ def workload_c1_fit(args, d: Dist):
     torch.cuda.set_device(dev)
     hyper = ocg.NcfHyper()
 
+    qb = quality_rows(m, c["dense_rows"])
+    qrows = np.concatenate([np.arange(r0, r0 + k) for r0, k in qb])
+
     def step():
         st = {}
         model = cf_fit(A.row_ptr, A.col, A.val, n, hyper, 42, SOLVER_NCF_REF, args.lane, ctx, st)
@@ -906,6 +1000,7 @@ def workload_c1_fit(args, d: Dist):
         plan = NcfPlan(dm, A.row_ptr, A.col, A.val, grid, args.gamma, EXACT, args.lane)
         ms, _ = plan.run(timed=True)
         r = plan.results(m)
+        st["completed"] = plan.completed_rows(qrows)
         plan.close()
         dm.close()
         return st["device_ms"] + ms, st, model, r
@@ -931,6 +1026,7 @@ def workload_c1_fit(args, d: Dist):
     e2e_t = d.max(time.perf_counter() - t0)
     assert np.array_equal(rr.idx, r[0])
     golden = C1_GOLDEN_EPOCHS.get(args.lane)
+    quality = completion_quality(m, grid, A, qb, st["completed"], r[0][qrows], args.gamma, ctx)
     cells = m * n * d.world
     out = {
         "metric": "CF-completed matrix cells/sec",
@@ -950,6 +1046,7 @@ def workload_c1_fit(args, d: Dist):
                    "parallelism": f"{d.world} replica(s)" if d.world > 1 else "1 GPU",
                    "l2": "fit state (2.7 MB) L2-resident by design; inputs re-uploaded per step"},
         "phases_ms_per_step": {"fit": fit_ms / args.steps, "complete_select": (tot - fit_ms) / args.steps},
+        "quality": quality,
         "parity": "epochs_run and every parameter bit-identical to the reference's C1 fit "
                   "(tests/test_gpu_joint_fit.py::test_joint_fit_bit_exact_c1)",
         "scaling": "weak",
@@ -1209,7 +1306,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2-ncf")
-    ap.add_argument("--sweeps", type=int, default=10, help="ALS sweeps per fit (c1/c2)")
+    ap.add_argument("--sweeps", type=int, default=0,
+                    help="ALS sweeps per fit (c1/c2/c3); 0 = the convergence rule (als_sweeps_rule)")
     ap.add_argument("--als-lambda", type=float, default=0.003)
     ap.add_argument("--gamma", type=float, default=0.05)
     ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")

@@ -405,6 +405,10 @@ int ocg_synth_csr_range_count(int64_t m, int64_t row0, int64_t row1, const int32
 int ocg_synth_csr_range_fill(int64_t m, int64_t row0, int64_t row1, const int32_t* cpu_caps, int32_t ncpu,
                              const int32_t* gpu_caps, int32_t ngpu, double density, int64_t dense_rows, uint64_t seed,
                              int nthreads, const int64_t* row_ptr, int32_t* col, float* val32, double* val64);
+/* sim::true_perf (simnode.cpp:43-45) of every cell of selected rows of the same joint
+ * matrix (nrows x n): the ground truth a completion's held-out quality is measured on */
+int ocg_synth_true_rows(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,
+                        uint64_t seed, const int64_t* rows, int64_t nrows, double* out);
 /* selected rows of the same joint matrix as dense values + mask (values as
  * the FP32 CSR carries them, widened) — CPU-baseline samples */
 int ocg_synth_rows_dense(int64_t m, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps, int32_t ngpu,

@@ -351,4 +351,19 @@ int ocg_synth_rows_dense(int64_t m, const int32_t* cpu, int32_t ncpu, const int3
     return OCG_OK;
 }
 
+// ground truth sim::true_perf (simnode.cpp:43-45) of every cell of selected rows of the
+// same joint matrix (nrows x n) — held-out quality of a completion (bench quality block)
+int ocg_synth_true_rows(int64_t m, const int32_t* cpu, int32_t ncpu, const int32_t* gpu, int32_t ngpu, uint64_t seed,
+                        const int64_t* rows, int64_t nrows, double* out) {
+    const Grid g{cpu, ncpu, gpu, ngpu};
+    const auto specs = joint_specs(m, seed, g);
+    const int64_t n = g.n();
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = rows[r];
+        if (i < 0 || i >= m) return OCG_E_RANGE;
+        for (int64_t j = 0; j < n; ++j) out[r * n + j] = true_perf(specs[i], g.cpu[j / g.ngpu], g.gpu[j % g.ngpu]);
+    }
+    return OCG_OK;
+}
+
 }  // extern "C"

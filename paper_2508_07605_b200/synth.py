@@ -54,6 +54,19 @@ def joint_rows_dense(m: int, grid: PowerGrid, density: float, dense_rows: int, r
     return vals, mask
 
 
+lib.ocg_synth_true_rows.argtypes = [c_i64, c_vp, c_i32, c_vp, c_i32, c_u64, c_vp, c_i64, c_vp]
+lib.ocg_synth_true_rows.restype = ctypes.c_int
+
+
+def true_rows(m: int, grid: PowerGrid, rows, seed: int = 42) -> np.ndarray:
+    """sim::true_perf of every cell of the given rows of the joint matrix (len(rows) x n)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    cpu, gpu = grid.arrays()
+    out = np.zeros((len(rows), grid.n))
+    check(lib.ocg_synth_true_rows(m, ptr(cpu), len(cpu), ptr(gpu), len(gpu), seed, ptr(rows), len(rows), ptr(out)))
+    return out
+
+
 def make_suite(counts, seed: int, role: int, grid: PowerGrid, noise_sigma=0.01, cpu_phase_fraction=0.0):
     cnt = np.asarray(counts, np.int32)
     out = (WorkloadSpecC * int(cnt.sum()))()
