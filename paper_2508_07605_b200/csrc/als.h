@@ -38,8 +38,7 @@ struct AlsHalf {
     const int32_t* seg_order = nullptr;
     int32_t* blk_ctr = nullptr;  // rank 32: work-block counter (zeroed per launch)
     cudaEvent_t ev_gram0 = nullptr, ev_gram1 = nullptr;  // optional: recorded around the Gram kernel
-    unsigned* xmax = nullptr;  // mode 0: the K4 leaves max |X| here (zeroed first), see als_solve_tracks_max
-    bool fuse_solve = false;  // rank 32, mode 0: single-segment items solved inside the Gram kernel
+    unsigned* xmax = nullptr;  // mode 0: the K4 leaves max |X| here (zeroed first)
 };
 
 cudaError_t launch_als_init(int64_t n, int k, uint64_t seed, float* V, cudaStream_t s);
@@ -59,7 +58,6 @@ cudaError_t launch_als_solve_records(int k, int64_t nitems, const float* G, floa
 size_t als_record_floats_mma(int k);
 cudaError_t launch_als_pack(int k, int64_t rows, const float* X, unsigned* maxbits, uint4* Xh, int sm_count,
                             cudaStream_t s, bool have_max = false);
-bool als_solve_tracks_max();
 cudaError_t launch_als_pack_vals(int64_t n, const float* val, const unsigned* vmax, uint32_t* out, cudaStream_t s);
 cudaError_t launch_absmax(int64_t count, const float* x, unsigned* maxbits, int sm_count, cudaStream_t s);
 cudaError_t launch_als_solve_from_gram(int k, int64_t nitems, const float* G, float* X, float lambda, int sm_count,

@@ -112,12 +112,6 @@ struct Cfg {
 static_assert(Cfg<32>::kRec == 612 && Cfg<32>::kRhs == 576, "rank-32 record layout");
 static_assert(Cfg<64>::kRec * 4 <= 32 * Cfg<64>::RS * 16, "rank-64 record fits a stage buffer");
 
-// K4 solver geometry: LPS lanes per system, SYS systems per warp (rank 64: 8 lanes,
-// so 4 systems = 36 KB per warp and 6 warps share an SM)
-template <int K>
-__host__ __device__ constexpr int lps() { return K == 32 ? 4 : 8; }
-template <int K>
-__host__ __device__ constexpr int nsys() { return 32 / lps<K>(); }
 // T(i + LPS) - T(i) for i = 4a + p (padded row lengths 4((r >> 2) + 1))
 template <int LPS>
 __device__ __forceinline__ int row_step(int a, int p) {
@@ -214,45 +208,31 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 //    16-byte coalesced writes).
 // (One TMA bulk copy per factor row was measured 1.4x slower than the cp.async
 // gathers: per-operation cost of the bulk-copy unit at 128 B.)
-template <int K>
-__device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, float* __restrict__ X, float lambda);
 
 constexpr int kRC = 8;     // ring slots (chunks)
 constexpr int kAhead = 5;  // refill distance (chunks); < kRC - 1
-// FUSED (rank 32, row side): single-segment items are not written to global
-// memory; their records go to a per-warp batch in shared memory and every
-// kSys of them are solved in place by the warp (solve_staged), so the K4 work
-// overlaps the gathers in flight (multi-segment items keep the record path).
 // SPLIT (rank 32, column side: long segments, MMA-bound): H^T L accumulated apart
 // on all tiles, 18 instead of 22 MMAs per 16 observations, at 56 more accumulator
 // registers (12 warps per SM instead of 16; the row side's short segments want
 // the occupancy and the cheaper epilogue)
-template <int K, bool FUSED, bool SPLIT = false>
-__host__ __device__ constexpr int gram_warps() { return FUSED ? 7 : (SPLIT ? 6 : kWarps); }
-template <int K, bool FUSED>
-__host__ __device__ constexpr int gram_warp_u4() {
-    return Cfg<K>::kStageU4 + (FUSED ? (nsys<K>() * Cfg<K>::kRec) / 4 + 4 : 0);
-}
+template <int K, bool SPLIT = false>
+__host__ __device__ constexpr int gram_warps() { return SPLIT ? 6 : kWarps; }
 
-template <int K, bool FUSED, bool SPLIT>
-__global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 : Cfg<K>::kMinBlocks) als_mma_gram_kernel(
+template <int K, bool SPLIT>
+__global__ void __launch_bounds__(gram_warps<K, SPLIT>() * 32, Cfg<K>::kMinBlocks) als_mma_gram_kernel(
     const int32_t* __restrict__ total_segs, const int32_t* __restrict__ seg_order, const int32_t* __restrict__ seg_item,
     const int64_t* __restrict__ seg_beg, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const uint32_t* __restrict__ valh, const uint4* __restrict__ Yh, const unsigned* __restrict__ ymax,
     const unsigned* __restrict__ vmax, float* __restrict__ rec, int32_t* __restrict__ blk_ctr,
-    const int32_t* __restrict__ nseg_of, float* __restrict__ X, float lambda) {
+    const int32_t* /*unused*/) {
     using C = Cfg<K>;
     constexpr int D = C::D, MT = C::MT, NLT = C::NLT, RU4 = C::RU4, RS = C::RS;
     constexpr int kRec = C::kRec, kRhs = C::kRhs, kCnt = C::kCnt;
-    constexpr int W = gram_warps<K, FUSED, SPLIT>();
-    constexpr int kSys = nsys<K>();
+    constexpr int W = gram_warps<K, SPLIT>();
     extern __shared__ __align__(16) uint4 dyn4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    uint4* stage = dyn4 + warp * gram_warp_u4<K, FUSED>();                 // [2][32][RS] uint4
-    float* batch = reinterpret_cast<float*>(stage + C::kStageU4);           // FUSED: [kSys][kRec]
-    int64_t* bitems = reinterpret_cast<int64_t*>(batch + kSys * kRec);      // FUSED: [kSys]
-    int bcount = 0;
+    uint4* stage = dyn4 + warp * C::kStageU4;                               // [2][32][RS] uint4
     int32_t* ring_j = reinterpret_cast<int32_t*>(stage + 2 * 32 * RS);     // [kRC][32]
     uint32_t* ring_r = reinterpret_cast<uint32_t*>(ring_j + kRC * 32);     // [kRC][32]
     const int ey = als_scale_exp(*ymax), ev = als_scale_exp(*vmax);
@@ -271,17 +251,15 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
     // lane i <- segment of work index 32 b + i, or b + i * nblk when the work
     // order is sorted by band (column side: the warps active at any moment then
     // gather from one band of the factor matrix); sg < 0: none
-    auto load_meta = [&](int32_t b, int32_t& sg, int64_t& beg, int64_t& end, int32_t& item) {
+    auto load_meta = [&](int32_t b, int32_t& sg, int64_t& beg, int64_t& end) {
         const int32_t k = seg_order ? b + lane * nblk : b * 32 + lane;
         sg = -1;
         beg = end = 0;
-        item = -1;  // FUSED: the segment's item when it is the item's only segment
         if (b < nblk && k < nsegs) {
             sg = seg_order ? seg_order[k] : k;
             const int32_t it = seg_item[sg];
             beg = seg_beg[sg];
             end = min(beg + kSeg, ptr[it + 1]);
-            if (FUSED && nseg_of[it] == 1) item = it;
         }
     };
     auto bcast64 = [&](int64_t v, int src) {
@@ -291,11 +269,11 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
     // ---- refill cursor (producer of ring slots)
     int32_t rb = grab();
     if (rb >= nblk) return;
-    int32_t r_sg, r_item;
+    int32_t r_sg;
     int64_t r_beg, r_end;
-    load_meta(rb, r_sg, r_beg, r_end, r_item);
+    load_meta(rb, r_sg, r_beg, r_end);
     // consumer block = the refill's first block
-    int32_t cb = rb, c_sg = r_sg, c_item = r_item;
+    int32_t cb = rb, c_sg = r_sg;
     int64_t c_beg = r_beg, c_end = r_end;
     int rk = 0;
     int64_t rpos = bcast64(r_beg, 0), r_e = bcast64(r_end, 0);  // refill segment: position, end
@@ -307,7 +285,7 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
         if (rex) {
             if (rb != cb) return;  // the consumer still needs the pending block's metadata: wait
             rb = grab();
-            load_meta(rb, r_sg, r_beg, r_end, r_item);
+            load_meta(rb, r_sg, r_beg, r_end);
             rk = 0;
             if (rb >= nblk || __shfl_sync(0xffffffffu, r_sg, 0) < 0) {
                 rdone = true;
@@ -373,7 +351,7 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
 
     // SPLIT: H^T L kept apart on all MT x D tiles (14 + 4 MMAs per 16 observations instead of
     // 18 + 4); rank 64 has no registers for it
-    static_assert(!SPLIT || (K == 32 && !FUSED), "split H^T L: rank 32, record path");
+    static_assert(!SPLIT || K == 32, "split H^T L: rank 32");
     constexpr bool kSplitHL = SPLIT;
     constexpr int NHL = kSplitHL ? MT * D : 1;
     float acc[NLT][4], racc[MT][4], hl[NHL][4];
@@ -477,13 +455,11 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
             }
         }
         __syncwarp();
-        const int32_t fitem = FUSED && last_of_seg ? __shfl_sync(0xffffffffu, c_item, ck) : -1;
         if (last_of_seg) {
-            // ---- record, assembled in the drained buffer (FUSED single-segment items: in the
-            // warp's batch slot), stored with 16-byte coalesced writes.
+            // ---- record, assembled in the drained buffer, stored with 16-byte coalesced writes.
             // Element e of lower tile (i,j) is MMA (M, N) = (16i + g + 8(e>>1), 8j + 2t + (e&1)) = factor
             // dims (M, N); each unordered pair is owned by exactly one (M >= N) element.
-            float* rs_ = fitem >= 0 ? batch + bcount * kRec : reinterpret_cast<float*>(stage + buf * 32 * RS);
+            float* rs_ = reinterpret_cast<float*>(stage + buf * 32 * RS);
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -525,28 +501,17 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
             const int32_t sg = __shfl_sync(0xffffffffu, c_sg, ck);
             const int64_t sbeg = bcast64(c_beg, ck);  // (outside the lane-0 branch: full-warp shuffle)
             if (lane == 0) rs_[kCnt] = static_cast<float>(cend - sbeg);
-            if (FUSED && fitem >= 0) {
-                if (lane == 0) bitems[bcount] = fitem;
-                if (++bcount == kSys) {  // a full batch: solve it (the next chunk's gathers are in flight)
-                    __syncwarp();
-                    solve_staged<K>(batch, kSys, bitems[lane % kSys], X, lambda);
-                    bcount = 0;
-                }
-                __syncwarp();
-            } else {
-                __syncwarp();
-                float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
-                const float4* src = reinterpret_cast<const float4*>(rs_);
+            __syncwarp();
+            float4* out = reinterpret_cast<float4*>(rec + static_cast<int64_t>(sg) * kRec);
+            const float4* src = reinterpret_cast<const float4*>(rs_);
 #pragma unroll
-                for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots: stale, never read
-                __syncwarp();
-            }
+            for (int c = lane; c < kRec / 4; c += 32) out[c] = src[c];  // padding slots: stale, never read
+            __syncwarp();
         }
         if (finished) break;
         if (nblock) {
             cb = rb;
             c_sg = r_sg;
-            c_item = r_item;
             c_beg = r_beg;
             c_end = r_end;
         }
@@ -556,10 +521,6 @@ __global__ void __launch_bounds__(gram_warps<K, FUSED, SPLIT>() * 32, FUSED ? 1 
         buf ^= 1;
     }
     cp_async_wait<0>();
-    if (FUSED && bcount > 0) {  // the last partial batch
-        __syncwarp();
-        solve_staged<K>(batch, bcount, bitems[(lane % kSys) < bcount ? lane % kSys : 0], X, lambda);
-    }
 }
 
 // observed values -> packed (fp16 hi, fp16 lo) of val * 2^ev
@@ -648,180 +609,6 @@ __global__ void __launch_bounds__(160) als_reduce_records_kernel(int64_t nitems,
     }
 }
 
-// K4: LPS lanes per item (32/LPS items per warp; lane = (32/LPS) * part + item):
-// the item's record is staged in shared memory and its lanes run a
-// left-looking Cholesky of G + lambda*cnt*I in place, lane `part` computing
-// the rows i == part (mod LPS) of each column, two rows per step (row K of the
-// record is the rhs, so the forward substitution rides along: L[K][j] = y_j).
-// All lanes of an item then run the back substitution.  Record of item i at
-// slot first[i] (first == nullptr: slot i).  The 8 lanes of a 16-byte
-// shared-memory phase are 8 different items at the same record offset (record
-// stride 153 x 16 B: 8 distinct bank groups).  With LPS = 4 a warp needs 19.6
-// KB, so 11 warps share an SM (the kernel is latency-bound: occupancy pays
-// for the redundant per-column work of the 4 lanes).
-template <int K>
-__host__ __device__ constexpr int solve_smem() { return nsys<K>() * Cfg<K>::kRec * 4; }
-// Factorise and solve the nb <= kSys systems staged at srec (record layout,
-// record s at srec + s * kRec); lane = kSys * part + sys; `item` = the item of
-// the lane's system (valid for sys < nb): x -> X[item * K].
-template <int K>
-__device__ __forceinline__ void solve_staged(float* srec, int nb, int64_t item, float* __restrict__ X,
-                                             float lambda) {
-    constexpr int kRec = Cfg<K>::kRec, kRhs = Cfg<K>::kRhs, kCnt = Cfg<K>::kCnt;
-    constexpr int kLPS = lps<K>(), kSys = nsys<K>();
-    const int lane = threadIdx.x & 31, sys = lane % kSys, par = lane / kSys;
-    float* S = srec + sys * kRec;
-    {
-        const bool live = sys < nb;
-        const float cnt = live ? S[kCnt] : 1.0f;
-        const float diag = lambda * cnt;
-        static_for<K>([&](auto jc) {
-            constexpr int j = decltype(jc)::value;
-            // row j of L (columns < j) -> registers (all lanes of the item: broadcast)
-            float rj[K];
-            const float* Rj = S + tri_off(j);
-#pragma unroll
-            for (int q = 0; q + 4 <= j; q += 4) {
-                const float4 v = *reinterpret_cast<const float4*>(Rj + q);
-                rj[q] = v.x;
-                rj[q + 1] = v.y;
-                rj[q + 2] = v.z;
-                rj[q + 3] = v.w;
-            }
-#pragma unroll
-            for (int q = j & ~3; q < j; ++q) rj[q] = Rj[q];
-            float d0 = Rj[j] + diag, d1 = 0.0f;
-#pragma unroll
-            for (int q = 0; q < j; ++q) {
-                if (q & 1) d1 = fmaf(-rj[q], rj[q], d1);
-                else d0 = fmaf(-rj[q], rj[q], d0);
-            }
-            const float r = rsqrt_ftz(d0 + d1);
-            // rows i > j with i == par (mod LPS), two per iteration (independent chains)
-            int i = j + 1 + ((par - (j + 1)) % kLPS + kLPS) % kLPS;
-            // T(i) and T(i + LPS) incrementally (row_step; row lengths padded to multiples of 4)
-            int offa = tri_off(i);
-#pragma unroll 1
-            for (; i + kLPS <= K; i += 2 * kLPS) {
-                const int offb = offa + row_step<kLPS>(i >> 2, i & 3);
-                const float* Ra = S + offa;
-                const float* Rb = S + offb;
-                float a0 = Ra[j], a1 = 0.0f, b0 = Rb[j], b1 = 0.0f;
-#pragma unroll
-                for (int q = 0; q + 4 <= j; q += 4) {
-                    const float4 va = *reinterpret_cast<const float4*>(Ra + q);
-                    const float4 vb = *reinterpret_cast<const float4*>(Rb + q);
-                    a0 = fmaf(-va.x, rj[q], a0);
-                    b0 = fmaf(-vb.x, rj[q], b0);
-                    a1 = fmaf(-va.y, rj[q + 1], a1);
-                    b1 = fmaf(-vb.y, rj[q + 1], b1);
-                    a0 = fmaf(-va.z, rj[q + 2], a0);
-                    b0 = fmaf(-vb.z, rj[q + 2], b0);
-                    a1 = fmaf(-va.w, rj[q + 3], a1);
-                    b1 = fmaf(-vb.w, rj[q + 3], b1);
-                }
-#pragma unroll
-                for (int q = j & ~3; q < j; ++q) {
-                    a0 = fmaf(-Ra[q], rj[q], a0);
-                    b0 = fmaf(-Rb[q], rj[q], b0);
-                }
-                S[offa + j] = (a0 + a1) * r;
-                S[offb + j] = (b0 + b1) * r;
-                offa = offb + row_step<kLPS>((i >> 2) + kLPS / 4, i & 3);
-            }
-            if (i <= K) {
-                const float* Ra = S + offa;
-                float a0 = Ra[j], a1 = 0.0f;
-#pragma unroll
-                for (int q = 0; q + 4 <= j; q += 4) {
-                    const float4 va = *reinterpret_cast<const float4*>(Ra + q);
-                    a0 = fmaf(-va.x, rj[q], a0);
-                    a1 = fmaf(-va.y, rj[q + 1], a1);
-                    a0 = fmaf(-va.z, rj[q + 2], a0);
-                    a1 = fmaf(-va.w, rj[q + 3], a1);
-                }
-#pragma unroll
-                for (int q = j & ~3; q < j; ++q) a0 = fmaf(-Ra[q], rj[q], a0);
-                S[offa + j] = (a0 + a1) * r;
-            }
-            __syncwarp();
-            if (par == 0) S[tri_off(j) + j] = r;  // the diagonal slot keeps 1 / L[j][j]
-        });
-        __syncwarp();
-        // L^T x = y (y = row K of the factorised record), column-oriented, all lanes of the item
-        float y[K];
-#pragma unroll
-        for (int q = 0; q < K; q += 4) {
-            const float4 v = *reinterpret_cast<const float4*>(S + kRhs + q);
-            y[q] = v.x;
-            y[q + 1] = v.y;
-            y[q + 2] = v.z;
-            y[q + 3] = v.w;
-        }
-        static_for<K>([&](auto qc) {
-            constexpr int q = K - 1 - decltype(qc)::value;
-            const float* Rq = S + tri_off(q);
-            y[q] *= Rq[q];
-#pragma unroll
-            for (int i = 0; i + 4 <= q; i += 4) {
-                const float4 v = *reinterpret_cast<const float4*>(Rq + i);
-                y[i] = fmaf(-v.x, y[q], y[i]);
-                y[i + 1] = fmaf(-v.y, y[q], y[i + 1]);
-                y[i + 2] = fmaf(-v.z, y[q], y[i + 2]);
-                y[i + 3] = fmaf(-v.w, y[q], y[i + 3]);
-            }
-#pragma unroll
-            for (int i = q & ~3; i < q; ++i) y[i] = fmaf(-Rq[i], y[q], y[i]);
-        });
-        if (live && par == 0) {  // every lane of the item holds x; part 0 writes the K-float row
-            float4* xo = reinterpret_cast<float4*>(X + item * K);
-            const bool empty = cnt == 0.0f;  // item without observations: x = 0 (ocgo_als_fit)
-#pragma unroll
-            for (int q = 0; q < K / 4; ++q)
-                xo[q] = empty ? make_float4(0.0f, 0.0f, 0.0f, 0.0f)
-                              : make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-        }
-        __syncwarp();
-    }
-}
-
-// K4 over records in global memory: items 0..nitems-1, or the listed items
-// (list != nullptr); item i's record at slot first[i] (first == nullptr: slot i).
-template <int K>
-__global__ void __launch_bounds__(32) als_solve_records_kernel(int64_t nitems, const int32_t* __restrict__ first,
-                                                               const float* __restrict__ rec, float* __restrict__ X,
-                                                               float lambda, const int32_t* __restrict__ list,
-                                                               const int32_t* __restrict__ list_count) {
-    constexpr int kRec = Cfg<K>::kRec, kSys = nsys<K>();
-    extern __shared__ __align__(16) float srec[];
-    const int lane = threadIdx.x;
-    const int64_t nwork = list ? static_cast<int64_t>(*list_count) : nitems;
-    const int64_t nbatch = (nwork + kSys - 1) / kSys;
-    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
-        const int64_t i0 = bt * kSys;
-        const int nb = static_cast<int>(nwork - i0 < kSys ? nwork - i0 : kSys);
-        // stage: the warp copies record r with coalesced 16-byte cp.async
-        int64_t myitem = 0, myslot = 0;
-        if (lane < nb) {
-            myitem = list ? static_cast<int64_t>(list[i0 + lane]) : i0 + lane;
-            myslot = first ? static_cast<int64_t>(first[myitem]) : myitem;
-        }
-        for (int r = 0; r < nb; ++r) {
-            const int64_t slot = __shfl_sync(0xffffffffu, myslot, r);
-            const float4* src = reinterpret_cast<const float4*>(rec + slot * kRec);
-            float4* dst = reinterpret_cast<float4*>(srec + r * kRec);
-            for (int c = lane; c < kRec / 4; c += 32) {
-                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + c));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + c) : "memory");
-            }
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-        const int64_t item = __shfl_sync(0xffffffffu, myitem, lane % kSys);
-        solve_staged<K>(srec, nb, item, X, lambda);
-    }
-}
 
 // register-row K4: lanes per system (rank 32: 4 lanes x 8 rows, rank 64: 16 lanes x 4 rows)
 template <int K>
@@ -833,19 +620,6 @@ __device__ __forceinline__ float& el(float2 (&r)[N], int i) {
     return (i & 1) ? r[i >> 1].y : r[i >> 1].x;
 }
 
-// OCG_SOLVE_STAGED=1 selects the shared-memory solver (A/B measurement)
-static bool solve_rows_off() {
-    static const bool off = [] {
-        const char* e = std::getenv("OCG_SOLVE_STAGED");
-        return e && e[0] == '1';
-    }();
-    return off;
-}
-
-// the register-row K4 also leaves max |x| in AlsHalf::xmax (launch_als_pack can skip its pass)
-bool als_solve_tracks_max() { return !solve_rows_off(); }
-
-
 // K4 at rank 32 with register-resident rows: lane (sys = lane & 7, par = lane >> 3)
 // holds rows i = 4m + par (m = 0..7, row m = columns 0..4m+3) of system sys in
 // registers, loaded straight from the record.  Left-looking: at column j the
@@ -853,9 +627,8 @@ bool als_solve_tracks_max() { return !solve_rows_off(); }
 // reads it once (float4, broadcast over the item's 4 lanes) and updates its rows
 // m >= j/4 with register operands only -- 8 independent chains, no shared-memory
 // operand per FMA.  The rhs is carried as row K by all four lanes (forward
-// substitution folded in, as in solve_staged); the published rows plus 1/L[j][j]
-// then serve the column-oriented back substitution L^T x = y.  Same arithmetic as
-// solve_staged up to the order of the row-dot partial sums.
+// substitution folded in); the published rows plus 1/L[j][j]
+// then serve the column-oriented back substitution L^T x = y.
 template <int K>
 __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, const int32_t* __restrict__ first,
                                                             const float* __restrict__ rec, float* __restrict__ X,
@@ -883,10 +656,6 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
     const int64_t nbatch = (nwork + kSys - 1) / kSys;
     int64_t bt = blockIdx.x;
     if (bt >= nbatch) return;
-    // Software pipeline over the warp's batches: the next batch's rows are loaded into the L
-    // registers (dead after the factorisation) and its rhs/count tail is copied into shared
-    // memory while the current batch runs its back substitution.
-    constexpr bool kPipe = false;
     float2 L[R][K / 2];  // column pairs; row m = LPS m + par uses (m + 1) LPS columns
     bool live;
     int64_t item;
@@ -1007,7 +776,6 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
         const bool cur_live = live;
         const int64_t cur_item = item;
         const int64_t nbt = bt + gridDim.x;
-        if (kPipe && nbt < nbatch) fetch(nbt);  // in flight during the back substitution
         // L^T x = y, column-oriented over the published rows, all lanes of the item
         if constexpr (DY) static_for<K>([&](auto qc) {  // x_q from its owner, then every lane's pairs
             constexpr int q = K - 1 - decltype(qc)::value, pq = q / 2;
@@ -1059,7 +827,7 @@ __global__ void __launch_bounds__(32) als_solve_rows_kernel(int64_t nitems, cons
         }
         __syncwarp();
         if (nbt >= nbatch) break;
-        if (!kPipe) fetch(nbt);
+        fetch(nbt);
         bt = nbt;
     }
     if (xmax) {
@@ -1073,46 +841,34 @@ template <int K>
 static cudaError_t launch_solve_k(int64_t nitems, const int32_t* first, const float* rec, float* X, float lambda,
                                   int sm_count, cudaStream_t s, const int32_t* list = nullptr,
                                   const int32_t* list_count = nullptr, unsigned* xmax = nullptr) {
-    if (!solve_rows_off()) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows_kernel<K>, 32, 0);
-        constexpr int kSys = 32 / rows_lps<K>();
-        int64_t blocks = (nitems + kSys - 1) / kSys;
-        const int64_t cap = static_cast<int64_t>(sm_count) * std::max(per_sm, 1);
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        als_solve_rows_kernel<K><<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda, list,
-                                                                              list_count, xmax);
-        return cudaGetLastError();
-    }
-    constexpr int smem = solve_smem<K>();
-    cudaFuncSetAttribute(als_solve_records_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int64_t nbatch = (nitems + nsys<K>() - 1) / nsys<K>();
-    int64_t blocks = nbatch;
-    const int64_t cap = static_cast<int64_t>(sm_count) * (K == 32 ? 11 : 6);  // shared-memory bound
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_solve_rows_kernel<K>, 32, 0);
+    constexpr int kSys = 32 / rows_lps<K>();
+    int64_t blocks = (nitems + kSys - 1) / kSys;
+    const int64_t cap = static_cast<int64_t>(sm_count) * std::max(per_sm, 1);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    als_solve_records_kernel<K><<<static_cast<unsigned>(blocks), 32, smem, s>>>(nitems, first, rec, X, lambda, list,
-                                                                             list_count);
+    als_solve_rows_kernel<K><<<static_cast<unsigned>(blocks), 32, 0, s>>>(nitems, first, rec, X, lambda, list,
+                                                                          list_count, xmax);
     return cudaGetLastError();
 }
 
 // one tensor-core half-sweep: K3 records per segment -> reduce -> K4 (mode 0), or
 // -> per-item Gram records in h.gram_out (mode 1, multi-GPU column side)
-template <int K, bool FUSED, bool SPLIT = false>
+template <int K, bool SPLIT = false>
 static cudaError_t launch_gram_k(const AlsHalf& h, int sm_count, cudaStream_t s) {
-    constexpr int W = gram_warps<K, FUSED, SPLIT>();
-    const size_t smem = sizeof(uint4) * W * gram_warp_u4<K, FUSED>();
+    constexpr int W = gram_warps<K, SPLIT>();
+    const size_t smem = sizeof(uint4) * W * Cfg<K>::kStageU4;
     int64_t blocks = (h.max_segs + W - 1) / W;
-    const int64_t cap = static_cast<int64_t>(sm_count) * (FUSED ? 1 : Cfg<K>::kMinBlocks);
+    const int64_t cap = static_cast<int64_t>(sm_count) * Cfg<K>::kMinBlocks;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    cudaFuncSetAttribute(als_mma_gram_kernel<K, FUSED, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(als_mma_gram_kernel<K, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     if (h.ev_gram0) cudaEventRecord(h.ev_gram0, s);
-    als_mma_gram_kernel<K, FUSED, SPLIT><<<static_cast<unsigned>(blocks), W * 32, smem, s>>>(
+    als_mma_gram_kernel<K, SPLIT><<<static_cast<unsigned>(blocks), W * 32, smem, s>>>(
         h.total_segs, h.seg_order, h.seg_item, h.seg_beg, h.ptr, h.idx, h.valh, h.Yh, h.ymax, h.vmax, h.partial,
-        h.blk_ctr, h.nseg, h.X, h.lambda);
+        h.blk_ctr, h.nseg);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (h.ev_gram1) cudaEventRecord(h.ev_gram1, s);
@@ -1123,12 +879,10 @@ template <int K>
 static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(h.blk_ctr, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return e;
-    const bool fused = K == 32 && mode == 0 && h.fuse_solve;
-    unsigned* xmax = (mode == 0 && !fused && h.xmax && als_solve_tracks_max()) ? h.xmax : nullptr;
+    unsigned* xmax = (mode == 0 && h.xmax) ? h.xmax : nullptr;
     if (xmax && (e = cudaMemsetAsync(xmax, 0, sizeof(unsigned), s)) != cudaSuccess) return e;
-    if (fused) e = launch_gram_k<32, true>(h, sm_count, s);
-    else if (K == 32 && h.seg_order) e = launch_gram_k<32, false, true>(h, sm_count, s);  // column side
-    else e = launch_gram_k<K, false>(h, sm_count, s);
+    if (K == 32 && h.seg_order) e = launch_gram_k<32, true>(h, sm_count, s);  // column side
+    else e = launch_gram_k<K>(h, sm_count, s);
     if (e != cudaSuccess) return e;
     const unsigned rblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(h.nitems, sm_count * 12)));
     // column side: a few items with many segments (y spreads their groups); row side: many short items
@@ -1146,9 +900,6 @@ static cudaError_t launch_half_k(const AlsHalf& h, int mode, int sm_count, cudaS
                                                          h.partial, nullptr);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (fused)  // the single-segment items were solved inside the Gram kernel
-        return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s, h.multi_list,
-                                 h.multi_count);
     return launch_solve_k<K>(h.nitems, h.first, h.partial, h.X, h.lambda, sm_count, s, nullptr, nullptr, xmax);
 }
 

@@ -223,7 +223,6 @@ static ocg::AlsHalf als_half(ocg_als_plan* P, int sd) {
     // K4 fused into the row-side Gram kernel (solve batches of single-segment rows
     // in shared memory): measured 5.1 ms/launch vs 2.0 + 1.7 ms split (7 warps/SM
     // for Gram + batches starve both); kept as an ablation switch, off
-    h.fuse_solve = false;
     h.Y = sd == 0 ? P->V.p : P->U.p;
     h.X = sd == 0 ? P->U.p : P->V.p;
     h.partial = S.partial.p;
@@ -875,7 +874,7 @@ int ocg_als_plan_run(ocg_als_plan* P, float* total_ms, float* phase_ms) {
             hc.ev_gram0 = P->ev[8];
             hc.ev_gram1 = P->ev[9];
         }
-        const bool track = mma_rank(P->k) && !hr.fuse_solve && ocg::als_solve_tracks_max();
+        const bool track = mma_rank(P->k);
         if (mma_rank(P->k)) {
             hr.xmax = P->maxbits.p + 0;  // U's packing scale, produced by the row-side K4
             hc.xmax = P->maxbits.p + 1;  // V's
