@@ -137,6 +137,27 @@ int ocg_online_plan_results(ocg_online_plan* plan, double* completed, int32_t* i
                             double* loss, int32_t* ncand, ocg_ncf_meta* meta, int32_t* status);
 void ocg_online_plan_destroy(ocg_online_plan* plan);
 
+/* ---- batched online-phase streams --------------------------
+ * phase::DetectorConfig (phasedet.hpp:13-20) */
+typedef struct {
+    double delta_s, window_s, p_th_w;  /* defaults 0.2 s, 5 s, 60 W */
+} ocg_detector_config;
+
+/* phase::Detector (phasedet.cpp:27-52) over nstreams GPU-power streams (row-major
+ * nstreams x nsamples host array; stream s uses its first lengths[s] samples, or all
+ * with lengths == NULL): fire_index[s] = index of the sample on which the
+ * sliding-window CPU->GPU transition detector first fires (every sample of a full
+ * window of window_s/delta_s fed samples >= p_th_w), -1 if it never does.
+ * armed_start = 0: every sample is fed (detect_offline, phasedet.cpp:61-67);
+ * 1: feeding starts at the first sample below the threshold (run_open_online's
+ * arming rule, policy.cpp:138-139).  Config errors as DetectorConfig::validate
+ * (OCG_E_INVALID); status[s] (may be NULL) = OCG_E_INVALID for a stream that feeds a
+ * negative sample before firing (Detector::feed's invalid_argument). */
+int ocg_phase_detect_batch(ocg_ctx* ctx, const ocg_detector_config* cfg, int64_t nstreams, int64_t nsamples,
+                           const double* power, const int64_t* lengths, int armed_start, int64_t* fire_index,
+                           int32_t* status);
+
+
 /* Fit-only variant returning every app's parameters in the flat layout
  * [app table | setting table | W0 b0 W1 b1 ... ] (the reference's Adam block
  * order, cfcomplete.cpp:107-110) for parameter-level parity tests. */
@@ -455,6 +476,26 @@ int ocg_predictor_parse(const char* text, int32_t* n_layers, int64_t* dims, int3
                         int64_t* nparams, double* mean7, double* std7, int* has_stats);
 int ocg_predictor_from_json(ocg_ctx* ctx, const char* text, ocg_predictor** out);
 int ocg_predictor_load(ocg_ctx* ctx, const char* path, ocg_predictor** out);
+
+/* run_open_online (policy.cpp:114-191) for napps apps from their counter samples:
+ * probe ingest wired into the per-app completion on the device.  For app a the
+ * estimates are pred::predict_perf (predictor.cpp:151-157) of its nplan counter
+ * samples (napps x nplan x 7, CounterSample field order) at the plan's columns
+ * plan_cols[nplan] (ProbePlan order) — the re-probe rule (policy.cpp:168-176): when
+ * transition != NULL and transition[a] != 0 the pre-transition samples are dropped
+ * and reprobe_counters (same shape) are used instead — then cf::complete of the
+ * dense block + that row and policy::select_caps, as ocg_online_complete_batch.
+ * estimates (napps x nplan, may be NULL) returns the probe estimates; per-app
+ * status OCG_E_INVALID for an invalid counter sample (validate_counters). */
+int ocg_online_ingest_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_vals,
+                                     const uint8_t* block_mask, int64_t napps, const int32_t* plan_cols,
+                                     int32_t nplan, ocg_predictor* predictor, const double* counters,
+                                     const double* reprobe_counters, const int32_t* transition,
+                                     const uint64_t* seeds, const int32_t* cpu_caps, int32_t ncpu,
+                                     const int32_t* gpu_caps, int32_t ngpu, const ocg_ncf_hyper* hyper,
+                                     double gamma, int lane, double* estimates, double* completed, int32_t* idx,
+                                     double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta,
+                                     int32_t* status);
 
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */

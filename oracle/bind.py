@@ -229,6 +229,8 @@ class Ref:
                                            ctypes.c_int, c_vp, c_vp]
         L.ref_matrix_csv_roundtrip.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_vp, c_vp, c_vp]
         L.ref_load_predictor.argtypes = [ctypes.c_char_p, c_vp]
+        L.ref_run_trace.argtypes = [c_vp, ctypes.c_int, ctypes.c_int, c_u64, c_vp, c_sz, c_vp, c_vp]
+        L.ref_detect.argtypes = [c_vp, c_sz, c_dbl, c_dbl, c_dbl, ctypes.c_int, c_vp]
         L.ref_time_fit_step.argtypes = [c_sz, c_sz, c_sz, c_vp, c_sz, ctypes.c_int, c_vp]
         L.ref_time_fit_step.restype = c_dbl
         L.ref_complete_select_batch.restype = c_dbl
@@ -345,6 +347,22 @@ class Ref:
         secs = self.L.ref_time_fit_step(m, n, k, P(hid), len(hid), iters, P(parts))
         assert secs > 0, self.err()
         return secs, parts
+
+    def run_trace(self, spec, cpu_cap, gpu_cap, seed, cap=1 << 16):
+        """sim::run's GPU-power trace: (power samples, dt)."""
+        out = np.zeros(cap)
+        cnt, dt = c_sz(), c_dbl()
+        rc = self.L.ref_run_trace(ctypes.byref(spec), cpu_cap, gpu_cap, seed, P(out), cap, ctypes.byref(cnt),
+                                  ctypes.byref(dt))
+        assert rc == 0, self.err()
+        return out[: min(cnt.value, cap)].copy(), dt.value
+
+    def detect(self, power, delta_s=0.2, window_s=5.0, p_th=60.0, armed=0):
+        """(rc, fire index or -1) of the reference detector on one stream."""
+        p = np.ascontiguousarray(power, np.float64)
+        f = ctypes.c_int64()
+        rc = self.L.ref_detect(P(p), len(p), delta_s, window_s, p_th, armed, ctypes.byref(f))
+        return rc, f.value
 
     def load_predictor(self, path):
         hs = ctypes.c_int()

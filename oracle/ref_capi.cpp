@@ -22,6 +22,7 @@
 #include "opencap/cfcomplete.hpp"
 #include "opencap/core.hpp"
 #include "opencap/kernels.hpp"
+#include "opencap/phasedet.hpp"
 #include "opencap/policy.hpp"
 #include "opencap/predictor.hpp"
 #include "opencap/rng.hpp"
@@ -751,6 +752,60 @@ double ref_time_fit_step(size_t m, size_t n, size_t k, const size_t* hidden, siz
     }
 }
 
+// sim::run (simnode.cpp) of a spec at one setting: its GPU-power trace (the stream the
+// phase detector watches); returns the sample count (<= cap) and the sampling interval
+int ref_run_trace(const ref_spec* spec, int cpu_cap, int gpu_cap, uint64_t seed, double* power, size_t cap,
+                  size_t* count, double* dt) {
+    try {
+        const auto r = sim::run(from_c(*spec), PowerSetting{cpu_cap, gpu_cap}, seed);
+        const size_t n = std::min(cap, r.trace.samples.size());
+        for (size_t i = 0; i < n; ++i) power[i] = r.trace.samples[i].gpu_power_w;
+        *count = r.trace.samples.size();
+        *dt = r.trace.dt;
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// phase::detect_offline (phasedet.cpp:58-67) on a GPU-power stream (armed = 0), or the
+// reference Detector fed under run_open_online's arming rule (armed = 1, policy.cpp:138-140):
+// index of the firing sample or -1
+int ref_detect(const double* power, size_t n, double delta_s, double window_s, double p_th, int armed,
+               int64_t* fire) {
+    try {
+        phase::DetectorConfig cfg{delta_s, window_s, p_th};
+        if (!armed) {
+            sim::PowerTrace tr;
+            tr.dt = delta_s;
+            for (size_t i = 0; i < n; ++i) tr.samples.push_back({static_cast<double>(i + 1) * delta_s, 0.0, power[i]});
+            const auto t = phase::detect_offline(tr, cfg);
+            *fire = -1;
+            if (t)
+                for (size_t i = 0; i < n; ++i)
+                    if (tr.samples[i].t_s == *t) {
+                        *fire = static_cast<int64_t>(i);
+                        break;
+                    }
+            return 0;
+        }
+        phase::Detector det(cfg);
+        bool on = false;
+        *fire = -1;
+        for (size_t i = 0; i < n; ++i) {
+            if (!on && power[i] < cfg.p_th_w) on = true;
+            if (on && det.feed(power[i]) == phase::Decision::transition) {
+                *fire = static_cast<int64_t>(i);
+                break;
+            }
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 }  // extern "C"
+
 
 

@@ -216,3 +216,14 @@ _sig("ocg_matrix_destroy", None, c_vp)
 _sig("ocg_predictor_parse", ctypes.c_int, ctypes.c_char_p, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_predictor_from_json", ctypes.c_int, c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp))
 _sig("ocg_predictor_load", ctypes.c_int, c_vp, ctypes.c_char_p, ctypes.POINTER(c_vp))
+
+# batched online-phase streams: phase detector, probe ingest wired into the per-app completion
+class DetectorConfigC(ctypes.Structure):
+    """ocg_detector_config == phase::DetectorConfig (phasedet.hpp:13-20)."""
+
+    _fields_ = [("delta_s", c_dbl), ("window_s", c_dbl), ("p_th_w", c_dbl)]
+
+
+_sig("ocg_phase_detect_batch", ctypes.c_int, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp)
+_sig("ocg_online_ingest_complete_batch", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp,
+     c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)

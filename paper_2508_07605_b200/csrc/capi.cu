@@ -711,6 +711,104 @@ int ocg_predictor_run(ocg_predictor* pred, const double* counters, int64_t count
     return OCG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// re-probe rule (policy.cpp:168-176): the counters an app's estimates come from
+__global__ void ingest_select_kernel(int64_t napps, int nplan, const double* __restrict__ probe,
+                                     const double* __restrict__ reprobe, const int32_t* __restrict__ transition,
+                                     double* __restrict__ out) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t per = static_cast<int64_t>(nplan) * 7;
+    if (q >= napps * per) return;
+    const int64_t a = q / per;
+    out[q] = (reprobe && transition && transition[a]) ? reprobe[q] : probe[q];
+}
+
+// validate_counters (core.cpp:74-83) per app, then the estimates into the app rows
+__global__ void ingest_scatter_kernel(int64_t napps, int nplan, int64_t n, const int32_t* __restrict__ plan_cols,
+                                      const double* __restrict__ counters, const double* __restrict__ est,
+                                      double* __restrict__ probe_vals, int32_t* __restrict__ bad_app) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= napps * nplan) return;
+    const int64_t a = q / nplan;
+    const int p = static_cast<int>(q - a * nplan);
+    const double* c = counters + q * 7;
+    bool ok = true;
+    for (int f = 0; f < 7; ++f) ok = ok && isfinite(c[f]);
+    ok = ok && c[2] >= 0 && c[3] >= 0 && c[4] >= 0 && c[5] >= 0 && c[5] <= 1 && c[6] >= 0 && c[6] <= 1;
+    if (!ok) atomicExch(bad_app + a, 1);
+    probe_vals[a * n + plan_cols[p]] = ok ? est[q] : 1.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ocg_online_ingest_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double* block_vals,
+                                     const uint8_t* block_mask, int64_t napps, const int32_t* plan_cols,
+                                     int32_t nplan, ocg_predictor* pred, const double* counters,
+                                     const double* reprobe_counters, const int32_t* transition,
+                                     const uint64_t* seeds, const int32_t* cpu, int32_t ncpu, const int32_t* gpu,
+                                     int32_t ngpu, const ocg_ncf_hyper* h, double gamma, int lane, double* estimates,
+                                     double* completed, int32_t* idx, double* saving, double* loss, int32_t* ncand,
+                                     ocg_ncf_meta* meta, int32_t* status) {
+    if (!ctx || !pred || !status || (napps > 0 && (!counters || !plan_cols || !seeds)))
+        return fail(OCG_E_INVALID, "null argument");
+    if (lane != OCG_LANE_SCALAR && lane != OCG_LANE_AVX2) return fail(OCG_E_INVALID, "unknown lane");
+    if (cpu && check_grid(cpu, ncpu, gpu, ngpu)) return OCG_E_INVALID;
+    const int64_t n = static_cast<int64_t>(ncpu) * ngpu;
+    if (nplan <= 0 || nplan > n) return fail(OCG_E_INVALID, "probe plan: bad size");
+    for (int32_t p = 0; p < nplan; ++p)  // ProbePlan::validate (policy.cpp:84-96): distinct grid settings
+        if (plan_cols[p] < 0 || plan_cols[p] >= n) return fail(OCG_E_INVALID, "probe plan: setting outside the grid");
+    if (napps == 0) return OCG_OK;
+    // the per-app plan, with placeholder estimates at the plan cells (overwritten on the device)
+    std::vector<double> pv(static_cast<size_t>(napps * n), 0.0);
+    std::vector<uint8_t> pm(static_cast<size_t>(napps * n), 0);
+    for (int64_t a = 0; a < napps; ++a)
+        for (int32_t p = 0; p < nplan; ++p) {
+            pv[static_cast<size_t>(a * n + plan_cols[p])] = 1.0;
+            pm[static_cast<size_t>(a * n + plan_cols[p])] = 1;
+        }
+    const BatchInputs in{d_rows, block_vals, block_mask, napps, pv.data(), pm.data(), seeds, static_cast<int32_t>(n)};
+    ocg_online_plan* P = nullptr;
+    int rc = plan_create(ctx, in, cpu, ncpu, gpu, ngpu, h, gamma, lane, completed != nullptr, 0, &P);
+    if (rc) return rc;
+    std::unique_ptr<ocg_online_plan> guard(P);
+    cudaStream_t s = ctx->stream;
+    const int64_t ns = napps * nplan;
+    DBuf<double> dprobe, dre, dsel, dest;
+    DBuf<int32_t> dtr, dplan, dbad;
+    OCG_CUDA(dprobe.upload(counters, static_cast<size_t>(ns * 7), s));
+    if (reprobe_counters && transition) {
+        OCG_CUDA(dre.upload(reprobe_counters, static_cast<size_t>(ns * 7), s));
+        OCG_CUDA(dtr.upload(transition, static_cast<size_t>(napps), s));
+    }
+    OCG_CUDA(dsel.alloc(static_cast<size_t>(ns * 7)));
+    OCG_CUDA(dest.alloc(static_cast<size_t>(ns)));
+    OCG_CUDA(dplan.upload(plan_cols, static_cast<size_t>(nplan), s));
+    OCG_CUDA(dbad.alloc(static_cast<size_t>(napps)));
+    OCG_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int32_t) * napps, s));
+    ingest_select_kernel<<<static_cast<unsigned>((ns * 7 + 255) / 256), 256, 0, s>>>(napps, nplan, dprobe.p, dre.p,
+                                                                                     dtr.p, dsel.p);
+    OCG_CUDA(cudaGetLastError());
+    // pred::predict_perf over every sample; invalid samples are flagged per app below, not fatal
+    OCG_CUDA(ocg::launch_predict_perf(pred->g, pred->params.p, dsel.p, ns, dest.p, pred->bad.p, lane, ctx->sm_count, s));
+    ingest_scatter_kernel<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, s>>>(napps, nplan, n, dplan.p, dsel.p,
+                                                                                  dest.p, P->d_pv.p, dbad.p);
+    OCG_CUDA(cudaGetLastError());
+    std::vector<int32_t> bad(static_cast<size_t>(napps));
+    OCG_CUDA(dbad.download(bad.data(), bad.size(), s));
+    if (estimates) OCG_CUDA(dest.download(estimates, static_cast<size_t>(ns), s));
+    OCG_CUDA(cudaStreamSynchronize(s));
+    for (int64_t a = 0; a < napps; ++a)
+        if (bad[static_cast<size_t>(a)] && P->hstatus[static_cast<size_t>(a)] == OCG_OK)
+            P->hstatus[static_cast<size_t>(a)] = OCG_E_INVALID;  // predict_perf's validate_counters
+    if ((rc = plan_run(P, nullptr))) return rc;
+    return plan_results(P, completed, idx, saving, loss, ncand, meta, status, nullptr);
+}
+
 int ocg_predictor_destroy(ocg_predictor* pred) {
     delete pred;
     return OCG_OK;
