@@ -209,10 +209,21 @@ __device__ __forceinline__ T* sp(char* base, uint32_t off) {
 
 extern __shared__ __align__(16) char g_jsmem[];
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Spin with relaxed loads and acquire once: an ld.acquire compiles to a load plus an
+// L1 invalidation (CCTL.IVALL), which inside a spin loop evicts the waiting SM's L1
+// on every iteration (76 % of the epoch kernel's stall samples in the first capture).
+__device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void wait_geq(const int* p, int want, bool sleep) {
+    if (ld_relaxed(p) < want) {
+        do {
+            if (sleep) __nanosleep(32);
+        } while (ld_relaxed(p) < want);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -293,8 +304,53 @@ __device__ __forceinline__ MlpParam decode_mlp(const JointArgs<T>& a, int e) {
 }
 
 // ------------------------------------------------------------- leader CTA
-template <class NUM, typename T>
+// Layer shapes: run-time (any NcfHyper within the kernel's limits) or compile-time
+// (FixShape: every layer loop unrolled, every index product folded).
+struct RtShape {
+    int L_, ka_, ks_, kmax_, dims_[kJMaxL + 1], stride_[kJMaxL + 1], offw_[kJMaxL], offb_[kJMaxL];
+    template <typename T>
+    __device__ explicit RtShape(const JointArgs<T>& a) : L_(a.L), ka_(a.ka), ks_(a.ks), kmax_(a.kmax) {
+#pragma unroll
+        for (int l = 0; l <= kJMaxL; ++l) {
+            dims_[l] = l <= a.L ? a.dims[l] : 0;
+            stride_[l] = l <= a.L ? a.stride[l] : 0;
+        }
+#pragma unroll
+        for (int l = 0; l < kJMaxL; ++l) {
+            offw_[l] = l < a.L ? a.off_w[l] : 0;
+            offb_[l] = l < a.L ? a.off_b[l] : 0;
+        }
+    }
+    __device__ int L() const { return L_; }
+    __device__ int ka() const { return ka_; }
+    __device__ int ks() const { return ks_; }
+    __device__ int kmax() const { return kmax_; }
+    __device__ int dim(int l) const { return dims_[l]; }
+    __device__ int stride(int l) const { return stride_[l]; }
+    __device__ int off_w(int l) const { return offw_[l]; }
+    __device__ int off_b(int l) const { return offb_[l]; }
+};
+
+template <int KA, int KS, int H0, int H1>
+struct FixShape {
+    template <typename T>
+    __device__ explicit FixShape(const JointArgs<T>&) {}
+    __device__ static constexpr int L() { return 3; }
+    __device__ static constexpr int ka() { return KA; }
+    __device__ static constexpr int ks() { return KS; }
+    __device__ static constexpr int kmax() { return KA > KS ? KA : KS; }
+    __device__ static constexpr int dim(int l) { return l == 0 ? KA + KS : (l == 1 ? H0 : (l == 2 ? H1 : 1)); }
+    __device__ static constexpr int stride(int l) { return dim(l) | 1; }
+    __device__ static constexpr int off_w(int l) {
+        return l == 0 ? 0 : (l == 1 ? (KA + KS) * H0 + H0 : (KA + KS) * H0 + H0 + H0 * H1 + H1);
+    }
+    __device__ static constexpr int off_b(int l) { return off_w(l) + dim(l) * dim(l + 1); }
+};
+using DefaultShape = FixShape<8, 8, 32, 16>;  // NcfHyper{} (cfcomplete.hpp:11-20)
+
+template <class NUM, class SH, typename T>
 __device__ void leader_epoch(const JointArgs<T>& a) {
+    const SH sh(a);
     char* sm = g_jsmem;
     const JLayout& ly = a.lay;
     T* P = sp<T>(sm, ly.P);
@@ -305,8 +361,8 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
     int* sss = sp<int>(sm, ly.sss);
     const ExpTabPtr tab{sp<uint64_t>(sm, ly.tab)};
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int L = a.L, kmax = a.kmax, rs = 3 * kmax;
-    const int in0 = a.dims[0], st0 = a.stride[0];
+    const int L = sh.L(), kmax = sh.kmax(), rs = 3 * kmax;
+    const int in0 = sh.dim(0), st0 = sh.stride(0);
 
     const uint32_t* dec = a.dec;
     for (int e = tid; e < a.T_mlp; e += kJT) {
@@ -328,8 +384,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         if (tid == 0) {
             c0 = clock64();
             const int want = a.need[s];
-            while (ld_acquire(a.ready + s) < want) {
-            }
+            wait_geq(a.ready + s, want, false);
             c1 = clock64();
         }
         if (tid < cnt) {
@@ -344,7 +399,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             const int sl = q / kmax, c = q - sl * kmax;
             const int64_t row = a.slot_row[so + sl];
             const bool is_app = row < a.m;
-            const int k = is_app ? a.ka : a.ks;
+            const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
             const int ps = a.slot_prev[so + sl];
             T* d = cur + sl * rs;
@@ -366,17 +421,19 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         T* X = sp<T>(sm, ly.act[0]);
         for (int w = tid; w < cnt * in0; w += kJT) {
             const int smp = w / in0, i = w - smp * in0;
-            X[smp * st0 + i] = i < a.ka ? cur[ssa[smp] * rs + i] : cur[sss[smp] * rs + (i - a.ka)];
+            X[smp * st0 + i] = i < sh.ka() ? cur[ssa[smp] * rs + i] : cur[sss[smp] * rs + (i - sh.ka())];
         }
         __syncthreads();
         // ---- forward_tape (nnkit.cpp:124-138)
-        for (int l = 0; l < L; ++l) {
-            const int in = a.dims[l], out = a.dims[l + 1];
-            const T* W = P + a.off_w[l];
-            const T* b = P + a.off_b[l];
-            const T* ain = sp<T>(sm, ly.act[l]) + lane * a.stride[l];
-            T* aout = sp<T>(sm, ly.act[l + 1]) + lane * a.stride[l + 1];
-            T* gfo = sp<T>(sm, ly.del[l]) + lane * a.stride[l + 1];
+#pragma unroll
+        for (int l = 0; l < kJMaxL; ++l) {
+            if (l >= L) break;
+            const int in = sh.dim(l), out = sh.dim(l + 1);
+            const T* W = P + sh.off_w(l);
+            const T* b = P + sh.off_b(l);
+            const T* ain = sp<T>(sm, ly.act[l]) + lane * sh.stride(l);
+            T* aout = sp<T>(sm, ly.act[l + 1]) + lane * sh.stride(l + 1);
+            T* gfo = sp<T>(sm, ly.del[l]) + lane * sh.stride(l + 1);
             const bool hidden = l + 1 < L;
             if (lane < cnt) {
                 for (int o = warp; o < out; o += kJW) {
@@ -392,20 +449,22 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         // ---- backprop_sample (nnkit.cpp:184-212)
         const T scale = NUM::kExact ? T(ddiv(1.0, static_cast<double>(cnt))) : T(1) / T(cnt);
         if (warp == 0 && lane < cnt) {
-            const T err = NUM::sub(sp<T>(sm, ly.act[L])[lane * a.stride[L]], T(sy[lane]));
-            sp<T>(sm, ly.del[L - 1])[lane * a.stride[L]] = NUM::mul(NUM::mul(NUM::mul(T(2), err), scale), T(1));
+            const T err = NUM::sub(sp<T>(sm, ly.act[L])[lane * sh.stride(L)], T(sy[lane]));
+            sp<T>(sm, ly.del[L - 1])[lane * sh.stride(L)] = NUM::mul(NUM::mul(NUM::mul(T(2), err), scale), T(1));
         }
         __syncthreads();
-        for (int l = L - 1; l >= 0; --l) {
-            const int in = a.dims[l], out = a.dims[l + 1];
-            const T* W = P + a.off_w[l];
-            const T* d = sp<T>(sm, ly.del[l]) + lane * a.stride[l + 1];
+#pragma unroll
+        for (int l = kJMaxL - 1; l >= 0; --l) {
+            if (l >= L) continue;
+            const int in = sh.dim(l), out = sh.dim(l + 1);
+            const T* W = P + sh.off_w(l);
+            const T* d = sp<T>(sm, ly.del[l]) + lane * sh.stride(l + 1);
             if (lane < cnt) {
                 for (int c = warp; c < in; c += kJW) {
                     T nd = T(0);  // matvec_t: out[c] = 0; out[c] += d[r] * w[r][c]
                     for (int r = 0; r < out; ++r) nd = NUM::axpy(nd, d[r], W[r * in + c]);
                     if (l > 0) {
-                        T* gf = sp<T>(sm, ly.del[l - 1]) + lane * a.stride[l] + c;
+                        T* gf = sp<T>(sm, ly.del[l - 1]) + lane * sh.stride(l) + c;
                         *gf = NUM::mul(nd, *gf);  // delta *= activate_grad
                     } else {
                         sp<T>(sm, ly.ig)[lane * st0 + c] = nd;
@@ -420,12 +479,17 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             const uint32_t d = __ldg(dec + e);
             const int layer = (d >> 16) & 15, r = (d >> 8) & 255, c = d & 255;
             const T* dl = sp<T>(sm, ly.del[layer]) + r;
-            const int sd = a.stride[layer + 1];
+            const int sd = sh.stride(layer + 1);
             T g = T(0);
             if (d & (1u << 20)) {  // outer_acc: G[r][c] += d[r] * x[c], samples in order
                 const T* al = sp<T>(sm, ly.act[layer]) + c;
-                const int sa = a.stride[layer];
+                const int sa = sh.stride(layer);
                 int q = 0;
+                if (cnt == kJMaxB) {
+#pragma unroll
+                    for (int q2 = 0; q2 < kJMaxB; ++q2) g = NUM::axpy(g, dl[q2 * sd], al[q2 * sa]);
+                    q = kJMaxB;
+                }
                 for (; q + 4 <= cnt; q += 4) {
                     const T d0 = dl[q * sd], d1 = dl[(q + 1) * sd], d2 = dl[(q + 2) * sd], d3 = dl[(q + 3) * sd];
                     const T x0 = al[q * sa], x1 = al[(q + 1) * sa], x2 = al[(q + 2) * sa], x3 = al[(q + 3) * sa];
@@ -445,7 +509,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             const int sl = q / kmax, c = q - sl * kmax;
             const int64_t row = a.slot_row[so + sl];
             const bool is_app = row < a.m;
-            const int k = is_app ? a.ka : a.ks;
+            const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
             T g = T(0);  // embedding-gradient scatter (cfcomplete.cpp:171-174)
             if (is_app) {
@@ -453,7 +517,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
                     if (ssa[q2] == sl) g = NUM::add(g, ig[q2 * st0 + c]);
             } else {
                 for (int q2 = 0; q2 < cnt; ++q2)
-                    if (sss[q2] == sl) g = NUM::add(g, ig[q2 * st0 + a.ka + c]);
+                    if (sss[q2] == sl) g = NUM::add(g, ig[q2 * st0 + sh.ka() + c]);
             }
             T* d = cur + sl * rs;
             const int64_t r = is_app ? row : row - a.m;
@@ -467,7 +531,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             const int sl = q / kmax, c = q - sl * kmax;
             const int64_t row = a.slot_row[so + sl];
             const bool is_app = row < a.m;
-            const int k = is_app ? a.ka : a.ks;
+            const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
             T* rec = is_app ? a.app_rec + row * 3 * k : a.set_rec + (row - a.m) * 3 * k;
             const T* d = cur + sl * rs;
@@ -513,7 +577,7 @@ __device__ void helper_epoch(const JointArgs<T>& a) {
         if (bi >= a.nbundle) break;
         const int wait = a.b_wait[bi];
         if (lane == 0 && wait >= 0)
-            while (ld_acquire(a.progress) < wait) __nanosleep(32);
+            wait_geq(a.progress, wait, true);
         __syncwarp();
         const int q0 = a.b_off[bi], cnt = a.b_off[bi + 1] - q0;
         int s = 0;
@@ -584,14 +648,14 @@ __device__ void eval_cells(const Arg& a, const T* mlp_p, const PView<T>& pv, con
         err2[i] = cell_sqerr<NUM>(a, W, pv, capp[i], cset[i], cy[i], tab);
 }
 
-template <class NUM>
+template <class NUM, class SH>
 __global__ void __launch_bounds__(kJT, 1) joint_epoch_kernel(JointArgs<typename NUM::T> a) {
     using T = typename NUM::T;
     cg::grid_group grid = cg::this_grid();
     if (blockIdx.x == 0) {
         for (int e = threadIdx.x; e < 256; e += kJT) sp<uint64_t>(g_jsmem, a.lay.tab)[e] = exp_tab(e);
         __syncthreads();
-        leader_epoch<NUM>(a);
+        leader_epoch<NUM, SH>(a);
     } else {
         helper_epoch<NUM>(a);
     }
@@ -1197,7 +1261,8 @@ int run_fit(cudaStream_t st, int sm_count, int64_t m, int64_t n, const int64_t* 
         a.prof = prof.p;
     }
 
-    auto kep = joint_epoch_kernel<NUM>;
+    const bool fixed = sh.L == 3 && sh.ka == 8 && sh.ks == 8 && sh.dims[1] == 32 && sh.dims[2] == 16 && h.batch_size == 32;
+    auto kep = fixed ? joint_epoch_kernel<NUM, DefaultShape> : joint_epoch_kernel<NUM, RtShape>;
     auto kev = joint_eval_kernel<NUM>;
     JCU(cudaFuncSetAttribute(kep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.lay.bytes)));
     JCU(cudaFuncSetAttribute(kev, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.lay.bytes)));
