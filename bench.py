@@ -1313,6 +1313,31 @@ def run_reference(args, d: Dist):
     raise SystemExit(f"unknown workload {args.workload}")
 
 
+def secondary_lines(args):
+    """Driver-visible measurements of the other reference-exact paths, run after the headline
+    (same process, 1 GPU): c1-fit (the reference's whole CF path at C1, bit-exact, one step) and
+    c0xn (the reference's per-app online semantics for 4096 apps), each with its own bounded
+    reference-CPU figure."""
+    import argparse as _ap
+
+    out = {}
+    d1 = Dist(None)
+    for name, over in (("c1-fit", dict(workload="c1-fit", steps=1, warmup=0)),
+                       ("c0xn", dict(workload="c0xn", steps=2, warmup=1, apps=4096))):
+        a2 = _ap.Namespace(**{**vars(args), **over})
+        try:
+            o, _ = WORKLOADS[name](a2, d1)
+            keep = {k: o[k] for k in ("metric", "value", "unit", "ms_per_step", "e2e", "dtype", "config", "quality",
+                                      "phases_ms_per_step", "parity", "roofline", "clocks") if k in o}
+            keep["steps"], keep["warmup"] = a2.steps, a2.warmup
+            if not args.no_cpu_baseline:
+                keep["cpu_baseline"] = cpu_baseline(name, os.cpu_count() or 1)
+            out[name] = keep
+        except Exception as e:  # reported, not fatal for the headline
+            out[name] = {"error": repr(e)}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1327,6 +1352,7 @@ def main():
     ap.add_argument("--apps", type=int, default=16384, help="c0xn: apps per GPU")
     ap.add_argument("--lane", type=int, default=1, help="reference FP lane to reproduce (0 scalar, 1 avx2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="c2-ncf: skip the secondary c1-fit / c0xn blocks")
     ap.add_argument("--exact-step", action="store_true",
                     help="c2-ncf/c1-ncf: also time one step of the bit-exact FP64 precision (outside the timed region)")
     args = ap.parse_args()
@@ -1353,6 +1379,8 @@ def main():
                 except Exception as e:  # reported, not fatal
                     line["cpu_baseline"] = {"value": None, "error": str(e)}
             line["peaks"] = PEAKS
+            if d.world == 1 and args.workload == "c2-ncf" and not args.no_secondary:
+                line["secondary"] = secondary_lines(args)
             print(json.dumps(line), flush=True)
     finally:
         d.close()
