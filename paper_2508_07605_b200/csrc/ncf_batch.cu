@@ -380,6 +380,61 @@ __device__ __forceinline__ double param_grad(const Smem& S, const A& a, uint32_t
     return gsum;
 }
 
+// Parameter ownership.  Run-time shapes: thread ctid owns parameters ctid + k kCT.
+// Compile-time shape (FixArch<8,8,32,16>): slots 0-3 are a 2x2 tile of W0 (threads 0-127)
+// or W1 (128-255), whose gradients share their operand loads (4 shared-memory loads per
+// 4 FMAs instead of 8); slots 4-5 take the remaining parameters in block order
+// (embeddings, b0, b1, W2, b2).  Each parameter still sums its gradient over the samples
+// in the reference's order.
+template <class ARCH>
+__device__ __forceinline__ int owned_index(const BatchGeom& g, int k, int ctid) {
+    if constexpr (!ARCH::kStatic) {
+        return ctid + k * kCT;
+    } else {
+        constexpr int in0 = ARCH::dim(0), h0 = ARCH::dim(1), h1 = ARCH::dim(2);
+        if (k < 4) {
+            if (ctid < 128) {  // W0: h0 x in0, tiles of 2 rows x 2 cols
+                const int r = 2 * (ctid / (in0 / 2)) + (k >> 1), c = 2 * (ctid % (in0 / 2)) + (k & 1);
+                return g.off_w[0] + r * in0 + c;
+            }
+            const int tt = ctid - 128;  // W1: h1 x h0
+            const int r = 2 * (tt / (h0 / 2)) + (k >> 1), c = 2 * (tt % (h0 / 2)) + (k & 1);
+            return g.off_w[1] + r * h0 + c;
+        }
+        int q = ctid + (k - 4) * kCT;
+        if (q < g.off_w[0]) return q;  // embedding tables
+        q -= g.off_w[0];
+        if (q < h0) return g.off_b[0] + q;
+        q -= h0;
+        if (q < h1) return g.off_b[1] + q;
+        q -= h1;
+        if (q < h1) return g.off_w[2] + q;
+        q -= h1;
+        if (q < 1) return g.off_b[2];
+        return g.T;  // no parameter
+    }
+}
+
+// gradients of the 2x2 tile W_LAY[r..r+1][c..c+1], each summed over the batch in sample order
+template <int LANE, int LAY, class A>
+__device__ __forceinline__ void tile_grad(const Smem& S, const A& a, int r, int c, int cnt, double (&gt)[4]) {
+    const double* dl = S.del(LAY) + r;
+    const double* al = S.act(LAY) + c;
+    constexpr int sd = A::stride(LAY + 1), sa = A::stride(LAY);
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+    for (int q = 0; q < cnt; ++q) {
+        const double d0 = dl[q * sd], d1 = dl[q * sd + 1], x0 = al[q * sa], x1 = al[q * sa + 1];
+        g0 = LaneOps<LANE>::axpy(g0, d0, x0);
+        g1 = LaneOps<LANE>::axpy(g1, d0, x1);
+        g2 = LaneOps<LANE>::axpy(g2, d1, x0);
+        g3 = LaneOps<LANE>::axpy(g3, d1, x1);
+    }
+    gt[0] = g0;
+    gt[1] = g1;
+    gt[2] = g2;
+    gt[3] = g3;
+}
+
 template <int LANE, class ARCH>
 __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO& io) {
     const ARCH a{g};
@@ -395,10 +450,12 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
 
     // owned parameters (compile-time indexed so moments stay in registers)
     uint32_t own[kEPT];
+    int eidx[kEPT];
     double M1[kEPT], V1[kEPT], BEST[kEPT];
 #pragma unroll
     for (int k = 0; k < kEPT; ++k) {
-        own[k] = is_rng ? 0u : describe(g, ctid + k * kCT);
+        eidx[k] = is_rng ? g.T : owned_index<ARCH>(g, k, ctid);
+        own[k] = is_rng ? 0u : describe(g, eidx[k]);
         M1[k] = V1[k] = BEST[k] = 0.0;
     }
 
@@ -498,7 +555,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
 #pragma unroll
                 for (int k = 0; k < kEPT; ++k) {
                     M1[k] = V1[k] = 0.0;
-                    if (own_valid(own[k])) BEST[k] = S.P()[ctid + k * kCT];
+                    if (own_valid(own[k])) BEST[k] = S.P()[eidx[k]];
                 }
                 init_train = cells_mse<LANE>(S, a, g, S.tset(), nt, warp, lane, ctid);
                 best_val = cells_mse<LANE>(S, a, g, mon, nmon, warp, lane, ctid);
@@ -538,12 +595,17 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                         b1p = dmul(b1p, b1);
                         b2p = dmul(b2p, b2);
                         const double mc = ddiv(1.0, dsub(1.0, b1p)), vc = ddiv(1.0, dsub(1.0, b2p));
+                        double gt[4] = {0.0, 0.0, 0.0, 0.0};
+                        if constexpr (ARCH::kStatic) {
+                            if (ctid < 128) tile_grad<LANE, 0>(S, a, own_r(own[0]), own_c(own[0]), cnt, gt);
+                            else tile_grad<LANE, 1>(S, a, own_r(own[0]), own_c(own[0]), cnt, gt);
+                        }
 #pragma unroll
                         for (int k = 0; k < kEPT; ++k) {
                             const uint32_t o = own[k];
                             if (!own_valid(o)) continue;
-                            const int e = ctid + k * kCT;
-                            const double gsum = param_grad<LANE>(S, a, o, cnt);
+                            const int e = eidx[k];
+                            const double gsum = (ARCH::kStatic && k < 4) ? gt[k < 4 ? k : 0] : param_grad<LANE>(S, a, o, cnt);
                             double p = S.P()[e];
                             LaneOps<LANE>::adam(p, M1[k], V1[k], gsum, lr, b1, omb1, b2, omb2, eps, mc, vc,
                                                 own_vec(o));
@@ -578,7 +640,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                 if (!is_rng && S.ctrl()[kImproved]) {
 #pragma unroll
                     for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) BEST[k] = S.P()[ctid + k * kCT];
+                        if (own_valid(own[k])) BEST[k] = S.P()[eidx[k]];
                 }
                 if (stop) {
                     ++epoch;
@@ -592,7 +654,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                 if (!is_rng) {
 #pragma unroll
                     for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) S.P()[ctid + k * kCT] = BEST[k];
+                        if (own_valid(own[k])) S.P()[eidx[k]] = BEST[k];
                 }
                 __syncthreads();
                 double final_train = 0.0;
