@@ -29,6 +29,7 @@
 //        x K = 32, FP16 hi/lo split: Ah.Wh + Ah.Wl + Al.Wh, FP32 accumulate in
 //        TMEM); B_j tiles arrive by TMA.  |dp|/p ~ 1e-6; selections exact
 //        wherever the row's margin exceeds that.
+#include <algorithm>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -447,24 +448,38 @@ __global__ void __launch_bounds__(kExW * 32) ncf_exact_generic_kernel(NcfSelArgs
 // ====================================================== fast path: prep
 // A_i = W0[:, :ka] . u_i + b0 and B_j = W0[:, ka:] . v_j (FP64, rounded once),
 // their exps, and the max magnitudes that set the FP16 split's scale.
+// warp max of |v| first, then one atomic per warp (a single-address atomic per thread
+// serialises ~32M updates at C2 in L2)
 __device__ __forceinline__ void atomic_max_f(unsigned* addr, float v) {
-    atomicMax(addr, __float_as_uint(fabsf(v)));  // non-negative floats order like their bits
+    unsigned b = __float_as_uint(fabsf(v));  // non-negative floats order like their bits
+    b = __reduce_max_sync(__activemask(), b);
+    if ((threadIdx.x & 31) == (__ffs(__activemask()) - 1)) atomicMax(addr, b);
 }
 
-__global__ void ncf_fast_rows_kernel(NcfFastArgs f) {
+// warp per row, lane o = layer-0 output; W0[:, :ka] staged transposed in shared memory
+// (Wt[q][o]: the 32 lanes read 32 consecutive doubles, not 32 rows 512 B apart)
+__global__ void __launch_bounds__(256) ncf_fast_rows_kernel(NcfFastArgs f) {
     const NcfSelArgs& a = f.s;
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (row, o)
-    if (t >= a.m * kNsH0) return;
-    const int64_t i = t >> 5;
-    const int o = static_cast<int>(t & 31);
-    const double* w = a.P + a.off_w[0] + static_cast<int64_t>(o) * (a.ka + a.ks);
-    const double* u = a.P + i * a.ka;
-    double acc = a.P[a.off_b[0] + o];
-    for (int q = 0; q < a.ka; ++q) acc = fma(w[q], u[q], acc);
-    const float av = static_cast<float>(acc);
-    f.A[t] = av;
-    f.EA[t] = static_cast<float>(exp(acc));
-    atomic_max_f(&f.scale->maxA, av);
+    extern __shared__ double wt[];  // [ka][32]
+    for (int e = threadIdx.x; e < a.ka * kNsH0; e += blockDim.x) {
+        const int q = e / kNsH0, o = e - q * kNsH0;
+        wt[e] = a.P[a.off_w[0] + static_cast<int64_t>(o) * (a.ka + a.ks) + q];
+    }
+    __syncthreads();
+    const int o = threadIdx.x & 31;
+    const double bo = a.P[a.off_b[0] + o];
+    float amax = 0.0f;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.m; i += nw) {
+        const double* u = a.P + i * a.ka;
+        double acc = bo;
+        for (int q = 0; q < a.ka; ++q) acc = fma(wt[q * kNsH0 + o], u[q], acc);
+        const float av = static_cast<float>(acc);
+        f.A[i * kNsH0 + o] = av;
+        f.EA[i * kNsH0 + o] = static_cast<float>(exp(acc));
+        amax = fmaxf(amax, fabsf(av));
+    }
+    atomic_max_f(&f.scale->maxA, amax);
 }
 
 __global__ void ncf_fast_cols_kernel(NcfFastArgs f) {
@@ -877,7 +892,10 @@ cudaError_t ncf_launch_fast_prep(const NcfFastArgs& f, cudaStream_t s) {
     const NcfSelArgs& a = f.s;
     cudaError_t e = cudaMemsetAsync(f.scale, 0, sizeof(NcfFastScale), s);
     if (e != cudaSuccess) return e;
-    if (a.m > 0) ncf_fast_rows_kernel<<<static_cast<unsigned>((a.m * kNsH0 + 255) / 256), 256, 0, s>>>(f);
+    if (a.m > 0) {
+        const int64_t blocks = std::min<int64_t>((a.m + 7) / 8, 148 * 16);
+        ncf_fast_rows_kernel<<<static_cast<unsigned>(blocks), 256, sizeof(double) * a.ka * kNsH0, s>>>(f);
+    }
     ncf_fast_cols_kernel<<<static_cast<unsigned>((a.n * kNsH0 + 255) / 256), 256, 0, s>>>(f);
     ncf_fast_scale_kernel<<<static_cast<unsigned>((a.n * kNsH0 + 255) / 256), 256, 0, s>>>(f);
     return cudaGetLastError();
