@@ -225,6 +225,14 @@ int ocg_ncf_plan_upload(ocg_ncf_plan* plan, const int64_t* row_ptr, const int32_
  * A/B precompute, baselines, observed cells; dense pass) as CUDA-event times (NULL = async) */
 int ocg_ncf_plan_run(ocg_ncf_plan* plan, float* total_ms, float* phase_ms);
 int ocg_ncf_plan_results(ocg_ncf_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand);
+/* pipelined serving: _stage copies the next step's host CSR (pinned memory for an async
+ * copy) on a side stream into spare buffers while the current step may still run; the next
+ * _run swaps it in (a device-side wait).  _results_async queues the decisions' device->host
+ * copies behind the run (the following _run may be enqueued at once); _results_wait blocks
+ * until they landed and reports the run's error as _results would.  One staged CSR at a time. */
+int ocg_ncf_plan_stage(ocg_ncf_plan* plan, const int64_t* row_ptr, const int32_t* col, const double* val);
+int ocg_ncf_plan_results_async(ocg_ncf_plan* plan, int32_t* idx, double* saving, double* loss, int32_t* ncand);
+int ocg_ncf_plan_results_wait(ocg_ncf_plan* plan);
 /* completed values (nrows x n, FP64) of the listed rows (test / inspection hook) */
 int ocg_ncf_plan_completed_rows(ocg_ncf_plan* plan, const int64_t* rows, int64_t nrows, double* out);
 void ocg_ncf_plan_destroy(ocg_ncf_plan* plan);

@@ -227,3 +227,6 @@ class DetectorConfigC(ctypes.Structure):
 _sig("ocg_phase_detect_batch", ctypes.c_int, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, ctypes.c_int, c_vp, c_vp)
 _sig("ocg_online_ingest_complete_batch", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp,
      c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp, c_dbl, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_stage", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_results_async", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("ocg_ncf_plan_results_wait", ctypes.c_int, c_vp)

@@ -143,9 +143,30 @@ struct ocg_ncf_plan {
     int e_w = 0;
     float b1[16] = {}, w2[16] = {}, b2 = 0.0f;
     cudaEvent_t ev[4] = {};
+    // pipelined serving (ocg_ncf_plan_stage / _results_async): the next CSR copied on a side
+    // stream into the spare buffers while the current step runs; swapped in by the next run
+    Buf<int64_t> rp_next;
+    Buf<int32_t> col_next;
+    Buf<double> val_next;
+    int64_t next_cap = 0, staged_nnz = 0;
+    bool staged = false;
+    cudaStream_t copy_stream = nullptr;
+    // ev_free[0]: recorded after the last run that read the current buffers, ev_free[1]: the
+    // same for the spare ones (swapped with the buffers), so staging into the spare set waits
+    // only for the run before last, not for the run in flight
+    cudaEvent_t ev_staged = nullptr, ev_free[2] = {nullptr, nullptr}, ev_results = nullptr;
+    bool free_rec[2] = {false, false};
+    int* h_err = nullptr;  // pinned error bits of the last async results
     ~ocg_ncf_plan() {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamSynchronize(copy_stream);
+        if (ev_staged) cudaEventDestroy(ev_staged);
+        for (auto e : ev_free)
+            if (e) cudaEventDestroy(e);
+        if (ev_results) cudaEventDestroy(ev_results);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (h_err) cudaFreeHost(h_err);
     }
 };
 
@@ -408,6 +429,17 @@ int ocg_ncf_plan_upload(ocg_ncf_plan* P, const int64_t* row_ptr, const int32_t* 
 static int plan_launch(ocg_ncf_plan* P, const int64_t* d_list, int64_t nlist, double* d_completed, float* phase_ms) {
     cudaStream_t s = ocg_internal_stream(P->model->ctx);
     const int sm = ocg_internal_sm_count(P->model->ctx);
+    if (P->staged) {  // swap in the CSR staged by ocg_ncf_plan_stage (a device-side wait, no host sync)
+        NCF_CUDA(cudaStreamWaitEvent(s, P->ev_staged, 0));
+        std::swap(P->row_ptr.p, P->rp_next.p);
+        std::swap(P->col.p, P->col_next.p);
+        std::swap(P->val.p, P->val_next.p);
+        std::swap(P->col_cap, P->next_cap);
+        std::swap(P->ev_free[0], P->ev_free[1]);
+        std::swap(P->free_rec[0], P->free_rec[1]);
+        P->nnz = P->staged_nnz;
+        P->staged = false;
+    }
     ocg::NcfSelArgs a = sel_args(P);
     NCF_CUDA(cudaEventRecord(P->ev[0], s));
     NCF_CUDA(cudaMemsetAsync(P->err.p, 0, sizeof(int), s));
@@ -432,6 +464,10 @@ static int plan_launch(ocg_ncf_plan* P, const int64_t* d_list, int64_t nlist, do
         NCF_CUDA(ocg::ncf_launch_exact(a, P->lane, sm, s));
     }
     NCF_CUDA(cudaEventRecord(P->ev[2], s));
+    if (P->ev_free[0]) {  // every read of this step's CSR is behind this point: its buffers may be restaged
+        NCF_CUDA(cudaEventRecord(P->ev_free[0], s));
+        P->free_rec[0] = true;
+    }
     if (phase_ms) {
         NCF_CUDA(cudaEventSynchronize(P->ev[2]));
         NCF_CUDA(cudaEventElapsedTime(phase_ms + 0, P->ev[0], P->ev[1]));
@@ -507,6 +543,72 @@ int ocg_ncf_plan_completed_rows(ocg_ncf_plan* P, const int64_t* rows, int64_t nr
     if (rc) return rc;
     NCF_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * nrows * P->n, cudaMemcpyDeviceToHost, s));
     NCF_CUDA(cudaStreamSynchronize(s));
+    return OCG_OK;
+}
+
+int ocg_ncf_plan_stage(ocg_ncf_plan* P, const int64_t* row_ptr, const int32_t* col, const double* val) {
+    if (!P || !row_ptr || !col || !val) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: null argument");
+    if (!P->row_ptr.own) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: plan uses caller device buffers");
+    if (P->staged) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: a staged CSR is pending (run first)");
+    if (row_ptr[0] != 0) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: row_ptr[0] != 0");
+    for (int64_t i = 0; i < P->m; ++i)
+        if (row_ptr[i + 1] < row_ptr[i]) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: row_ptr decreases");
+    const int64_t nnz = row_ptr[P->m];
+    cudaStream_t s = ocg_internal_stream(P->model->ctx);
+    if (!P->copy_stream) {
+        NCF_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+        NCF_CUDA(cudaEventCreateWithFlags(&P->ev_staged, cudaEventDisableTiming));
+        NCF_CUDA(cudaEventCreateWithFlags(&P->ev_free[0], cudaEventDisableTiming));
+        NCF_CUDA(cudaEventCreateWithFlags(&P->ev_free[1], cudaEventDisableTiming));
+        NCF_CUDA(P->rp_next.alloc(static_cast<size_t>(P->m + 1)));
+    }
+    if (nnz > P->next_cap) {  // growth (rare): drain, then size the spare buffers
+        NCF_CUDA(cudaStreamSynchronize(s));
+        NCF_CUDA(cudaStreamSynchronize(P->copy_stream));
+        P->next_cap = nnz + nnz / 16 + 1024;
+        NCF_CUDA(P->col_next.alloc(static_cast<size_t>(P->next_cap)));
+        NCF_CUDA(P->val_next.alloc(static_cast<size_t>(P->next_cap)));
+    }
+    cudaStream_t c = P->copy_stream;
+    if (P->free_rec[1]) NCF_CUDA(cudaStreamWaitEvent(c, P->ev_free[1], 0));  // the spare buffers' last reader is done
+    NCF_CUDA(cudaMemcpyAsync(P->rp_next.p, row_ptr, sizeof(int64_t) * (P->m + 1), cudaMemcpyHostToDevice, c));
+    if (nnz > 0) {
+        NCF_CUDA(cudaMemcpyAsync(P->col_next.p, col, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c));
+        NCF_CUDA(cudaMemcpyAsync(P->val_next.p, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c));
+    }
+    NCF_CUDA(cudaEventRecord(P->ev_staged, c));
+    P->staged_nnz = nnz;
+    P->staged = true;
+    return OCG_OK;
+}
+
+int ocg_ncf_plan_results_async(ocg_ncf_plan* P, int32_t* idx, double* saving, double* loss, int32_t* ncand) {
+    if (!P || !idx || !saving || !loss || !ncand) return ocg_internal_fail(OCG_E_INVALID, "ncf plan: null argument");
+    if (!P->model->cold_cols.empty()) {  // the cold-column rule needs a host-side count: synchronous path
+        int rc = plan_error(P);
+        if (rc) return rc;
+    }
+    cudaStream_t s = ocg_internal_stream(P->model->ctx);
+    if (!P->ev_results) {
+        NCF_CUDA(cudaEventCreateWithFlags(&P->ev_results, cudaEventDisableTiming));
+        NCF_CUDA(cudaMallocHost(&P->h_err, sizeof(int)));
+    }
+    const size_t m = static_cast<size_t>(P->m);
+    NCF_CUDA(cudaMemcpyAsync(P->h_err, P->err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NCF_CUDA(cudaMemcpyAsync(idx, P->idx.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    NCF_CUDA(cudaMemcpyAsync(saving, P->saving.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    NCF_CUDA(cudaMemcpyAsync(loss, P->loss.p, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    NCF_CUDA(cudaMemcpyAsync(ncand, P->ncand.p, sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+    NCF_CUDA(cudaEventRecord(P->ev_results, s));
+    return OCG_OK;
+}
+
+int ocg_ncf_plan_results_wait(ocg_ncf_plan* P) {
+    if (!P) return ocg_internal_fail(OCG_E_INVALID, "null plan");
+    if (!P->ev_results) return OCG_OK;
+    NCF_CUDA(cudaEventSynchronize(P->ev_results));
+    const int code = first_error(*P->h_err);
+    if (code) return ocg_internal_fail(code, error_text(code));
     return OCG_OK;
 }
 

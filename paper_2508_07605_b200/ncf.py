@@ -79,6 +79,17 @@ class NcfPlan:
             args = tuple(ptr(a) for a in self._keep)
         check(lib.ocg_ncf_plan_upload(self._h, *args))
 
+    def stage(self, row_ptr: int, col: int, val: int):
+        """Queue the next step's CSR (host pointers, pinned memory) on the side copy stream."""
+        check(lib.ocg_ncf_plan_stage(self._h, ctypes.c_void_p(row_ptr), ctypes.c_void_p(col), ctypes.c_void_p(val)))
+
+    def results_async(self, out):
+        """Queue the decisions' copies into host pointers out = (idx, saving, loss, ncand)."""
+        check(lib.ocg_ncf_plan_results_async(self._h, *(ctypes.c_void_p(int(p)) for p in out)))
+
+    def results_wait(self):
+        check(lib.ocg_ncf_plan_results_wait(self._h))
+
     def run(self, timed: bool = True):
         """One completion + selection; returns (total_ms, [prep_ms, dense_ms]) when timed."""
         tot = ctypes.c_float(0.0)

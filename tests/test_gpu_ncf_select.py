@@ -270,3 +270,40 @@ def test_c2_scale_sampled_rows_match_reference(ctx, ref, precision):
         safe = _margin_safe(c_ref, grid, 0.05, FAST_RTOL)
         assert safe.mean() > 0.5, safe.mean()
         np.testing.assert_array_equal(idx[rows][safe], i_ref[safe])
+
+
+def test_pipelined_stage_and_async_results_match_sync(ctx):
+    """ocg_ncf_plan_stage + _results_async/_wait (the next CSR staged on a side stream while the
+    current step runs) give the decisions the synchronous upload + run + results give, step by step."""
+    import torch
+
+    from paper_2508_07605_b200 import PowerGrid, synth
+    from paper_2508_07605_b200.ncf import FAST, DeviceNcfModel, NcfPlan, random_model
+
+    grid = PowerGrid.spanning(16, 16)
+    mats = [synth.joint_csr(3000, grid, 0.05 + 0.01 * k, 3, seed=40 + k, dtype=np.float64) for k in range(3)]
+    model = random_model(3000, grid.n, 8, seed=1, emb_scale=0.6)
+    dm = DeviceNcfModel(model, ctx=ctx)
+    want = []
+    for A in mats:
+        p = NcfPlan(dm, A.row_ptr, A.col, A.val, grid, 0.05, FAST)
+        p.run(timed=False)
+        want.append(p.results(A.m))
+        p.close()
+    pins = [[torch.from_numpy(x).pin_memory() for x in (A.row_ptr, A.col, A.val)] for A in mats]
+    out = [torch.empty(3000, dtype=dt).pin_memory() for dt in (torch.int32, torch.float64, torch.float64, torch.int32)]
+    plan = NcfPlan(dm, mats[0].row_ptr, mats[0].col, mats[0].val, grid, 0.05, FAST)
+    order = [0, 1, 2, 1, 0, 2]
+    plan.stage(*(int(x.data_ptr()) for x in pins[order[0]]))
+    plan.run(timed=False)
+    for i, k in enumerate(order):
+        if i + 1 < len(order):
+            plan.stage(*(int(x.data_ptr()) for x in pins[order[i + 1]]))
+        plan.results_async([int(x.data_ptr()) for x in out])
+        if i + 1 < len(order):
+            plan.run(timed=False)
+        plan.results_wait()
+        for got, exp in zip(out, want[k]):
+            np.testing.assert_array_equal(got.numpy(), exp)
+    plan.close()
+    dm.close()
