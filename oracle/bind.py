@@ -156,7 +156,7 @@ class Port:
 
     def ncf_predict(self, m, n, params, aseen, sseen, rows, cols, **hyper):
         h = _hyper(Hyper, **hyper)
-        rows, cols = np.asarray(rows, np.int64), np.asarray(cols, np.int64)
+        rows, cols = np.ascontiguousarray(rows, np.int64), np.ascontiguousarray(cols, np.int64)
         out = np.zeros(len(rows))
         rc = self.L.ocgo_ncf_predict(m, n, ctypes.byref(h), P(params), P(aseen), P(sseen), P(rows), P(cols),
                                      len(rows), P(out))
@@ -294,7 +294,7 @@ class Ref:
         return rc, out
 
     def ncf_predict(self, model_json, rows, cols):
-        rows, cols = np.asarray(rows, np.int64), np.asarray(cols, np.int64)
+        rows, cols = np.ascontiguousarray(rows, np.int64), np.ascontiguousarray(cols, np.int64)
         out = np.zeros(len(rows))
         rc = self.L.ref_ncf_predict(model_json.encode(), P(rows), P(cols), len(rows), P(out))
         return rc, out
