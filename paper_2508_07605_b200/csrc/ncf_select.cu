@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
     const float sd = sc.sd, as = sc.alpha_s;
     constexpr float kAlpha = 1.6732632423543772f, kLog2e = 1.4426950408889634f;
     const uint32_t a_base = saddr(abuf), w_base = saddr(wimg);
+    const uint64_t adesc0 = umma_desc(a_base, 128, 256), wdesc0 = umma_desc(w_base, 128, 256);
 
     if (t == 0) {
         mbar_expect_tx(bars + 0, kStageBytes);
@@ -765,15 +766,16 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
                 mbar_expect_tx(bars + s2, kStageBytes);
                 tma_load_2d(stage + s2 * kNsTileCols * kNsColFloats, &tmap, 0, (T + 1) * kNsTileCols, bars + s2);
             }
-            const uint32_t ah = a_base + b * kBufBytes, al = ah + kABytes;
+            // descriptors = the base descriptors + (byte offset >> 4) in the start-address field
+            const uint64_t ah = adesc0 + static_cast<uint64_t>((b * kBufBytes) >> 4), al = ah + (kABytes >> 4);
             const uint32_t d = tmem + static_cast<uint32_t>(b * 16);
             // D = Ah.Wh + Ah.Wl + Al.Wh over K = 32 (2 slabs of 16)
-            umma_f16(d, umma_desc(ah, 128, 256), umma_desc(w_base, 128, 256), 0u);
-            umma_f16(d, umma_desc(ah + 4096, 128, 256), umma_desc(w_base + 512, 128, 256), 1u);
-            umma_f16(d, umma_desc(ah, 128, 256), umma_desc(w_base + 1024, 128, 256), 1u);
-            umma_f16(d, umma_desc(ah + 4096, 128, 256), umma_desc(w_base + 1536, 128, 256), 1u);
-            umma_f16(d, umma_desc(al, 128, 256), umma_desc(w_base, 128, 256), 1u);
-            umma_f16(d, umma_desc(al + 4096, 128, 256), umma_desc(w_base + 512, 128, 256), 1u);
+            umma_f16(d, ah, wdesc0, 0u);
+            umma_f16(d, ah + (4096 >> 4), wdesc0 + (512 >> 4), 1u);
+            umma_f16(d, ah, wdesc0 + (1024 >> 4), 1u);
+            umma_f16(d, ah + (4096 >> 4), wdesc0 + (1536 >> 4), 1u);
+            umma_f16(d, al, wdesc0, 1u);
+            umma_f16(d, al + (4096 >> 4), wdesc0 + (512 >> 4), 1u);
             umma_commit(bars + 2 + b);
         }
         __syncwarp();
