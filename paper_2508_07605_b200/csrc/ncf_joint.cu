@@ -155,6 +155,10 @@ struct ExactNum {
     }
     __device__ static void selu(T z, T& a, T& gf, ExpTabPtr tab) { selu_fwd(z, a, gf, tab); }
     __device__ static double sq(T e) { return dmul(e, e); }
+    // a zero-gradient step, the reference lane's exact operations (g = +0)
+    __device__ static void zadam(T& p, T& m, T& v, T lr, double mc, double vc, bool vec) {
+        adam(p, m, v, T(0), lr, mc, vc, vec);
+    }
 };
 
 // FP32 on the reference schedule (FastNumT<double>: the same formulas in FP64,
@@ -199,6 +203,19 @@ struct FastNumT {
         }
     }
     __device__ static double sq(T e) { return static_cast<double>(e) * static_cast<double>(e); }
+    // a zero-gradient step: the g terms vanish; FP32 mode uses the approximate sqrt / divide
+    // (a few ulp, like any FP32 Adam) on this replay path
+    __device__ static void zadam(T& p, T& m, T& v, T lr, double mc, double vc, bool) {
+        if constexpr (sizeof(T) == 4) {
+            m = m * 0.9f;
+            v = v * 0.999f;
+            float r;
+            asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v * static_cast<float>(vc)));
+            p = __fmaf_rn(-lr, __fdividef(m * static_cast<float>(mc), r + 1e-8f), p);
+        } else {
+            adam(p, m, v, T(0), lr, mc, vc, false);  // (the FP64 diagnostic build keeps the full step)
+        }
+    }
 };
 using FastNum = FastNumT<float>;
 
@@ -259,11 +276,22 @@ __device__ __forceinline__ void replay_chunk(const JointArgs<T>& a, int64_t row,
         mm[j] = c < k ? __ldcg(rec + k + c) : T(0);
         vv[j] = c < k ? __ldcg(rec + 2 * k + c) : T(0);
     }
-    for (int64_t t = t0; t <= t1; ++t) {
-        double mc, vc;
-        step_corr(a.tab_mc, a.tab_vc, a.tab_len, t, mc, vc);
+    // bias corrections of step t + 1 are loaded while step t computes; once both reach 1.0
+    // (t >= tab_len: ~37K steps into a fit) the loop needs no table at all
+    double mc, vc;
+    step_corr(a.tab_mc, a.tab_vc, a.tab_len, t0, mc, vc);
+    int64_t t = t0;
+    for (; t <= t1 && t < a.tab_len; ++t) {
+        double mcn, vcn;
+        step_corr(a.tab_mc, a.tab_vc, a.tab_len, t + 1, mcn, vcn);
 #pragma unroll
-        for (int j = 0; j < kRC; ++j) NUM::adam(p[j], mm[j], vv[j], T(0), a.lr, mc, vc, c0 + j < vlim);
+        for (int j = 0; j < kRC; ++j) NUM::zadam(p[j], mm[j], vv[j], a.lr, mc, vc, c0 + j < vlim);
+        mc = mcn;
+        vc = vcn;
+    }
+    for (; t <= t1; ++t) {
+#pragma unroll
+        for (int j = 0; j < kRC; ++j) NUM::zadam(p[j], mm[j], vv[j], a.lr, 1.0, 1.0, c0 + j < vlim);
     }
 #pragma unroll
     for (int j = 0; j < kRC; ++j) {
@@ -1261,8 +1289,10 @@ int run_fit(cudaStream_t st, int sm_count, int64_t m, int64_t n, const int64_t* 
         a.prof = prof.p;
     }
 
-    const bool fixed = sh.L == 3 && sh.ka == 8 && sh.ks == 8 && sh.dims[1] == 32 && sh.dims[2] == 16 && h.batch_size == 32;
-    auto kep = fixed ? joint_epoch_kernel<NUM, DefaultShape> : joint_epoch_kernel<NUM, RtShape>;
+    const bool h3216 = sh.L == 3 && sh.dims[1] == 32 && sh.dims[2] == 16 && h.batch_size == 32;
+    auto kep = (h3216 && sh.ka == 8 && sh.ks == 8)     ? joint_epoch_kernel<NUM, DefaultShape>
+               : (h3216 && sh.ka == 32 && sh.ks == 32) ? joint_epoch_kernel<NUM, FixShape<32, 32, 32, 16>>
+                                                       : joint_epoch_kernel<NUM, RtShape>;
     auto kev = joint_eval_kernel<NUM>;
     JCU(cudaFuncSetAttribute(kep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.lay.bytes)));
     JCU(cudaFuncSetAttribute(kev, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(a.lay.bytes)));
