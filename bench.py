@@ -635,7 +635,7 @@ def workload_joint(args, d: Dist):
                 "d2h_bytes_per_step": int(idx.nbytes + sav.nbytes + loss.nbytes + ncand.nbytes) * d.world,
                 "selections_per_sec": m / e2e_t, "mode": e2e_mode,
                 "serial_value": cells / e2e_serial_t},
-        "dtype": "f32 factors / f64 selection",
+        "dtype": "f32 factors (rank 32/64 Gram and imputation on fp16 hi/lo split operands, the L^T L term dropped, FP32 accumulation) / f64 selection",
         "config": {"workload": args.workload, "apps": m, "settings": n, "rank": k, "observed_per_gpu": nnz,
                    "density": cfg["density"], "offline_dense_rows": cfg["dense_rows"], "solver": "als",
                    "sweeps": args.sweeps, "lambda": args.als_lambda, "gamma": args.gamma,
@@ -745,7 +745,7 @@ def workload_c4(args, d: Dist):
     assert bool((r[0] >= 0).all())
     lat = statistics.median(ts)
     out = {"metric": "CF-completed matrix cells/sec", "value": m * n / lat, "unit": "cells/s",
-           "ms_per_step": lat * 1e3, "scaling": "strong", "dtype": "f32 factors / f64 selection",
+           "ms_per_step": lat * 1e3, "scaling": "strong", "dtype": "f32 factors (rank 32/64 Gram and imputation on fp16 hi/lo split operands, the L^T L term dropped, FP32 accumulation) / f64 selection",
            "refit_latency_ms": {"from_scratch_median": lat * 1e3, "all": [t * 1e3 for t in ts]},
            "selections_per_sec": m / lat,
            "e2e": {"value": m * n / lat, "unit": "cells/s",
