@@ -505,6 +505,35 @@ int ocg_online_ingest_complete_batch(ocg_ctx* ctx, int64_t d_rows, const double*
                                      double* saving, double* loss, int32_t* ncand, ocg_ncf_meta* meta,
                                      int32_t* status);
 
+/* Evaluation harness: policy::evaluate_suite (policy.cpp:373-405) over napps apps on
+ * the device, from the simulator's repetition runs (sim::run is the simulator and stays
+ * with the caller).  base_runs[a][r] is sim::run(app a, baseline, rep seed r) and
+ * runs[a][j][r] the same at grid setting j (PowerGrid::settings order, cpu-major), rep
+ * seed r = derive_seed(derive_seed(seed, "eval." + app_id), "rep", r) as measure_truth
+ * (policy.cpp:213-256) draws them.  policies[npol] are ocg_policy_kind values; for the
+ * open policy open_idx[a] / open_pred_saving[a] are its run_open_online decision
+ * (setting index, pred_saving) and may be NULL otherwise.  rows is napps x npol in the
+ * reference's report order; aggs (npol, may be NULL) as its PolicyAggregate (by policy
+ * kind).  FP64 in the reference's operation order: bit-exact. */
+enum { OCG_POLICY_OPEN = 0, OCG_POLICY_NO_CAP = 1, OCG_POLICY_GPU_CAP_ONLY = 2, OCG_POLICY_CPU_CAP_ONLY = 3,
+       OCG_POLICY_ORACLE = 4 };
+typedef struct {
+    double runtime_s, energy_j, avg_power_w; /* sim::RunResult (simnode.hpp:55-61) scalars */
+} ocg_run_result;
+typedef struct {
+    int32_t policy, setting; /* ocg_policy_kind, setting index */
+    int32_t cpu_cap_w, gpu_cap_w;
+    double gamma, true_perf, true_loss, energy_j, avg_power_w, efficiency, pred_saving; /* EvalRow */
+} ocg_eval_row;
+typedef struct {
+    int32_t policy;
+    double mean_efficiency, mean_gain_vs_no_cap, mean_true_loss, mean_true_perf; /* PolicyAggregate */
+} ocg_eval_aggregate;
+int ocg_eval_suite(ocg_ctx* ctx, int64_t napps, const int32_t* cpu_caps, int32_t ncpu, const int32_t* gpu_caps,
+                   int32_t ngpu, int32_t repetitions, const ocg_run_result* base_runs, const ocg_run_result* runs,
+                   double gamma, int32_t npolicies, const int32_t* policies, const int32_t* open_idx,
+                   const double* open_pred_saving, ocg_eval_row* rows, ocg_eval_aggregate* aggs);
+
 /* debug / parity probes of device building blocks */
 int ocg_debug_exp(ocg_ctx* ctx, const double* x, int64_t n, double* out); /* device glibc-exact exp */
 double ocg_debug_exp_host(double x);                                       /* same code, host build */

@@ -231,6 +231,7 @@ class Ref:
         L.ref_load_predictor.argtypes = [ctypes.c_char_p, c_vp]
         L.ref_run_trace.argtypes = [c_vp, ctypes.c_int, ctypes.c_int, c_u64, c_vp, c_sz, c_vp, c_vp]
         L.ref_detect.argtypes = [c_vp, c_sz, c_dbl, c_dbl, c_dbl, ctypes.c_int, c_vp]
+        L.ref_eval_default.argtypes = [c_u64, ctypes.c_int, c_dbl, c_vp, c_sz, c_vp, c_vp, c_vp, c_vp, c_vp]
         L.ref_time_fit_step.argtypes = [c_sz, c_sz, c_sz, c_vp, c_sz, ctypes.c_int, c_vp]
         L.ref_time_fit_step.restype = c_dbl
         L.ref_complete_select_batch.restype = c_dbl
@@ -363,6 +364,20 @@ class Ref:
         f = ctypes.c_int64()
         rc = self.L.ref_detect(P(p), len(p), delta_s, window_s, p_th, armed, ctypes.byref(f))
         return rc, f.value
+
+    def eval_default(self, pols, seed=42, reps=5, gamma=0.05, napps=20, n=20):
+        """policy::evaluate_suite of the default evaluation suite for baseline policies, and the
+        sim::run results its truth tables come from: (rows, aggs, base, runs)."""
+        pols = np.ascontiguousarray(pols, np.int32)
+        rows = np.zeros((napps, len(pols), 8))
+        aggs = np.zeros((len(pols), 4))
+        base = np.zeros((napps, reps, 3))
+        runs = np.zeros((napps, n, reps, 3))
+        na = c_sz()
+        rc = self.L.ref_eval_default(seed, reps, gamma, P(pols), len(pols), P(rows), P(aggs), P(base), P(runs),
+                                     ctypes.byref(na))
+        assert rc == 0 and na.value == napps, self.err()
+        return rows, aggs, base, runs
 
     def load_predictor(self, path):
         hs = ctypes.c_int()

@@ -805,7 +805,74 @@ int ref_detect(const double* power, size_t n, double delta_s, double window_s, d
     }
 }
 
+// policy::evaluate_suite (policy.cpp:355-405) for the CLI's default evaluation suite and the
+// given baseline policies (1 no_cap, 2 gpu_cap_only, 3 cpu_cap_only, 4 oracle) on the default
+// grid, plus the simulator runs its truth tables come from (the same sim::run calls
+// measure_truth makes): base[a][r] and runs[a][j][r] = {runtime_s, avg_power_w, energy_j}.
+// rows[a][p] = {cpu, gpu, true_perf, true_loss, energy_j, avg_power_w, efficiency, pred_saving},
+// aggs[p] = {mean_efficiency, mean_gain_vs_no_cap, mean_true_loss, mean_true_perf}
+int ref_eval_default(uint64_t seed, int reps, double gamma, const int32_t* pols, size_t npol, double* rows,
+                     double* aggs, double* base, double* runs, size_t* napps_out) {
+    try {
+        const auto grid = PowerGrid::default_grid();
+        const auto suite = sim::make_suite(sim::default_evaluation_params(seed), grid);
+        std::vector<policy::PolicyKind> kinds;
+        for (size_t p = 0; p < npol; ++p) kinds.push_back(static_cast<policy::PolicyKind>(pols[p]));
+        auto cfg = policy::EvalConfig::defaults(grid);
+        cfg.repetitions = reps;
+        cfg.online.selection.gamma = gamma;
+        PerformanceMatrix dense({"unused"}, grid);
+        pred::PredictorModel predictor;
+        const auto report = policy::evaluate_suite(suite, kinds, dense, predictor, cfg, seed);
+        const auto settings = grid.settings();
+        const size_t n = settings.size();
+        for (size_t a = 0; a < suite.size(); ++a) {
+            const auto app_seed = derive_seed(seed, "eval." + suite[a].app_id);
+            for (int r = 0; r < reps; ++r) {
+                const auto rep_seed = derive_seed(app_seed, "rep", static_cast<uint64_t>(r));
+                const auto b = sim::run(suite[a], grid.baseline(), rep_seed);
+                double* bo = base + (a * reps + r) * 3;
+                bo[0] = b.runtime_s;
+                bo[1] = b.avg_power_w;
+                bo[2] = b.energy_j;
+                for (size_t j = 0; j < n; ++j) {
+                    const auto c = sim::run(suite[a], settings[j], rep_seed);
+                    double* o = runs + ((a * n + j) * reps + r) * 3;
+                    o[0] = c.runtime_s;
+                    o[1] = c.avg_power_w;
+                    o[2] = c.energy_j;
+                }
+            }
+        }
+        for (size_t q = 0; q < report.rows.size(); ++q) {
+            const auto& w = report.rows[q];
+            double* o = rows + q * 8;
+            o[0] = w.setting.cpu_cap_w;
+            o[1] = w.setting.gpu_cap_w;
+            o[2] = w.true_perf;
+            o[3] = w.true_loss;
+            o[4] = w.energy_j;
+            o[5] = w.avg_power_w;
+            o[6] = w.efficiency;
+            o[7] = w.pred_saving;
+        }
+        for (size_t p = 0; p < report.aggregates.size(); ++p) {
+            const auto& g = report.aggregates[p];
+            double* o = aggs + p * 4;
+            o[0] = g.mean_efficiency;
+            o[1] = g.mean_gain_vs_no_cap;
+            o[2] = g.mean_true_loss;
+            o[3] = g.mean_true_perf;
+        }
+        *napps_out = suite.size();
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 }  // extern "C"
+
 
 
 

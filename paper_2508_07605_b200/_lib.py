@@ -230,3 +230,22 @@ _sig("ocg_online_ingest_complete_batch", ctypes.c_int, c_vp, c_i64, c_vp, c_vp, 
 _sig("ocg_ncf_plan_stage", ctypes.c_int, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_ncf_plan_results_async", ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("ocg_ncf_plan_results_wait", ctypes.c_int, c_vp)
+
+# evaluation harness: policy::evaluate_suite's truth tables, exhaustive choices and aggregates
+class RunResultC(ctypes.Structure):
+    _fields_ = [("runtime_s", c_dbl), ("energy_j", c_dbl), ("avg_power_w", c_dbl)]
+
+
+class EvalRowC(ctypes.Structure):
+    _fields_ = [("policy", c_i32), ("setting", c_i32), ("cpu_cap_w", c_i32), ("gpu_cap_w", c_i32), ("gamma", c_dbl),
+                ("true_perf", c_dbl), ("true_loss", c_dbl), ("energy_j", c_dbl), ("avg_power_w", c_dbl),
+                ("efficiency", c_dbl), ("pred_saving", c_dbl)]
+
+
+class EvalAggregateC(ctypes.Structure):
+    _fields_ = [("policy", c_i32), ("mean_efficiency", c_dbl), ("mean_gain_vs_no_cap", c_dbl),
+                ("mean_true_loss", c_dbl), ("mean_true_perf", c_dbl)]
+
+
+_sig("ocg_eval_suite", ctypes.c_int, c_vp, c_i64, c_vp, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_dbl, c_i32, c_vp,
+     c_vp, c_vp, c_vp, c_vp)
