@@ -400,8 +400,9 @@ int ocg_ncf_plan_create(ocg_ncf_model* M, const int64_t* row_ptr, const int32_t*
         NCF_CUDA(cudaMemcpyAsync(P->w1img.p, img.data(), 2048, cudaMemcpyHostToDevice, s));
         NCF_CUDA(cudaStreamSynchronize(s));
         for (int p = 0; p < 16; ++p) {
-            P->b1[p] = static_cast<float>(B1[p]);
-            P->w2[p] = static_cast<float>(kLambda * W2[p]);
+            // the dense epilogue works in log2 units (ncf_select.cu): b1 log2(e), lambda W2 ln(2)
+            P->b1[p] = static_cast<float>(B1[p] * 1.4426950408889634);
+            P->w2[p] = static_cast<float>(kLambda * W2[p] * 0.6931471805599453);
         }
         P->b2 = static_cast<float>(B2[0]);
         auto enc = tensor_map_encoder();

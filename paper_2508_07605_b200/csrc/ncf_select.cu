@@ -519,7 +519,7 @@ __global__ void ncf_fast_scale_kernel(NcfFastArgs f) {
     }
     if (t == 0) {
         f.scale->s_h = s_h;
-        f.scale->sd = ldexpf(1.0f, -(eh + f.e_w));
+        f.scale->sd = ldexpf(1.0f, -(eh + f.e_w)) * 1.4426950408889634f;  // z1 log2(e) per accumulator unit
         f.scale->alpha_s = 1.6732632423543772f * s_h;
         // exp(A) exp(B) needs both factors finite and normal
         f.scale->bad = !(ma < 80.0f && mb < 80.0f) ? 1 : 0;
@@ -651,10 +651,10 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
         As[q + 1] = x.y * sc.s_h;
         As[q + 2] = x.z * sc.s_h;
         As[q + 3] = x.w * sc.s_h;
-        EA[q] = y.x;
-        EA[q + 1] = y.y;
-        EA[q + 2] = y.z;
-        EA[q + 3] = y.w;
+        EA[q] = y.x * sc.alpha_s;  // alpha s_h exp(A_i): the negative branch is one FFMA per unit
+        EA[q + 1] = y.y * sc.alpha_s;
+        EA[q + 2] = y.z * sc.alpha_s;
+        EA[q + 3] = y.w * sc.alpha_s;
     }
     // observed-column cursor (ascending CSR columns; the thread sweeps j ascending)
     int64_t cur = work ? a.row_ptr[i] : 0;
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
     float tb = tbest * kBandF;
     int cnt = 0;
     const float sd = sc.sd, as = sc.alpha_s;
-    constexpr float kAlpha = 1.6732632423543772f, kLog2e = 1.4426950408889634f;
+    constexpr float kAlphaL = 1.6732632423543772f * 1.4426950408889634f;
     const uint32_t a_base = saddr(abuf), w_base = saddr(wimg);
     const uint64_t adesc0 = umma_desc(a_base, 128, 256), wdesc0 = umma_desc(w_base, 128, 256);
 
@@ -693,10 +693,12 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
         float out = f.b2;
 #pragma unroll
         for (int p = 0; p < 16; ++p) {
-            const float z = fmaf(d[p], sd, f.b1[p]);
-            const float e = ex2_approx(z * kLog2e);
-            const float h = z > 0.0f ? z : fmaf(kAlpha, e, -kAlpha);
-            out = fmaf(f.w2[p], h, out);
+            // in log2 units: zl = z1 log2(e) (sd and b1 carry the factor), hl = SELU(z1)/lambda log2(e),
+            // and w2 carries lambda ln(2)
+            const float zl = fmaf(d[p], sd, f.b1[p]);
+            const float e = ex2_approx(zl);
+            const float hl = zl > 0.0f ? zl : fmaf(kAlphaL, e, -kAlphaL);
+            out = fmaf(f.w2[p], hl, out);
         }
         const bool obs = jc == nxt;
         if (obs) {
@@ -744,8 +746,7 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
                 for (int v = 0; v < 2; ++v) {
                     const int k = 8 * q + 2 * u + v;
                     const float z = As[k] + bb[2 * u + v];
-                    const float e = EA[k] * eb[2 * u + v];
-                    h2[v] = z > 0.0f ? z : fmaf(as, e, -as);
+                    h2[v] = z > 0.0f ? z : fmaf(EA[k], eb[2 * u + v], -as);
                 }
                 const __half2 hh = __floats2half2_rn(h2[0], h2[1]);
                 const float2 hf = __half22float2(hh);

@@ -33,7 +33,7 @@ struct NcfRowState {
 struct NcfFastScale {
     unsigned maxA, maxB;  // float bits of max |A_i[o]|, max |B_j[o]|
     float s_h;            // power-of-two scale of the layer-0 activations
-    float sd;             // 2^-(e_h + e_w): accumulator -> z1
+    float sd;             // 2^-(e_h + e_w) log2(e): accumulator -> z1 log2(e)
     float alpha_s;        // alpha * s_h
     int bad;              // exp(A) * exp(B) would overflow: the fast path refuses (OCG_E_UNSUPPORTED)
 };
@@ -74,7 +74,7 @@ struct NcfFastArgs {
     float* BE;   // n x kNsColFloats
     const uint4* w1img;  // 2 KB: (lambda W1 * s_w) as fp16 hi/lo in the UMMA core-matrix layout
     NcfFastScale* scale;
-    float b1[16], w2[16], b2;  // w2 = lambda * W2
+    float b1[16], w2[16], b2;  // b1 log2(e), lambda W2 ln(2): the epilogue's log2 units
     int e_w;                   // log2 s_w
 };
 
