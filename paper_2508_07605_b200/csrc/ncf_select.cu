@@ -680,12 +680,12 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
             tma_load_2d(stage + kNsTileCols * kNsColFloats, &tmap, 0, kNsTileCols, bars + 1);
         }
     }
-    uint32_t tph[2] = {0u, 0u}, mph[2] = {0u, 0u};
+    uint32_t tph = 0u, mph = 0u;  // mbarrier phase bits per buffer (registers, not a local array)
 
     float cs_prev = 0.0f;  // c+g of the column whose epilogue is pending (read while its tile is staged)
     auto epilogue = [&](int64_t jc, int b, float csf) {
-        mbar_wait(bars + 2 + b, mph[b]);
-        mph[b] ^= 1u;
+        mbar_wait(bars + 2 + b, (mph >> b) & 1u);
+        mph ^= 1u << b;
         tc_fence_after();
         float d[16];
         tmem_ld16(tmem + ((static_cast<uint32_t>(warp) * 32u) << 16) + static_cast<uint32_t>(b * 16), d);
@@ -723,8 +723,8 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
     for (int64_t j = 0; j < n; ++j) {
         const int T = static_cast<int>(j / kNsTileCols), jj = static_cast<int>(j % kNsTileCols), stg = T & 1;
         if (jj == 0) {
-            mbar_wait(bars + stg, tph[stg]);
-            tph[stg] ^= 1u;
+            mbar_wait(bars + stg, (tph >> stg) & 1u);
+            tph ^= 1u << stg;
         }
         const int b = static_cast<int>(j & 1);
         // ---- operand: h'(z) = s_h SELU(z)/lambda for the 32 layer-0 outputs, as fp16 hi/lo
