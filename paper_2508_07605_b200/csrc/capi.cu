@@ -225,7 +225,7 @@ struct ocg_online_plan {
     int64_t napps = 0, n = 0;
     int grid = 0;
     std::vector<int32_t> hstatus;
-    DBuf<double> d_bval, d_pv, d_comp, d_sav, d_loss, d_params;
+    DBuf<double> d_bval, d_pv, d_comp, d_sav, d_loss, d_params, d_best;
     DBuf<uint32_t> d_brc;
     DBuf<uint8_t> d_bseen, d_pm;
     DBuf<uint64_t> d_seeds;
@@ -310,6 +310,9 @@ int plan_create(ocg_ctx* ctx, const BatchInputs& in, const int32_t* cpu, int32_t
     const int per_sm = ocg::batch_max_active_per_sm(g, lane);
     if (per_sm < 1) return fail(OCG_E_CUDA, "per-app kernel cannot be resident (smem " + std::to_string(smem) + ")");
     P->grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(napps, 1), static_cast<int64_t>(per_sm) * ctx->sm_count));
+    io.best_stride = (g.T + 31) & ~31;
+    OCG_CUDA(P->d_best.alloc(static_cast<size_t>(P->grid) * static_cast<size_t>(io.best_stride)));
+    io.best = P->d_best.p;
     OCG_CUDA(cudaEventCreate(&P->ev0));
     OCG_CUDA(cudaEventCreate(&P->ev1));
     OCG_CUDA(cudaStreamSynchronize(s));

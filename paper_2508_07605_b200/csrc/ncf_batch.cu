@@ -113,10 +113,12 @@ __device__ __forceinline__ uint32_t carve(uint32_t& p, size_t bytes) {
     return r;
 }
 
+// Fixed-size regions first: with FixArch every layer stride is a compile-time constant,
+// so the offsets of the hot per-step regions (activations, deltas, sample ids, control,
+// exp table) fold to immediates and cost no registers; the app-sized regions follow.
 template <class A>
 __device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom& g) {
     uint32_t p = 0;
-    S.oP = carve(p, sizeof(double) * g.T);
 #pragma unroll
     for (int l = 0; l <= kMaxLayers; ++l)
         if (l <= a.L()) S.oact[l] = carve(p, sizeof(double) * 32 * a.stride(l));
@@ -124,6 +126,13 @@ __device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom&
     for (int l = 0; l < kMaxLayers; ++l)
         if (l < a.L()) S.odel[l] = carve(p, sizeof(double) * 32 * a.stride(l + 1));
     S.oig = carve(p, sizeof(double) * 32 * a.stride(0));
+    S.os_app = carve(p, sizeof(int) * 32);
+    S.os_set = carve(p, sizeof(int) * 32);
+    S.os_y = carve(p, sizeof(double) * 32);
+    S.octrl = carve(p, sizeof(int) * 16);
+    S.otab = carve(p, sizeof(uint64_t) * 256);
+    S.omt = carve(p, sizeof(uint64_t) * 313);
+    S.oP = carve(p, sizeof(double) * g.T);
     S.ocval = carve(p, sizeof(double) * g.max_cells);
     S.ocrc = carve(p, sizeof(uint32_t) * g.max_cells);
     S.otset = carve(p, sizeof(uint16_t) * g.max_cells);
@@ -131,13 +140,7 @@ __device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom&
     S.operm[0] = carve(p, sizeof(uint16_t) * g.max_cells);
     S.operm[1] = carve(p, sizeof(uint16_t) * g.max_cells);
     S.odraw = carve(p, sizeof(uint32_t) * g.max_cells);
-    S.omt = carve(p, sizeof(uint64_t) * 313);
     S.orow = carve(p, sizeof(double) * g.n);
-    S.os_app = carve(p, sizeof(int) * 32);
-    S.os_set = carve(p, sizeof(int) * 32);
-    S.os_y = carve(p, sizeof(double) * 32);
-    S.octrl = carve(p, sizeof(int) * 16);
-    S.otab = carve(p, sizeof(uint64_t) * 256);
 }
 
 enum Ctrl { kMtIdx = 0, kStop = 1, kImproved = 2, kNt = 3, kNv = 4, kNc = 5, kDiverged = 6 };
@@ -185,6 +188,37 @@ __device__ void uniform_fill(double* dst, int cnt, double lo, double hi, MtWarp&
 // forward() / forward_tape() (nnkit.cpp:74-89, :124-138) for cnt <= 32 cells
 // whose (app, setting) ids are in s_app/s_set.  Leaves layer outputs in act[],
 // and (tape) SELU derivative factors in del[].
+// compile-time layer (FixArch): the warp's NO outputs are formed together, so their dot
+// chains and SELU exps are independent instruction streams (ILP) instead of a loop
+template <int LANE, class A, int LAY>
+__device__ __forceinline__ void forward_layer_fix(const Smem& S, const A& a, const BatchGeom& g, int cnt, bool tape,
+                                                  int warp, int lane) {
+    constexpr int in = A::dim(LAY), out = A::dim(LAY + 1), NO = (out + kCW - 1) / kCW;
+    constexpr bool hidden = LAY + 1 < A::L();
+    const double* W = S.P() + g.off_w[LAY];
+    const double* b = S.P() + g.off_b[LAY];
+    const double* ain = S.act(LAY) + lane * A::stride(LAY);
+    if (lane < cnt) {
+        double z[NO];
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+            const int o = warp + q * kCW;
+            if (out % kCW == 0 || o < out) z[q] = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
+        }
+#pragma unroll
+        for (int q = 0; q < NO; ++q) {
+            const int o = warp + q * kCW;
+            if (out % kCW == 0 || o < out) {
+                double v = z[q], gf = 1.0;
+                if (hidden) selu_fwd(z[q], v, gf, S.tab());
+                S.act(LAY + 1)[lane * A::stride(LAY + 1) + o] = v;
+                if (tape) S.del(LAY)[lane * A::stride(LAY + 1) + o] = gf;
+            }
+        }
+    }
+    bar_compute();
+}
+
 template <int LANE, class A>
 __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt, bool tape,
                                               int warp, int lane, int ctid) {
@@ -196,60 +230,113 @@ __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const B
         S.act(0)[s * a.stride(0) + i] = v;
     }
     bar_compute();
+    if constexpr (A::kStatic && LANE == 0) {  // (the AVX2 lane's 4-accumulator dots would spill)
+        static_assert(A::L() == 3, "FixArch is the 3-layer default stack");
+        forward_layer_fix<LANE, A, 0>(S, a, g, cnt, tape, warp, lane);
+        forward_layer_fix<LANE, A, 1>(S, a, g, cnt, tape, warp, lane);
+        forward_layer_fix<LANE, A, 2>(S, a, g, cnt, tape, warp, lane);
+    } else {
 #pragma unroll
-    for (int l = 0; l < kMaxLayers; ++l) {
-        if (l >= a.L()) break;
-        const int in = a.dim(l), out = a.dim(l + 1);
-        const double* W = S.P() + g.off_w[l];
-        const double* b = S.P() + g.off_b[l];
-        const double* ain = S.act(l) + lane * a.stride(l);
-        const bool hidden = l + 1 < a.L();
-        if (lane < cnt) {
-            for (int o = warp; o < out; o += kCW) {
-                const double z = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
-                double v = z, gf = 1.0;
-                if (hidden) selu_fwd(z, v, gf, S.tab());
-                S.act(l + 1)[lane * a.stride(l + 1) + o] = v;
-                if (tape) S.del(l)[lane * a.stride(l + 1) + o] = gf;
+        for (int l = 0; l < kMaxLayers; ++l) {
+            if (l >= a.L()) break;
+            const int in = a.dim(l), out = a.dim(l + 1);
+            const double* W = S.P() + g.off_w[l];
+            const double* b = S.P() + g.off_b[l];
+            const double* ain = S.act(l) + lane * a.stride(l);
+            const bool hidden = l + 1 < a.L();
+            if (lane < cnt) {
+                for (int o = warp; o < out; o += kCW) {
+                    const double z = dadd(LaneOps<LANE>::dot(W + o * in, ain, in), b[o]);
+                    double v = z, gf = 1.0;
+                    if (hidden) selu_fwd(z, v, gf, S.tab());
+                    S.act(l + 1)[lane * a.stride(l + 1) + o] = v;
+                    if (tape) S.del(l)[lane * a.stride(l + 1) + o] = gf;
+                }
             }
+            bar_compute();
         }
-        bar_compute();
     }
 }
 
 // backprop_sample (nnkit.cpp:184-212) deltas for a minibatch already
 // forwarded with tape; writes del[l] = deltas and ig = input gradients.
-template <int LANE, class A>
-__device__ __forceinline__ void backward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt,
-                                               double scale, int warp, int lane) {
-    const int L = a.L();
+// compile-time layer (FixArch): the warp's NC input columns' matvec_t chains side by side
+template <int LANE, class A, int LAY>
+__device__ __forceinline__ void backward_layer_fix(const Smem& S, const A& a, const BatchGeom& g, int cnt, int warp,
+                                                   int lane) {
+    constexpr int in = A::dim(LAY), out = A::dim(LAY + 1), NC = (in + kCW - 1) / kCW;
+    const double* W = S.P() + g.off_w[LAY];
+    const double* d = S.del(LAY) + lane * A::stride(LAY + 1);
+    if (lane < cnt) {
+        double nd[NC];
 #pragma unroll
-    for (int l = kMaxLayers - 1; l >= 0; --l) {
-        if (l >= L) continue;
-        if (l == L - 1) {
-            if (warp == 0 && lane < cnt) {
-                const double err = dsub(S.act(l + 1)[lane * a.stride(l + 1)], S.s_y()[lane]);
-                // delta = 2*err*scale, then *= identity grad 1.0
-                S.del(l)[lane * a.stride(l + 1)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
+        for (int q = 0; q < NC; ++q) nd[q] = 0.0;  // matvec_t: out[c] = 0; out[c] += d[r]*w[r][c]
+        for (int r = 0; r < out; ++r) {
+            const double dr = d[r];
+#pragma unroll
+            for (int q = 0; q < NC; ++q) {
+                const int c = warp + q * kCW;
+                if (in % kCW == 0 || c < in) nd[q] = LaneOps<LANE>::axpy(nd[q], dr, W[r * in + c]);
             }
-            bar_compute();
         }
-        const int in = a.dim(l), out = a.dim(l + 1);
-        const double* W = S.P() + g.off_w[l];
-        const double* d = S.del(l) + lane * a.stride(l + 1);
-        if (lane < cnt) {
-            for (int c = warp; c < in; c += kCW) {
-                double nd = 0.0;  // matvec_t: out[c] = 0; out[c] += d[r]*w[r][c]
-                for (int r = 0; r < out; ++r) nd = LaneOps<LANE>::axpy(nd, d[r], W[r * in + c]);
-                if (l > 0) {
-                    double* gf = S.del(l > 0 ? l - 1 : 0) + lane * a.stride(l) + c;
-                    *gf = dmul(nd, *gf);  // delta[o] *= activate_grad
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            const int c = warp + q * kCW;
+            if (in % kCW == 0 || c < in) {
+                if (LAY > 0) {
+                    double* gf = S.del(LAY > 0 ? LAY - 1 : 0) + lane * A::stride(LAY) + c;
+                    *gf = dmul(nd[q], *gf);  // delta[o] *= activate_grad
                 } else {
-                    S.ig()[lane * a.stride(0) + c] = nd;
+                    S.ig()[lane * A::stride(0) + c] = nd[q];
                 }
             }
         }
+    }
+    bar_compute();
+}
+
+template <int LANE, class A>
+__device__ __forceinline__ void backward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt,
+                                               double scale, int warp, int lane) {
+    if constexpr (A::kStatic && LANE == 1) {  // (with the scalar lane's ILP forward this would spill)
+        if (warp == 0 && lane < cnt) {
+            const double err = dsub(S.act(3)[lane * A::stride(3)], S.s_y()[lane]);
+            S.del(2)[lane * A::stride(3)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
+        }
         bar_compute();
+        backward_layer_fix<LANE, A, 2>(S, a, g, cnt, warp, lane);
+        backward_layer_fix<LANE, A, 1>(S, a, g, cnt, warp, lane);
+        backward_layer_fix<LANE, A, 0>(S, a, g, cnt, warp, lane);
+    } else {
+        const int L = a.L();
+#pragma unroll
+        for (int l = kMaxLayers - 1; l >= 0; --l) {
+            if (l >= L) continue;
+            if (l == L - 1) {
+                if (warp == 0 && lane < cnt) {
+                    const double err = dsub(S.act(l + 1)[lane * a.stride(l + 1)], S.s_y()[lane]);
+                    // delta = 2*err*scale, then *= identity grad 1.0
+                    S.del(l)[lane * a.stride(l + 1)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
+                }
+                bar_compute();
+            }
+            const int in = a.dim(l), out = a.dim(l + 1);
+            const double* W = S.P() + g.off_w[l];
+            const double* d = S.del(l) + lane * a.stride(l + 1);
+            if (lane < cnt) {
+                for (int c = warp; c < in; c += kCW) {
+                    double nd = 0.0;  // matvec_t: out[c] = 0; out[c] += d[r]*w[r][c]
+                    for (int r = 0; r < out; ++r) nd = LaneOps<LANE>::axpy(nd, d[r], W[r * in + c]);
+                    if (l > 0) {
+                        double* gf = S.del(l > 0 ? l - 1 : 0) + lane * a.stride(l) + c;
+                        *gf = dmul(nd, *gf);  // delta[o] *= activate_grad
+                    } else {
+                        S.ig()[lane * a.stride(0) + c] = nd;
+                    }
+                }
+            }
+            bar_compute();
+        }
     }
 }
 
@@ -449,15 +536,35 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
     for (int e = tid; e < 256; e += blockDim.x) smp<uint64_t>(S.otab)[e] = exp_tab(e);  // first app's sync publishes it
 
     // owned parameters (compile-time indexed so moments stay in registers)
-    uint32_t own[kEPT];
-    int eidx[kEPT];
-    double M1[kEPT], V1[kEPT], BEST[kEPT];
-#pragma unroll
-    for (int k = 0; k < kEPT; ++k) {
-        eidx[k] = is_rng ? g.T : owned_index<ARCH>(g, k, ctid);
-        own[k] = is_rng ? 0u : describe(g, eidx[k]);
-        M1[k] = V1[k] = BEST[k] = 0.0;
+    // (compile-time shape: the 2x2 weight tile of slots 0-3 is implied by ctid and kept as
+    // its first index only; descriptors are stored for the remaining slots)
+    constexpr int kK0 = ARCH::kStatic ? 4 : 0;  // slots [0, kK0) are the tile
+    uint32_t own[kEPT - kK0];
+    int eidx[kEPT - kK0];
+    double M1[kEPT], V1[kEPT];
+    int tile_r = 0, tile_c = 0, tile_e = 0;
+    if constexpr (ARCH::kStatic) {
+        constexpr int in0 = ARCH::dim(0), h0 = ARCH::dim(1);
+        if (ctid < 128) {
+            tile_r = 2 * (ctid / (in0 / 2));
+            tile_c = 2 * (ctid % (in0 / 2));
+            tile_e = g.off_w[0] + tile_r * in0 + tile_c;
+        } else {
+            tile_r = 2 * ((ctid - 128) / (h0 / 2));
+            tile_c = 2 * ((ctid - 128) % (h0 / 2));
+            tile_e = g.off_w[1] + tile_r * h0 + tile_c;
+        }
     }
+#pragma unroll
+    for (int k = kK0; k < kEPT; ++k) {
+        eidx[k - kK0] = is_rng ? g.T : owned_index<ARCH>(g, k, ctid);
+        own[k - kK0] = is_rng ? 0u : describe(g, eidx[k - kK0]);
+    }
+#pragma unroll
+    for (int k = 0; k < kEPT; ++k) M1[k] = V1[k] = 0.0;
+    // best snapshot in global scratch (L2-resident): written when validation improves,
+    // read once at restore; keeping it in registers cost the hot loops their spills
+    double* const bestbuf = io.best + static_cast<int64_t>(blockIdx.x) * io.best_stride;
 
     const double lr = g.lr, b1 = 0.9, b2 = 0.999, eps = 1e-8;  // nnkit.hpp:95
     const double omb1 = dsub(1.0, b1), omb2 = dsub(1.0, b2);
@@ -553,10 +660,8 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
             double init_train = 0.0, best_val = 0.0;
             if (!is_rng) {
 #pragma unroll
-                for (int k = 0; k < kEPT; ++k) {
-                    M1[k] = V1[k] = 0.0;
-                    if (own_valid(own[k])) BEST[k] = S.P()[eidx[k]];
-                }
+                for (int k = 0; k < kEPT; ++k) M1[k] = V1[k] = 0.0;
+                for (int q = ctid; q < g.T; q += kCT) bestbuf[q] = S.P()[q];
                 init_train = cells_mse<LANE>(S, a, g, S.tset(), nt, warp, lane, ctid);
                 best_val = cells_mse<LANE>(S, a, g, mon, nmon, warp, lane, ctid);
             } else {
@@ -597,15 +702,26 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                         const double mc = ddiv(1.0, dsub(1.0, b1p)), vc = ddiv(1.0, dsub(1.0, b2p));
                         double gt[4] = {0.0, 0.0, 0.0, 0.0};
                         if constexpr (ARCH::kStatic) {
-                            if (ctid < 128) tile_grad<LANE, 0>(S, a, own_r(own[0]), own_c(own[0]), cnt, gt);
-                            else tile_grad<LANE, 1>(S, a, own_r(own[0]), own_c(own[0]), cnt, gt);
+                            if (!is_rng) {
+                                if (ctid < 128) tile_grad<LANE, 0>(S, a, tile_r, tile_c, cnt, gt);
+                                else tile_grad<LANE, 1>(S, a, tile_r, tile_c, cnt, gt);
+                                const int rstep = ctid < 128 ? ARCH::dim(0) : ARCH::dim(1);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {  // W0 / W1 sizes are multiples of 4: vector part
+                                    const int e = tile_e + (k >> 1) * rstep + (k & 1);
+                                    double p = S.P()[e];
+                                    LaneOps<LANE>::adam(p, M1[k], V1[k], gt[k], lr, b1, omb1, b2, omb2, eps, mc, vc,
+                                                        true);
+                                    S.P()[e] = p;
+                                }
+                            }
                         }
 #pragma unroll
-                        for (int k = 0; k < kEPT; ++k) {
-                            const uint32_t o = own[k];
+                        for (int k = kK0; k < kEPT; ++k) {
+                            const uint32_t o = own[k - kK0];
                             if (!own_valid(o)) continue;
-                            const int e = eidx[k];
-                            const double gsum = (ARCH::kStatic && k < 4) ? gt[k < 4 ? k : 0] : param_grad<LANE>(S, a, o, cnt);
+                            const int e = eidx[k - kK0];
+                            const double gsum = param_grad<LANE>(S, a, o, cnt);
                             double p = S.P()[e];
                             LaneOps<LANE>::adam(p, M1[k], V1[k], gsum, lr, b1, omb1, b2, omb2, eps, mc, vc,
                                                 own_vec(o));
@@ -637,11 +753,8 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                     diverged = true;
                     break;
                 }
-                if (!is_rng && S.ctrl()[kImproved]) {
-#pragma unroll
-                    for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) BEST[k] = S.P()[eidx[k]];
-                }
+                if (!is_rng && S.ctrl()[kImproved])
+                    for (int q = ctid; q < g.T; q += kCT) bestbuf[q] = S.P()[q];
                 if (stop) {
                     ++epoch;
                     break;
@@ -651,11 +764,8 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                 status = OCG_E_DIVERGE;
             } else {
                 // restore(best) (:190)
-                if (!is_rng) {
-#pragma unroll
-                    for (int k = 0; k < kEPT; ++k)
-                        if (own_valid(own[k])) S.P()[eidx[k]] = BEST[k];
-                }
+                if (!is_rng)
+                    for (int q = ctid; q < g.T; q += kCT) S.P()[q] = bestbuf[q];
                 __syncthreads();
                 double final_train = 0.0;
                 if (!is_rng) final_train = cells_mse<LANE>(S, a, g, S.tset(), nt, warp, lane, ctid);

@@ -56,6 +56,8 @@ struct BatchIO {
     int32_t* status;
     double* params;
     int64_t params_stride;
+    double* best;         // per-CTA best-parameter snapshot (gridDim.x x best_stride), device scratch
+    int64_t best_stride;
 };
 
 size_t batch_smem_bytes(const BatchGeom& g);
