@@ -64,6 +64,11 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        if self.world > 1 and os.environ.get("OCG_BENCH_SHARE_GPU") == "1":
+            # dry run of the N > 1 code paths on a one-GPU box: every rank on cuda:0, gloo
+            # for the barrier / max (NCCL refuses two ranks on one device); timings meaningless
+            self.local = 0
+            backend = "gloo" if backend else backend
         if self.world > 1 and backend:
             import torch
             import torch.distributed as dist
