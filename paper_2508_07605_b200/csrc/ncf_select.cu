@@ -30,6 +30,7 @@
 //        TMEM); B_j tiles arrive by TMA.  |dp|/p ~ 1e-6; selections exact
 //        wherever the row's margin exceeds that.
 #include <algorithm>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -720,13 +721,16 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
         }
     };
 
-    for (int64_t j = 0; j < n; ++j) {
+    // one column: operand -> barrier -> MMA issue -> the previous column's epilogue.  The loop
+    // runs column pairs so the buffer index B is a compile-time constant (and a tile, 32
+    // columns, always starts on an even column)
+    auto step = [&](int64_t j, auto Bc) {
+        constexpr int b = decltype(Bc)::value;
         const int T = static_cast<int>(j / kNsTileCols), jj = static_cast<int>(j % kNsTileCols), stg = T & 1;
-        if (jj == 0) {
+        if (b == 0 && jj == 0) {
             mbar_wait(bars + stg, (tph >> stg) & 1u);
             tph ^= 1u << stg;
         }
-        const int b = static_cast<int>(j & 1);
         // ---- operand: h'(z) = s_h SELU(z)/lambda for the 32 layer-0 outputs, as fp16 hi/lo
         const float* bcol = stage + stg * kNsTileCols * kNsColFloats + jj * kNsColFloats;
         const float4* bj = reinterpret_cast<const float4*>(bcol);
@@ -762,7 +766,7 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
         __syncthreads();
         if (t == 0) {
             tc_fence_after();
-            if (jj == 0 && T >= 1 && T + 1 < ntiles) {  // stage (T+1)&1 held tile T-1: every thread is past it
+            if (b == 0 && jj == 0 && T >= 1 && T + 1 < ntiles) {  // stage (T+1)&1 held tile T-1: all are past it
                 const int s2 = (T + 1) & 1;
                 mbar_expect_tx(bars + s2, kStageBytes);
                 tma_load_2d(stage + s2 * kNsTileCols * kNsColFloats, &tmap, 0, (T + 1) * kNsTileCols, bars + s2);
@@ -780,9 +784,15 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
             umma_commit(bars + 2 + b);
         }
         __syncwarp();
-        if (j > 0) epilogue(j - 1, b ^ 1, cs_prev);
+        if (b == 1 || j > 0) epilogue(j - 1, b ^ 1, cs_prev);
         cs_prev = cs_cur;
+    };
+    int64_t j = 0;
+    for (; j + 1 < n; j += 2) {
+        step(j, std::integral_constant<int, 0>{});
+        step(j + 1, std::integral_constant<int, 1>{});
     }
+    if (j < n) step(j, std::integral_constant<int, 0>{});
     epilogue(n - 1, static_cast<int>((n - 1) & 1), cs_prev);
 
     if (!LIST && live) {
