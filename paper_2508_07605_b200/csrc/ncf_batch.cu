@@ -86,7 +86,7 @@ struct Smem {
     uint32_t oP;                    // [T] parameters
     uint32_t oact[kMaxLayers + 1];  // act[0] = gathered inputs X; act[l+1] = layer l output
     uint32_t odel[kMaxLayers];      // del[l]: act-grad factors, then deltas, of layer l output
-    uint32_t oig, ocval, ocrc, otset, ovset, operm[2], odraw, omt, orow, os_app, os_set, os_y, octrl, otab;
+    uint32_t oig, ocval, ocrc, otset, ovset, operm[2], odraw, omt, orow, os_app, os_set, os_y, octrl, otab, omask;
     __device__ __forceinline__ double* P() const { return smp<double>(oP); }
     __device__ __forceinline__ double* act(int l) const { return smp<double>(oact[l]); }
     __device__ __forceinline__ double* del(int l) const { return smp<double>(odel[l]); }
@@ -99,6 +99,8 @@ struct Smem {
     __device__ __forceinline__ uint32_t* draw() const { return smp<uint32_t>(odraw); }
     __device__ __forceinline__ uint64_t* mt() const { return smp<uint64_t>(omt); }
     __device__ __forceinline__ double* row() const { return smp<double>(orow); }  // completed app row
+    // per embedding row (apps 0..m-1, then settings): bit s = minibatch sample s touches it
+    __device__ __forceinline__ uint32_t* mask() const { return smp<uint32_t>(omask); }
     __device__ __forceinline__ int* s_app() const { return smp<int>(os_app); }
     __device__ __forceinline__ int* s_set() const { return smp<int>(os_set); }
     __device__ __forceinline__ double* s_y() const { return smp<double>(os_y); }
@@ -141,6 +143,7 @@ __device__ __forceinline__ void setup_smem(Smem& S, const A& a, const BatchGeom&
     S.operm[1] = carve(p, sizeof(uint16_t) * g.max_cells);
     S.odraw = carve(p, sizeof(uint32_t) * g.max_cells);
     S.orow = carve(p, sizeof(double) * g.n);
+    S.omask = carve(p, sizeof(uint32_t) * (g.m + g.n));
 }
 
 enum Ctrl { kMtIdx = 0, kStop = 1, kImproved = 2, kNt = 3, kNv = 4, kNc = 5, kDiverged = 6 };
@@ -457,13 +460,16 @@ __device__ __forceinline__ double param_grad(const Smem& S, const A& a, uint32_t
     }
     double gsum = 0.0;
     const int st0 = a.stride(0);
-    if (kind == 0) {  // app-embedding scatter (cfcomplete.cpp:171-172)
-        for (int s = 0; s < cnt; ++s)
-            if (S.s_app()[s] == orow) gsum = dadd(gsum, S.ig()[s * st0 + ocol]);
-    } else {  // setting-embedding scatter (:173-174)
-        for (int s = 0; s < cnt; ++s)
-            if (S.s_set()[s] == orow) gsum = dadd(gsum, S.ig()[s * st0 + a.ka() + ocol]);
+    // embedding scatter (cfcomplete.cpp:171-174): the samples that touch the row, in sample
+    // order, from the step's row mask (built by warp 0 when it loads the minibatch)
+    const double* ig = S.ig() + (kind == 0 ? ocol : a.ka() + ocol);
+    uint32_t mk = S.mask()[kind == 0 ? orow : a.g.m + orow];
+    while (mk) {
+        const int s = __ffs(mk) - 1;
+        mk &= mk - 1;
+        gsum = dadd(gsum, ig[s * st0]);
     }
+    (void)cnt;
     return gsum;
 }
 
@@ -601,6 +607,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
             }
         }
         for (int j = tid; j < g.n; j += kThreads) S.row()[j] = prow[j];
+        for (int q = tid; q < g.m + g.n; q += kThreads) S.mask()[q] = 0u;
         __syncthreads();
         const int nc = S.ctrl()[kNc];
         const int napp_obs = nc - g.block_nnz;
@@ -686,12 +693,22 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                     for (int start = 0; start < nt; start += g.batch) {
                         const int cnt = min(g.batch, nt - start);
                         const double scale = ddiv(1.0, static_cast<double>(cnt));
-                        if (ctid < cnt) {
-                            const int c = S.tset()[perm[start + ctid]];
-                            const uint32_t rc = S.crc()[c];
-                            S.s_app()[ctid] = static_cast<int>(rc >> 16);
-                            S.s_set()[ctid] = static_cast<int>(rc & 0xffff);
-                            S.s_y()[ctid] = S.cval()[c];
+                        if (warp == 0) {  // (cnt <= 32: the minibatch is warp 0's)
+                            if (start > 0 && lane < g.batch) {  // the previous step's rows: masks back to 0
+                                S.mask()[S.s_app()[lane]] = 0u;
+                                S.mask()[g.m + S.s_set()[lane]] = 0u;
+                            }
+                            __syncwarp();
+                            if (lane < cnt) {
+                                const int c = S.tset()[perm[start + lane]];
+                                const uint32_t rc = S.crc()[c];
+                                const int ra = static_cast<int>(rc >> 16), rs = static_cast<int>(rc & 0xffff);
+                                S.s_app()[lane] = ra;
+                                S.s_set()[lane] = rs;
+                                S.s_y()[lane] = S.cval()[c];
+                                atomicOr(S.mask() + ra, 1u << lane);
+                                atomicOr(S.mask() + g.m + rs, 1u << lane);
+                            }
                         }
                         bar_compute();
                         forward_chunk<LANE>(S, a, g, cnt, true, warp, lane, ctid);
@@ -728,6 +745,14 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                             S.P()[e] = p;
                         }
                         bar_compute();
+                    }
+                    if (warp == 0 && nt > 0) {  // the epoch's last step: masks back to 0 (before validation reuses s_app)
+                        const int last = nt - ((nt - 1) / g.batch) * g.batch;
+                        if (lane < last) {
+                            S.mask()[S.s_app()[lane]] = 0u;
+                            S.mask()[g.m + S.s_set()[lane]] = 0u;
+                        }
+                        __syncwarp();
                     }
                     const double vl = cells_mse<LANE>(S, a, g, mon, nmon, warp, lane, ctid);
                     if (ctid == 0) {
@@ -865,6 +890,7 @@ size_t batch_smem_bytes(const BatchGeom& g) {
     add(sizeof(double) * 32);
     add(sizeof(int) * 16);
     add(sizeof(uint64_t) * 256);
+    add(sizeof(uint32_t) * (g.m + g.n));
     return b;
 }
 
