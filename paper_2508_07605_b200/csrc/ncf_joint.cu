@@ -83,7 +83,7 @@ struct JointCtl {
 
 // shared-memory carve-up (byte offsets), computed on the host
 struct JLayout {
-    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab;
+    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab, smask;
     uint32_t bytes;
 };
 
@@ -387,6 +387,8 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
     double* sy = sp<double>(sm, ly.sy);
     int* ssa = sp<int>(sm, ly.ssa);
     int* sss = sp<int>(sm, ly.sss);
+    // per slot, bit q = minibatch sample q touches the slot's row; double-buffered by step parity
+    uint32_t* smask = sp<uint32_t>(sm, ly.smask);
     const ExpTabPtr tab{sp<uint64_t>(sm, ly.tab)};
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int L = sh.L(), kmax = sh.kmax(), rs = 3 * kmax;
@@ -398,6 +400,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         M[e] = __ldcg(a.mlp + a.T_mlp + e);
         V[e] = __ldcg(a.mlp + 2 * a.T_mlp + e);
     }
+    for (int q = tid; q < 2 * kJMaxSlots; q += kJT) smask[q] = 0u;
     __syncthreads();
 
     for (int s = 0; s < a.S; ++s) {
@@ -415,12 +418,17 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             wait_geq(a.ready + s, want, false);
             c1 = clock64();
         }
+        uint32_t* mk_cur = smask + (s & 1) * kJMaxSlots;
         if (tid < cnt) {
             const uint16_t sl = a.smp_slot[static_cast<int64_t>(s) * a.B + tid];
             ssa[tid] = sl & 0xff;
             sss[tid] = sl >> 8;
             sy[tid] = a.smp_y[static_cast<int64_t>(s) * a.B + tid];
+            atomicOr(mk_cur + (sl & 0xff), 1u << tid);
+            atomicOr(mk_cur + (sl >> 8), 1u << tid);
         }
+        // the other buffer was last read in step s - 1 (finished): clear it for step s + 1
+        if (tid >= kJT - kJMaxSlots) smask[((s + 1) & 1) * kJMaxSlots + tid - (kJT - kJMaxSlots)] = 0u;
         __syncthreads();
         // ---- slots: from the previous step's smem, or (replayed) from HBM
         for (int q = tid; q < nsl * kmax; q += kJT) {
@@ -539,14 +547,9 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
             const bool is_app = row < a.m;
             const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
-            T g = T(0);  // embedding-gradient scatter (cfcomplete.cpp:171-174)
-            if (is_app) {
-                for (int q2 = 0; q2 < cnt; ++q2)
-                    if (ssa[q2] == sl) g = NUM::add(g, ig[q2 * st0 + c]);
-            } else {
-                for (int q2 = 0; q2 < cnt; ++q2)
-                    if (sss[q2] == sl) g = NUM::add(g, ig[q2 * st0 + sh.ka() + c]);
-            }
+            T g = T(0);  // embedding-gradient scatter (cfcomplete.cpp:171-174), samples in order
+            const T* igc = ig + (is_app ? c : sh.ka() + c);
+            for (uint32_t mk = mk_cur[sl]; mk; mk &= mk - 1) g = NUM::add(g, igc[(__ffs(mk) - 1) * st0]);
             T* d = cur + sl * rs;
             const int64_t r = is_app ? row : row - a.m;
             const bool vec = r * k + c < (is_app ? a.app_vec : a.set_vec);
@@ -1043,6 +1046,7 @@ JLayout make_layout(int T_mlp, int kmax, int L, const int* stride, size_t tsz) {
     ly.ssa = carve(sizeof(int) * kJMaxB);
     ly.sss = carve(sizeof(int) * kJMaxB);
     ly.tab = carve(sizeof(uint64_t) * 256);
+    ly.smask = carve(sizeof(uint32_t) * 2 * kJMaxSlots);
     ly.bytes = p;
     return ly;
 }
