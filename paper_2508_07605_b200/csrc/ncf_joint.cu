@@ -83,7 +83,7 @@ struct JointCtl {
 
 // shared-memory carve-up (byte offsets), computed on the host
 struct JLayout {
-    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab, smask;
+    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab, smask, ones;
     uint32_t bytes;
 };
 
@@ -401,6 +401,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         V[e] = __ldcg(a.mlp + 2 * a.T_mlp + e);
     }
     for (int q = tid; q < 2 * kJMaxSlots; q += kJT) smask[q] = 0u;
+    if (tid == 0) *sp<T>(sm, ly.ones) = T(1);
     __syncthreads();
 
     for (int s = 0; s < a.S; ++s) {
@@ -511,34 +512,48 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         }
         long long c3 = tid == 0 ? clock64() : 0;
         // ---- gradient sums in sample order + Adam (nnkit.cpp:239-251)
-        for (int e = tid; e < a.T_mlp; e += kJT) {
-            const uint32_t d = __ldg(dec + e);
-            const int layer = (d >> 16) & 15, r = (d >> 8) & 255, c = d & 255;
-            const T* dl = sp<T>(sm, ly.del[layer]) + r;
-            const int sd = sh.stride(layer + 1);
-            T g = T(0);
-            if (d & (1u << 20)) {  // outer_acc: G[r][c] += d[r] * x[c], samples in order
-                const T* al = sp<T>(sm, ly.act[layer]) + c;
-                const int sa = sh.stride(layer);
-                int q = 0;
-                if (cnt == kJMaxB) {
+        if (cnt == kJMaxB) {
+            // full minibatch: two parameters per pass, their 32-sample chains side by side.  A bias
+            // chain is the weight chain against x = 1 (fma(d, 1, g) and g + d*1 both round d + g
+            // once, exactly the reference's add), so both chains are the same straight-line code.
+            const T* ones = sp<T>(sm, ly.ones);
+            for (int e0 = tid; e0 < a.T_mlp; e0 += 2 * kJT) {
+                const int e1 = e0 + kJT;
+                const bool has1 = e1 < a.T_mlp;
+                const uint32_t d0 = __ldg(dec + e0), d1 = has1 ? __ldg(dec + e1) : d0;
+                const int l0 = (d0 >> 16) & 15, l1 = (d1 >> 16) & 15;
+                const T* dl0 = sp<T>(sm, ly.del[l0]) + ((d0 >> 8) & 255);
+                const T* dl1 = sp<T>(sm, ly.del[l1]) + ((d1 >> 8) & 255);
+                const int sd0 = sh.stride(l0 + 1), sd1 = sh.stride(l1 + 1);
+                const bool w0 = d0 & (1u << 20), w1 = d1 & (1u << 20);
+                const T* al0 = w0 ? sp<T>(sm, ly.act[l0]) + (d0 & 255) : ones;
+                const T* al1 = w1 ? sp<T>(sm, ly.act[l1]) + (d1 & 255) : ones;
+                const int sa0 = w0 ? sh.stride(l0) : 0, sa1 = w1 ? sh.stride(l1) : 0;
+                T g0 = T(0), g1 = T(0);
 #pragma unroll
-                    for (int q2 = 0; q2 < kJMaxB; ++q2) g = NUM::axpy(g, dl[q2 * sd], al[q2 * sa]);
-                    q = kJMaxB;
+                for (int q2 = 0; q2 < kJMaxB; ++q2) {
+                    g0 = NUM::axpy(g0, dl0[q2 * sd0], al0[q2 * sa0]);
+                    g1 = NUM::axpy(g1, dl1[q2 * sd1], al1[q2 * sa1]);
                 }
-                for (; q + 4 <= cnt; q += 4) {
-                    const T d0 = dl[q * sd], d1 = dl[(q + 1) * sd], d2 = dl[(q + 2) * sd], d3 = dl[(q + 3) * sd];
-                    const T x0 = al[q * sa], x1 = al[(q + 1) * sa], x2 = al[(q + 2) * sa], x3 = al[(q + 3) * sa];
-                    g = NUM::axpy(g, d0, x0);
-                    g = NUM::axpy(g, d1, x1);
-                    g = NUM::axpy(g, d2, x2);
-                    g = NUM::axpy(g, d3, x3);
-                }
-                for (; q < cnt; ++q) g = NUM::axpy(g, dl[q * sd], al[q * sa]);
-            } else {
-                for (int q = 0; q < cnt; ++q) g = NUM::add(g, dl[q * sd]);
+                NUM::adam(P[e0], M[e0], V[e0], g0, a.lr, mc, vc, (d0 >> 21) & 1);
+                if (has1) NUM::adam(P[e1], M[e1], V[e1], g1, a.lr, mc, vc, (d1 >> 21) & 1);
             }
-            NUM::adam(P[e], M[e], V[e], g, a.lr, mc, vc, (d >> 21) & 1);
+        } else {
+            for (int e = tid; e < a.T_mlp; e += kJT) {
+                const uint32_t d = __ldg(dec + e);
+                const int layer = (d >> 16) & 15, r = (d >> 8) & 255, c = d & 255;
+                const T* dl = sp<T>(sm, ly.del[layer]) + r;
+                const int sd = sh.stride(layer + 1);
+                T g = T(0);
+                if (d & (1u << 20)) {  // outer_acc: G[r][c] += d[r] * x[c], samples in order
+                    const T* al = sp<T>(sm, ly.act[layer]) + c;
+                    const int sa = sh.stride(layer);
+                    for (int q = 0; q < cnt; ++q) g = NUM::axpy(g, dl[q * sd], al[q * sa]);
+                } else {
+                    for (int q = 0; q < cnt; ++q) g = NUM::add(g, dl[q * sd]);
+                }
+                NUM::adam(P[e], M[e], V[e], g, a.lr, mc, vc, (d >> 21) & 1);
+            }
         }
         const T* ig = sp<T>(sm, ly.ig);
         for (int q = tid; q < nsl * kmax; q += kJT) {
@@ -1047,6 +1062,7 @@ JLayout make_layout(int T_mlp, int kmax, int L, const int* stride, size_t tsz) {
     ly.sss = carve(sizeof(int) * kJMaxB);
     ly.tab = carve(sizeof(uint64_t) * 256);
     ly.smask = carve(sizeof(uint32_t) * 2 * kJMaxSlots);
+    ly.ones = carve(tsz);  // one element = 1 (bias chains)
     ly.bytes = p;
     return ly;
 }
