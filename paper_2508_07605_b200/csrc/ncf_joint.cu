@@ -83,7 +83,7 @@ struct JointCtl {
 
 // shared-memory carve-up (byte offsets), computed on the host
 struct JLayout {
-    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab, smask, ones;
+    uint32_t P, M, V, slot[2], act[kJMaxL + 1], del[kJMaxL], ig, sy, ssa, sss, tab, smask, ones, srow;
     uint32_t bytes;
 };
 
@@ -404,27 +404,48 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
     if (tid == 0) *sp<T>(sm, ly.ones) = T(1);
     __syncthreads();
 
+    int64_t* srow = sp<int64_t>(sm, ly.srow);
+    // the host-built schedule of step s + 1 is read during step s (off the critical path)
+    int so_n = a.S > 0 ? a.slot_off[0] : 0, so1_n = a.S > 0 ? a.slot_off[1] : 0;
+    int need_n = tid == 0 && a.S > 0 ? a.need[0] : 0;
+    uint16_t smp_n = 0;
+    double y_n = 0.0;
+    if (a.S > 0 && tid < min(a.B, a.nt)) {
+        smp_n = a.smp_slot[tid];
+        y_n = a.smp_y[tid];
+    }
     for (int s = 0; s < a.S; ++s) {
         const int cnt = min(a.B, a.nt - s * a.B);
         const int64_t t = a.epoch_base + s + 1;
         double mc, vc;
         step_corr(a.tab_mc, a.tab_vc, a.tab_len, t, mc, vc);
-        const int so = a.slot_off[s], nsl = a.slot_off[s + 1] - so;
+        const int so = so_n, nsl = so1_n - so_n;
+        const int want_s = need_n;
+        const uint16_t smp_s = smp_n;
+        const double y_s = y_n;
+        if (s + 1 < a.S) {
+            so_n = so1_n;
+            so1_n = a.slot_off[s + 2];
+            if (tid == 0) need_n = a.need[s + 1];
+            if (tid < min(a.B, a.nt - (s + 1) * a.B)) {
+                smp_n = a.smp_slot[static_cast<int64_t>(s + 1) * a.B + tid];
+                y_n = a.smp_y[static_cast<int64_t>(s + 1) * a.B + tid];
+            }
+        }
         T* cur = sp<T>(sm, ly.slot[s & 1]);
         const T* prv = sp<T>(sm, ly.slot[(s + 1) & 1]);
         long long c0 = 0, c1 = 0;
         if (tid == 0) {
             c0 = clock64();
-            const int want = a.need[s];
-            wait_geq(a.ready + s, want, false);
+            wait_geq(a.ready + s, want_s, false);
             c1 = clock64();
         }
         uint32_t* mk_cur = smask + (s & 1) * kJMaxSlots;
         if (tid < cnt) {
-            const uint16_t sl = a.smp_slot[static_cast<int64_t>(s) * a.B + tid];
+            const uint16_t sl = smp_s;
             ssa[tid] = sl & 0xff;
             sss[tid] = sl >> 8;
-            sy[tid] = a.smp_y[static_cast<int64_t>(s) * a.B + tid];
+            sy[tid] = y_s;
             atomicOr(mk_cur + (sl & 0xff), 1u << tid);
             atomicOr(mk_cur + (sl >> 8), 1u << tid);
         }
@@ -435,6 +456,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         for (int q = tid; q < nsl * kmax; q += kJT) {
             const int sl = q / kmax, c = q - sl * kmax;
             const int64_t row = a.slot_row[so + sl];
+            if (c == 0) srow[sl] = row;  // for the Adam and write-back phases (no second HBM/L2 trip)
             const bool is_app = row < a.m;
             const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
@@ -558,7 +580,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         const T* ig = sp<T>(sm, ly.ig);
         for (int q = tid; q < nsl * kmax; q += kJT) {
             const int sl = q / kmax, c = q - sl * kmax;
-            const int64_t row = a.slot_row[so + sl];
+            const int64_t row = srow[sl];
             const bool is_app = row < a.m;
             const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
@@ -575,7 +597,7 @@ __device__ void leader_epoch(const JointArgs<T>& a) {
         // ---- write the touched rows back, then publish the step
         for (int q = tid; q < nsl * kmax; q += kJT) {
             const int sl = q / kmax, c = q - sl * kmax;
-            const int64_t row = a.slot_row[so + sl];
+            const int64_t row = srow[sl];
             const bool is_app = row < a.m;
             const int k = is_app ? sh.ka() : sh.ks();
             if (c >= k) continue;
@@ -1063,6 +1085,7 @@ JLayout make_layout(int T_mlp, int kmax, int L, const int* stride, size_t tsz) {
     ly.tab = carve(sizeof(uint64_t) * 256);
     ly.smask = carve(sizeof(uint32_t) * 2 * kJMaxSlots);
     ly.ones = carve(tsz);  // one element = 1 (bias chains)
+    ly.srow = carve(sizeof(int64_t) * kJMaxSlots);  // the step's slot rows
     ly.bytes = p;
     return ly;
 }
