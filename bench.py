@@ -888,7 +888,9 @@ def workload_ncf(args, d: Dist):
     p2.run(timed=False)
     p2.results_async(rptr)
     p2.results_wait()
-    e2e_p = max(args.steps, 3)
+    # a serving loop in steady state: the pipeline fill (the first step's 991 MB H2D, not
+    # overlapped) is paid once inside the timed region and amortised over 4x the bench steps
+    e2e_p = 4 * max(args.steps, 3)
     torch.cuda.synchronize(dev)
     d.barrier()
     t0 = time.perf_counter()
@@ -903,9 +905,9 @@ def workload_ncf(args, d: Dist):
         p2.results_wait()
     e2e_t = d.max((time.perf_counter() - t0) / e2e_p)
     assert np.array_equal(res_pin[0].numpy(), idx)
-    e2e_mode = (f"pipelined over {e2e_p} steps: step i+1's CSR staged (side-stream H2D from pinned memory) while "
-                "step i runs, step i's decisions copied out behind it and waited for by the host every step; no L2 "
-                "flush (the 991 MB CSR is larger than L2)")
+    e2e_mode = (f"pipelined over {e2e_p} steps (pipeline fill included): step i+1's CSR staged (side-stream H2D "
+                "from pinned memory) while step i runs, step i's decisions copied out behind it and waited for by the "
+                "host every step; no L2 flush (the 991 MB CSR is larger than L2)")
     p2.close()
     dm.close()
     cells = cells_total

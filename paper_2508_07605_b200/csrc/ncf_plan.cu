@@ -371,7 +371,7 @@ int ocg_ncf_plan_create(ocg_ncf_model* M, const int64_t* row_ptr, const int32_t*
         NCF_CUDA(P->EA.alloc(static_cast<size_t>(P->m) * 32));
         NCF_CUDA(P->BE.alloc(static_cast<size_t>(P->n) * ocg::kNsColFloats));
         NCF_CUDA(P->scale.alloc(1));
-        NCF_CUDA(P->w1img.alloc(128));
+        NCF_CUDA(P->w1img.alloc(192));
         // lambda W1 (SELU's lambda folded out of layer 0), power-of-two scaled, FP16 hi/lo,
         // in the UMMA K-major core-matrix layout (ncf_select.cu aoff: slab / group / chunk / row)
         const double* W1 = M->mlp.data() + (M->off_w[1] - M->off_w[0]);
@@ -383,7 +383,7 @@ int ocg_ncf_plan_create(ocg_ncf_model* M, const int64_t* row_ptr, const int32_t*
         int e2 = 0;
         std::frexp(mx > 0.0 ? mx : 1.0, &e2);
         P->e_w = 14 - e2;
-        std::vector<uint16_t> img(1024, 0);
+        std::vector<uint16_t> img(1536, 0);  // hi | lo | -hi
         for (int p = 0; p < 16; ++p)
             for (int o = 0; o < 32; ++o) {
                 const float w = static_cast<float>(std::ldexp(kLambda * W1[p * 32 + o], P->e_w));
@@ -396,8 +396,9 @@ int ocg_ncf_plan_create(ocg_ncf_model* M, const int64_t* row_ptr, const int32_t*
                 std::memcpy(&lb, &lo, 2);
                 img[off] = hb;
                 img[512 + off] = lb;
+                img[1024 + off] = static_cast<uint16_t>(hb ^ 0x8000u);
             }
-        NCF_CUDA(cudaMemcpyAsync(P->w1img.p, img.data(), 2048, cudaMemcpyHostToDevice, s));
+        NCF_CUDA(cudaMemcpyAsync(P->w1img.p, img.data(), 3072, cudaMemcpyHostToDevice, s));
         NCF_CUDA(cudaStreamSynchronize(s));
         for (int p = 0; p < 16; ++p) {
             // the dense epilogue works in log2 units (ncf_select.cu): b1 log2(e), lambda W2 ln(2)

@@ -597,7 +597,8 @@ constexpr int kFT = 128;                       // threads = rows per CTA = UMMA 
 constexpr int kABytes = 128 * 32 * 2;          // one operand (hi or lo): 128 rows x K 32 fp16
 constexpr int kBufBytes = 2 * kABytes;         // hi + lo
 constexpr int kStageBytes = kNsTileCols * kNsColFloats * 4;
-constexpr int kFastSmem = 2 * kBufBytes + 2 * kStageBytes + 2048 + 64;
+constexpr int kWImgBytes = 3072;  // W1 image: lambda W1 s_w as fp16 hi | lo | -hi (1 KB each)
+constexpr int kFastSmem = 2 * kBufBytes + 2 * kStageBytes + kWImgBytes + 64;
 
 // operand byte offset of (row t, 8-element chunk q) inside one hi/lo operand:
 // slab s = q >> 1 (K 16s..16s+15) at s * 4096; within a slab, 8-row group g at g * 256,
@@ -612,8 +613,8 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* abuf = sm;                                                  // [2][hi|lo]
     float* stage = reinterpret_cast<float*>(sm + 2 * kBufBytes);         // [2][kNsTileCols][68]
-    uint8_t* wimg = sm + 2 * kBufBytes + 2 * kStageBytes;                // W1 hi/lo (2 KB)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wimg + 2048);           // [0,1] TMA, [2,3] MMA
+    uint8_t* wimg = sm + 2 * kBufBytes + 2 * kStageBytes;                // W1 hi | lo | -hi (3 KB)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wimg + kWImgBytes);     // [0,1] TMA, [2,3] MMA
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
     const int t = threadIdx.x, warp = t >> 5;
     const int64_t n = a.n;
@@ -628,7 +629,8 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
         for (int q = 0; q < 4; ++q) mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    reinterpret_cast<uint4*>(wimg)[t] = f.w1img[t];  // 128 x 16 B
+    reinterpret_cast<uint4*>(wimg)[t] = f.w1img[t];  // 192 x 16 B
+    if (t < 64) reinterpret_cast<uint4*>(wimg)[128 + t] = f.w1img[128 + t];
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
@@ -753,8 +755,14 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
                     h2[v] = z > 0.0f ? z : fmaf(EA[k], eb[2 * u + v], -as);
                 }
                 const __half2 hh = __floats2half2_rn(h2[0], h2[1]);
-                const float2 hf = __half22float2(hh);
-                const __half2 ll = __floats2half2_rn(h2[0] - hf.x, h2[1] - hf.y);
+                // the split's residual as hi - h (exact), one mixed-precision FHADD per unit; the
+                // lo product then runs against -W_hi (third W image block)
+                float r0, r1;
+                asm("{\n\t.reg .f16 a, b;\n\tmov.b32 {a, b}, %2;\n\tsub.rn.f32.f16 %0, a, %3;\n\t"
+                    "sub.rn.f32.f16 %1, b, %4;\n\t}"
+                    : "=f"(r0), "=f"(r1)
+                    : "r"(h2u(hh)), "f"(h2[0]), "f"(h2[1]));
+                const __half2 ll = __floats2half2_rn(r0, r1);
                 hw[u] = h2u(hh);
                 lw[u] = h2u(ll);
             }
@@ -774,13 +782,14 @@ __global__ void __launch_bounds__(kFT, 4) ncf_fast_kernel(const __grid_constant_
             // descriptors = the base descriptors + (byte offset >> 4) in the start-address field
             const uint64_t ah = adesc0 + static_cast<uint64_t>((b * kBufBytes) >> 4), al = ah + (kABytes >> 4);
             const uint32_t d = tmem + static_cast<uint32_t>(b * 16);
-            // D = Ah.Wh + Ah.Wl + Al.Wh over K = 32 (2 slabs of 16)
+            // D = Ah.Wh + Ah.Wl + (-Al).(-Wh) over K = 32 (2 slabs of 16); the operand's lo
+            // half holds hi - h = -Al
             umma_f16(d, ah, wdesc0, 0u);
             umma_f16(d, ah + (4096 >> 4), wdesc0 + (512 >> 4), 1u);
             umma_f16(d, ah, wdesc0 + (1024 >> 4), 1u);
             umma_f16(d, ah + (4096 >> 4), wdesc0 + (1536 >> 4), 1u);
-            umma_f16(d, al, wdesc0, 1u);
-            umma_f16(d, al + (4096 >> 4), wdesc0 + (512 >> 4), 1u);
+            umma_f16(d, al, wdesc0 + (2048 >> 4), 1u);
+            umma_f16(d, al + (4096 >> 4), wdesc0 + (2560 >> 4), 1u);
             umma_commit(bars + 2 + b);
         }
         __syncwarp();

@@ -72,7 +72,7 @@ struct NcfFastArgs {
     float* A;    // m x 32: W0[:, :ka] . u_i + b0 (unscaled)
     float* EA;   // m x 32: exp(A)
     float* BE;   // n x kNsColFloats
-    const uint4* w1img;  // 2 KB: (lambda W1 * s_w) as fp16 hi/lo in the UMMA core-matrix layout
+    const uint4* w1img;  // 3 KB: (lambda W1 * s_w) as fp16 hi | lo | -hi in the UMMA core-matrix layout
     NcfFastScale* scale;
     float b1[16], w2[16], b2;  // b1 log2(e), lambda W2 ln(2): the epilogue's log2 units
     int e_w;                   // log2 s_w
