@@ -190,6 +190,10 @@ __global__ void __launch_bounds__(256) ncf_rowprep_kernel(NcfSelArgs a) {
         const double pbase = base_obs ? a.val[re - 1] : (st.status == OCG_OK ? a.rows[i].pbase : 1.0);
         st.pbase = pbase;
         const double thr = valid_threshold(pbase, a.gamma);
+        // valid is monotone in p, so a verified threshold turns each cell's exact test (an FP64
+        // divide) into one compare
+        st.thr = thr;
+        st.thr_ok = valid_exact(thr, pbase, a.gamma) && !valid_exact(next_down(thr), pbase, a.gamma) ? 1 : 0;
         float f = static_cast<float>(thr);
         if (static_cast<double>(f) < thr) f = __uint_as_float(__float_as_uint(f) + 1u);
         st.fthr = f;
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(256) ncf_rowprep_kernel(NcfSelArgs a) {
         for (int64_t e = rb + lane; e < re; e += 32) {
             const int j = a.col[e];
             const double p = a.val[e];
-            if (!valid_exact(p, pbase, a.gamma)) continue;
+            if (st.thr_ok ? !(p >= thr) : !valid_exact(p, pbase, a.gamma)) continue;
             ++oc;
             exact_consider(&b, p, capsum(a, j), j, a.e_base);
         }
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kExW * 32) ncf_exact_kernel(NcfSelArgs a) {
             }
             const double pd = clamp_perf(dadd(dotN<LANE, H1>(w2, h1), b2[0]));
             if (LIST) a.completed[r * n + j] = pd;
-            if (!valid_exact(pd, st.pbase, a.gamma)) continue;
+            if (st.thr_ok ? !(pd >= st.thr) : !valid_exact(pd, st.pbase, a.gamma)) continue;
             ++cnt;
             exact_consider(&b, pd, capsum(a, j), static_cast<int>(j), a.e_base);
         }
@@ -433,7 +437,7 @@ __global__ void __launch_bounds__(kExW * 32) ncf_exact_generic_kernel(NcfSelArgs
             if ((mybits[j >> 5] >> (j & 31)) & 1u) continue;
             const double pd = cell_generic<LANE>(a, sw, a.P + i * a.ka, a.P + a.set_off + j * a.ks, ExpTabPtr{stab});
             if (LIST) a.completed[r * n + j] = pd;
-            if (!valid_exact(pd, st.pbase, a.gamma)) continue;
+            if (st.thr_ok ? !(pd >= st.thr) : !valid_exact(pd, st.pbase, a.gamma)) continue;
             ++cnt;
             exact_consider(&b, pd, capsum(a, j), static_cast<int>(j), a.e_base);
         }

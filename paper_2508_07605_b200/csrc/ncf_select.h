@@ -26,7 +26,8 @@ struct NcfRowState {
     float fthr;        // smallest float p with loss(p) <= gamma (exact FP64 test)
     int32_t lov;       // 1: a completed value clamped to 0.01 is valid
     int32_t status;    // OCG_* code of the exception the reference would throw for the row
-    int32_t pad;
+    int32_t thr_ok;    // 1: thr is verified exact, so loss(p) <= gamma  <=>  p >= thr
+    double thr;        // smallest double p with loss(p) <= gamma
 };
 
 // device scalars of the fast path (written by the prep kernels)
