@@ -955,7 +955,8 @@ def workload_ncf(args, d: Dist):
                              f"fp16 hi/lo split); SURVEY 8d K2 counted all {_ncf_flops_per_cell(k)} flop/cell on the "
                              f"SIMT pipe (floor ~66 ms), which this kernel beats (k2_all_flops). The gap to the SIMT "
                              f"floor is instruction overhead per SIMT flop (SELU select, fp16 hi/lo split, operand "
-                             f"stores, per-column barrier): the kernel is issue-bound (ncu: "
+                             f"stores, per-column barrier): the kernel is issue-bound (ncu, ~370 instructions per cell, issue "
+                             f"0.70/cycle/SMSP: "
                              f"profiles/r02_c2ncf_fast_ncu.txt). HBM is irrelevant: DRAM 0.69 GB per launch.",
                      "floors_ms": {"fp32_simt": simt_fpc * imputed / (peaks["fp32_tflops"] * 1e12) * 1e3,
                                    "mufu_ex2 (16 per cell, 16/clk/SM)": 16 * imputed / (16 * 148 * 1.965e9) * 1e3,
