@@ -26,8 +26,8 @@
 //        W0 [u;v] + b0 = A_i + B_j, and its exp factorises, exp(A+B) =
 //        exp(A) exp(B), so SELU needs no MUFU op; the 32 -> 16 layer runs on
 //        the 5th-gen tensor cores (tcgen05.mma kind::f16, M = 128 rows x N = 16
-//        x K = 32, FP16 hi/lo split: Ah.Wh + Ah.Wl + Al.Wh, FP32 accumulate in
-//        TMEM); B_j tiles arrive by TMA.  |dp|/p ~ 1e-6; selections exact
+//        x K = 32, FP16 hi/lo split: Ah.Wh + Ah.Wl + (-Al).(-Wh), FP32 accumulate
+//        in TMEM); B_j tiles arrive by TMA.  |dp|/p ~ 1e-6; selections exact
 //        wherever the row's margin exceeds that.
 #include <algorithm>
 #include <type_traits>
