@@ -335,17 +335,14 @@ __global__ void __launch_bounds__(kExW * 32) ncf_exact_kernel(NcfSelArgs a) {
                 v[q] = t.x;
                 v[q + 1] = t.y;
             }
-            // layer 0 (continued over v) -> SELU -> streamed into layer 1's accumulators
-            double acc1[H1][NACC];
+            double h1[H1];
+            if constexpr (K <= 32) {
+                // layer 0 (continued over v) -> SELU into registers, then layer 1 one output at a
+                // time: v's registers die as h0's fill, and layer 1 needs 4 accumulators instead of
+                // 64 -- the same operation order (dotN = the lane's dot), half the registers
+                double h0[H0];
 #pragma unroll
-            for (int p = 0; p < H1; ++p)
-#pragma unroll
-                for (int c = 0; c < NACC; ++c) acc1[p][c] = 0.0;
-#pragma unroll 1
-            for (int o0 = 0; o0 < H0; o0 += NACC) {
-#pragma unroll
-                for (int oo = 0; oo < NACC; ++oo) {
-                    const int o = o0 + oo;
+                for (int o = 0; o < H0; ++o) {
                     const double* w = wv + o * K;
                     double z;
                     if (LANE == 0) {
@@ -365,25 +362,65 @@ __global__ void __launch_bounds__(kExW * 32) ncf_exact_kernel(NcfSelArgs a) {
                         z = dadd(dadd(dadd(c0, c2), dadd(c1, c3)), 0.0);  // IN % 4 == 0: empty tail
                     }
                     z = dadd(z, b0[o]);
-                    double h, gf;
-                    selu_fwd(z, h, gf, tab);
+                    double gf;
+                    selu_fwd(z, h0[o], gf, tab);
+                }
 #pragma unroll
-                    for (int p = 0; p < H1; ++p) {
-                        if (LANE == 0) acc1[p][0] = dadd(acc1[p][0], dmul(w1[p * H0 + o], h));
-                        else acc1[p][oo] = dfma(w1[p * H0 + o], h, acc1[p][oo]);
+                for (int p = 0; p < H1; ++p) {
+                    const double z = dadd(dotN<LANE, H0>(w1 + p * H0, h0), b1[p]);
+                    double gf;
+                    selu_fwd(z, h1[p], gf, tab);
+                }
+            } else {
+                // layer 0 (continued over v) -> SELU -> streamed into layer 1's accumulators
+                double acc1[H1][NACC];
+#pragma unroll
+                for (int p = 0; p < H1; ++p)
+#pragma unroll
+                    for (int c = 0; c < NACC; ++c) acc1[p][c] = 0.0;
+#pragma unroll 1
+                for (int o0 = 0; o0 < H0; o0 += NACC) {
+#pragma unroll
+                    for (int oo = 0; oo < NACC; ++oo) {
+                        const int o = o0 + oo;
+                        const double* w = wv + o * K;
+                        double z;
+                        if (LANE == 0) {
+                            double acc = myst[o];
+#pragma unroll
+                            for (int q = 0; q < K; ++q) acc = dadd(acc, dmul(w[q], v[q]));
+                            z = acc;
+                        } else {
+                            double c0 = myst[4 * o], c1 = myst[4 * o + 1], c2 = myst[4 * o + 2], c3 = myst[4 * o + 3];
+#pragma unroll
+                            for (int q = 0; q < K; q += 4) {
+                                c0 = dfma(w[q], v[q], c0);
+                                c1 = dfma(w[q + 1], v[q + 1], c1);
+                                c2 = dfma(w[q + 2], v[q + 2], c2);
+                                c3 = dfma(w[q + 3], v[q + 3], c3);
+                            }
+                            z = dadd(dadd(dadd(c0, c2), dadd(c1, c3)), 0.0);  // IN % 4 == 0: empty tail
+                        }
+                        z = dadd(z, b0[o]);
+                        double h, gf;
+                        selu_fwd(z, h, gf, tab);
+#pragma unroll
+                        for (int p = 0; p < H1; ++p) {
+                            if (LANE == 0) acc1[p][0] = dadd(acc1[p][0], dmul(w1[p * H0 + o], h));
+                            else acc1[p][oo] = dfma(w1[p * H0 + o], h, acc1[p][oo]);
+                        }
                     }
                 }
-            }
-            double h1[H1];
 #pragma unroll
-            for (int p = 0; p < H1; ++p) {
-                double z = LANE == 0 ? acc1[p][0]
-                                     : dadd(dadd(dadd(acc1[p][0], acc1[p][NACC > 2 ? 2 : 0]),
-                                                 dadd(acc1[p][NACC > 1 ? 1 : 0], acc1[p][NACC > 3 ? 3 : 0])),
-                                            0.0);
-                z = dadd(z, b1[p]);
-                double gf;
-                selu_fwd(z, h1[p], gf, tab);
+                for (int p = 0; p < H1; ++p) {
+                    double z = LANE == 0 ? acc1[p][0]
+                                         : dadd(dadd(dadd(acc1[p][0], acc1[p][NACC > 2 ? 2 : 0]),
+                                                     dadd(acc1[p][NACC > 1 ? 1 : 0], acc1[p][NACC > 3 ? 3 : 0])),
+                                                0.0);
+                    z = dadd(z, b1[p]);
+                    double gf;
+                    selu_fwd(z, h1[p], gf, tab);
+                }
             }
             const double pd = clamp_perf(dadd(dotN<LANE, H1>(w2, h1), b2[0]));
             if (LIST) a.completed[r * n + j] = pd;
