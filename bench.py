@@ -942,7 +942,7 @@ def workload_ncf(args, d: Dist):
         "exact_precision": exact if exact else "not run (--exact-step; r02: 1.88 s/step, decisions equal to the "
                                                  "fast path on all 1M rows, profiles/r02_bench_c2ncf_exact.json)",
         "scaling": "weak",
-        "gpu_launches": args.steps * 9,
+        "gpu_launches": args.steps * 7,  # validate, fast_rows, fast_cols, fast_scale, base, rowprep, fast
         "roofline": {"bound": "fp32", "kernel": "ncf_fast_kernel (tcgen05.mma kind::f16 M128 N16 K16 x6 per "
                                                 "128 cells, TMA-staged B_j tiles)",
                      "achieved": simt_achieved, "peak": peaks["fp32_tflops"], "unit": "TFLOP/s",
