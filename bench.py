@@ -709,6 +709,14 @@ def workload_c4(args, d: Dist):
     m, n = cfg["m"], grid.n
     ctx = ocg.Context(d.local)
     dev = torch.device("cuda", d.local)
+    sweeps_rule = {"rule": "fixed by --sweeps", "sweeps": args.sweeps}
+    if args.sweeps <= 0:  # the same stated convergence rule as c2 (rank 0 decides, all ranks use it)
+        from paper_2508_07605_b200.dist import shard_rows as _sr
+
+        sw, sweeps_rule = als_sweeps_rule(A, grid, AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=1, seed=42),
+                                          args.gamma, ctx, m, goff=_sr(m, d.world, d.rank)[0])
+        args.sweeps = int(d.max(float(sw)))
+        sweeps_rule["sweeps"] = args.sweeps
     hyp = AlsHyper(rank=cfg["rank"], lam=args.als_lambda, sweeps=args.sweeps, seed=42)
     nref = args.warmup + args.steps + (1 + args.steps if d.world == 1 else 0)
     deltas, B = [], A
@@ -758,7 +766,7 @@ def workload_c4(args, d: Dist):
                    "d2h_bytes_per_step": int(sum(x.numel() * x.element_size() for x in r)) * d.world},
            "config": {"workload": "c4", "apps": m, "settings": n, "rank": cfg["rank"],
                       "arrivals": "1 new observation in each of 1% of rows per refit, cumulative",
-                      "observed_per_gpu": A.nnz, "sweeps": args.sweeps,
+                      "observed_per_gpu": A.nnz, "sweeps": args.sweeps, "sweeps_rule": sweeps_rule,
                       "parallelism": f"rows sharded over {d.world} GPU(s)" if d.world > 1 else "1 GPU",
                       "timing": "wall clock per synchronous refit (new cells H2D + device CSR merge + run + "
                                 "readback), max over ranks, L2 flushed before each"},
@@ -770,7 +778,7 @@ def workload_c4(args, d: Dist):
         plan.set_warm(0)
         out["refit_latency_ms"]["warm_2_sweeps_median"] = statistics.median(tw) * 1e3
         out["refit_latency_ms"]["warm_note"] = ("deviation: starts from the previous factors with 2 sweeps "
-                                                "instead of a from-scratch 10-sweep fit")
+                                                f"instead of a from-scratch {args.sweeps}-sweep fit")
     plan.close()
     return out, ("c4", m)
 
