@@ -195,7 +195,7 @@ __device__ void uniform_fill(double* dst, int cnt, double lo, double hi, MtWarp&
 // chains and SELU exps are independent instruction streams (ILP) instead of a loop
 template <int LANE, class A, int LAY>
 __device__ __forceinline__ void forward_layer_fix(const Smem& S, const A& a, const BatchGeom& g, int cnt, bool tape,
-                                                  int warp, int lane) {
+                                                  double scale, int warp, int lane) {
     constexpr int in = A::dim(LAY), out = A::dim(LAY + 1), NO = (out + kCW - 1) / kCW;
     constexpr bool hidden = LAY + 1 < A::L();
     const double* W = S.P() + g.off_w[LAY];
@@ -215,16 +215,20 @@ __device__ __forceinline__ void forward_layer_fix(const Smem& S, const A& a, con
                 double v = z[q], gf = 1.0;
                 if (hidden) selu_fwd(z[q], v, gf, S.tab());
                 S.act(LAY + 1)[lane * A::stride(LAY + 1) + o] = v;
-                if (tape) S.del(LAY)[lane * A::stride(LAY + 1) + o] = gf;
+                // output layer with tape: backprop's first delta here (2 err scale * 1), saving a barrier
+                if (tape) S.del(LAY)[lane * A::stride(LAY + 1) + o] =
+                    hidden ? gf : dmul(dmul(dmul(2.0, dsub(v, S.s_y()[lane])), scale), 1.0);
             }
         }
     }
     bar_compute();
 }
 
+// forward() / forward_tape(); with tape the output layer also writes backprop's first delta
+// (2 err scale, identity grad 1) so backward_chunk starts at the output layer's matvec_t
 template <int LANE, class A>
 __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt, bool tape,
-                                              int warp, int lane, int ctid) {
+                                              int warp, int lane, int ctid, double scale = 0.0) {
     const int in0 = a.dim(0);
     for (int w = ctid; w < cnt * in0; w += kCT) {
         const int s = w / in0, i = w - s * in0;
@@ -235,9 +239,9 @@ __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const B
     bar_compute();
     if constexpr (A::kStatic && LANE == 0) {  // (the AVX2 lane's 4-accumulator dots would spill)
         static_assert(A::L() == 3, "FixArch is the 3-layer default stack");
-        forward_layer_fix<LANE, A, 0>(S, a, g, cnt, tape, warp, lane);
-        forward_layer_fix<LANE, A, 1>(S, a, g, cnt, tape, warp, lane);
-        forward_layer_fix<LANE, A, 2>(S, a, g, cnt, tape, warp, lane);
+        forward_layer_fix<LANE, A, 0>(S, a, g, cnt, tape, scale, warp, lane);
+        forward_layer_fix<LANE, A, 1>(S, a, g, cnt, tape, scale, warp, lane);
+        forward_layer_fix<LANE, A, 2>(S, a, g, cnt, tape, scale, warp, lane);
     } else {
 #pragma unroll
         for (int l = 0; l < kMaxLayers; ++l) {
@@ -253,7 +257,8 @@ __device__ __forceinline__ void forward_chunk(const Smem& S, const A& a, const B
                     double v = z, gf = 1.0;
                     if (hidden) selu_fwd(z, v, gf, S.tab());
                     S.act(l + 1)[lane * a.stride(l + 1) + o] = v;
-                    if (tape) S.del(l)[lane * a.stride(l + 1) + o] = gf;
+                    if (tape) S.del(l)[lane * a.stride(l + 1) + o] =
+                        hidden ? gf : dmul(dmul(dmul(2.0, dsub(v, S.s_y()[lane])), scale), 1.0);
                 }
             }
             bar_compute();
@@ -301,12 +306,8 @@ __device__ __forceinline__ void backward_layer_fix(const Smem& S, const A& a, co
 template <int LANE, class A>
 __device__ __forceinline__ void backward_chunk(const Smem& S, const A& a, const BatchGeom& g, int cnt,
                                                double scale, int warp, int lane) {
+    (void)scale;  // the output delta was written by forward_chunk (tape)
     if constexpr (A::kStatic && LANE == 1) {  // (with the scalar lane's ILP forward this would spill)
-        if (warp == 0 && lane < cnt) {
-            const double err = dsub(S.act(3)[lane * A::stride(3)], S.s_y()[lane]);
-            S.del(2)[lane * A::stride(3)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
-        }
-        bar_compute();
         backward_layer_fix<LANE, A, 2>(S, a, g, cnt, warp, lane);
         backward_layer_fix<LANE, A, 1>(S, a, g, cnt, warp, lane);
         backward_layer_fix<LANE, A, 0>(S, a, g, cnt, warp, lane);
@@ -315,14 +316,6 @@ __device__ __forceinline__ void backward_chunk(const Smem& S, const A& a, const 
 #pragma unroll
         for (int l = kMaxLayers - 1; l >= 0; --l) {
             if (l >= L) continue;
-            if (l == L - 1) {
-                if (warp == 0 && lane < cnt) {
-                    const double err = dsub(S.act(l + 1)[lane * a.stride(l + 1)], S.s_y()[lane]);
-                    // delta = 2*err*scale, then *= identity grad 1.0
-                    S.del(l)[lane * a.stride(l + 1)] = dmul(dmul(dmul(2.0, err), scale), 1.0);
-                }
-                bar_compute();
-            }
             const int in = a.dim(l), out = a.dim(l + 1);
             const double* W = S.P() + g.off_w[l];
             const double* d = S.del(l) + lane * a.stride(l + 1);
@@ -711,7 +704,7 @@ __device__ __forceinline__ void app_batch_body(const BatchGeom& g, const BatchIO
                             }
                         }
                         bar_compute();
-                        forward_chunk<LANE>(S, a, g, cnt, true, warp, lane, ctid);
+                        forward_chunk<LANE>(S, a, g, cnt, true, warp, lane, ctid, scale);
                         backward_chunk<LANE>(S, a, g, cnt, scale, warp, lane);
                         // AdamState::step (nnkit.cpp:239-251): dense over every block
                         b1p = dmul(b1p, b1);
