@@ -86,11 +86,15 @@ __device__ __forceinline__ bool better(double s, double p, int sum, int j, const
 __device__ __forceinline__ void merge(Best& b, const Best& o) {
     if (o.j >= 0 && better(o.s, o.p, o.sum, o.j, b)) b = o;
 }
-// FP64 evaluation of a valid cell (policy.cpp:37-38) + the 4-key compare
-__device__ __noinline__ void exact_consider(Best* b, double pd, int cs, int j, double e_base) {
+// FP64 evaluation of a valid cell (policy.cpp:37-38) + the 4-key compare; out of line for the
+// dense kernels (a rare band path), inline for the observed-cell pass
+__device__ __forceinline__ void exact_consider_inl(Best& b, double pd, int cs, int j, double e_base) {
     const double e_pred = ddiv(static_cast<double>(cs), pd);
     const double s = ddiv(dsub(e_base, e_pred), e_base);
-    if (better(s, pd, cs, j, *b)) *b = Best{s, pd, j, cs};
+    if (better(s, pd, cs, j, b)) b = Best{s, pd, j, cs};
+}
+__device__ __noinline__ void exact_consider(Best* b, double pd, int cs, int j, double e_base) {
+    exact_consider_inl(*b, pd, cs, j, e_base);
 }
 __device__ __forceinline__ Best warp_best(Best b) {
     for (int off = 16; off > 0; off >>= 1) {
@@ -206,13 +210,13 @@ __global__ void __launch_bounds__(256) ncf_rowprep_kernel(NcfSelArgs a) {
             const double p = a.val[e];
             if (st.thr_ok ? !(p >= thr) : !valid_exact(p, pbase, a.gamma)) continue;
             ++oc;
-            exact_consider(&b, p, capsum(a, j), j, a.e_base);
+            exact_consider_inl(b, p, capsum(a, j), j, a.e_base);
         }
         b = warp_best(b);
         for (int off = 16; off > 0; off >>= 1) oc += __shfl_xor_sync(0xffffffffu, oc, off);
         if (!base_obs && st.status == OCG_OK) {  // the predicted baseline cell: loss 0, always valid
             ++oc;
-            if (lane == 0) exact_consider(&b, pbase, capsum(a, n - 1), static_cast<int>(n - 1), a.e_base);
+            if (lane == 0) exact_consider_inl(b, pbase, capsum(a, n - 1), static_cast<int>(n - 1), a.e_base);
         }
         st.best_s = b.s;
         st.best_p = b.p;
